@@ -1,0 +1,429 @@
+"""Pins for the oracle (oracle/krylov.py) against things other than itself:
+closed forms, the mathematics (dense exponentials, Krylov-space definition,
+mpmath), special cases that reduce to textbook results, and the paper's printed
+values (tests/golden/).  CPU only.
+"""
+import json
+import math
+import os
+
+import mpmath
+import numpy as np
+import pytest
+import scipy.integrate as si
+import scipy.linalg as sl
+import scipy.sparse as sp
+
+from oracle import krylov as K
+from workloads import memory_burden as mb
+from workloads import models
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def csr_from_dense(A):
+    S = sp.csr_matrix(A)
+    S.sort_indices()
+    return S.indptr.astype(np.int64), S.indices.astype(np.int32), S.data.astype(A.dtype)
+
+
+def rand_herm(n, density, seed, complex_=True):
+    g = np.random.default_rng(seed)
+    A = g.standard_normal((n, n)) + (1j * g.standard_normal((n, n)) if complex_ else 0)
+    A = A * (g.random((n, n)) < density)
+    A = A + A.conj().T
+    np.fill_diagonal(A, np.diag(A).real + 0.1)  # keep an explicit diagonal
+    return A if complex_ else A.real
+
+
+def dense_evolve(A, v0, t):
+    lam, U = np.linalg.eigh(A)
+    return U @ (np.exp(-1j * lam * t) * (U.conj().T @ v0))
+
+
+# ---------------------------------------------------------------- spmv / norm
+
+def test_spmv_matches_dense_matvec():
+    A = rand_herm(57, 0.1, 1)
+    rp, c, v = csr_from_dense(A)
+    x = np.random.default_rng(2).standard_normal(57) + 1j
+    assert np.allclose(K.spmv(rp, c, v, x), A @ x, rtol=0, atol=1e-13)
+
+
+def test_spmv_identity_and_permutation():
+    rp, c, v = csr_from_dense(np.eye(3, dtype=complex))
+    x = np.array([1 + 2j, -3, 0.5j])
+    assert np.array_equal(K.spmv(rp, c, v, x), x)
+    rp, c, v = csr_from_dense(np.array([[0, 1], [1, 0]], dtype=complex))
+    assert np.array_equal(K.spmv(rp, c, v, np.array([1, 0], complex)), np.array([0, 1], complex))
+
+
+def test_one_norm_hand_values():
+    rp, c, v = csr_from_dense(np.array([[0, 1], [1, 0]], dtype=float))
+    assert K.one_norm(rp, c, v, 2) == 1.0
+    rp, c, v = csr_from_dense(np.diag([2.0, -3.0]))
+    assert K.one_norm(rp, c, v, 2) == 3.0
+    A = rand_herm(40, 0.2, 3)
+    rp, c, v = csr_from_dense(A)
+    assert math.isclose(K.one_norm(rp, c, v, 40), np.abs(A).sum(axis=0).max(), rel_tol=1e-14)
+
+
+# ---------------------------------------------------------------- Arnoldi
+
+@pytest.mark.parametrize("ortho", ["cgs2", "lanczos3"])
+def test_arnoldi_relation_and_orthonormality(ortho):
+    n, m = 120, 12
+    A = rand_herm(n, 0.08, 4)
+    v = np.random.default_rng(5).standard_normal(n) + 1j * np.random.default_rng(6).standard_normal(n)
+    v /= np.linalg.norm(v)
+    kr = K.arnoldi(lambda x: A @ x, v, m, 1e-14, ortho)
+    V, a, b = kr["V"], kr["alpha"], kr["beta"]
+    T = np.diag(a) + np.diag(b[:-1], 1) + np.diag(b[:-1], -1)
+    R = A @ V - V @ T
+    # Eq. 9: H V_m = V_m H_m + h v_{m+1} e_m^T -> first m-1 residual columns ~ 0, last has norm h
+    norm1 = np.abs(A).sum(axis=0).max()
+    assert np.linalg.norm(R[:, :-1]) <= 32 * 2**-52 * n * norm1
+    assert math.isclose(np.linalg.norm(R[:, -1]), kr["h"], rel_tol=1e-9)
+    if ortho == "cgs2":
+        assert np.abs(V.conj().T @ V - np.eye(m)).max() <= 1e-13
+
+
+def test_arnoldi_spans_krylov_space():
+    """span(V_m) = span{v, Hv, ..., H^{m-1} v} (Eq. 2)."""
+    n, m = 60, 6
+    A = rand_herm(n, 0.15, 7)
+    v = np.random.default_rng(8).standard_normal(n).astype(complex)
+    v /= np.linalg.norm(v)
+    kr = K.arnoldi(lambda x: A @ x, v, m, 1e-14)
+    P = np.stack([np.linalg.matrix_power(A, k) @ v for k in range(m)], axis=1)
+    Q, _ = np.linalg.qr(P)
+    # projectors onto the two subspaces agree
+    assert np.abs(Q @ Q.conj().T - kr["V"] @ kr["V"].conj().T).max() < 1e-9
+
+
+def test_arnoldi_tridiagonal_matches_projection():
+    """H_m = V_m^H H V_m."""
+    n, m = 80, 10
+    A = rand_herm(n, 0.1, 9)
+    v = np.ones(n, complex) / math.sqrt(n)
+    kr = K.arnoldi(lambda x: A @ x, v, m, 1e-14)
+    V = kr["V"]
+    Hm = V.conj().T @ A @ V
+    T = np.diag(kr["alpha"]) + np.diag(kr["beta"][:-1], 1) + np.diag(kr["beta"][:-1], -1)
+    assert np.abs(Hm - T).max() < 1e-12
+
+
+def test_breakdown_pauli_pair_and_eigenvector():
+    X = np.array([[0, 1], [1, 0]], complex)
+    kr = K.arnoldi(lambda x: X @ x, np.array([1, 0], complex), 5, 1e-10)
+    assert kr["m_eff"] == 2 and kr["breakdown"]
+    assert np.allclose(kr["alpha"], [0, 0]) and kr["beta"][0] == 1.0 and kr["h"] == 0.0
+    D = np.diag([2.5, -1.0, 4.0]).astype(complex)
+    kr = K.arnoldi(lambda x: D @ x, np.array([1, 0, 0], complex), 3, 1e-10)
+    assert kr["m_eff"] == 1 and kr["alpha"][0] == 2.5 and kr["h"] == 0.0
+
+
+# ---------------------------------------------------------------- small eig / integrand
+
+def test_small_eig_against_mpmath():
+    g = np.random.default_rng(10)
+    a, b = g.standard_normal(7), np.abs(g.standard_normal(7))
+    lam, U = K.small_eig(a, b)
+    T = mpmath.matrix(7, 7)
+    for i in range(7):
+        T[i, i] = a[i]
+        if i < 6:
+            T[i, i + 1] = T[i + 1, i] = b[i]
+    mpmath.mp.dps = 40
+    E, Q = mpmath.eigsy(T)
+    ev = sorted(float(x) for x in E)
+    assert np.allclose(lam, ev, rtol=0, atol=1e-13)
+    Tn = np.diag(a) + np.diag(b[:6], 1) + np.diag(b[:6], -1)
+    assert np.abs(U @ np.diag(lam) @ U.T - Tn).max() <= 100 * 2**-52 * 7 * np.abs(Tn).max()
+
+
+def test_integrand_2x2_closed_form():
+    a, b, c, h = 0.3, 0.7, -1.1, 0.25
+    lam, U = K.small_eig(np.array([a, c]), np.array([b, 0.0]))
+    Om = math.sqrt(((a - c) / 2) ** 2 + b ** 2)
+    tau = np.linspace(0, 3, 17)
+    exact = h * np.abs(b / Om * np.sin(Om * tau))   # |e2^T e^{-iT tau} e1|
+    assert np.allclose(K.integrand(lam, U, h, tau), exact, rtol=0, atol=1e-15)
+
+
+def test_integrand_against_dense_expm():
+    g = np.random.default_rng(11)
+    a, b = g.standard_normal(8), np.abs(g.standard_normal(8))
+    T = np.diag(a) + np.diag(b[:7], 1) + np.diag(b[:7], -1)
+    lam, U = K.small_eig(a, b)
+    for tau in (0.0, 0.5, 2.3):
+        ref = 0.3 * abs(sl.expm(-1j * T * tau)[7, 0])
+        assert abs(K.integrand(lam, U, 0.3, tau) - ref) < 1e-12
+    assert K.integrand(lam, U, 0.0, 1.7) == 0.0
+    assert K.integrand(lam, U, 0.3, 0.0) < 1e-15
+
+
+def test_omega_against_dense_expm():
+    g = np.random.default_rng(12)
+    a, b = g.standard_normal(6), np.abs(g.standard_normal(6))
+    T = np.diag(a) + np.diag(b[:5], 1) + np.diag(b[:5], -1)
+    lam, U = K.small_eig(a, b)
+    e1 = np.zeros(6); e1[0] = 1
+    assert np.abs(K.omega(lam, U, 0.7) - sl.expm(-1j * T * 0.7) @ e1).max() < 1e-13
+    lam, U = K.small_eig(np.zeros(2), np.array([1.0, 0]))       # Pauli: (cos t, -i sin t)
+    assert np.allclose(K.omega(lam, U, 0.4), [math.cos(0.4), -1j * math.sin(0.4)], atol=1e-15)
+
+
+# ---------------------------------------------------------------- quadrature
+
+def test_tanh_sinh_textbook_integrals():
+    v, ok = K.tanh_sinh(np.sin, 0.0, math.pi)
+    assert ok and abs(v - 2.0) <= 2e-3
+    v, ok = K.tanh_sinh(np.sin, 0.0, math.pi, rel=1e-13)
+    assert ok and abs(v - 2.0) <= 1e-12
+    v, ok = K.tanh_sinh(lambda x: 1 / np.sqrt(x), 0.0, 1.0, rel=1e-10)
+    assert abs(v - 2.0) <= 1e-6
+    v, ok = K.tanh_sinh(np.exp, 0.0, 1.0, rel=1e-13)
+    assert abs(v - (math.e - 1)) <= 1e-12
+    v, ok = K.tanh_sinh(lambda x: np.ones_like(x), 0.0, 1.0)
+    assert ok and abs(v - 1.0) < 1e-12
+    assert K.tanh_sinh(np.sin, 1.0, 1.0) == (0.0, True)
+
+
+def test_error_integral_2x2_closed_form():
+    """int_0^t h |b/Om sin(Om tau)| dtau = h |b| (1 - cos Om t) / Om^2  for Om t <= pi."""
+    a, b, c, h = 0.1, 0.9, 0.4, 0.6
+    lam, U = K.small_eig(np.array([a, c]), np.array([b, 0.0]))
+    Om = math.sqrt(((a - c) / 2) ** 2 + b ** 2)
+    t = 0.9 * math.pi / Om
+    exact = h * abs(b) * (1 - math.cos(Om * t)) / Om ** 2
+    v, ok = K.tanh_sinh(lambda x: K.integrand(lam, U, h, x), 0.0, t)
+    assert ok and abs(v - exact) <= 1e-3 * exact
+    v, _ = K.tanh_sinh(lambda x: K.integrand(lam, U, h, x), 0.0, t, rel=1e-12)
+    assert abs(v - exact) <= 1e-12
+
+
+def test_error_integral_against_mpmath_quad():
+    g = np.random.default_rng(13)
+    a, b = g.standard_normal(10), np.abs(g.standard_normal(10)) + 0.1
+    lam, U = K.small_eig(a, b)
+    f = lambda x: K.integrand(lam, U, 0.5, x)  # noqa: E731
+    ref = float(mpmath.quad(lambda x: float(f(float(x))), [0, 0.4, 0.8, 1.2]))
+    v, ok = K.tanh_sinh(f, 0.0, 1.2)
+    assert ok and abs(v - ref) <= 1e-3 * ref
+
+
+# ---------------------------------------------------------------- step search
+
+def _setup_step(seed, m=8, h=0.3):
+    g = np.random.default_rng(seed)
+    a, b = g.standard_normal(m), np.abs(g.standard_normal(m)) + 0.2
+    lam, U = K.small_eig(a, b)
+    f = lambda x: K.integrand(lam, U, h, x)  # noqa: E731
+    integ = lambda lo, hi: K.tanh_sinh(f, lo, hi)[0]  # noqa: E731
+    return f, integ
+
+
+def test_step_search_breakdown_takes_remaining_time():
+    integ = lambda lo, hi: 0.0  # noqa: E731   h = 0: f == 0
+    tau, e = K.find_step(integ, True, False, 0.5, 3.7, 1e-6, 10.0)
+    assert tau == 3.7 and e == 0.0
+    tau, e = K.find_step(integ, False, True, None, 3.7, 1e-6, 10.0)
+    assert tau == 3.7 and e == 0.0
+
+
+@pytest.mark.parametrize("first", [True, False])
+def test_step_search_rate_and_bracket(first):
+    f, integ = _setup_step(14)
+    tol_rate = 1e-6
+    tau, e = K.find_step(integ, False, first, 0.3, 50.0, tol_rate, 100.0)
+    # independent integrals (scipy adaptive Gauss-Kronrod)
+    E = lambda x: si.quad(f, 0, x, limit=200, epsabs=0, epsrel=1e-12)[0]  # noqa: E731
+    assert e <= tol_rate * tau
+    assert abs(E(tau) - e) <= 2e-3 * E(tau)
+    s = None
+    # the step cannot be extended by one more substep (it stops at the first failure)
+    # bisection bracket: the rate inequality fails somewhere within (tau, tau + tau/5]
+    s = tau / 10 * 2
+    assert E(tau + s) > tol_rate * (tau + s) * (1 - 2e-3)
+
+
+def test_step_search_monotone_in_tol_rate():
+    f, integ = _setup_step(15)
+    prev = 0.0
+    for tr in (1e-9, 1e-8, 1e-7, 1e-6, 1e-5):
+        tau, _ = K.find_step(integ, False, True, None, 1e3, tr, 1e3)
+        assert tau >= prev
+        prev = tau
+
+
+def test_step_collapse():
+    integ = lambda lo, hi: 1.0 * (hi - lo)  # noqa: E731   f == h = 1 (m = 1)
+    with pytest.raises(K.StepCollapse):
+        K.find_step(integ, False, True, None, 1.0, 1e-3, 1.0)
+
+
+def test_roundoff_arithmetic():
+    rp, c, v = csr_from_dense(np.array([[0, 1], [1, 0]], dtype=float))
+    r = K.evolve(rp, c, v, np.array([1, 0], complex), 1.0, 1e-6, 2)
+    assert r["roundoff_step"] == 2 * 1.0 * 2 ** -52  # 4.44e-16 (Eq. 17)
+
+
+# ---------------------------------------------------------------- evolution
+
+def test_evolve_pauli_t_pi():
+    rp, c, v = csr_from_dense(np.array([[0, 1], [1, 0]], dtype=complex))
+    r = K.evolve(rp, c, v, np.array([1, 0], complex), math.pi, 1e-10, 10)
+    assert np.abs(r["v"] - np.array([-1, 0])).max() < 1e-10
+
+
+def test_evolve_rabi_closed_form():
+    """H = (Delta/2) sz + (Om/2) sx: P_1(t) = Om^2/(Om^2+D^2) sin^2(sqrt(Om^2+D^2) t/2)."""
+    D, Om, t = 0.7, 1.3, 3.1
+    A = np.array([[D / 2, Om / 2], [Om / 2, -D / 2]], complex)
+    rp, c, v = csr_from_dense(A)
+    r = K.evolve(rp, c, v, np.array([1, 0], complex), t, 1e-10, 10)
+    W = math.sqrt(Om ** 2 + D ** 2)
+    assert abs(abs(r["v"][1]) ** 2 - Om ** 2 / W ** 2 * math.sin(W * t / 2) ** 2) < 1e-10
+
+
+def test_evolve_block_rabi_ensemble():
+    """Block-diagonal ensemble of independent 2x2 Rabi problems: closed form at any n,
+    and the Krylov space is not exact (many distinct frequencies) so real stepping occurs."""
+    nb = 300
+    g = np.random.default_rng(16)
+    D, Om = g.uniform(-1, 1, nb), g.uniform(0.2, 2, nb)
+    A = sp.block_diag([np.array([[d / 2, o / 2], [o / 2, -d / 2]]) for d, o in zip(D, Om)]).tocsr()
+    A.sort_indices()
+    v0 = (g.standard_normal(2 * nb) + 1j * g.standard_normal(2 * nb))
+    v0 /= np.linalg.norm(v0)
+    t, tol = 6.0, 1e-9
+    r = K.evolve(A.indptr.astype(np.int64), A.indices.astype(np.int32), A.data, v0, t, tol, 20)
+    exact = np.zeros_like(v0)
+    for k in range(nb):
+        W = math.sqrt(D[k] ** 2 + Om[k] ** 2)
+        Hk = np.array([[D[k] / 2, Om[k] / 2], [Om[k] / 2, -D[k] / 2]])
+        # e^{-iHt} = cos(Wt/2) I - i sin(Wt/2) (2H/W)
+        Uk = math.cos(W * t / 2) * np.eye(2) - 1j * math.sin(W * t / 2) * (2 * Hk / W)
+        exact[2 * k: 2 * k + 2] = Uk @ v0[2 * k: 2 * k + 2]
+    err = np.linalg.norm(r["v"] - exact)
+    assert r["restarts"] > 1
+    assert err <= r["bound"] + 10 * r["roundoff_total"]
+    assert r["bound"] <= tol
+
+
+@pytest.mark.parametrize("seed,n,complex_", [(17, 64, True), (18, 150, False), (19, 200, True)])
+def test_evolve_vs_dense_and_bound(seed, n, complex_):
+    A = rand_herm(n, 0.05, seed, complex_)
+    rp, c, v = csr_from_dense(A)
+    g = np.random.default_rng(seed + 100)
+    v0 = g.standard_normal(n) + 1j * g.standard_normal(n)
+    v0 /= np.linalg.norm(v0)
+    t, tol = 5.0, 1e-7
+    r = K.evolve(rp, c, v, v0, t, tol, 15)
+    ve = dense_evolve(A, v0, t)
+    err = np.linalg.norm(r["v"] - ve)
+    assert r["bound"] <= tol
+    assert err <= r["bound"] + 10 * r["roundoff_total"]          # bound validity (Eq. 16)
+    assert abs(np.linalg.norm(r["v"]) - 1) <= r["bound"] + 10 * r["roundoff_total"]
+    e0 = np.vdot(v0, A @ v0).real
+    e1 = np.vdot(r["v"], A @ r["v"]).real
+    assert abs(e1 - e0) <= 2 * np.abs(A).sum(0).max() * (r["bound"] + r["roundoff_total"])
+    assert math.fsum(s[0] for s in r["schedule"]) == pytest.approx(t, rel=0, abs=1e-12)
+    assert sum(s[1] for s in r["schedule"]) == r["krylov_steps"]
+
+
+def test_evolve_time_reversal_and_determinism():
+    A = rand_herm(90, 0.06, 20)
+    rp, c, v = csr_from_dense(A)
+    v0 = np.ones(90, complex) / math.sqrt(90)
+    r1 = K.evolve(rp, c, v, v0, 4.0, 1e-8, 12)
+    r1b = K.evolve(rp, c, v, v0, 4.0, 1e-8, 12)
+    assert np.array_equal(r1["v"], r1b["v"]) and r1["schedule"] == r1b["schedule"]
+    r2 = K.evolve(rp, c, -v, r1["v"] / np.linalg.norm(r1["v"]), 4.0, 1e-8, 12)
+    assert np.linalg.norm(r2["v"] - v0) <= 2e-8
+
+
+def test_evolve_edge_cases():
+    rp, c, v = csr_from_dense(np.diag([1.0, 2.0]))
+    v0 = np.array([1, 0], complex)
+    r = K.evolve(rp, c, v, v0, 0.0, 1e-8, 5)
+    assert r["restarts"] == 0 and np.array_equal(r["v"], v0) and r["bound"] == 0
+    with pytest.raises(K.NotNormalized):
+        K.evolve(rp, c, v, np.array([1, 1], complex), 1.0, 1e-8, 5)
+    # eigenvector: one restart, breakdown at j=0, exact phase
+    r = K.evolve(rp, c, v, v0, 3.0, 1e-8, 5)
+    assert r["restarts"] == 1 and r["breakdowns"] == 1
+    assert abs(r["v"][0] - np.exp(-3j)) < 1e-14
+    # m_max > n: capped at n
+    A = rand_herm(5, 0.5, 21)
+    rp, c, v = csr_from_dense(A)
+    v0 = np.ones(5, complex) / math.sqrt(5)
+    r = K.evolve(rp, c, v, v0, 2.0, 1e-9, 40)
+    assert np.linalg.norm(r["v"] - dense_evolve(A, v0, 2.0)) < 1e-9
+
+
+def test_lanczos3_agrees_with_cgs2_within_bounds():
+    A = rand_herm(100, 0.05, 22)
+    rp, c, v = csr_from_dense(A)
+    v0 = np.ones(100, complex) / 10
+    ra = K.evolve(rp, c, v, v0, 3.0, 1e-9, 10, ortho="cgs2")
+    rb = K.evolve(rp, c, v, v0, 3.0, 1e-9, 10, ortho="lanczos3")
+    assert np.linalg.norm(ra["v"] - rb["v"]) <= ra["bound"] + rb["bound"] + 1e-12
+
+
+def test_xxz_one_magnon_exact():
+    """One-magnon sector of the XXZ(+NNN) chain is an L x L problem (SURVEY §8(c) pin):
+    exact L x L exponential vs the oracle on the full 2^L space."""
+    L = 10
+    h = models.xxz_fields(L, 5)
+    J1, J2, Dl = 1.0, 0.5, 1.0
+    rp, c, v = models.xxz_csr(L, J1, Dl, h, J2=J2)
+    # reference state all-down has diagonal energy E_ref
+    E_ref = (J1 * L + J2 * L) * Dl / 4 - 0.5 * h.sum()
+    M = np.zeros((L, L))
+    for k in range(L):
+        M[k, k] = E_ref - J1 * Dl - J2 * Dl + h[k]
+        M[k, (k + 1) % L] = M[(k + 1) % L, k] = J1 / 2
+        M[k, (k + 2) % L] = M[(k + 2) % L, k] = J2 / 2
+    g = np.random.default_rng(23)
+    a = g.standard_normal(L) + 1j * g.standard_normal(L)
+    a /= np.linalg.norm(a)
+    v0 = np.zeros(1 << L, complex)
+    v0[[1 << k for k in range(L)]] = a
+    t = 3.0
+    r = K.evolve(rp, c, v, v0, t, 1e-10, 30)
+    exact = sl.expm(-1j * M * t) @ a
+    out = r["v"][[1 << k for k in range(L)]]
+    assert np.linalg.norm(out - exact) <= r["bound"] + 1e-13
+    mask = np.ones(1 << L, bool)
+    mask[[1 << k for k in range(L)]] = False
+    assert np.all(r["v"][mask] == 0)      # other Sz sectors stay exactly zero
+
+
+# ---------------------------------------------------------------- paper's printed values
+
+def test_paper_forward_backward_p509():
+    gold = json.load(open(os.path.join(GOLDEN, "paper_p509_forward_backward.json")))
+    H = mb.hamiltonian()
+    assert H["n"] == gold["dimension"]
+    v0 = np.zeros(H["n"], complex)
+    v0[H["init_index"]] = 1
+    t, tol = gold["t"], gold["err_max_each_way"]
+    r1 = K.evolve(H["rowptr"], H["col"], H["val"], v0, t, tol, 40)
+    r2 = K.evolve(H["rowptr"], H["col"], -H["val"], r1["v"], t, tol, 40)
+    err = np.linalg.norm(r2["v"] - v0)
+    assert err <= gold["requested_bound"]
+    assert r1["bound"] + r2["bound"] <= gold["requested_bound"]
+    # true forward error against the dense exponential of the d = 588 matrix
+    Hd = sp.csr_matrix((H["val"], H["col"], H["rowptr"])).toarray()
+    assert np.linalg.norm(sl.expm(-1j * t * Hd) @ v0 - r1["v"]) <= r1["bound"] + 1e-12
+
+
+def test_paper_dimensions_p527_p535():
+    gold = json.load(open(os.path.join(GOLDEN, "paper_dimensions.json")))
+    for case in gold["cases"]:
+        p = dict(mb.DEFAULTS, **case["params"])
+        assert mb.dimension(p) == case["d"]
+    occ, _, _ = mb.basis(mb.DEFAULTS)
+    assert occ.shape[0] == 588
