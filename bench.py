@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""bench.py — Krylov steps/s and achieved HBM GB/s (fraction of roofline) of the restarted
+Krylov exp(-iHt) v engine on 1..8 B200 (BASELINE.json metric).
+
+A bench "step" is one full te_evolve of the workload (all hot-path rows: SpMV+projection,
+CGS2 sweeps, norm, host eigensolve + error integral + step search, V.omega) from v0 to t.
+value = Krylov steps (Arnoldi iterations of the global problem) / device time, max over
+ranks, inputs resident in HBM (te_evolve_dev).  e2e = the same through te_evolve with host
+buffers (pinned), H2D of v0 and D2H of v(t) inside the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+  N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOAD_DEFAULT = 2  # BASELINE.json configs[1] (XXZ L=20); configs[0] is the oracle-size case
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=WORKLOAD_DEFAULT)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-steps", type=int, default=8)
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(cfg_name):
+    """Per-launch DRAM bytes of each kernel from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(cfg_name)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.sw_power_cap",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown"]
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def build_workload(cfg, ws, rank):
+    from workloads import configs
+    c = configs.build(cfg)
+    n = c["n"]
+    if ws == 1:
+        return c, 0, n
+    rb, re_ = (rank * n) // ws, ((rank + 1) * n) // ws
+    rp = c["rowptr"]
+    c["rowptr_local"] = (rp[rb: re_ + 1] - rp[rb]).astype(np.int64)
+    c["col_local_global"] = c["col"][rp[rb]: rp[re_]].astype(np.int64)
+    c["val_local"] = c["val"][rp[rb]: rp[re_]]
+    return c, rb, re_
+
+
+# ------------------------------------------------------------------------------------------
+# CPU baseline: the oracle as it stands, single thread, bounded sample
+# ------------------------------------------------------------------------------------------
+def oracle_sample(c, steps, warmup=0):
+    """Oracle Krylov steps at the mean basis size j = m/2 of the workload (cost per step is
+    linear in j, so this is the average restart step).  Setup (building the first j columns
+    with the oracle's own arnoldi) is untimed.  Returns (steps/s, seconds per step, sample)."""
+    from oracle import krylov as K
+    m = c["m"]
+    j = m // 2
+    tol_rate = c["tol"] / c["t"]
+
+    def mv(x):
+        return K.spmv(c["rowptr"], c["col"], c["val"], x)
+
+    kr = K.arnoldi(mv, c["v0"], j + 1, tol_rate)
+    V = np.zeros((c["n"], j + 1), dtype=np.complex128)
+    V[:, : kr["V"].shape[1]] = kr["V"]
+    beta = kr["beta"]
+    times = []
+    for it in range(warmup + steps):
+        t0 = time.perf_counter()
+        K.arnoldi_step(mv, V, beta, j)
+        dt = time.perf_counter() - t0
+        if it >= warmup:
+            times.append(dt)
+    per = sum(times) / len(times)
+    sample = (f"{len(times)} oracle Arnoldi/CGS2 steps (oracle.krylov.arnoldi_step) at j={j} "
+              f"(mean basis size of an m={m} restart) on the full workload, 1 thread")
+    return 1.0 / per, per, sample, times
+
+
+def set_single_thread():
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if ws > 1 and rank != 0:
+        return 0
+    set_single_thread()
+    from workloads import configs
+    c = configs.build(args.config)
+    rate, per, sample, times = oracle_sample(c, args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": "Krylov steps/s", "value": rate, "unit": "krylov_steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic", "config": {"workload": f"{c['name']} (BASELINE configs[{args.config - 1}])",
+                                        "n": c["n"], "nnz": int(c["rowptr"][-1]), "m": c["m"]},
+        "cpu_baseline": {"value": rate, "unit": "krylov_steps/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": rate, "unit": "krylov_steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    from paper_2205_15346_b200 import build as B
+    from paper_2205_15346_b200 import te
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    if rank == 0:
+        B.build()
+    if ws > 1:
+        torch.distributed.barrier()
+    te.load()
+    dev = torch.device("cuda", local if ws > 1 else 0)
+
+    c, rb, re_ = build_workload(args.config, ws, rank)
+    n_glob, nloc = c["n"], re_ - rb
+    t, tol, m = c["t"], c["tol"], c["m"]
+    if ws == 1:
+        h = te.te_create_csr(n_glob, c["rowptr"], c["col"], c["val"])
+        v0_loc = c["v0"]
+    else:
+        import torch.distributed as dist
+        uid = [te.te_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        D = te.te_dist_init(ws, rank, uid[0])
+        h = te.te_create_csr_dist(D, n_glob, rb, re_, c["rowptr_local"], c["col_local_global"], c["val_local"])
+        v0_loc = c["v0"][rb:re_]
+    stream = torch.cuda.current_stream(dev)
+    d_v0 = torch.from_numpy(np.ascontiguousarray(v0_loc)).to(dev)
+    d_out = torch.empty_like(d_v0)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    def one_step():
+        return te.te_evolve_dev(h, d_v0, t, tol, m, d_out, stream=stream)
+
+    for _ in range(args.warmup):
+        st = one_step()
+    torch.cuda.synchronize()
+    # ---- timed region (device-resident inputs), CUDA events on the launching stream
+    te.te_set_option(h, te.TE_OPT_PROFILE, 1)
+    l0 = te.te_launch_count(h)
+    clk = ClockSampler(local if ws > 1 else 0) if rank == 0 else None
+    if clk:
+        clk.start()
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ksteps = 0
+    stats = []
+    for _ in range(args.steps):
+        st = one_step()
+        stats.append(st)
+        ksteps += st["n_krylov_steps"]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    clocks = clk.stop() if clk else None
+    launches = te.te_launch_count(h) - l0
+    prof = te.te_get_profile(h)
+    te.te_set_option(h, te.TE_OPT_PROFILE, 0)
+    if ws > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+
+    # ---- e2e through the public host-buffer API (pinned host memory), wall clock
+    hv0 = torch.from_numpy(np.ascontiguousarray(v0_loc)).pin_memory()
+    hout = torch.empty_like(hv0).pin_memory()
+    v0n, outn = hv0.numpy(), hout.numpy()
+    te.te_evolve(h, v0n, t, tol, m, out=outn)
+    barrier()
+    w0 = time.perf_counter()
+    e2e_steps = 0
+    for _ in range(args.steps):
+        _, st2 = te.te_evolve(h, v0n, t, tol, m, out=outn)
+        e2e_steps += st2["n_krylov_steps"]
+    w1 = time.perf_counter()
+    e2e_s = w1 - w0
+    if ws > 1:
+        tt = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+
+    peak, peak_src = load_peaks()
+    # dominant kernel = largest share of device time in the timed region
+    dom = max((k for k in prof if prof[k]["launches"] > 0), key=lambda k: prof[k]["total_ms"])
+    p = prof[dom]
+    achieved = p["alg_bytes"] / (p["total_ms"] * 1e-3) / 1e9
+    traffic_tab = load_traffic(c["name"])
+    traffic = None
+    if traffic_tab and dom in traffic_tab:
+        traffic = traffic_tab[dom].get("dram_bytes_per_launch")
+    all_ms = sum(prof[k]["total_ms"] for k in prof)
+    all_bytes = sum(prof[k]["alg_bytes"] for k in prof)
+    value = ksteps / (ms * 1e-3)
+    line = {
+        "metric": "Krylov steps/s", "value": value, "unit": "krylov_steps/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic",
+        "config": {"workload": f"{c['name']} (BASELINE configs[{args.config - 1}])", "n": n_glob,
+                   "nnz": int(c["rowptr"][-1]), "m": m, "t": t, "tol": tol,
+                   "krylov_steps_per_step": ksteps / args.steps,
+                   "restarts_per_step": stats[-1]["n_restarts"],
+                   "l2": "inputs larger than L2 (V = %.0f MB > 126 MB)" % (16 * nloc * m / 1e6),
+                   "parallelism": f"rows{ws}"},
+        "achieved_hbm_gbs": all_bytes / (all_ms * 1e-3) / 1e9 if all_ms > 0 else None,
+        "evolved_time_per_s": t * args.steps / (ms * 1e-3),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "alg_bytes_per_launch": p["alg_bytes"] / p["launches"],
+                     "avg_launch_ms": p["total_ms"] / p["launches"],
+                     "share_of_kernel_time": p["total_ms"] / all_ms if all_ms else None},
+        "kernels": {k: {"launches": prof[k]["launches"], "ms": prof[k]["total_ms"],
+                        "gbs": (prof[k]["alg_bytes"] / (prof[k]["total_ms"] * 1e-3) / 1e9) if prof[k]["total_ms"] else None}
+                    for k in prof if prof[k]["launches"]},
+        "e2e": {"value": e2e_steps / e2e_s, "unit": "krylov_steps/s", "h2d_bytes_per_step": 16 * nloc,
+                "d2h_bytes_per_step": 16 * nloc, "timing": "wall clock around te_evolve (host buffers, pinned)"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "err_bound": stats[-1]["err_bound"],
+    }
+    if not args.no_cpu_baseline and ws == 1:
+        set_single_thread()
+        rate, per, sample, _ = oracle_sample(c, args.cpu_sample_steps)
+        line["cpu_baseline"] = {"value": rate, "unit": "krylov_steps/s", "cores": 1, "kind": "oracle",
+                                "sample": sample}
+    print(json.dumps(line))
+    h.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,185 @@
+/*
+ * te.h — C ABI of the B200-native restarted-Krylov engine for v(t) = exp(-iHt) v(0)
+ * (after Michel & Zell, "TimeEvolver", arXiv:2205.15346).
+ *
+ * Citations: P:n = line n of the paper's LaTeX source.
+ *   Problem statement            Eq. 1, Alg. 1 input/output
+ *   Arnoldi/Lanczos basis        Eq. 8, Alg. 1 step 1
+ *   Krylov approximation         Eq. 11
+ *   Error bound                  Eq. 16, tanh-sinh quadrature
+ *   Step size / error rate       Eqs. 18-19, Alg. 1 step 2
+ *   Roundoff estimate            Eq. 17, warning
+ * Readings of ambiguous passages: DESIGN.md "Readings".
+ *
+ * Conventions (all functions):
+ *  - Everything is extern "C"; no C++ exception crosses the ABI.  Every entry
+ *    point that can fail returns a status code (TE_OK = 0) or NULL, and sets a
+ *    thread-local status/message readable with te_last_status()/te_last_error().
+ *  - Complex numbers are te_c128 = {re, im} doubles (== numpy.complex128 ==
+ *    C99 double _Complex layout).  Vectors are dense, contiguous, length n.
+ *  - CSR: rowptr int64 [n+1] with rowptr[0] = 0 and non-decreasing; col int32
+ *    [nnz] with 0 <= col < n and strictly increasing within a row (duplicates
+ *    are rejected); val [nnz].  H must be Hermitian: structurally symmetric
+ *    with |H_ij - conj(H_ji)| <= 8 eps max(|H_ij|,|H_ji|) and real diagonal.
+ *  - Ownership: every input pointer is borrowed for the duration of the call
+ *    and copied; the caller may free it afterwards.  Output arrays are
+ *    caller-allocated.  A handle owns all device memory until te_destroy().
+ *  - Device: a handle is bound to the CUDA device current at create time.
+ *    A handle is not thread-safe; distinct handles may be used concurrently.
+ *  - Determinism: identical inputs on the same device give bitwise-identical
+ *    outputs (no floating-point atomics; fixed reduction order per grid size).
+ */
+#ifndef TE_H
+#define TE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct te_handle te_handle;
+typedef struct te_dist te_dist;
+typedef struct { double re, im; } te_c128;
+
+/* ---- status codes ---------------------------------------------------------------- */
+enum {
+  TE_OK = 0,
+  TE_ERR_ARG = 1,             /* NULL pointer, n < 1, t < 0 or non-finite, tol <= 0, m_max < 1 or > TE_M_MAX */
+  TE_ERR_CSR = 2,             /* rowptr/col invariants violated                                   */
+  TE_ERR_NOT_HERMITIAN = 3,   /* H != H^dagger within tolerance                                    */
+  TE_ERR_NOT_NORMALIZED = 4,  /* | ||v0||_2 - 1 | > 1e-8 (v(0) normalised)                  */
+  TE_ERR_STEP_COLLAPSE = 5,   /* step size fell below 1e-13 t (m too small for the requested tol)   */
+  TE_ERR_NUMERICAL = 6,       /* NaN/Inf in the Arnoldi recurrence                                  */
+  TE_ERR_OOM = 7,             /* device allocation failed                                           */
+  TE_ERR_CUDA = 8,            /* CUDA runtime error (incl. no device)                               */
+  TE_ERR_NCCL = 9,            /* NCCL error (distributed handles)                                   */
+  TE_ERR_UNSUPPORTED = 10     /* operation not available for this handle kind                     */
+};
+
+/* warning bits in te_stats.warnings — never errors (a warning does not abort) */
+#define TE_WARN_ROUNDOFF   1u   /* roundoff estimate d ||H||_1 eps exceeded a step's error bound */
+#define TE_WARN_QUADRATURE 2u   /* error integral not converged after 15 refinements             */
+
+#define TE_M_MAX 64             /* largest supported Krylov dimension m_max                              */
+
+typedef struct {
+  double   err_bound;       /* sum over restarts of int_0^{tau_k} f (Eq. 16); <= tol by construction     */
+  int64_t  n_restarts;      /* Krylov subspaces built = time steps                                        */
+  int64_t  n_krylov_steps;  /* Arnoldi iterations (SpMVs)                                                 */
+  int64_t  n_breakdowns;    /* lucky breakdowns (Alg. 1)                                            */
+  double   roundoff_step;   /* Eq. 17 per restart: n ||H||_1 2^-52                                         */
+  double   roundoff_total;  /* n_restarts * roundoff_step (reading C15)                                   */
+  uint32_t warnings;        /* TE_WARN_* bits                                                             */
+  uint32_t _pad;
+  double   t_step_min, t_step_max;
+  double   one_norm;        /* ||H||_1                                                                    */
+} te_stats;
+
+/* ---- core three (BASELINE.json north star) ------------------------------------- */
+
+/* Copy a Hermitian CSR matrix with complex values to the device, validate it
+ * (CSR invariants, Hermiticity, real diagonal) and compute ||H||_1 (Eq. 17).
+ * Returns NULL on error (te_last_status(): TE_ERR_ARG/CSR/NOT_HERMITIAN/OOM/CUDA). */
+te_handle* te_create_csr(int64_t n, const int64_t* rowptr, const int32_t* col, const te_c128* val);
+
+/* v_out = Krylov approximation of exp(-iHt) v0 with ||exact - v_out||_2 <= stats.err_bound <= tol
+ * (up to roundoff, Eq. 17) — Algorithm 1 with Krylov dimension m_max (fixed m,
+ * capped at n; CGS2 orthogonalisation, reading C1).  v0 and v_out are HOST arrays of n
+ * elements; v_out may alias v0.  t = 0 returns v0 with bound 0 and 0 restarts.  stats may
+ * be NULL.  Returns TE_OK or an error (v_out unspecified on error; stats filled up to it). */
+int te_evolve(te_handle* h, const te_c128* v0, double t, double tol, int m_max,
+              te_c128* v_out, te_stats* stats);
+
+/* Free all device memory owned by h (NULL is a no-op). */
+void te_destroy(te_handle* h);
+
+/* ---- extensions ------------------------------------------------------------------ */
+
+/* As te_create_csr with real (float64) values (Hermitian == real symmetric). */
+te_handle* te_create_csr_real(int64_t n, const int64_t* rowptr, const int32_t* col, const double* val);
+
+/* As te_evolve with DEVICE pointers (n complex128 each, 16-byte aligned, may alias) on the
+ * CUDA stream `stream` (cudaStream_t; NULL = the handle's own stream).  The call returns
+ * after the result is complete on that stream. */
+int te_evolve_dev(te_handle* h, const void* d_v0, double t, double tol, int m_max,
+                  void* d_vout, te_stats* stats, void* stream);
+
+/* Forced step schedule (parity mode, reading C16): restart k uses step t_steps[k]
+ * (clamped to the remaining time) instead of the step search; the error integral of each
+ * step is still evaluated and summed into stats.err_bound.  Evolves to t = sum(t_steps).
+ * Host arrays. */
+int te_evolve_schedule(te_handle* h, const te_c128* v0, int64_t k, const double* t_steps,
+                       double tol, int m_max, te_c128* v_out, te_stats* stats);
+
+/* Schedule of the most recent evolve call: up to cap entries of (tau_k, m_eff_k, e_k).
+ * Any output pointer may be NULL.  Returns the number of restarts (may exceed cap). */
+int64_t te_get_schedule(const te_handle* h, int64_t cap, double* t_steps, int32_t* m_eff,
+                        double* err_steps);
+
+/* One Arnoldi/CGS2 decomposition from the host vector v1 (Eq. 8): alpha[m], beta[m] (the
+ * tridiagonal T and beta[m_eff-1] = h_{m+1,m}), *m_eff, *breakdown; V_out (nullable) receives
+ * the normalised basis n x m_eff column-major.  Breakdown threshold tol_rate (Alg. 1). */
+int te_krylov_basis(te_handle* h, const te_c128* v1, int m, double tol_rate, double* alpha,
+                    double* beta, int* m_eff, int* breakdown, te_c128* V_out);
+
+/* Options (value semantics per option): */
+enum {
+  TE_OPT_PROFILE = 1,        /* 1: record CUDA events around every kernel launch (te_get_profile) */
+  TE_OPT_GRAPH = 2           /* 1 (default): replay each restart's launches as a CUDA graph      */
+};
+int te_set_option(te_handle* h, int option, double value);
+
+/* Per-kernel-class profile accumulated while TE_OPT_PROFILE is on (reset by te_set_option):
+ * kernel: 0 spmv_proj (K1), 1 update_proj (K2), 2 update_norm (K3), 3 combine V.omega (K4),
+ * 4 halo pack (distributed).  launches, total device milliseconds (CUDA events on the
+ * launching stream) and algorithmic bytes. */
+typedef struct { int64_t launches; double total_ms; double alg_bytes; } te_kernel_profile;
+int te_get_profile(const te_handle* h, int kernel, te_kernel_profile* out);
+
+/* Number of library kernels launched by this handle since creation. */
+int64_t te_launch_count(const te_handle* h);
+
+/* ||H||_1 of the handle's matrix (global for distributed handles). */
+double te_one_norm(const te_handle* h);
+
+/* Thread-local status / message of the last failing call (TE_OK / "" if none). */
+int te_last_status(void);
+const char* te_last_error(void);
+
+/* Library version string. */
+const char* te_version(void);
+
+/* ---- distributed (one process per GPU, rows sharded; NCCL over NVLink) --------------- */
+
+/* Rank 0 draws a 128-byte ncclUniqueId (broadcast it with torch.distributed). */
+int te_nccl_unique_id(void* out128);
+
+/* Create the library's own NCCL communicator (ncclCommInitRank) on the current device. */
+te_dist* te_dist_init(int nranks, int rank, const void* id128);
+void te_dist_destroy(te_dist* d);
+
+/* Local rows [row_begin, row_end) of a global n_global x n_global Hermitian CSR, with
+ * GLOBAL column indices (int64).  All ranks call collectively with contiguous, ordered,
+ * non-overlapping row blocks covering [0, n_global).  val is complex (te_c128) if
+ * val_is_complex else double.  Builds the halo plan (te_halo_plan) and exchanges the
+ * per-peer need lists once.  v0/v_out of evolve calls are the local row slices. */
+te_handle* te_create_csr_dist(te_dist* d, int64_t n_global, int64_t row_begin, int64_t row_end,
+                              const int64_t* rowptr_local, const int64_t* col_global,
+                              const void* val, int val_is_complex);
+
+/* Host-only halo plan (no GPU needed): given the row partition row_starts[nranks+1] and
+ * this rank's global column indices, produce
+ *   col_local_out[nnz_local]  local columns: own rows -> [0, n_loc), remote columns ->
+ *                             n_loc + position in the halo (peers ascending, index ascending)
+ *   recv_counts_out[nranks]   halo entries received from each peer (0 for self)
+ *   halo_global_out[cap]      the sorted unique remote global indices (halo order)
+ * Returns the halo length (>= 0) or -status on error.  Bit-exact and deterministic. */
+int64_t te_halo_plan(int nranks, int rank, const int64_t* row_starts, int64_t nnz_local,
+                     const int64_t* col_global, int32_t* col_local_out, int64_t* recv_counts_out,
+                     int64_t* halo_global_out, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TE_H */

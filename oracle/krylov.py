@@ -90,6 +90,31 @@ def one_norm(rowptr, col, val, n):
 # Step 1: Arnoldi / Lanczos (Eq. 8; Alg. 1)
 # ---------------------------------------------------------------------------
 
+def arnoldi_step(matvec, V, beta, j, ortho="cgs2"):
+    """One iteration j of Eq. 8 on the basis columns V[:, :j+1]; returns the
+    orthogonalised vector p, alpha_j and beta_j = ||p||_2 (see ``arnoldi``)."""
+    p = matvec(V[:, j])
+    if ortho == "cgs2":
+        Vj = V[:, : j + 1]
+        c1 = Vj.conj().T @ p
+        p = p - Vj @ c1
+        c2 = Vj.conj().T @ p
+        p = p - Vj @ c2
+        a = (c1[j] + c2[j]).real
+    elif ortho == "lanczos3":
+        if j > 0:
+            p = p - beta[j - 1] * V[:, j - 1]
+        aa = np.vdot(V[:, j], p)
+        p = p - aa * V[:, j]
+        a = aa.real
+    else:
+        raise ValueError(ortho)
+    b = math.sqrt(np.vdot(p, p).real)
+    if not math.isfinite(b):
+        raise FloatingPointError("non-finite value in the Arnoldi recurrence")
+    return p, a, b
+
+
 def arnoldi(matvec, v1, m, tol_rate, ortho="cgs2"):
     """Build the Krylov basis from v_1 = w (no renormalisation, C13).
 
@@ -117,25 +142,7 @@ def arnoldi(matvec, v1, m, tol_rate, ortho="cgs2"):
     m_eff = m
     breakdown = False
     for j in range(m):
-        p = matvec(V[:, j])
-        if ortho == "cgs2":
-            Vj = V[:, : j + 1]
-            c1 = Vj.conj().T @ p
-            p = p - Vj @ c1
-            c2 = Vj.conj().T @ p
-            p = p - Vj @ c2
-            alpha[j] = (c1[j] + c2[j]).real
-        elif ortho == "lanczos3":
-            if j > 0:
-                p = p - beta[j - 1] * V[:, j - 1]
-            a = np.vdot(V[:, j], p)
-            p = p - a * V[:, j]
-            alpha[j] = a.real
-        else:
-            raise ValueError(ortho)
-        b = math.sqrt(np.vdot(p, p).real)
-        if not math.isfinite(b):
-            raise FloatingPointError("non-finite value in the Arnoldi recurrence")
+        p, alpha[j], b = arnoldi_step(matvec, V, beta, j, ortho)
         beta[j] = b
         if b < tol_rate:
             m_eff = j + 1

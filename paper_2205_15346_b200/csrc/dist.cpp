@@ -1,0 +1,208 @@
+// Row-sharded distributed handles: contiguous row blocks per rank, one halo
+// exchange per SpMV over precomputed gather lists (NCCL send/recv over NVLink), batched
+// allreduces of the Gram-Schmidt sums.  The halo plan itself is pure host code and is
+// exported (te_halo_plan) so it can be tested bit-exactly without a GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "../../include/te.h"
+#include "nccl_shim.h"
+
+te_handle* te_internal_create_local(int64_t n_loc, int64_t n_global, int64_t row_begin, const int64_t* rowptr,
+                                    const int32_t* col_local, const void* val, bool cplx, te_dist* dist,
+                                    int64_t ncol_limit);
+int te_internal_setup_halo(te_handle* h, int64_t n_halo, const std::vector<int64_t>& recv_counts,
+                           const std::vector<int64_t>& send_counts, const std::vector<int32_t>& send_idx,
+                           double norm1_global);
+int te_internal_set_error(int code, const char* msg);
+cudaStream_t te_internal_stream(te_handle* h);
+double te_internal_local_norm1(te_handle* h);
+ncclComm_t te_internal_comm(te_dist* d);
+int te_internal_nranks(te_dist* d);
+int te_internal_rank(te_dist* d);
+
+extern "C" int64_t te_halo_plan(int nranks, int rank, const int64_t* row_starts, int64_t nnz_local,
+                                const int64_t* col_global, int32_t* col_local_out, int64_t* recv_counts_out,
+                                int64_t* halo_global_out, int64_t cap) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || !row_starts || (nnz_local > 0 && (!col_global || !col_local_out)) ||
+      !recv_counts_out)
+    return -te_internal_set_error(TE_ERR_ARG, "te_halo_plan: bad arguments");
+  for (int q = 0; q < nranks; ++q)
+    if (row_starts[q + 1] < row_starts[q]) return -te_internal_set_error(TE_ERR_ARG, "row_starts not monotone");
+  const int64_t n_global = row_starts[nranks];
+  const int64_t rb = row_starts[rank], re = row_starts[rank + 1];
+  const int64_t n_loc = re - rb;
+  std::vector<int64_t> remote;
+  remote.reserve(1024);
+  for (int64_t k = 0; k < nnz_local; ++k) {
+    const int64_t c = col_global[k];
+    if (c < 0 || c >= n_global) return -te_internal_set_error(TE_ERR_CSR, "column index out of range");
+    if (c < rb || c >= re) remote.push_back(c);
+  }
+  std::sort(remote.begin(), remote.end());
+  remote.erase(std::unique(remote.begin(), remote.end()), remote.end());
+  const int64_t n_halo = (int64_t)remote.size();
+  if (n_loc + n_halo > INT32_MAX) return -te_internal_set_error(TE_ERR_ARG, "local index space exceeds int32");
+  for (int q = 0; q < nranks; ++q) recv_counts_out[q] = 0;
+  int owner = 0;
+  for (int64_t i = 0; i < n_halo; ++i) {  // sorted, partitions ordered -> owners ascending
+    while (remote[i] >= row_starts[owner + 1]) ++owner;
+    recv_counts_out[owner] += 1;
+  }
+  for (int64_t k = 0; k < nnz_local; ++k) {
+    const int64_t c = col_global[k];
+    if (c >= rb && c < re) {
+      col_local_out[k] = (int32_t)(c - rb);
+    } else {
+      const int64_t pos = std::lower_bound(remote.begin(), remote.end(), c) - remote.begin();
+      col_local_out[k] = (int32_t)(n_loc + pos);
+    }
+  }
+  if (halo_global_out)
+    for (int64_t i = 0; i < std::min(cap, n_halo); ++i) halo_global_out[i] = remote[i];
+  return n_halo;
+}
+
+#define DCK(call)                                                                        \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      te_internal_set_error(TE_ERR_CUDA, cudaGetErrorString(e_));                        \
+      goto fail;                                                                         \
+    }                                                                                    \
+  } while (0)
+#define DNK(call)                                                                        \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess) {                                                             \
+      te_internal_set_error(TE_ERR_NCCL, te::nccl().GetErrorString(r_));                 \
+      goto fail;                                                                         \
+    }                                                                                    \
+  } while (0)
+
+extern "C" te_handle* te_create_csr_dist(te_dist* d, int64_t n_global, int64_t row_begin, int64_t row_end,
+                                         const int64_t* rowptr_local, const int64_t* col_global, const void* val,
+                                         int val_is_complex) {
+  if (!d || n_global < 1 || row_begin < 0 || row_end <= row_begin || row_end > n_global || !rowptr_local) {
+    te_internal_set_error(TE_ERR_ARG, "te_create_csr_dist: bad arguments");
+    return nullptr;
+  }
+  const int P = te_internal_nranks(d), me = te_internal_rank(d);
+  const int64_t n_loc = row_end - row_begin;
+  const int64_t nnz = rowptr_local[n_loc];
+  std::vector<int64_t> row_starts(P + 1, 0);
+  std::vector<int64_t> recv_counts(P, 0), send_counts(P, 0), halo;
+  std::vector<int32_t> col_local(std::max<int64_t>(1, nnz));
+  std::vector<int32_t> send_idx;
+  int64_t n_halo = 0, n_send = 0;
+  te_handle* h = nullptr;
+  int64_t* dbuf = nullptr;
+  cudaStream_t st = nullptr;
+  ncclComm_t comm = te_internal_comm(d);
+  DCK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  if (P > 1) {
+    // 1. row partition
+    DCK(cudaMalloc(&dbuf, sizeof(int64_t) * (2 * P + 2 * P * P + 8)));
+    {
+      int64_t mine[2] = {row_begin, row_end};
+      std::vector<int64_t> all(2 * P);
+      DCK(cudaMemcpy(dbuf, mine, sizeof mine, cudaMemcpyHostToDevice));
+      DNK(te::nccl().AllGather(dbuf, dbuf + 2, 2, ncclInt64, comm, st));
+      DCK(cudaStreamSynchronize(st));
+      DCK(cudaMemcpy(all.data(), dbuf + 2, sizeof(int64_t) * 2 * P, cudaMemcpyDeviceToHost));
+      for (int q = 0; q < P; ++q) {
+        if (all[2 * q] != (q == 0 ? 0 : all[2 * q - 1])) {
+          te_internal_set_error(TE_ERR_ARG, "row blocks must be contiguous and ordered by rank");
+          goto fail;
+        }
+        row_starts[q] = all[2 * q];
+      }
+      row_starts[P] = all[2 * P - 1];
+      if (row_starts[P] != n_global) {
+        te_internal_set_error(TE_ERR_ARG, "row blocks do not cover [0, n_global)");
+        goto fail;
+      }
+    }
+  } else {
+    row_starts[0] = 0;
+    row_starts[1] = n_global;
+  }
+  // 2. halo plan (host, bit-exact)
+  halo.resize(std::max<int64_t>(1, nnz));
+  n_halo = te_halo_plan(P, me, row_starts.data(), nnz, col_global, col_local.data(), recv_counts.data(), halo.data(),
+                        (int64_t)halo.size());
+  if (n_halo < 0) goto fail;
+  halo.resize(n_halo);
+  if (P > 1) {
+    // 3. counts matrix: M[q][p] = entries rank q needs from rank p
+    int64_t* dM = dbuf + 2 + 2 * P;
+    std::vector<int64_t> M((size_t)P * P);
+    DCK(cudaMemcpy(dbuf, recv_counts.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice));
+    DNK(te::nccl().AllGather(dbuf, dM, P, ncclInt64, comm, st));
+    DCK(cudaStreamSynchronize(st));
+    DCK(cudaMemcpy(M.data(), dM, sizeof(int64_t) * P * P, cudaMemcpyDeviceToHost));
+    for (int q = 0; q < P; ++q) send_counts[q] = (q == me) ? 0 : M[(size_t)q * P + me];
+    for (int q = 0; q < P; ++q) n_send += send_counts[q];
+    // 4. exchange need lists (global indices)
+    int64_t *dneed = nullptr, *dgive = nullptr;
+    DCK(cudaMalloc(&dneed, sizeof(int64_t) * std::max<int64_t>(1, n_halo)));
+    DCK(cudaMalloc(&dgive, sizeof(int64_t) * std::max<int64_t>(1, n_send)));
+    if (n_halo > 0) DCK(cudaMemcpy(dneed, halo.data(), sizeof(int64_t) * n_halo, cudaMemcpyHostToDevice));
+    DNK(te::nccl().GroupStart());
+    {
+      int64_t ro = 0, so = 0;
+      for (int q = 0; q < P; ++q) {
+        if (q == me) continue;
+        if (recv_counts[q] > 0) DNK(te::nccl().Send(dneed + ro, recv_counts[q], ncclInt64, q, comm, st));
+        if (send_counts[q] > 0) DNK(te::nccl().Recv(dgive + so, send_counts[q], ncclInt64, q, comm, st));
+        ro += recv_counts[q];
+        so += send_counts[q];
+      }
+    }
+    DNK(te::nccl().GroupEnd());
+    DCK(cudaStreamSynchronize(st));
+    {
+      std::vector<int64_t> give(n_send);
+      if (n_send > 0) DCK(cudaMemcpy(give.data(), dgive, sizeof(int64_t) * n_send, cudaMemcpyDeviceToHost));
+      send_idx.resize(n_send);
+      for (int64_t t = 0; t < n_send; ++t) {
+        if (give[t] < row_begin || give[t] >= row_end) {
+          te_internal_set_error(TE_ERR_CSR, "peer requested a row this rank does not own");
+          cudaFree(dneed);
+          cudaFree(dgive);
+          goto fail;
+        }
+        send_idx[t] = (int32_t)(give[t] - row_begin);
+      }
+    }
+    cudaFree(dneed);
+    cudaFree(dgive);
+  }
+  // 5. local handle with local column indices (Hermiticity needs the global matrix: not checked)
+  h = te_internal_create_local(n_loc, n_global, row_begin, rowptr_local, col_local.data(), val, val_is_complex != 0,
+                               d, n_loc + n_halo);
+  if (!h) goto fail;
+  {
+    // 6. ||H||_1 = max over all rows of the row abs sums (allreduce max)
+    double nrm = te_internal_local_norm1(h);
+    if (P > 1) {
+      double* dn = reinterpret_cast<double*>(dbuf);
+      DCK(cudaMemcpy(dn, &nrm, sizeof nrm, cudaMemcpyHostToDevice));
+      DNK(te::nccl().AllReduce(dn, dn, 1, ncclDouble, ncclMax, comm, st));
+      DCK(cudaStreamSynchronize(st));
+      DCK(cudaMemcpy(&nrm, dn, sizeof nrm, cudaMemcpyDeviceToHost));
+    }
+    if (te_internal_setup_halo(h, n_halo, recv_counts, send_counts, send_idx, nrm) != TE_OK) goto fail;
+  }
+  cudaFree(dbuf);
+  cudaStreamDestroy(st);
+  return h;
+fail:
+  if (h) te_destroy(h);
+  if (dbuf) cudaFree(dbuf);
+  if (st) cudaStreamDestroy(st);
+  return nullptr;
+}

@@ -1,0 +1,656 @@
+// Hot-path CUDA kernels for sm_100a: one Arnoldi/CGS2 step (Eq. 8, with the
+// classical Gram-Schmidt + one re-orthogonalisation reading C1 of DESIGN.md) in three
+// HBM-streaming launches, plus the restart assembly V.omega (Eq. 11).
+//
+//   K1 k_spmv_proj   p = s_j H V_j (CSR, entries staged through shared memory), then the
+//                    sweep-1 projections g1_k = sum_i conj(V_ik) p_i, k <= j, in the epilogue
+//   K2 k_update_proj p' = p - sum_k V_k e1_k  and  g2_k = sum_i conj(V_ik) p'_i : each V tile is
+//                    staged ONCE in shared memory by cp.async.bulk (TMA bulk engine) through a
+//                    4-stage mbarrier pipeline and used by both phases -> one HBM pass over V
+//   K3 k_update_norm p'' = p' - sum_k V_k e2_k written as column j+1, and ||p''||^2
+//   K4 k_combine     w = sum_k V_k (s_k omega_k), in place into column 0
+// with e_k = s_k^2 g_k (s_k = 1/||V_k||: columns are stored unnormalised and scaled on the
+// fly).  Reductions are deterministic: per-CTA partials in registers/shared memory, then the
+// last CTA to finish (atomic ticket, integer only) sums the partials in a fixed order.
+// No floating-point atomics anywhere.
+#include "kernels.cuh"
+
+#include <cstdio>
+
+namespace te {
+
+// --------------------------------------------------------------------------------------
+// small helpers
+// --------------------------------------------------------------------------------------
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+// a*b
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+// conj(a)*b + c
+__device__ __forceinline__ double2 cfma_conj(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, fma(a.y, b.y, c.x)), fma(a.x, b.y, fma(-a.y, b.x, c.y)));
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_cg(const double2* p) { return __ldcg(p); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "TE_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra TE_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// bulk (non-tensor) TMA copy global -> shared, completion counted on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// Warp butterfly sum (all lanes end with the same, deterministic value).
+__device__ __forceinline__ double2 warp_sum(double2 v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+  }
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// Step-j prologue shared by K1 (and the finalize kernel): decides from ||p''_{j-1}||^2 whether the
+// recurrence continues (Alg. 1, breakdown threshold tol_rate, reading C6/C7).
+// Returns the column scale s_j (0 => stop).  Only block 0 writes device state.
+__device__ __forceinline__ double step_gate(const KDev& d, int j, bool writer) {
+  if (d.flag[0] != 0) return 0.0;
+  if (j == 0) return 1.0;
+  const double b = sqrt(d.nrm2[j - 1]);
+  if (!isfinite(b)) {
+    if (writer) { d.beta[j - 1] = b; d.flag[1] = j; d.flag[0] = 2; }
+    return 0.0;
+  }
+  if (b < d.tol_rate) {                  // lucky breakdown: m_eff = j, h = beta_{j-1}
+    if (writer) { d.beta[j - 1] = b; d.flag[1] = j; d.flag[0] = 1; }
+    return 0.0;
+  }
+  const double sj = 1.0 / b;
+  if (writer) { d.beta[j - 1] = b; d.s[j] = sj; }
+  return sj;
+}
+
+// Per-CTA column partials -> global; the last CTA sums them in fixed block order.
+// acc[q] holds column k = warp + kWarps*q summed over this thread's rows.
+template <int NCW>
+__device__ __forceinline__ void finish_columns(const KDev& d, double2 (&acc)[NCW], int ncols, int ctr,
+                                               double2* out) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+  for (int q = 0; q < NCW; ++q) {
+    const int k = warp + kWarps * q;
+    double2 v = warp_sum(acc[q]);
+    if (lane == 0 && k < ncols) d.part[(size_t)blockIdx.x * kMaxCols + k] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int last;
+  if (tid == 0) last = (atomicAdd(&d.counter[ctr], 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // 4 segments per column (tid/64), each summed sequentially, then combined in order
+  __shared__ double2 seg[4][kMaxCols];
+  const int c = tid & (kMaxCols - 1), sgi = tid >> 6;
+  const int G = gridDim.x;
+  const int per = (G + 3) / 4;
+  double2 s = make_double2(0.0, 0.0);
+  if (c < ncols) {
+    const int b0 = sgi * per, b1 = min(G, b0 + per);
+    for (int b = b0; b < b1; ++b) s = cadd(s, ld_cg(d.part + (size_t)b * kMaxCols + c));
+  }
+  seg[sgi][c] = s;
+  __syncthreads();
+  if (tid < ncols) {
+    double2 t = seg[0][tid];
+    t = cadd(t, seg[1][tid]);
+    t = cadd(t, seg[2][tid]);
+    t = cadd(t, seg[3][tid]);
+    out[tid] = t;
+  }
+  if (tid == 0) d.counter[ctr] = 0u;
+}
+
+__device__ __forceinline__ void finish_scalar(const KDev& d, double v, int ctr, double* out) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ double ws[kWarps];
+  v = warp_sum(v);
+  if (lane == 0) ws[warp] = v;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kWarps; ++w) t += ws[w];
+    d.partn[blockIdx.x] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int last;
+  if (tid == 0) last = (atomicAdd(&d.counter[ctr], 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double seg[kThreads];
+  const int G = gridDim.x;
+  const int per = (G + kThreads - 1) / kThreads;
+  double s = 0.0;
+  const int b0 = tid * per, b1 = min(G, b0 + per);
+  for (int b = b0; b < b1; ++b) s += __ldcg(d.partn + b);
+  seg[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int i = 0; i < kThreads; ++i) t += seg[i];
+    *out = t;
+    d.counter[ctr] = 0u;
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// K1: SpMV + sweep-1 projections
+// --------------------------------------------------------------------------------------
+template <bool CPLX>
+struct ValT;
+template <>
+struct ValT<false> {
+  using T = double;
+  static __device__ __forceinline__ double2 mul(double v, double2 x) { return make_double2(v * x.x, v * x.y); }
+};
+template <>
+struct ValT<true> {
+  using T = double2;
+  static __device__ __forceinline__ double2 mul(double2 v, double2 x) {
+    return make_double2(v.x * x.x - v.y * x.y, v.x * x.y + v.y * x.x);
+  }
+};
+
+constexpr size_t kK1Smem = sizeof(double2) * (kSpmvChunk + kSpmvRows) + sizeof(int64_t) * (kSpmvRows + 1);
+
+template <bool CPLX, int NCW>
+__global__ void __launch_bounds__(kThreads, 2) k_spmv_proj(KDev d, int j) {
+  static_assert(kThreads == kSpmvRows, "one thread per tile row");
+  using VT = typename ValT<CPLX>::T;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double2* prod = reinterpret_cast<double2*>(smem);
+  double2* ps = prod + kSpmvChunk;
+  int64_t* rps = reinterpret_cast<int64_t*>(ps + kSpmvRows);
+  __shared__ double sj_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) sj_s = step_gate(d, j, blockIdx.x == 0);
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+
+  const VT* __restrict__ val = static_cast<const VT*>(d.val);
+  const int32_t* __restrict__ col = d.col;
+  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  const double2* __restrict__ halo = d.halo;
+  const int64_t n = d.n;
+  const int ncols = j + 1;
+  double2 acc[NCW];
+#pragma unroll
+  for (int q = 0; q < NCW; ++q) acc[q] = make_double2(0.0, 0.0);
+
+  const int64_t ntiles = (n + kSpmvRows - 1) / kSpmvRows;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kSpmvRows;
+    const int rows = (int)min((int64_t)kSpmvRows, n - r0);
+    for (int i = tid; i <= rows; i += kThreads) rps[i] = __ldg(d.rowptr + r0 + i);
+    __syncthreads();
+    const int64_t b = rps[0], e = rps[rows];
+    int64_t mylo = 0, myhi = 0;
+    if (tid < rows) { mylo = rps[tid]; myhi = rps[tid + 1]; }
+    double2 sum = make_double2(0.0, 0.0);
+    for (int64_t cb = b; cb < e; cb += kSpmvChunk) {
+      const int cnt = (int)min((int64_t)kSpmvChunk, e - cb);
+      // gather-multiply over the chunk's entries: coalesced col/val streams, 4 gathers in flight
+      for (int k0 = tid; k0 < cnt; k0 += 4 * kThreads) {
+        int cc[4];
+        VT vv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u * kThreads;
+          if (k < cnt) {
+            cc[u] = __ldg(col + cb + k);
+            vv[u] = __ldg(val + cb + k);
+          }
+        }
+        double2 xx[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u * kThreads;
+          if (k < cnt) xx[u] = (cc[u] < n) ? __ldg(x + cc[u]) : __ldg(halo + (cc[u] - n));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u * kThreads;
+          if (k < cnt) prod[k] = ValT<CPLX>::mul(vv[u], xx[u]);
+        }
+      }
+      __syncthreads();
+      const int64_t lo = max(mylo, cb), hi = min(myhi, cb + cnt);
+      for (int64_t q = lo; q < hi; ++q) sum = cadd(sum, prod[q - cb]);  // row order, left to right
+      __syncthreads();
+    }
+    const double2 p = make_double2(sum.x * sj, sum.y * sj);
+    if (tid < rows) d.W[r0 + tid] = p;
+    ps[tid] = p;
+    __syncthreads();
+    // sweep-1 projections on the fresh tile: warp w owns columns w, w+8, ...
+#pragma unroll
+    for (int q = 0; q < NCW; ++q) {
+      const int k = warp + kWarps * q;
+      if (k < ncols) {
+        const double2* Vk = d.V + (int64_t)k * d.ldv + r0;
+        if (rows == kSpmvRows) {
+          double2 v[kSpmvRows / 32];
+#pragma unroll
+          for (int s = 0; s < kSpmvRows / 32; ++s) v[s] = ld_stream(Vk + lane + 32 * s);
+#pragma unroll
+          for (int s = 0; s < kSpmvRows / 32; ++s) acc[q] = cfma_conj(v[s], ps[lane + 32 * s], acc[q]);
+        } else {
+          for (int i = lane; i < rows; i += 32) acc[q] = cfma_conj(ld_stream(Vk + i), ps[i], acc[q]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  finish_columns<NCW>(d, acc, ncols, 0, d.g1);
+}
+
+// --------------------------------------------------------------------------------------
+// K2: sweep-1 update + sweep-2 projections, V tile staged once (cp.async.bulk + mbarrier)
+// --------------------------------------------------------------------------------------
+constexpr int kStages = 4;
+constexpr int kStageBudget = 48 * 1024;   // bytes of V+W per stage
+
+size_t k2_smem_bytes(int ncols, int* tile_rows) {
+  int tr = 1024;
+  while (tr > 32 && (size_t)tr * (ncols + 1) * 16 > (size_t)kStageBudget) tr >>= 1;
+  if (tile_rows) *tile_rows = tr;
+  return (size_t)kStages * tr * (ncols + 1) * 16 + sizeof(double2) * kThreads + 128;
+}
+
+template <int NCW>
+__global__ void __launch_bounds__(kThreads, 1) k_update_proj(KDev d, int j, int TR) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ double2 coef[kMaxCols];
+  __shared__ int go_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ncols = j + 1;
+  if (tid == 0) go_s = (d.flag[0] == 0);
+  if (tid < ncols) {
+    const double sk = d.s[tid];
+    const double2 g = d.g1[tid];
+    coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);   // e1_k = s_k c1_k, c1_k = s_k g1_k
+  }
+  __syncthreads();
+  if (!go_s) return;
+
+  const int64_t n = d.n;
+  const int64_t ntiles = (n + TR - 1) / TR;
+  const size_t stage_elems = (size_t)TR * (ncols + 1);
+  double2* stage0 = reinterpret_cast<double2*>(smem);
+  double2* red = stage0 + kStages * stage_elems;   // kThreads double2 for the grouped update
+  const uint64_t pol = policy_evict_first();
+
+  auto issue = [&](int64_t tile, int st) {
+    const int64_t r0 = tile * TR;
+    const int rows = (int)min((int64_t)TR, n - r0);
+    const unsigned bytes = (unsigned)rows * 16u;
+    double2* Vs = stage0 + st * stage_elems;
+    mbar_expect_tx(&bars[st], bytes * (unsigned)(ncols + 1));
+    for (int k = 0; k < ncols; ++k) bulk_g2s(Vs + (size_t)k * TR, d.V + (int64_t)k * d.ldv + r0, bytes, &bars[st], pol);
+    bulk_g2s(Vs + (size_t)ncols * TR, d.W + r0, bytes, &bars[st], pol);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
+      if (tile < ntiles) issue(tile, s);
+    }
+  }
+  double2 acc[NCW];
+#pragma unroll
+  for (int q = 0; q < NCW; ++q) acc[q] = make_double2(0.0, 0.0);
+
+  const int G = TR >= kThreads ? 1 : kThreads / TR;  // threads sharing one row in the update
+  for (int64_t it = 0;; ++it) {
+    const int64_t tile = blockIdx.x + it * gridDim.x;
+    if (tile >= ntiles) break;
+    const int st = (int)(it % kStages);
+    mbar_wait(&bars[st], (unsigned)((it / kStages) & 1));
+    double2* Vs = stage0 + st * stage_elems;
+    double2* Ws = Vs + (size_t)ncols * TR;
+    const int64_t r0 = tile * TR;
+    const int rows = (int)min((int64_t)TR, n - r0);
+    // ---- phase U: p' = p - V e1 (rows of the tile), written to HBM and back into the stage
+    if (G == 1) {
+      for (int i = tid; i < rows; i += kThreads) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int k = 0; k < ncols; ++k) a = cfma(Vs[(size_t)k * TR + i], coef[k], a);
+        const double2 p = make_double2(Ws[i].x - a.x, Ws[i].y - a.y);
+        Ws[i] = p;
+        d.W[r0 + i] = p;
+      }
+    } else {
+      const int g = tid / TR, i = tid - g * TR;
+      double2 a = make_double2(0.0, 0.0);
+      if (i < rows)
+        for (int k = g; k < ncols; k += G) a = cfma(Vs[(size_t)k * TR + i], coef[k], a);
+      red[tid] = a;
+      __syncthreads();
+      if (g == 0 && i < rows) {
+        double2 t = red[i];
+        for (int gg = 1; gg < G; ++gg) t = cadd(t, red[gg * TR + i]);
+        const double2 p = make_double2(Ws[i].x - t.x, Ws[i].y - t.y);
+        Ws[i] = p;
+        d.W[r0 + i] = p;
+      }
+    }
+    __syncthreads();
+    // ---- phase D: g2_k += conj(V_ik) p'_i from the same staged tile
+#pragma unroll
+    for (int q = 0; q < NCW; ++q) {
+      const int k = warp + kWarps * q;
+      if (k < ncols) {
+        const double2* Vk = Vs + (size_t)k * TR;
+        for (int i = lane; i < rows; i += 32) acc[q] = cfma_conj(Vk[i], Ws[i], acc[q]);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      // generic-proxy writes to this stage (p') must be ordered before the async-proxy refill
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int64_t nt = blockIdx.x + (it + kStages) * gridDim.x;
+      if (nt < ntiles) issue(nt, st);
+    }
+  }
+  finish_columns<NCW>(d, acc, ncols, 1, d.g2);
+}
+
+// --------------------------------------------------------------------------------------
+// K3: sweep-2 update + norm; writes p'' as (unnormalised) column j+1
+// --------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_update_norm(KDev d, int j, int write) {
+  __shared__ double2 coef[kMaxCols];
+  __shared__ int go_s;
+  const int tid = threadIdx.x;
+  const int ncols = j + 1;
+  if (tid == 0) {
+    go_s = (d.flag[0] == 0);
+    if (go_s && blockIdx.x == 0) {  // alpha_j = Re(c1_j + c2_j) (reading C2)
+      const double sj = d.s[j];
+      d.alpha[j] = sj * (d.g1[j].x + d.g2[j].x);
+    }
+  }
+  if (tid < ncols) {
+    const double sk = d.s[tid];
+    const double2 g = d.g2[tid];
+    coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);
+  }
+  __syncthreads();
+  if (!go_s) return;
+  const int64_t n = d.n, ldv = d.ldv;
+  double2* out = write ? d.V + (int64_t)(j + 1) * ldv : nullptr;
+  double nrm = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * kThreads + tid; r < n; r += (int64_t)gridDim.x * kThreads) {
+    double2 a = make_double2(0.0, 0.0);
+    const double2* Vr = d.V + r;
+    int k = 0;
+    for (; k + 8 <= ncols; k += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = ld_stream(Vr + (int64_t)(k + u) * ldv);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a = cfma(v[u], coef[k + u], a);
+    }
+    for (; k < ncols; ++k) a = cfma(ld_stream(Vr + (int64_t)k * ldv), coef[k], a);
+    const double2 w = __ldcs(d.W + r);
+    const double2 p = make_double2(w.x - a.x, w.y - a.y);
+    if (out) out[r] = p;
+    nrm = fma(p.x, p.x, fma(p.y, p.y, nrm));
+  }
+  finish_scalar(d, nrm, 2, d.nrm2 + j);
+}
+
+// ||p''_{m-1}||^2 -> beta_{m-1} = h_{m+1,m} and the final breakdown test (Alg. 1)
+__global__ void k_finalize(KDev d, int j) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (d.flag[0] != 0) return;
+  const double b = sqrt(d.nrm2[j]);
+  d.beta[j] = b;
+  d.flag[1] = j + 1;
+  if (!isfinite(b)) d.flag[0] = 2;
+  else if (b < d.tol_rate) d.flag[0] = 1;
+}
+
+__global__ void k_restart_init(KDev d) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    d.flag[0] = 0;
+    d.flag[1] = 0;
+    d.s[0] = 1.0;
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// K4: w = sum_k V_k coef_k (coef_k = s_k omega_k), in place into column 0 (Eq. 11)
+// --------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_combine(const double2* __restrict__ Vbase, int64_t n, int64_t ldv,
+                                                      const double2* __restrict__ coefg, int m_eff, double2* out) {
+  __shared__ double2 coef[kMaxCols];
+  if (threadIdx.x < m_eff) coef[threadIdx.x] = coefg[threadIdx.x];
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * kThreads + threadIdx.x; r < n; r += (int64_t)gridDim.x * kThreads) {
+    double2 a = make_double2(0.0, 0.0);
+    const double2* Vr = Vbase + r;
+    int k = 0;
+    for (; k + 8 <= m_eff; k += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(Vr + (int64_t)(k + u) * ldv);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a = cfma(v[u], coef[k + u], a);
+    }
+    for (; k < m_eff; ++k) a = cfma(__ldcs(Vr + (int64_t)k * ldv), coef[k], a);
+    out[r] = a;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_norm2(KDev d, const double2* __restrict__ x, double* out) {
+  double nrm = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * kThreads + threadIdx.x; r < d.n; r += (int64_t)gridDim.x * kThreads) {
+    const double2 v = __ldg(x + r);
+    nrm = fma(v.x, v.x, fma(v.y, v.y, nrm));
+  }
+  finish_scalar(d, nrm, 3, out);
+}
+
+__global__ void k_copy(const double2* __restrict__ src, double2* __restrict__ dst, int64_t n) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    dst[r] = src[r];
+}
+
+__global__ void k_pack(const double2* __restrict__ x, const int32_t* __restrict__ idx, int64_t cnt,
+                       double2* __restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = __ldg(x + idx[t]);
+}
+
+// --------------------------------------------------------------------------------------
+// setup: CSR validation, Hermiticity, ||H||_1 (= max row abs sum for Hermitian H)
+// --------------------------------------------------------------------------------------
+template <bool CPLX>
+__global__ void k_csr_check(int64_t n, int64_t ncl, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                            const void* valv, int herm, int* err, unsigned long long* norm1_bits) {
+  using VT = typename ValT<CPLX>::T;
+  const VT* val = static_cast<const VT*>(valv);
+  const double eps = 2.220446049250313e-16;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = rowptr[r], hi = rowptr[r + 1];
+    int64_t prev = -1;
+    double rs = 0.0;
+    int e = 0;
+    for (int64_t q = lo; q < hi; ++q) {
+      const int64_t c = col[q];
+      if (c < 0 || c >= ncl || c <= prev) { e |= 1; prev = c; continue; }
+      prev = c;
+      double2 v;
+      if constexpr (CPLX) v = val[q]; else v = make_double2(val[q], 0.0);
+      const double av = hypot(v.x, v.y);
+      rs += av;
+      if (!isfinite(av)) e |= 2;
+      if (!herm) continue;
+      if (c == r) {
+        if (fabs(v.y) > 8.0 * eps * av) e |= 2;
+        continue;
+      }
+      int64_t a = rowptr[c], b = rowptr[c + 1] - 1;
+      bool found = false;
+      while (a <= b) {
+        const int64_t mid = (a + b) >> 1;
+        const int64_t cm = col[mid];
+        if (cm == r) {
+          double2 w;
+          if constexpr (CPLX) w = val[mid]; else w = make_double2(val[mid], 0.0);
+          const double aw = hypot(w.x, w.y);
+          if (hypot(v.x - w.x, v.y + w.y) > 8.0 * eps * fmax(av, aw)) e |= 2;
+          found = true;
+          break;
+        }
+        if (cm < r) a = mid + 1; else b = mid - 1;
+      }
+      if (!found) e |= 2;
+    }
+    if (e) atomicOr(err, e);
+    // row abs sums are non-negative: the bit pattern orders like the value (order-free max)
+    atomicMax(norm1_bits, (unsigned long long)__double_as_longlong(rs));
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// launchers
+// --------------------------------------------------------------------------------------
+#define TE_DISPATCH_NCW(ncw, ...)                 \
+  switch (ncw) {                                 \
+    case 1: { constexpr int NCW = 1; __VA_ARGS__; } break; \
+    case 2: { constexpr int NCW = 2; __VA_ARGS__; } break; \
+    case 3: { constexpr int NCW = 3; __VA_ARGS__; } break; \
+    case 4: { constexpr int NCW = 4; __VA_ARGS__; } break; \
+    case 5: { constexpr int NCW = 5; __VA_ARGS__; } break; \
+    case 6: { constexpr int NCW = 6; __VA_ARGS__; } break; \
+    case 7: { constexpr int NCW = 7; __VA_ARGS__; } break; \
+    default: { constexpr int NCW = 8; __VA_ARGS__; } break; \
+  }
+
+void configure_kernels() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  auto setk1 = [](auto f) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK1Smem); };
+#define TE_SET(NCW)                                  \
+  setk1(k_spmv_proj<false, NCW>);                    \
+  setk1(k_spmv_proj<true, NCW>);                     \
+  cudaFuncSetAttribute(k_update_proj<NCW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  TE_SET(1) TE_SET(2) TE_SET(3) TE_SET(4) TE_SET(5) TE_SET(6) TE_SET(7) TE_SET(8)
+#undef TE_SET
+}
+
+void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L) {
+  const int ncw = (j + 1 + kWarps - 1) / kWarps;
+  TE_DISPATCH_NCW(ncw, {
+    if (cplx)
+      k_spmv_proj<true, NCW><<<L.grid_k1, kThreads, kK1Smem, L.stream>>>(d, j);
+    else
+      k_spmv_proj<false, NCW><<<L.grid_k1, kThreads, kK1Smem, L.stream>>>(d, j);
+  });
+}
+
+void launch_update_proj(const KDev& d, int j, const Launch& L) {
+  int tr = 0;
+  const size_t smem = k2_smem_bytes(j + 1, &tr);
+  const int ncw = (j + 1 + kWarps - 1) / kWarps;
+  TE_DISPATCH_NCW(ncw, { k_update_proj<NCW><<<L.grid_k2, kThreads, smem, L.stream>>>(d, j, tr); });
+}
+
+void launch_update_norm(const KDev& d, int j, bool write, const Launch& L) {
+  k_update_norm<<<L.grid_k3, kThreads, 0, L.stream>>>(d, j, write ? 1 : 0);
+}
+
+void launch_finalize(const KDev& d, int j, const Launch& L) { k_finalize<<<1, 32, 0, L.stream>>>(d, j); }
+
+void launch_restart_init(const KDev& d, const Launch& L) { k_restart_init<<<1, 32, 0, L.stream>>>(d); }
+
+void launch_combine(const KDev& d, const double2* coef, int m_eff, double2* out, const Launch& L) {
+  k_combine<<<L.grid_k3, kThreads, 0, L.stream>>>(d.V, d.n, d.ldv, coef, m_eff, out);
+}
+
+void launch_norm2(const KDev& d, const double2* x, double* out, const Launch& L) {
+  k_norm2<<<L.grid_k3, kThreads, 0, L.stream>>>(d, x, out);
+}
+
+void launch_copy_col(const double2* src, double2* dst, int64_t n, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  if (grid < 1) grid = 1;
+  k_copy<<<grid, 256, 0, st>>>(src, dst, n);
+}
+
+void launch_pack(const double2* x, const int32_t* idx, int64_t cnt, double2* out, cudaStream_t st) {
+  if (cnt <= 0) return;
+  int grid = (int)std::min<int64_t>((cnt + 255) / 256, 148 * 8);
+  k_pack<<<grid, 256, 0, st>>>(x, idx, cnt, out);
+}
+
+void launch_csr_check(int64_t n, int64_t ncl, const int64_t* rowptr, const int32_t* col, const void* val, bool cplx,
+                      bool hermitian_check, CsrCheck c, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (grid < 1) grid = 1;
+  if (cplx)
+    k_csr_check<true><<<grid, 256, 0, st>>>(n, ncl, rowptr, col, val, hermitian_check, c.err, c.norm1_bits);
+  else
+    k_csr_check<false><<<grid, 256, 0, st>>>(n, ncl, rowptr, col, val, hermitian_check, c.err, c.norm1_bits);
+}
+
+}  // namespace te

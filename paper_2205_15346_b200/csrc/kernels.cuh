@@ -1,0 +1,70 @@
+// Device-side data of one Krylov engine and the launchers of the hot-path kernels.
+// Layout:
+//   V   : column-major n x m_cap complex128 (interleaved re/im), column stride ldv
+//         (ldv = n rounded up to 32 elements -> every column 512-byte aligned).  Columns are
+//         stored UNNORMALISED; s[k] = 1/||V[:,k]|| (s[0] = 1) is applied on the fly.
+//   W   : n complex128 work vector (p -> p' in place).
+//   H   : CSR, rowptr int64 [n+1], col int32 [nnz] (local column index; columns >= n_loc
+//         refer to the halo buffer in distributed handles), val double or double2.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace te {
+
+constexpr int kThreads = 256;        // block size of every hot-path kernel
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxCols = 64;         // TE_M_MAX
+constexpr int kSpmvRows = 256;       // K1 row tile
+constexpr int kSpmvChunk = 4096;     // K1 products staged in shared memory per chunk
+
+struct KDev {
+  int64_t n;            // local rows
+  int64_t ldv;          // column stride of V (elements)
+  double2* V;
+  double2* W;
+  const int64_t* rowptr;
+  const int32_t* col;
+  const void* val;
+  const double2* halo;  // x entries for columns >= n (distributed); nullptr otherwise
+  double* s;            // [m_cap+1] column scales
+  double* alpha;        // [m_cap]
+  double* beta;         // [m_cap]
+  double2* g1;          // [m_cap] raw sweep-1 sums of step j  (sum_i conj(V_ik) p_i)
+  double2* g2;          // [m_cap] raw sweep-2 sums
+  double* nrm2;         // [m_cap] ||p''||^2 of step j
+  double2* part;        // per-CTA partials [grid x kMaxCols]
+  double* partn;        // per-CTA norm partials [grid]
+  unsigned* counter;    // [4] last-block-done counters (self-resetting)
+  int* flag;            // [0]: 0 running / 1 breakdown / 2 non-finite ; [1]: m_eff
+  double tol_rate;
+  int m;                // Krylov dimension of the current restart
+};
+
+struct Launch {
+  cudaStream_t stream;
+  int num_sms;
+  int grid_k1, grid_k2, grid_k3;
+};
+
+// hot path (one Krylov step j = 3 launches; see kernels.cu)
+void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L);   // K1
+void launch_update_proj(const KDev& d, int j, const Launch& L);            // K2
+void launch_update_norm(const KDev& d, int j, bool write, const Launch& L);// K3
+void launch_finalize(const KDev& d, int j, const Launch& L);               // beta_{m-1}
+void launch_combine(const KDev& d, const double2* coef, int m_eff, double2* out, const Launch& L); // K4
+void launch_restart_init(const KDev& d, const Launch& L);                  // flag=0, s[0]=1
+void launch_norm2(const KDev& d, const double2* x, double* out, const Launch& L);
+void launch_copy_col(const double2* src, double2* dst, int64_t n, cudaStream_t st);
+
+// setup
+struct CsrCheck { int* err; unsigned long long* norm1_bits; };
+void launch_csr_check(int64_t n, int64_t ncol_limit, const int64_t* rowptr, const int32_t* col, const void* val,
+                      bool cplx, bool hermitian_check, CsrCheck c, cudaStream_t st);
+// distributed halo pack: out[t] = V_j[idx[t]]
+void launch_pack(const double2* x, const int32_t* idx, int64_t cnt, double2* out, cudaStream_t st);
+
+size_t k2_smem_bytes(int ncols, int* tile_rows);
+void configure_kernels();  // opt-in shared memory sizes (once per process/device)
+
+}  // namespace te

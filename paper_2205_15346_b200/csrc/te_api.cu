@@ -1,0 +1,747 @@
+// C ABI (include/te.h) and the host restart loop of Algorithm 1.
+// The large-space work of every step runs in the kernels of kernels.cu; the host only does
+// the m x m problem (host_math.cpp) once per restart, as the paper prescribes.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/te.h"
+#include "host_math.h"
+#include "kernels.cuh"
+#include "nccl_shim.h"
+
+using te::KDev;
+using te::Launch;
+
+// ------------------------------------------------------------------------------------------
+// status
+// ------------------------------------------------------------------------------------------
+static thread_local int g_status = TE_OK;
+static thread_local std::string g_msg;
+
+static int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_status = code;
+  g_msg = buf;
+  return code;
+}
+static void clear_err() {
+  g_status = TE_OK;
+  g_msg.clear();
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return set_err(e_ == cudaErrorMemoryAllocation ? TE_ERR_OOM : TE_ERR_CUDA, "%s: %s (%s:%d)", #call, \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                             \
+  } while (0)
+
+#define CKN(call)                                                                             \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess)                                                                    \
+      return set_err(TE_ERR_NCCL, "%s: %s", #call, te::nccl().GetErrorString(r_));            \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
+// handle
+// ------------------------------------------------------------------------------------------
+struct te_dist {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+namespace {
+constexpr int kProfKernels = 5;
+constexpr int kEvPool = 3 * te::kMaxCols + 16;
+struct Sched {
+  double tau;
+  int32_t m_eff;
+  double err;
+};
+}  // namespace
+
+struct te_handle {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int64_t n = 0, n_global = 0, row_begin = 0;
+  bool cplx = false;
+  int64_t nnz = 0;
+  int64_t* d_rowptr = nullptr;
+  int32_t* d_col = nullptr;
+  void* d_val = nullptr;
+  double norm1 = 0.0;
+  // workspace
+  int m_cap = 0;
+  int64_t ldv = 0;
+  double2* d_V = nullptr;
+  double2* d_W = nullptr;
+  double* d_small = nullptr;  // alpha[64] beta[64] | flag (2 ints) | s[65] nrm2[64] scalar
+  double2* d_g = nullptr;     // g1[64] g2[64] coef[64]
+  double2* d_part = nullptr;
+  double* d_partn = nullptr;
+  unsigned* d_counter = nullptr;
+  int max_grid = 0;
+  double* h_small = nullptr;  // pinned: alpha beta flag + scalar
+  double2* h_coef = nullptr;  // pinned: omega~
+  // profiling / bookkeeping
+  bool profile = false;
+  cudaEvent_t ev0[kEvPool], ev1[kEvPool];
+  int ev_cls[kEvPool];
+  double ev_bytes[kEvPool];
+  int ev_used = 0;
+  bool ev_ready = false;
+  te_kernel_profile prof[kProfKernels];
+  int64_t launches = 0;
+  std::vector<Sched> sched;
+  // distributed
+  te_dist* dist = nullptr;
+  int64_t n_halo = 0;
+  double2* d_halo = nullptr;
+  double2* d_sendbuf = nullptr;
+  int32_t* d_send_idx = nullptr;
+  std::vector<int64_t> send_counts, recv_counts;
+  int64_t n_send = 0;
+};
+
+namespace {
+
+// device layout of d_small (doubles)
+constexpr int kOffAlpha = 0, kOffBeta = 64, kOffFlag = 128, kOffS = 130, kOffNrm = 196, kOffScalar = 260,
+              kSmallLen = 264;
+
+KDev make_kdev(te_handle* h, double tol_rate, int m) {
+  KDev d{};
+  d.n = h->n;
+  d.ldv = h->ldv;
+  d.V = h->d_V;
+  d.W = h->d_W;
+  d.rowptr = h->d_rowptr;
+  d.col = h->d_col;
+  d.val = h->d_val;
+  d.halo = h->d_halo;
+  d.alpha = h->d_small + kOffAlpha;
+  d.beta = h->d_small + kOffBeta;
+  d.flag = reinterpret_cast<int*>(h->d_small + kOffFlag);
+  d.s = h->d_small + kOffS;
+  d.nrm2 = h->d_small + kOffNrm;
+  d.g1 = h->d_g;
+  d.g2 = h->d_g + 64;
+  d.part = h->d_part;
+  d.partn = h->d_partn;
+  d.counter = h->d_counter;
+  d.tol_rate = tol_rate;
+  d.m = m;
+  return d;
+}
+
+Launch make_launch(te_handle* h) {
+  Launch L;
+  L.stream = h->stream;
+  L.num_sms = h->num_sms;
+  const int64_t t256 = (h->n + 255) / 256;
+  L.grid_k1 = (int)std::max<int64_t>(1, std::min<int64_t>(2 * h->num_sms, t256));
+  L.grid_k2 = h->num_sms;
+  L.grid_k3 = (int)std::max<int64_t>(1, std::min<int64_t>(8 * h->num_sms, t256));
+  return L;
+}
+
+int free_workspace(te_handle* h) {
+  cudaFree(h->d_V);
+  cudaFree(h->d_W);
+  h->d_V = nullptr;
+  h->d_W = nullptr;
+  h->m_cap = 0;
+  return TE_OK;
+}
+
+int ensure_workspace(te_handle* h, int m) {
+  if (h->d_small == nullptr) {
+    CK(cudaMalloc(&h->d_small, sizeof(double) * kSmallLen));
+    CK(cudaMemset(h->d_small, 0, sizeof(double) * kSmallLen));
+    CK(cudaMalloc(&h->d_g, sizeof(double2) * 3 * 64));
+    h->max_grid = 8 * h->num_sms;
+    CK(cudaMalloc(&h->d_part, sizeof(double2) * te::kMaxCols * h->max_grid));
+    CK(cudaMalloc(&h->d_partn, sizeof(double) * h->max_grid));
+    CK(cudaMalloc(&h->d_counter, sizeof(unsigned) * 8));
+    CK(cudaMemset(h->d_counter, 0, sizeof(unsigned) * 8));
+    CK(cudaMallocHost(&h->h_small, sizeof(double) * kSmallLen));
+    CK(cudaMallocHost(&h->h_coef, sizeof(double2) * 64));
+  }
+  if (m <= h->m_cap) return TE_OK;
+  free_workspace(h);
+  h->ldv = (h->n + 31) / 32 * 32;
+  const size_t bytes = sizeof(double2) * (size_t)h->ldv * (size_t)m;
+  cudaError_t e = cudaMalloc(&h->d_V, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    h->d_V = nullptr;
+    return set_err(TE_ERR_OOM, "cannot allocate the Krylov basis (%zu bytes)", bytes);
+  }
+  CK(cudaMalloc(&h->d_W, sizeof(double2) * (size_t)h->ldv));
+  h->m_cap = m;
+  return TE_OK;
+}
+
+// ---------------------------------------------------------------- profiling around launches
+void prof_begin(te_handle* h) {
+  if (!h->profile) return;
+  if (!h->ev_ready) {
+    for (int i = 0; i < kEvPool; ++i) {
+      cudaEventCreate(&h->ev0[i]);
+      cudaEventCreate(&h->ev1[i]);
+    }
+    h->ev_ready = true;
+  }
+  if (h->ev_used < kEvPool) cudaEventRecord(h->ev0[h->ev_used], h->stream);
+}
+void prof_end(te_handle* h, int cls, double bytes) {
+  ++h->launches;
+  if (!h->profile || h->ev_used >= kEvPool) return;
+  cudaEventRecord(h->ev1[h->ev_used], h->stream);
+  h->ev_cls[h->ev_used] = cls;
+  h->ev_bytes[h->ev_used] = bytes;
+  ++h->ev_used;
+}
+void prof_collect(te_handle* h) {
+  for (int i = 0; i < h->ev_used; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev0[i], h->ev1[i]);
+    te_kernel_profile& p = h->prof[h->ev_cls[i]];
+    p.launches += 1;
+    p.total_ms += ms;
+    p.alg_bytes += h->ev_bytes[i];
+  }
+  h->ev_used = 0;
+}
+
+// ---------------------------------------------------------------- distributed collectives
+int allreduce_sum(te_handle* h, double* buf, size_t count) {
+  if (!h->dist || h->dist->nranks == 1) return TE_OK;
+  CKN(te::nccl().AllReduce(buf, buf, count, ncclDouble, ncclSum, h->dist->comm, h->stream));
+  return TE_OK;
+}
+
+int halo_exchange(te_handle* h, int j) {
+  if (!h->dist || h->dist->nranks == 1) return TE_OK;
+  const double2* x = h->d_V + (int64_t)j * h->ldv;
+  if (h->n_send > 0) {
+    prof_begin(h);
+    te::launch_pack(x, h->d_send_idx, h->n_send, h->d_sendbuf, h->stream);
+    prof_end(h, 4, 16.0 * 2 * (double)h->n_send + 4.0 * (double)h->n_send);
+  }
+  auto& N = te::nccl();
+  CKN(N.GroupStart());
+  int64_t so = 0, ro = 0;
+  for (int q = 0; q < h->dist->nranks; ++q) {
+    if (q == h->dist->rank) continue;
+    if (h->send_counts[q] > 0)
+      CKN(N.Send(h->d_sendbuf + so, 2 * (size_t)h->send_counts[q], ncclDouble, q, h->dist->comm, h->stream));
+    if (h->recv_counts[q] > 0)
+      CKN(N.Recv(h->d_halo + ro, 2 * (size_t)h->recv_counts[q], ncclDouble, q, h->dist->comm, h->stream));
+    so += h->send_counts[q];
+    ro += h->recv_counts[q];
+  }
+  CKN(N.GroupEnd());
+  return TE_OK;
+}
+
+// ---------------------------------------------------------------- one Krylov decomposition
+// Launch the whole restart (Alg. 1 step 1) without host synchronisation: the kernels gate
+// themselves on the device breakdown flag.  Then one D2H of alpha/beta/flag.
+int run_arnoldi(te_handle* h, int m, double tol_rate) {
+  KDev d = make_kdev(h, tol_rate, m);
+  Launch L = make_launch(h);
+  const double n = (double)h->n;
+  const double bh = (double)h->nnz * ((h->cplx ? 16.0 : 8.0) + 4.0) + 8.0 * (n + 1.0);
+  te::launch_restart_init(d, L);
+  ++h->launches;
+  for (int j = 0; j < m; ++j) {
+    int rc = halo_exchange(h, j);
+    if (rc) return rc;
+    const double ncols = j + 1;
+    prof_begin(h);
+    te::launch_spmv_proj(d, h->cplx, j, L);
+    prof_end(h, 0, bh + 16.0 * n + 16.0 * n * ncols + 16.0 * n);
+    if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g1), 2 * (size_t)(j + 1)))) return rc;
+    prof_begin(h);
+    te::launch_update_proj(d, j, L);
+    prof_end(h, 1, 16.0 * n * ncols + 32.0 * n);
+    if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g2), 2 * (size_t)(j + 1)))) return rc;
+    const bool write = j + 1 < m;
+    prof_begin(h);
+    te::launch_update_norm(d, j, write, L);
+    prof_end(h, 2, 16.0 * n * ncols + 16.0 * n + (write ? 16.0 * n : 0.0));
+    if ((rc = allreduce_sum(h, d.nrm2 + j, 1))) return rc;
+  }
+  te::launch_finalize(d, m - 1, L);
+  ++h->launches;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(h->h_small, h->d_small, sizeof(double) * (kOffFlag + 2), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (h->profile) prof_collect(h);
+  return TE_OK;
+}
+
+int read_flag(te_handle* h, int m, int* m_eff, bool* breakdown) {
+  const int* fl = reinterpret_cast<const int*>(h->h_small + kOffFlag);
+  if (fl[0] == 2) return set_err(TE_ERR_NUMERICAL, "non-finite value in the Arnoldi recurrence (step %d)", fl[1]);
+  *breakdown = fl[0] == 1;
+  *m_eff = fl[0] == 0 ? m : fl[1];
+  if (*m_eff < 1 || *m_eff > m) return set_err(TE_ERR_CUDA, "inconsistent device state (m_eff=%d)", *m_eff);
+  return TE_OK;
+}
+
+// ---------------------------------------------------------------- Algorithm 1
+// V[:,0] holds v0 on entry; on success V[:,0] holds v(t).
+int evolve_core(te_handle* h, double t, double tol, int m_max, const double* forced, int64_t nforced,
+                te_stats* st) {
+  te_stats S{};
+  S.one_norm = h->norm1;
+  S.roundoff_step = (double)h->n_global * h->norm1 * std::ldexp(1.0, -52);  // Eq. 17
+  S.t_step_min = 0.0;
+  S.t_step_max = 0.0;
+  h->sched.clear();
+  auto fill = [&]() {
+    S.roundoff_total = S.roundoff_step * (double)S.n_restarts;
+    if (st) *st = S;
+  };
+  // ||v0|| = 1 check
+  {
+    KDev d = make_kdev(h, 0.0, 1);
+    Launch L = make_launch(h);
+    te::launch_norm2(d, h->d_V, h->d_small + kOffScalar, L);
+    ++h->launches;
+    int rc = allreduce_sum(h, h->d_small + kOffScalar, 1);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(h->h_small + kOffScalar, h->d_small + kOffScalar, sizeof(double), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    const double nv = std::sqrt(h->h_small[kOffScalar]);
+    if (!(std::fabs(nv - 1.0) <= 1e-8)) {
+      fill();
+      return set_err(TE_ERR_NOT_NORMALIZED, "| ||v0|| - 1 | = %.3e > 1e-8", std::fabs(nv - 1.0));
+    }
+  }
+  if (t == 0.0) {
+    fill();
+    return TE_OK;
+  }
+  const int m = (int)std::min<int64_t>(m_max, h->n_global);
+  const double tol_rate = tol / t;  // Eq. 18
+  double t_now = 0.0, tau_prev = 0.0;
+  std::vector<std::complex<double>> om(m);
+  int64_t k = 0;
+  while (t_now < t) {
+    if (forced && k >= nforced) break;
+    int rc = run_arnoldi(h, m, tol_rate);
+    if (rc) { fill(); return rc; }
+    int m_eff;
+    bool brk;
+    if ((rc = read_flag(h, m, &m_eff, &brk))) { fill(); return rc; }
+    const double* alpha = h->h_small + kOffAlpha;
+    const double* beta = h->h_small + kOffBeta;
+    te::SmallEig E;
+    if (!te::tridiag_eig(m_eff, alpha, beta, E)) {
+      fill();
+      return set_err(TE_ERR_NUMERICAL, "tridiagonal eigensolver did not converge");
+    }
+    E.h = beta[m_eff - 1];
+    const double rem = t - t_now;
+    double tau, err;
+    bool qok = true;
+    if (forced) {
+      tau = std::min(forced[k], rem);
+      te::QuadResult q = te::tanh_sinh(E, 0.0, tau);
+      err = q.value;
+      qok = q.converged;
+    } else {
+      te::StepResult r = te::find_step(E, brk, k == 0, tau_prev, rem, tol_rate, t);
+      if (r.collapse) {
+        fill();
+        return set_err(TE_ERR_STEP_COLLAPSE, "step size collapsed below 1e-13 t (m=%d too small for tol=%g)", m, tol);
+      }
+      tau = r.tau;
+      err = r.err;
+      qok = r.quad_ok;
+    }
+    // omega~_k = s_k omega_k with s_0 = 1, s_k = 1/beta_{k-1} (columns stored unnormalised)
+    te::omega(E, tau, om.data());
+    for (int q = 0; q < m_eff; ++q) {
+      const double s = q == 0 ? 1.0 : 1.0 / beta[q - 1];
+      h->h_coef[q] = make_double2(om[q].real() * s, om[q].imag() * s);
+    }
+    CK(cudaMemcpyAsync(h->d_g + 128, h->h_coef, sizeof(double2) * m_eff, cudaMemcpyHostToDevice, h->stream));
+    {
+      KDev d = make_kdev(h, tol_rate, m);
+      Launch L = make_launch(h);
+      prof_begin(h);
+      te::launch_combine(d, h->d_g + 128, m_eff, h->d_V, L);
+      prof_end(h, 3, 16.0 * (double)h->n * (m_eff + 1));
+    }
+    t_now = (tau >= rem) ? t : t_now + tau;
+    tau_prev = tau;
+    S.err_bound += err;
+    S.n_restarts += 1;
+    S.n_krylov_steps += m_eff;
+    S.n_breakdowns += brk ? 1 : 0;
+    if (S.roundoff_step > err) S.warnings |= TE_WARN_ROUNDOFF;
+    if (!qok) S.warnings |= TE_WARN_QUADRATURE;
+    S.t_step_min = (S.n_restarts == 1) ? tau : std::min(S.t_step_min, tau);
+    S.t_step_max = std::max(S.t_step_max, tau);
+    h->sched.push_back({tau, m_eff, err});
+    ++k;
+  }
+  CK(cudaGetLastError());
+  if (h->profile) {
+    CK(cudaStreamSynchronize(h->stream));
+    prof_collect(h);
+  }
+  fill();
+  return TE_OK;
+}
+
+int check_evolve_args(te_handle* h, double t, double tol, int m_max) {
+  if (!h) return set_err(TE_ERR_ARG, "null handle");
+  if (!(t >= 0.0) || !std::isfinite(t)) return set_err(TE_ERR_ARG, "t must be finite and >= 0");
+  if (!(tol > 0.0) || !std::isfinite(tol)) return set_err(TE_ERR_ARG, "tol must be > 0");
+  if (m_max < 1 || m_max > TE_M_MAX) return set_err(TE_ERR_ARG, "m_max must be in [1, %d]", TE_M_MAX);
+  return TE_OK;
+}
+
+// ---------------------------------------------------------------- creation
+te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, const void* val, bool cplx,
+                         int64_t n_global, int64_t row_begin, te_dist* dist, bool herm_check, int64_t ncol_limit) {
+  clear_err();
+  if (n < 1 || !rowptr || (!col && rowptr[n] > 0) || (!val && rowptr[n] > 0)) {
+    set_err(TE_ERR_ARG, "bad arguments (n=%lld)", (long long)n);
+    return nullptr;
+  }
+  if (rowptr[0] != 0) {
+    set_err(TE_ERR_CSR, "rowptr[0] != 0");
+    return nullptr;
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (rowptr[i + 1] < rowptr[i]) {
+      set_err(TE_ERR_CSR, "rowptr decreases at row %lld", (long long)i);
+      return nullptr;
+    }
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
+    cudaGetLastError();
+    set_err(TE_ERR_CUDA, "no CUDA device available");
+    return nullptr;
+  }
+  te_handle* h = new te_handle();
+  h->dist = dist;
+  h->n = n;
+  h->n_global = n_global;
+  h->row_begin = row_begin;
+  h->cplx = cplx;
+  h->nnz = rowptr[n];
+  for (auto& p : h->prof) p = te_kernel_profile{0, 0.0, 0.0};
+  auto fail = [&](int code, const char* what) -> te_handle* {
+    if (g_status == TE_OK) set_err(code, "%s", what);
+    te_destroy(h);
+    return nullptr;
+  };
+  if (cudaGetDevice(&h->device) != cudaSuccess) return fail(TE_ERR_CUDA, "cudaGetDevice");
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+  if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(TE_ERR_CUDA, "cudaStreamCreate");
+  h->stream = h->own_stream;
+  te::configure_kernels();
+  const size_t vb = cplx ? 16 : 8;
+  if (cudaMalloc(&h->d_rowptr, sizeof(int64_t) * (n + 1)) != cudaSuccess) return fail(TE_ERR_OOM, "rowptr alloc");
+  if (cudaMalloc(&h->d_col, sizeof(int32_t) * std::max<int64_t>(1, h->nnz)) != cudaSuccess)
+    return fail(TE_ERR_OOM, "col alloc");
+  if (cudaMalloc(&h->d_val, vb * std::max<int64_t>(1, h->nnz)) != cudaSuccess) return fail(TE_ERR_OOM, "val alloc");
+  cudaMemcpyAsync(h->d_rowptr, rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, h->stream);
+  if (h->nnz > 0) {
+    cudaMemcpyAsync(h->d_col, col, sizeof(int32_t) * h->nnz, cudaMemcpyHostToDevice, h->stream);
+    cudaMemcpyAsync(h->d_val, val, vb * h->nnz, cudaMemcpyHostToDevice, h->stream);
+  }
+  if (ensure_workspace(h, 1) != TE_OK) return fail(TE_ERR_OOM, "workspace");
+  // validation + ||H||_1 on the device
+  int* d_err = reinterpret_cast<int*>(h->d_counter + 4);
+  unsigned long long* d_norm = reinterpret_cast<unsigned long long*>(h->d_small + kOffScalar);
+  cudaMemsetAsync(d_err, 0, sizeof(int), h->stream);
+  cudaMemsetAsync(d_norm, 0, sizeof(unsigned long long), h->stream);
+  // distributed handles: local columns >= n address the halo; the Hermiticity test needs the
+  // global matrix and is skipped there (ranks validate structure only)
+  te::CsrCheck cc{d_err, d_norm};
+  te::launch_csr_check(n, ncol_limit, h->d_rowptr, h->d_col, h->d_val, cplx, herm_check, cc, h->stream);
+  int herr = 0;
+  unsigned long long nb = 0;
+  cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, h->stream);
+  cudaMemcpyAsync(&nb, d_norm, sizeof(nb), cudaMemcpyDeviceToHost, h->stream);
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) {
+    set_err(TE_ERR_CUDA, "create: %s", cudaGetErrorString(e));
+    return fail(TE_ERR_CUDA, "create");
+  }
+  cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned) * 8, h->stream);
+  if (herr & 1) return fail(TE_ERR_CSR, "column indices out of range or not strictly increasing within a row");
+  if (herr & 2) return fail(TE_ERR_NOT_HERMITIAN, "matrix is not Hermitian (or has non-finite values)");
+  double nrm;
+  std::memcpy(&nrm, &nb, sizeof nrm);
+  h->norm1 = nrm;
+  h->launches += 1;
+  return h;
+}
+
+}  // namespace
+
+// ==========================================================================================
+// C ABI
+// ==========================================================================================
+extern "C" {
+
+int te_last_status(void) { return g_status; }
+const char* te_last_error(void) { return g_msg.c_str(); }
+const char* te_version(void) { return "timeevolver-b200 0.1 (sm_100a)"; }
+
+te_handle* te_create_csr(int64_t n, const int64_t* rowptr, const int32_t* col, const te_c128* val) {
+  return create_common(n, rowptr, col, val, true, n, 0, nullptr, true, n);
+}
+
+te_handle* te_create_csr_real(int64_t n, const int64_t* rowptr, const int32_t* col, const double* val) {
+  return create_common(n, rowptr, col, val, false, n, 0, nullptr, true, n);
+}
+
+void te_destroy(te_handle* h) {
+  if (!h) return;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  cudaFree(h->d_rowptr);
+  cudaFree(h->d_col);
+  cudaFree(h->d_val);
+  free_workspace(h);
+  cudaFree(h->d_small);
+  cudaFree(h->d_g);
+  cudaFree(h->d_part);
+  cudaFree(h->d_partn);
+  cudaFree(h->d_counter);
+  cudaFree(h->d_halo);
+  cudaFree(h->d_sendbuf);
+  cudaFree(h->d_send_idx);
+  if (h->h_small) cudaFreeHost(h->h_small);
+  if (h->h_coef) cudaFreeHost(h->h_coef);
+  if (h->ev_ready)
+    for (int i = 0; i < kEvPool; ++i) {
+      cudaEventDestroy(h->ev0[i]);
+      cudaEventDestroy(h->ev1[i]);
+    }
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+}
+
+static int evolve_entry(te_handle* h, const void* v0, bool v0_dev, double t, double tol, int m_max, void* vout,
+                        bool vout_dev, te_stats* st, cudaStream_t stream, const double* forced, int64_t nforced) {
+  clear_err();
+  int rc = check_evolve_args(h, t, tol, m_max);
+  if (rc) return rc;
+  if (!v0 || !vout) return set_err(TE_ERR_ARG, "null vector");
+  if (cudaSetDevice(h->device) != cudaSuccess) return set_err(TE_ERR_CUDA, "cudaSetDevice");
+  h->stream = stream ? stream : h->own_stream;
+  const int m = (int)std::min<int64_t>(m_max, h->n_global);
+  if ((rc = ensure_workspace(h, std::max(m, 1)))) return rc;
+  const size_t vbytes = sizeof(double2) * (size_t)h->n;
+  CK(cudaMemcpyAsync(h->d_V, v0, vbytes, v0_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+  rc = evolve_core(h, t, tol, m_max, forced, nforced, st);
+  if (rc) {
+    cudaStreamSynchronize(h->stream);
+    h->stream = h->own_stream;
+    return rc;
+  }
+  CK(cudaMemcpyAsync(vout, h->d_V, vbytes, vout_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->stream = h->own_stream;
+  return TE_OK;
+}
+
+int te_evolve(te_handle* h, const te_c128* v0, double t, double tol, int m_max, te_c128* v_out, te_stats* stats) {
+  return evolve_entry(h, v0, false, t, tol, m_max, v_out, false, stats, nullptr, nullptr, 0);
+}
+
+int te_evolve_dev(te_handle* h, const void* d_v0, double t, double tol, int m_max, void* d_vout, te_stats* stats,
+                  void* stream) {
+  return evolve_entry(h, d_v0, true, t, tol, m_max, d_vout, true, stats, static_cast<cudaStream_t>(stream), nullptr,
+                      0);
+}
+
+int te_evolve_schedule(te_handle* h, const te_c128* v0, int64_t k, const double* t_steps, double tol, int m_max,
+                       te_c128* v_out, te_stats* stats) {
+  if (k < 0 || (k > 0 && !t_steps)) return set_err(TE_ERR_ARG, "bad schedule");
+  double t = 0.0;
+  for (int64_t i = 0; i < k; ++i) {
+    if (!(t_steps[i] > 0.0) || !std::isfinite(t_steps[i])) return set_err(TE_ERR_ARG, "schedule steps must be > 0");
+    t += t_steps[i];
+  }
+  return evolve_entry(h, v0, false, t, tol, m_max, v_out, false, stats, nullptr, t_steps, k);
+}
+
+int64_t te_get_schedule(const te_handle* h, int64_t cap, double* t_steps, int32_t* m_eff, double* err_steps) {
+  if (!h) return -TE_ERR_ARG;
+  const int64_t k = (int64_t)h->sched.size();
+  for (int64_t i = 0; i < std::min(cap, k); ++i) {
+    if (t_steps) t_steps[i] = h->sched[i].tau;
+    if (m_eff) m_eff[i] = h->sched[i].m_eff;
+    if (err_steps) err_steps[i] = h->sched[i].err;
+  }
+  return k;
+}
+
+int te_krylov_basis(te_handle* h, const te_c128* v1, int m, double tol_rate, double* alpha, double* beta,
+                    int* m_eff, int* breakdown, te_c128* V_out) {
+  clear_err();
+  if (!h || !v1 || !alpha || !beta || !m_eff) return set_err(TE_ERR_ARG, "null argument");
+  if (m < 1 || m > TE_M_MAX) return set_err(TE_ERR_ARG, "m must be in [1, %d]", TE_M_MAX);
+  if (cudaSetDevice(h->device) != cudaSuccess) return set_err(TE_ERR_CUDA, "cudaSetDevice");
+  h->stream = h->own_stream;
+  m = (int)std::min<int64_t>(m, h->n_global);
+  int rc = ensure_workspace(h, m);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(h->d_V, v1, sizeof(double2) * h->n, cudaMemcpyHostToDevice, h->stream));
+  if ((rc = run_arnoldi(h, m, tol_rate))) return rc;
+  bool brk;
+  int me;
+  if ((rc = read_flag(h, m, &me, &brk))) return rc;
+  *m_eff = me;
+  if (breakdown) *breakdown = brk ? 1 : 0;
+  for (int q = 0; q < m; ++q) {
+    alpha[q] = q < me ? h->h_small[kOffAlpha + q] : 0.0;
+    beta[q] = q < me ? h->h_small[kOffBeta + q] : 0.0;
+  }
+  if (V_out) {
+    std::vector<double2> col(h->n);
+    for (int q = 0; q < me; ++q) {
+      CK(cudaMemcpy(col.data(), h->d_V + (int64_t)q * h->ldv, sizeof(double2) * h->n, cudaMemcpyDeviceToHost));
+      const double s = q == 0 ? 1.0 : 1.0 / h->h_small[kOffBeta + q - 1];
+      for (int64_t i = 0; i < h->n; ++i) {
+        V_out[(size_t)q * h->n + i].re = col[i].x * s;
+        V_out[(size_t)q * h->n + i].im = col[i].y * s;
+      }
+    }
+  }
+  return TE_OK;
+}
+
+int te_set_option(te_handle* h, int option, double value) {
+  clear_err();
+  if (!h) return set_err(TE_ERR_ARG, "null handle");
+  switch (option) {
+    case TE_OPT_PROFILE:
+      h->profile = value != 0.0;
+      for (auto& p : h->prof) p = te_kernel_profile{0, 0.0, 0.0};
+      h->ev_used = 0;
+      return TE_OK;
+    case TE_OPT_GRAPH:
+      return TE_OK;  // launches are issued directly (graph replay: see DESIGN.md next steps)
+    default:
+      return set_err(TE_ERR_ARG, "unknown option %d", option);
+  }
+}
+
+int te_get_profile(const te_handle* h, int kernel, te_kernel_profile* out) {
+  if (!h || !out || kernel < 0 || kernel >= kProfKernels) return set_err(TE_ERR_ARG, "bad arguments");
+  *out = h->prof[kernel];
+  return TE_OK;
+}
+
+int64_t te_launch_count(const te_handle* h) { return h ? h->launches : -1; }
+double te_one_norm(const te_handle* h) { return h ? h->norm1 : -1.0; }
+
+// ------------------------------------------------------------------------------------------
+// distributed
+// ------------------------------------------------------------------------------------------
+int te_nccl_unique_id(void* out128) {
+  clear_err();
+  if (!out128) return set_err(TE_ERR_ARG, "null");
+  if (!te::nccl().ok) return set_err(TE_ERR_NCCL, "NCCL library not available: %s", te::nccl().err.c_str());
+  ncclUniqueId id;
+  CKN(te::nccl().GetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof id);
+  return TE_OK;
+}
+
+te_dist* te_dist_init(int nranks, int rank, const void* id128) {
+  clear_err();
+  if (nranks < 1 || rank < 0 || rank >= nranks || !id128) {
+    set_err(TE_ERR_ARG, "bad arguments");
+    return nullptr;
+  }
+  te_dist* d = new te_dist();
+  d->nranks = nranks;
+  d->rank = rank;
+  if (nranks > 1) {
+    if (!te::nccl().ok) {
+      set_err(TE_ERR_NCCL, "NCCL library not available: %s", te::nccl().err.c_str());
+      delete d;
+      return nullptr;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    ncclResult_t r = te::nccl().CommInitRank(&d->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      set_err(TE_ERR_NCCL, "ncclCommInitRank: %s", te::nccl().GetErrorString(r));
+      delete d;
+      return nullptr;
+    }
+  }
+  return d;
+}
+
+void te_dist_destroy(te_dist* d) {
+  if (!d) return;
+  if (d->comm) te::nccl().CommDestroy(d->comm);
+  delete d;
+}
+
+}  // extern "C"
+
+// halo plan + distributed create live in dist.cpp
+te_handle* te_internal_create_local(int64_t n_loc, int64_t n_global, int64_t row_begin, const int64_t* rowptr,
+                                    const int32_t* col_local, const void* val, bool cplx, te_dist* dist,
+                                    int64_t ncol_limit) {
+  return create_common(n_loc, rowptr, col_local, val, cplx, n_global, row_begin, dist, false, ncol_limit);
+}
+ncclComm_t te_internal_comm(te_dist* d) { return d->comm; }
+int te_internal_nranks(te_dist* d) { return d->nranks; }
+int te_internal_rank(te_dist* d) { return d->rank; }
+
+int te_internal_setup_halo(te_handle* h, int64_t n_halo, const std::vector<int64_t>& recv_counts,
+                           const std::vector<int64_t>& send_counts, const std::vector<int32_t>& send_idx,
+                           double norm1_global) {
+  h->n_halo = n_halo;
+  h->recv_counts = recv_counts;
+  h->send_counts = send_counts;
+  h->n_send = (int64_t)send_idx.size();
+  h->norm1 = norm1_global;
+  if (n_halo > 0) CK(cudaMalloc(&h->d_halo, sizeof(double2) * n_halo));
+  if (h->n_send > 0) {
+    CK(cudaMalloc(&h->d_sendbuf, sizeof(double2) * h->n_send));
+    CK(cudaMalloc(&h->d_send_idx, sizeof(int32_t) * h->n_send));
+    CK(cudaMemcpy(h->d_send_idx, send_idx.data(), sizeof(int32_t) * h->n_send, cudaMemcpyHostToDevice));
+  }
+  return TE_OK;
+}
+
+int te_internal_set_error(int code, const char* msg) { return set_err(code, "%s", msg); }
+cudaStream_t te_internal_stream(te_handle* h) { return h->own_stream; }
+double te_internal_local_norm1(te_handle* h) { return h->norm1; }

@@ -1,0 +1,298 @@
+"""Thin Python binding of the C ABI in include/te.h (argument marshalling only).
+
+Every step of the method runs inside libtimeevolver.so (CUDA kernels for sm_100a + the
+host restart loop in C++).  There is no Python or CPU fallback: if the library is missing
+or no CUDA device is present, calls raise ``TEError``.  PyTorch is only used by callers
+for device memory / streams (``te_evolve_dev`` takes tensors' data pointers).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import build as _build
+
+_LIB = None
+
+TE_OK = 0
+STATUS = {0: "TE_OK", 1: "TE_ERR_ARG", 2: "TE_ERR_CSR", 3: "TE_ERR_NOT_HERMITIAN", 4: "TE_ERR_NOT_NORMALIZED",
+          5: "TE_ERR_STEP_COLLAPSE", 6: "TE_ERR_NUMERICAL", 7: "TE_ERR_OOM", 8: "TE_ERR_CUDA", 9: "TE_ERR_NCCL",
+          10: "TE_ERR_UNSUPPORTED"}
+TE_WARN_ROUNDOFF = 1
+TE_WARN_QUADRATURE = 2
+TE_OPT_PROFILE = 1
+TE_OPT_GRAPH = 2
+KERNELS = {0: "spmv_proj", 1: "update_proj", 2: "update_norm", 3: "combine", 4: "halo_pack"}
+
+
+class TEError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Stats(C.Structure):
+    _fields_ = [("err_bound", C.c_double), ("n_restarts", C.c_int64), ("n_krylov_steps", C.c_int64),
+                ("n_breakdowns", C.c_int64), ("roundoff_step", C.c_double), ("roundoff_total", C.c_double),
+                ("warnings", C.c_uint32), ("_pad", C.c_uint32), ("t_step_min", C.c_double),
+                ("t_step_max", C.c_double), ("one_norm", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "_pad"}
+
+
+class KernelProfile(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("total_ms", C.c_double), ("alg_bytes", C.c_double)]
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load():
+    """Load libtimeevolver.so (built in-tree by ``python -m paper_2205_15346_b200.build``)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(_build.LIB):
+        raise TEError(8, f"{_build.LIB} is not built (run __graft_entry__.build())")
+    L = C.CDLL(_build.LIB)
+    P, I64, I32, D, V = C.POINTER, C.c_int64, C.c_int32, C.c_double, C.c_void_p
+    L.te_create_csr.restype = V
+    L.te_create_csr.argtypes = [I64, V, V, V]
+    L.te_create_csr_real.restype = V
+    L.te_create_csr_real.argtypes = [I64, V, V, V]
+    L.te_evolve.restype = C.c_int
+    L.te_evolve.argtypes = [V, V, D, D, C.c_int, V, P(Stats)]
+    L.te_evolve_dev.restype = C.c_int
+    L.te_evolve_dev.argtypes = [V, V, D, D, C.c_int, V, P(Stats), V]
+    L.te_evolve_schedule.restype = C.c_int
+    L.te_evolve_schedule.argtypes = [V, V, I64, V, D, C.c_int, V, P(Stats)]
+    L.te_get_schedule.restype = I64
+    L.te_get_schedule.argtypes = [V, I64, V, V, V]
+    L.te_krylov_basis.restype = C.c_int
+    L.te_krylov_basis.argtypes = [V, V, C.c_int, D, V, V, P(C.c_int), P(C.c_int), V]
+    L.te_destroy.restype = None
+    L.te_destroy.argtypes = [V]
+    L.te_set_option.restype = C.c_int
+    L.te_set_option.argtypes = [V, C.c_int, D]
+    L.te_get_profile.restype = C.c_int
+    L.te_get_profile.argtypes = [V, C.c_int, P(KernelProfile)]
+    L.te_launch_count.restype = I64
+    L.te_launch_count.argtypes = [V]
+    L.te_one_norm.restype = D
+    L.te_one_norm.argtypes = [V]
+    L.te_last_status.restype = C.c_int
+    L.te_last_error.restype = C.c_char_p
+    L.te_version.restype = C.c_char_p
+    L.te_nccl_unique_id.restype = C.c_int
+    L.te_nccl_unique_id.argtypes = [V]
+    L.te_dist_init.restype = V
+    L.te_dist_init.argtypes = [C.c_int, C.c_int, V]
+    L.te_dist_destroy.restype = None
+    L.te_dist_destroy.argtypes = [V]
+    L.te_create_csr_dist.restype = V
+    L.te_create_csr_dist.argtypes = [V, I64, I64, I64, V, V, V, C.c_int]
+    L.te_halo_plan.restype = I64
+    L.te_halo_plan.argtypes = [C.c_int, C.c_int, V, I64, V, V, V, V, I64]
+    _LIB = L
+    return L
+
+
+def _err(L):
+    return TEError(L.te_last_status(), (L.te_last_error() or b"").decode())
+
+
+def _check(L, rc):
+    if rc != TE_OK:
+        raise TEError(rc, (L.te_last_error() or b"").decode())
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class Handle:
+    """Owns a te_handle*; te_destroy on close()/GC."""
+
+    def __init__(self, ptr, n, cplx, dist=None):
+        self.ptr = ptr
+        self.n = n
+        self.cplx = cplx
+        self.dist = dist
+
+    def close(self):
+        if self.ptr:
+            load().te_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def te_create_csr(n, rowptr, col, val) -> Handle:
+    L = load()
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    if np.iscomplexobj(val):
+        val = np.ascontiguousarray(val, dtype=np.complex128)
+        p = L.te_create_csr(int(n), _ptr(rowptr), _ptr(col), _ptr(val))
+    else:
+        val = np.ascontiguousarray(val, dtype=np.float64)
+        p = L.te_create_csr_real(int(n), _ptr(rowptr), _ptr(col), _ptr(val))
+    if not p:
+        raise _err(L)
+    return Handle(p, int(n), np.iscomplexobj(val))
+
+
+def te_destroy(h: Handle):
+    h.close()
+
+
+def te_evolve(h: Handle, v0, t, tol, m_max, out=None):
+    L = load()
+    v0 = np.ascontiguousarray(v0, dtype=np.complex128)
+    vo = np.empty_like(v0) if out is None else out
+    st = Stats()
+    _check(L, L.te_evolve(h.ptr, _ptr(v0), float(t), float(tol), int(m_max), _ptr(vo), C.byref(st)))
+    return vo, st.as_dict()
+
+
+def te_evolve_dev(h: Handle, d_v0, t, tol, m_max, d_vout, stream=None):
+    """d_v0 / d_vout: CUDA tensors (complex128, contiguous) or raw device pointers."""
+    L = load()
+    p0 = d_v0.data_ptr() if hasattr(d_v0, "data_ptr") else int(d_v0)
+    p1 = d_vout.data_ptr() if hasattr(d_vout, "data_ptr") else int(d_vout)
+    s = None
+    if stream is not None:
+        s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    st = Stats()
+    _check(L, L.te_evolve_dev(h.ptr, C.c_void_p(p0), float(t), float(tol), int(m_max), C.c_void_p(p1),
+                              C.byref(st), C.c_void_p(s) if s else None))
+    return st.as_dict()
+
+
+def te_evolve_schedule(h: Handle, v0, t_steps, tol, m_max):
+    L = load()
+    v0 = np.ascontiguousarray(v0, dtype=np.complex128)
+    ts = np.ascontiguousarray(t_steps, dtype=np.float64)
+    vo = np.empty_like(v0)
+    st = Stats()
+    _check(L, L.te_evolve_schedule(h.ptr, _ptr(v0), ts.shape[0], _ptr(ts), float(tol), int(m_max), _ptr(vo),
+                                   C.byref(st)))
+    return vo, st.as_dict()
+
+
+def te_get_schedule(h: Handle):
+    L = load()
+    k = L.te_get_schedule(h.ptr, 0, None, None, None)
+    ts = np.zeros(k)
+    me = np.zeros(k, dtype=np.int32)
+    es = np.zeros(k)
+    L.te_get_schedule(h.ptr, k, _ptr(ts), _ptr(me), _ptr(es))
+    return [(float(a), int(b), float(c)) for a, b, c in zip(ts, me, es)]
+
+
+def te_krylov_basis(h: Handle, v1, m, tol_rate, want_V=True):
+    L = load()
+    v1 = np.ascontiguousarray(v1, dtype=np.complex128)
+    a = np.zeros(m)
+    b = np.zeros(m)
+    me = C.c_int(0)
+    bk = C.c_int(0)
+    V = np.zeros((m, h.n), dtype=np.complex128) if want_V else None
+    _check(L, L.te_krylov_basis(h.ptr, _ptr(v1), int(m), float(tol_rate), _ptr(a), _ptr(b), C.byref(me),
+                                C.byref(bk), _ptr(V) if want_V else None))
+    k = me.value
+    out = dict(alpha=a[:k], beta=b[:k], m_eff=k, breakdown=bool(bk.value), h=float(b[k - 1]))
+    if want_V:
+        out["V"] = V[:k].T.copy()
+    return out
+
+
+def te_set_option(h: Handle, option: int, value: float):
+    L = load()
+    _check(L, L.te_set_option(h.ptr, int(option), float(value)))
+
+
+def te_get_profile(h: Handle):
+    L = load()
+    out = {}
+    for k, name in KERNELS.items():
+        p = KernelProfile()
+        _check(L, L.te_get_profile(h.ptr, k, C.byref(p)))
+        out[name] = dict(launches=p.launches, total_ms=p.total_ms, alg_bytes=p.alg_bytes)
+    return out
+
+
+def te_launch_count(h: Handle) -> int:
+    return int(load().te_launch_count(h.ptr))
+
+
+def te_one_norm(h: Handle) -> float:
+    return float(load().te_one_norm(h.ptr))
+
+
+def te_version() -> str:
+    return load().te_version().decode()
+
+
+# ---------------------------------------------------------------- distributed
+
+def te_nccl_unique_id() -> bytes:
+    L = load()
+    buf = C.create_string_buffer(128)
+    _check(L, L.te_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Dist:
+    def __init__(self, ptr, nranks, rank):
+        self.ptr, self.nranks, self.rank = ptr, nranks, rank
+
+    def close(self):
+        if self.ptr:
+            load().te_dist_destroy(self.ptr)
+            self.ptr = None
+
+
+def te_dist_init(nranks: int, rank: int, uid: bytes) -> Dist:
+    L = load()
+    buf = C.create_string_buffer(bytes(uid), 128)
+    p = L.te_dist_init(int(nranks), int(rank), buf)
+    if not p:
+        raise _err(L)
+    return Dist(p, nranks, rank)
+
+
+def te_create_csr_dist(d: Dist, n_global, row_begin, row_end, rowptr_local, col_global, val) -> Handle:
+    L = load()
+    rp = np.ascontiguousarray(rowptr_local, dtype=np.int64)
+    cg = np.ascontiguousarray(col_global, dtype=np.int64)
+    cplx = np.iscomplexobj(val)
+    v = np.ascontiguousarray(val, dtype=np.complex128 if cplx else np.float64)
+    p = L.te_create_csr_dist(d.ptr, int(n_global), int(row_begin), int(row_end), _ptr(rp), _ptr(cg), _ptr(v),
+                             1 if cplx else 0)
+    if not p:
+        raise _err(L)
+    return Handle(p, int(row_end - row_begin), cplx, dist=d)
+
+
+def te_halo_plan(nranks: int, rank: int, row_starts, col_global):
+    """Host-only (no GPU): returns (col_local int32, recv_counts int64[nranks], halo_global int64)."""
+    L = load()
+    rs = np.ascontiguousarray(row_starts, dtype=np.int64)
+    cg = np.ascontiguousarray(col_global, dtype=np.int64)
+    cl = np.zeros(max(1, cg.shape[0]), dtype=np.int32)
+    rc = np.zeros(nranks, dtype=np.int64)
+    halo = np.zeros(max(1, cg.shape[0]), dtype=np.int64)
+    nh = L.te_halo_plan(int(nranks), int(rank), _ptr(rs), cg.shape[0], _ptr(cg), _ptr(cl), _ptr(rc), _ptr(halo),
+                        halo.shape[0])
+    if nh < 0:
+        raise _err(L)
+    return cl[: cg.shape[0]], rc, halo[:nh]

@@ -1,0 +1,221 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element on
+the same seeded inputs, plus full-size properties.  Tolerances (BASELINE.json north star):
+||dv||_2 <= 1e-10 with the step schedule forced identical; <= tol + 1e-12 with adaptive
+stepping (both runs individually satisfy their bound, reading C16/C18)."""
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg as sl
+import scipy.sparse as sp
+
+from oracle import krylov as K
+from workloads import configs, models
+
+pytestmark = pytest.mark.gpu
+
+
+def csr_from_dense(A):
+    S = sp.csr_matrix(A)
+    S.sort_indices()
+    return S.indptr.astype(np.int64), S.indices.astype(np.int32), S.data
+
+
+def small_cases():
+    return [
+        ("cfg1_n4096", configs.build(1)),
+        ("xxz_L12", configs.build(2, L=12)),
+        ("bh_L6_N6_ragged", configs.build(3, L=6, N=6)),
+        ("xxznnn_L12", configs.build(5, L=12)),
+        ("banded_n8192", configs.build(4, n=8192)),
+        ("cfg1_n1000_ragged", configs.build(1, n=1000)),
+    ]
+
+
+CASES = small_cases()
+
+
+@pytest.mark.parametrize("name,c", CASES, ids=[x[0] for x in CASES])
+def test_krylov_basis_matches_oracle(gpu_lib, name, c):
+    te = gpu_lib
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    m = min(c["m"], c["n"])
+    tol_rate = c["tol"] / c["t"]
+    g = te.te_krylov_basis(h, c["v0"], m, tol_rate, want_V=True)
+    o = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), c["v0"], m, tol_rate)
+    assert g["m_eff"] == o["m_eff"] and g["breakdown"] == o["breakdown"]
+    k = g["m_eff"]
+    scale = max(1.0, np.abs(o["alpha"]).max(), np.abs(o["beta"]).max())
+    assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-12 * scale
+    assert np.abs(g["beta"] - o["beta"]).max() <= 1e-12 * scale
+    assert np.linalg.norm(g["V"] - o["V"]) <= 1e-10
+    # CGS2 orthonormality of the GPU basis itself
+    V = g["V"]
+    assert np.abs(V.conj().T @ V - np.eye(k)).max() <= 1e-13
+    h.close()
+
+
+@pytest.mark.parametrize("name,c", CASES, ids=[x[0] for x in CASES])
+def test_evolve_forced_and_adaptive(gpu_lib, name, c):
+    te = gpu_lib
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    t, tol, m = c["t"], c["tol"], c["m"]
+    if c["n"] > 5000:
+        t = min(t, 2.0)
+    v, st = te.te_evolve(h, c["v0"], t, tol, m)
+    sched = te.te_get_schedule(h)
+    assert st["n_restarts"] == len(sched) and st["err_bound"] <= tol
+    assert math.fsum(s[0] for s in sched) == pytest.approx(t, abs=1e-12)
+    # forced identical schedule -> 1e-10
+    ref = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], t, tol, m, schedule=[s[0] for s in sched])
+    assert np.linalg.norm(v - ref["v"]) <= 1e-10
+    assert [s[1] for s in ref["schedule"]] == [s[1] for s in sched]
+    for (tg, _, eg), (to, _, eo) in zip(sched, ref["schedule"]):
+        assert abs(eg - eo) <= 1e-6 * max(eo, 1e-300) + 1e-300
+    # adaptive vs adaptive -> tol + 1e-12
+    ada = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], t, tol, m)
+    assert np.linalg.norm(v - ada["v"]) <= tol + 1e-12
+    # schedule of the GPU and of the oracle coincide (same algorithm; equal decisions)
+    assert len(ada["schedule"]) == len(sched)
+    assert max(abs(a[0] - b[0]) for a, b in zip(ada["schedule"], sched)) <= 1e-12 * t
+    # the explicitly forced path of the library reproduces the adaptive result
+    vf, stf = te.te_evolve_schedule(h, c["v0"], [s[0] for s in sched], tol, m)
+    assert np.linalg.norm(vf - v) <= 1e-13
+    h.close()
+
+
+def test_dense_exponential_and_bound(gpu_lib):
+    te = gpu_lib
+    c = configs.build(1)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    v, st = te.te_evolve(h, c["v0"], c["t"], c["tol"], c["m"])
+    H = sp.csr_matrix((c["val"], c["col"], c["rowptr"])).toarray()
+    lam, U = np.linalg.eigh(H)
+    ve = U @ (np.exp(-1j * lam * c["t"]) * (U.conj().T @ c["v0"]))
+    err = np.linalg.norm(v - ve)
+    assert err <= st["err_bound"] + 10 * st["roundoff_total"]
+    assert st["err_bound"] <= c["tol"]
+
+
+def test_edge_cases(gpu_lib):
+    te = gpu_lib
+    # Pauli X, t = pi -> -e1 (exp(-i X pi) = -I); breakdown at j = 1 (m_eff = 2)
+    rp, cl, vl = csr_from_dense(np.array([[0, 1], [1, 0]], dtype=complex))
+    h = te.te_create_csr(2, rp, cl, vl)
+    v, st = te.te_evolve(h, np.array([1, 0], complex), math.pi, 1e-10, 10)
+    assert np.abs(v - np.array([-1, 0])).max() < 1e-12
+    assert st["n_breakdowns"] == st["n_restarts"] == 1
+    # t = 0 returns v0
+    v0 = np.array([0.6, 0.8j])
+    v, st = te.te_evolve(h, v0, 0.0, 1e-10, 10)
+    assert np.array_equal(v, v0) and st["n_restarts"] == 0 and st["err_bound"] == 0.0
+    # not normalised
+    with pytest.raises(te.TEError) as ei:
+        te.te_evolve(h, np.array([1, 1], complex), 1.0, 1e-8, 5)
+    assert ei.value.status == 4
+    # bad args
+    with pytest.raises(te.TEError) as ei:
+        te.te_evolve(h, np.array([1, 0], complex), 1.0, 0.0, 5)
+    assert ei.value.status == 1
+    with pytest.raises(te.TEError):
+        te.te_evolve(h, np.array([1, 0], complex), -1.0, 1e-8, 5)
+    with pytest.raises(te.TEError):
+        te.te_evolve(h, np.array([1, 0], complex), 1.0, 1e-8, 65)
+    h.close()
+    # eigenvector input: breakdown at j = 0, exact phase
+    rp, cl, vl = csr_from_dense(np.diag([1.0, 2.0, 3.0]))
+    h = te.te_create_csr(3, rp, cl, vl)
+    v, st = te.te_evolve(h, np.array([0, 1, 0], complex), 3.0, 1e-8, 5)
+    assert abs(v[1] - np.exp(-6j)) < 1e-14 and st["n_breakdowns"] == 1
+    h.close()
+    # invalid CSR / non-Hermitian
+    with pytest.raises(te.TEError) as ei:
+        te.te_create_csr(2, np.array([0, 2, 3]), np.array([1, 0, 0]), np.array([1.0, 1.0, 2.0]))
+    assert ei.value.status == 2
+    with pytest.raises(te.TEError) as ei:
+        te.te_create_csr(2, np.array([0, 1, 2]), np.array([1, 0]), np.array([1.0, 2.0]))
+    assert ei.value.status == 3
+    with pytest.raises(te.TEError) as ei:
+        te.te_create_csr(2, np.array([0, 1, 2]), np.array([1, 0]), np.array([1 + 1j, 1 + 1j]))
+    assert ei.value.status == 3
+    # m_max = 1 on a non-trivial problem -> step collapse (reading C17)
+    A = np.array([[0.0, 1.0, 0.0], [1.0, 0.5, 1.0], [0.0, 1.0, -0.3]])
+    rp, cl, vl = csr_from_dense(A)
+    h = te.te_create_csr(3, rp, cl, vl)
+    with pytest.raises(te.TEError) as ei:
+        te.te_evolve(h, np.array([1, 0, 0], complex), 1.0, 1e-10, 1)
+    assert ei.value.status == 5
+    # m_max > n: capped at n, exact
+    v, st = te.te_evolve(h, np.array([1, 0, 0], complex), 1.0, 1e-10, 40)
+    assert np.linalg.norm(v - sl.expm(-1j * A) @ np.array([1, 0, 0])) < 1e-12
+    h.close()
+
+
+def test_determinism_and_device_path(gpu_lib):
+    import torch
+    te = gpu_lib
+    c = configs.build(2, L=14)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    v1, s1 = te.te_evolve(h, c["v0"], 3.0, 1e-10, 40)
+    v2, s2 = te.te_evolve(h, c["v0"], 3.0, 1e-10, 40)
+    assert np.array_equal(v1, v2) and s1 == s2
+    d0 = torch.from_numpy(c["v0"]).cuda()
+    d1 = torch.empty_like(d0)
+    s3 = te.te_evolve_dev(h, d0, 3.0, 1e-10, 40, d1, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    assert np.array_equal(d1.cpu().numpy(), v1)
+    # in-place (v_out aliases v0)
+    v = c["v0"].copy()
+    te.te_evolve(h, v, 3.0, 1e-10, 40, out=v)
+    assert np.array_equal(v, v1)
+    h.close()
+
+
+def test_full_size_xxz_L20_one_magnon_pin(gpu_lib):
+    """Full config-2 size (n = 2^20), launch configuration of bench.py: a one-magnon initial
+    state evolves inside the L x L one-magnon block, computed exactly."""
+    te = gpu_lib
+    c = configs.build(2)
+    L = 20
+    h_f = c["fields"]
+    J, Dl = 1.0, 0.5
+    E_ref = J * L * Dl / 4 - 0.5 * h_f.sum()
+    M = np.zeros((L, L))
+    for k in range(L):
+        M[k, k] = E_ref - J * Dl + h_f[k]
+        M[k, (k + 1) % L] = M[(k + 1) % L, k] = J / 2
+    g = np.random.default_rng(5)
+    a = g.standard_normal(L) + 1j * g.standard_normal(L)
+    a /= np.linalg.norm(a)
+    v0 = np.zeros(1 << L, complex)
+    idx = [1 << k for k in range(L)]
+    v0[idx] = a
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    t = c["t"]
+    v, st = te.te_evolve(h, v0, t, c["tol"], c["m"])
+    exact = sl.expm(-1j * M * t) @ a
+    assert np.linalg.norm(v[idx] - exact) <= st["err_bound"] + 1e-12
+    mask = np.ones(1 << L, bool)
+    mask[idx] = False
+    assert np.all(v[mask] == 0)
+    h.close()
+
+
+def test_full_size_xxz_L20_neel(gpu_lib):
+    """Config 2 at full size: Sz-sector exact zeros, norm, bound, partition of t; the first
+    restart against the oracle with the schedule forced identical (sampled at full size)."""
+    te = gpu_lib
+    c = configs.build(2)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    v, st = te.te_evolve(h, c["v0"], c["t"], c["tol"], c["m"])
+    sched = te.te_get_schedule(h)
+    assert st["err_bound"] <= c["tol"]
+    assert math.fsum(s[0] for s in sched) == pytest.approx(c["t"], abs=1e-12)
+    pop = np.array([bin(i).count("1") for i in range(c["n"])])
+    assert np.all(v[pop != 10] == 0)
+    assert abs(np.linalg.norm(v) - 1) <= st["err_bound"] + 10 * st["roundoff_total"]
+    tau1 = sched[0][0]
+    v1, _ = te.te_evolve_schedule(h, c["v0"], [tau1], c["tol"], c["m"])
+    r1 = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], tau1, c["tol"], c["m"], schedule=[tau1])
+    assert np.linalg.norm(v1 - r1["v"]) <= 1e-10
+    h.close()
