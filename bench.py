@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=8)
+    ap.add_argument("--kernels", type=int, default=0, help="0 register-streaming K1/K2, 1 smem/TMA-staged")
+    ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (library default if unset)")
     return ap.parse_args()
 
 
@@ -226,6 +228,9 @@ def run_ours(args):
         D = te.te_dist_init(ws, rank, uid[0])
         h = te.te_create_csr_dist(D, n_glob, rb, re_, c["rowptr_local"], c["col_local_global"], c["val_local"])
         v0_loc = c["v0"][rb:re_]
+    te.te_set_option(h, te.TE_OPT_KERNELS, args.kernels)
+    if args.prefetch is not None:
+        te.te_set_option(h, te.TE_OPT_PREFETCH, args.prefetch)
     stream = torch.cuda.current_stream(dev)
     d_v0 = torch.from_numpy(np.ascontiguousarray(v0_loc)).to(dev)
     d_out = torch.empty_like(d_v0)
@@ -315,7 +320,8 @@ def run_ours(args):
                    "krylov_steps_per_step": ksteps / args.steps,
                    "restarts_per_step": stats[-1]["n_restarts"],
                    "l2": "inputs larger than L2 (V = %.0f MB > 126 MB)" % (16 * nloc * m / 1e6),
-                   "parallelism": f"rows{ws}"},
+                   "parallelism": f"rows{ws}", "kernels": ["register", "staged"][args.kernels],
+                   "prefetch": args.prefetch},
         "achieved_hbm_gbs": all_bytes / (all_ms * 1e-3) / 1e9 if all_ms > 0 else None,
         "evolved_time_per_s": t * args.steps / (ms * 1e-3),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

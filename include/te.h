@@ -126,7 +126,10 @@ int te_krylov_basis(te_handle* h, const te_c128* v1, int m, double tol_rate, dou
 /* Options (value semantics per option): */
 enum {
   TE_OPT_PROFILE = 1,        /* 1: record CUDA events around every kernel launch (te_get_profile) */
-  TE_OPT_GRAPH = 2           /* 1 (default): replay each restart's launches as a CUDA graph      */
+  TE_OPT_GRAPH = 2,          /* 1 (default): replay each restart's launches as a CUDA graph      */
+  TE_OPT_KERNELS = 3,        /* 0 (default): register-streaming K1/K2; 1: shared-memory staged K1 and
+                                cp.async.bulk (TMA) staged K2 — same arithmetic, kept for comparison */
+  TE_OPT_PREFETCH = 4        /* L2 bulk-prefetch distance (block iterations, 0..16; default 0)     */
 };
 int te_set_option(te_handle* h, int option, double value);
 

@@ -66,6 +66,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// bulk L2 prefetch of a contiguous global range (no registers, no shared memory)
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// prefetch an arbitrary byte range, widened to 16-byte alignment
+__device__ __forceinline__ void prefetch_range(const void* base, size_t begin, size_t end) {
+  if (end <= begin) return;
+  const uintptr_t a = ((uintptr_t)base + begin) & ~(uintptr_t)15;
+  const uintptr_t b = ((uintptr_t)base + end + 15) & ~(uintptr_t)15;
+  prefetch_l2((const void*)a, (unsigned)(b - a));
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -412,12 +423,229 @@ __global__ void __launch_bounds__(kThreads, 1) k_update_proj(KDev d, int j, int 
 }
 
 // --------------------------------------------------------------------------------------
-// K3: sweep-2 update + norm; writes p'' as (unnormalised) column j+1
+// Register-streaming variants (default): a group of TPR lanes owns one row; lane q of the group
+// holds the row's V entries of columns k = q + TPR*c (c < kCPT) in registers, so each V element
+// is read from HBM exactly once per kernel and reused from registers by both the update and the
+// projection phase.  No shared-memory staging and no block-wide barriers inside the row loop.
 // --------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_update_norm(KDev d, int j, int write) {
+constexpr int kCPT = 8;  // columns per lane
+
+// Cross-lane/cross-warp column sums of acc (lanes with equal q = lane % TPR share columns), in
+// a fixed order, then the same last-CTA reduction as finish_columns.
+template <int TPR>
+__device__ __forceinline__ void finish_grouped(const KDev& d, double2 (&acc)[kCPT], int ncols, int ctr,
+                                               double2* out) {
+  __shared__ double2 red[kWarps][kMaxCols];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = lane % TPR;
+#pragma unroll
+  for (int c = 0; c < kCPT; ++c) {
+#pragma unroll
+    for (int off = TPR; off < 32; off <<= 1) {
+      acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, off);
+      acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, off);
+    }
+    const int k = q + TPR * c;
+    if (lane < TPR && k < ncols) red[warp][k] = acc[c];
+  }
+  __syncthreads();
+  if (tid < ncols) {
+    double2 s = red[0][tid];
+    for (int w = 1; w < kWarps; ++w) s = cadd(s, red[w][tid]);
+    d.part[(size_t)blockIdx.x * kMaxCols + tid] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int last;
+  if (tid == 0) last = (atomicAdd(&d.counter[ctr], 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double2 seg[4][kMaxCols];
+  const int c = tid & (kMaxCols - 1), sgi = tid >> 6;
+  const int G = gridDim.x;
+  const int per = (G + 3) / 4;
+  double2 s = make_double2(0.0, 0.0);
+  if (c < ncols) {
+    const int b0 = sgi * per, b1 = min(G, b0 + per);
+    for (int b = b0; b < b1; ++b) s = cadd(s, ld_cg(d.part + (size_t)b * kMaxCols + c));
+  }
+  seg[sgi][c] = s;
+  __syncthreads();
+  if (tid < ncols) {
+    double2 t = seg[0][tid];
+    t = cadd(t, seg[1][tid]);
+    t = cadd(t, seg[2][tid]);
+    t = cadd(t, seg[3][tid]);
+    out[tid] = t;
+  }
+  if (tid == 0) d.counter[ctr] = 0u;
+}
+
+template <int TPR>
+__device__ __forceinline__ double2 group_sum(double2 v) {
+#pragma unroll
+  for (int off = 1; off < TPR; off <<= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, off);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, off);
+  }
+  return v;
+}
+
+// K1 (register variant): CSR-vector SpMV with TPR lanes per row + in-register projections.
+// Rows of the block iteration pf ahead are pulled into L2 with bulk prefetches (V column
+// segments, rowptr, col and val ranges) so the register loads of the current iteration hit L2.
+template <bool CPLX, int TPR>
+__global__ void __launch_bounds__(kThreads, 2) k_spmv_proj_r(KDev d, int j, int pf) {
+  using VT = typename ValT<CPLX>::T;
+  __shared__ double sj_s;
+  const int tid = threadIdx.x, q = tid % TPR, grp = tid / TPR, warp = tid >> 5, lane = tid & 31;
+  constexpr int RPB = kThreads / TPR;
+  if (tid == 0) sj_s = step_gate(d, j, blockIdx.x == 0);
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+  const VT* __restrict__ val = static_cast<const VT*>(d.val);
+  const int32_t* __restrict__ col = d.col;
+  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  const double2* __restrict__ halo = d.halo;
+  const int64_t n = d.n, ldv = d.ldv;
+  const int ncols = j + 1;
+  const int64_t stride = (int64_t)gridDim.x * RPB;
+  // warp 0 prefetches V column segments; warp 1 lane 0 the CSR ranges (rowptr values of the
+  // block iteration pf ahead are loaded one iteration earlier to keep the issue non-blocking)
+  auto pf_v = [&](int64_t rbp) {
+    if (rbp >= n) return;
+    const unsigned bytes = (unsigned)min((int64_t)RPB, n - rbp) * 16u;
+    for (int k = lane; k < ncols; k += 32) prefetch_l2(d.V + rbp + (int64_t)k * ldv, bytes);
+  };
+  auto pf_csr = [&](int64_t rbp, int64_t lo, int64_t hi) {
+    if (rbp >= n) return;
+    const int64_t rows = min((int64_t)RPB, n - rbp);
+    prefetch_range(d.rowptr, (size_t)rbp * 8, (size_t)(rbp + rows + 1) * 8);
+    prefetch_range(col, (size_t)lo * 4, (size_t)hi * 4);
+    prefetch_range(val, (size_t)lo * sizeof(VT), (size_t)hi * sizeof(VT));
+  };
+  int64_t nlo = 0, nhi = 0;  // rowptr bounds of block iteration (it + pf), loaded at it - 1
+  if (pf > 0) {
+    for (int i = 0; i < pf; ++i) {
+      const int64_t rbp = (int64_t)blockIdx.x * RPB + i * stride;
+      if (warp == 0) pf_v(rbp);
+      if (warp == 1 && lane == 0 && rbp < n) {
+        const int64_t lo = __ldg(d.rowptr + rbp), hi = __ldg(d.rowptr + min(rbp + RPB, n));
+        pf_csr(rbp, lo, hi);
+      }
+    }
+    const int64_t rbp = (int64_t)blockIdx.x * RPB + pf * stride;
+    if (warp == 1 && lane == 0 && rbp < n) {
+      nlo = __ldg(d.rowptr + rbp);
+      nhi = __ldg(d.rowptr + min(rbp + RPB, n));
+    }
+  }
+  double2 acc[kCPT];
+#pragma unroll
+  for (int c = 0; c < kCPT; ++c) acc[c] = make_double2(0.0, 0.0);
+  for (int64_t rb = (int64_t)blockIdx.x * RPB; rb < n; rb += stride) {
+    if (pf > 0) {
+      const int64_t rbp = rb + pf * stride;
+      if (warp == 0) pf_v(rbp);
+      if (warp == 1 && lane == 0 && rbp < n) {
+        pf_csr(rbp, nlo, nhi);
+        const int64_t rbn = rbp + stride;
+        if (rbn < n) {
+          nlo = __ldg(d.rowptr + rbn);
+          nhi = __ldg(d.rowptr + min(rbn + RPB, n));
+        }
+      }
+    }
+    const int64_t r = rb + grp;
+    const bool act = r < n;
+    double2 v[kCPT];
+#pragma unroll
+    for (int c = 0; c < kCPT; ++c) {
+      const int k = q + TPR * c;
+      v[c] = (act && k < ncols) ? ld_stream(d.V + r + (int64_t)k * ldv) : make_double2(0.0, 0.0);
+    }
+    double2 sum = make_double2(0.0, 0.0);
+    if (act) {
+      const int64_t lo = __ldg(d.rowptr + r), hi = __ldg(d.rowptr + r + 1);
+      for (int64_t e = lo + q; e < hi; e += TPR) {
+        const int c = __ldg(col + e);
+        const VT w = __ldg(val + e);
+        const double2 xv = (c < n) ? __ldg(x + c) : __ldg(halo + (c - n));
+        sum = cadd(sum, ValT<CPLX>::mul(w, xv));
+      }
+    }
+    sum = group_sum<TPR>(sum);
+    const double2 p = make_double2(sum.x * sj, sum.y * sj);
+    if (act && q == 0) d.W[r] = p;
+#pragma unroll
+    for (int c = 0; c < kCPT; ++c) acc[c] = cfma_conj(v[c], p, acc[c]);
+  }
+  finish_grouped<TPR>(d, acc, ncols, 0, d.g1);
+}
+
+// K2 (register variant): p' = p - V e1 and g2 = V^H p' with the row's V entries in registers
+template <int TPR>
+__global__ void __launch_bounds__(kThreads, 2) k_update_proj_r(KDev d, int j, int pf) {
   __shared__ double2 coef[kMaxCols];
   __shared__ int go_s;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, q = tid % TPR, grp = tid / TPR, warp = tid >> 5, lane = tid & 31;
+  constexpr int RPB = kThreads / TPR;
+  const int ncols = j + 1;
+  if (tid == 0) go_s = (d.flag[0] == 0);
+  if (tid < ncols) {
+    const double sk = d.s[tid];
+    const double2 g = d.g1[tid];
+    coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);
+  }
+  __syncthreads();
+  if (!go_s) return;
+  const int64_t n = d.n, ldv = d.ldv;
+  const int64_t stride = (int64_t)gridDim.x * RPB;
+  auto pf_rows = [&](int64_t rbp) {
+    if (rbp >= n) return;
+    const unsigned bytes = (unsigned)min((int64_t)RPB, n - rbp) * 16u;
+    for (int k = lane; k <= ncols; k += 32)
+      prefetch_l2(k < ncols ? (const void*)(d.V + rbp + (int64_t)k * ldv) : (const void*)(d.W + rbp), bytes);
+  };
+  if (warp == 0)
+    for (int i = 0; i < pf; ++i) pf_rows((int64_t)blockIdx.x * RPB + i * stride);
+  double2 acc[kCPT];
+#pragma unroll
+  for (int c = 0; c < kCPT; ++c) acc[c] = make_double2(0.0, 0.0);
+  for (int64_t rb = (int64_t)blockIdx.x * RPB; rb < n; rb += stride) {
+    if (pf > 0 && warp == 0) pf_rows(rb + pf * stride);
+    const int64_t r = rb + grp;
+    const bool act = r < n;
+    double2 v[kCPT];
+#pragma unroll
+    for (int c = 0; c < kCPT; ++c) {
+      const int k = q + TPR * c;
+      v[c] = (act && k < ncols) ? ld_stream(d.V + r + (int64_t)k * ldv) : make_double2(0.0, 0.0);
+    }
+    const double2 w = act ? __ldcs(d.W + r) : make_double2(0.0, 0.0);
+    double2 a = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < kCPT; ++c) {
+      const int k = q + TPR * c;
+      if (k < ncols) a = cfma(v[c], coef[k], a);
+    }
+    a = group_sum<TPR>(a);
+    const double2 p = make_double2(w.x - a.x, w.y - a.y);
+    if (act && q == 0) d.W[r] = p;
+#pragma unroll
+    for (int c = 0; c < kCPT; ++c) acc[c] = cfma_conj(v[c], p, acc[c]);
+  }
+  finish_grouped<TPR>(d, acc, ncols, 1, d.g2);
+}
+
+// --------------------------------------------------------------------------------------
+// K3: sweep-2 update + norm; writes p'' as (unnormalised) column j+1
+// --------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_update_norm(KDev d, int j, int write, int pf) {
+  __shared__ double2 coef[kMaxCols];
+  __shared__ int go_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ncols = j + 1;
   if (tid == 0) {
     go_s = (d.flag[0] == 0);
@@ -435,8 +663,20 @@ __global__ void __launch_bounds__(kThreads) k_update_norm(KDev d, int j, int wri
   if (!go_s) return;
   const int64_t n = d.n, ldv = d.ldv;
   double2* out = write ? d.V + (int64_t)(j + 1) * ldv : nullptr;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  auto pf_rows = [&](int64_t rbp) {
+    if (rbp >= n) return;
+    const unsigned bytes = (unsigned)min((int64_t)kThreads, n - rbp) * 16u;
+    for (int k = lane; k <= ncols; k += 32)
+      prefetch_l2(k < ncols ? (const void*)(d.V + rbp + (int64_t)k * ldv) : (const void*)(d.W + rbp), bytes);
+  };
+  if (warp == 0)
+    for (int i = 0; i < pf; ++i) pf_rows((int64_t)blockIdx.x * kThreads + i * stride);
   double nrm = 0.0;
-  for (int64_t r = (int64_t)blockIdx.x * kThreads + tid; r < n; r += (int64_t)gridDim.x * kThreads) {
+  for (int64_t rb = (int64_t)blockIdx.x * kThreads; rb < n; rb += stride) {
+    if (pf > 0 && warp == 0) pf_rows(rb + pf * stride);
+    const int64_t r = rb + tid;
+    if (r >= n) continue;
     double2 a = make_double2(0.0, 0.0);
     const double2* Vr = d.V + r;
     int k = 0;
@@ -585,20 +825,58 @@ __global__ void k_csr_check(int64_t n, int64_t ncl, const int64_t* __restrict__ 
     default: { constexpr int NCW = 8; __VA_ARGS__; } break; \
   }
 
-void configure_kernels() {
-  static bool done = false;
-  if (done) return;
-  done = true;
-  auto setk1 = [](auto f) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK1Smem); };
-#define TE_SET(NCW)                                  \
-  setk1(k_spmv_proj<false, NCW>);                    \
-  setk1(k_spmv_proj<true, NCW>);                     \
-  cudaFuncSetAttribute(k_update_proj<NCW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+cudaError_t configure_kernels() {
+  static cudaError_t status = cudaErrorNotReady;
+  if (status != cudaErrorNotReady) return status;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaError_t err = cudaSuccess;
+  auto set = [&](const void* f, size_t want) {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e == cudaSuccess) {
+      const size_t lim = (size_t)optin - a.sharedSizeBytes;
+      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min(want, lim));
+    }
+    if (e != cudaSuccess && err == cudaSuccess) err = e;
+  };
+#define TE_SET(NCW)                                                        \
+  set((const void*)k_spmv_proj<false, NCW>, kK1Smem);                      \
+  set((const void*)k_spmv_proj<true, NCW>, kK1Smem);                       \
+  set((const void*)k_update_proj<NCW>, k2_smem_bytes(kMaxCols, nullptr) + 64 * 1024);
   TE_SET(1) TE_SET(2) TE_SET(3) TE_SET(4) TE_SET(5) TE_SET(6) TE_SET(7) TE_SET(8)
 #undef TE_SET
+  status = err;
+  return status;
 }
 
+static int tpr_for(int ncols, int min_tpr) {
+  int t = min_tpr;
+  while (t * kCPT < ncols) t <<= 1;
+  return t;
+}
+
+#define TE_DISPATCH_TPR(tpr, ...)                               \
+  switch (tpr) {                                               \
+    case 1: { constexpr int TPR = 1; __VA_ARGS__; } break;     \
+    case 2: { constexpr int TPR = 2; __VA_ARGS__; } break;     \
+    case 4: { constexpr int TPR = 4; __VA_ARGS__; } break;     \
+    default: { constexpr int TPR = 8; __VA_ARGS__; } break;    \
+  }
+
 void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L) {
+  if (L.variant == 0) {
+    const int tpr = tpr_for(j + 1, 4);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * L.num_sms, (d.n * tpr + kThreads - 1) / kThreads));
+    TE_DISPATCH_TPR(tpr, {
+      if (cplx)
+        k_spmv_proj_r<true, TPR><<<grid, kThreads, 0, L.stream>>>(d, j, L.prefetch);
+      else
+        k_spmv_proj_r<false, TPR><<<grid, kThreads, 0, L.stream>>>(d, j, L.prefetch);
+    });
+    return;
+  }
   const int ncw = (j + 1 + kWarps - 1) / kWarps;
   TE_DISPATCH_NCW(ncw, {
     if (cplx)
@@ -609,14 +887,22 @@ void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L) {
 }
 
 void launch_update_proj(const KDev& d, int j, const Launch& L) {
+  if (L.variant == 0) {
+    const int tpr = tpr_for(j + 1, 1);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * L.num_sms, (d.n * tpr + kThreads - 1) / kThreads));
+    TE_DISPATCH_TPR(tpr, { k_update_proj_r<TPR><<<grid, kThreads, 0, L.stream>>>(d, j, L.prefetch); });
+    return;
+  }
   int tr = 0;
   const size_t smem = k2_smem_bytes(j + 1, &tr);
+  const int64_t ntiles = (d.n + tr - 1) / tr;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(L.grid_k2, ntiles));
   const int ncw = (j + 1 + kWarps - 1) / kWarps;
-  TE_DISPATCH_NCW(ncw, { k_update_proj<NCW><<<L.grid_k2, kThreads, smem, L.stream>>>(d, j, tr); });
+  TE_DISPATCH_NCW(ncw, { k_update_proj<NCW><<<grid, kThreads, smem, L.stream>>>(d, j, tr); });
 }
 
 void launch_update_norm(const KDev& d, int j, bool write, const Launch& L) {
-  k_update_norm<<<L.grid_k3, kThreads, 0, L.stream>>>(d, j, write ? 1 : 0);
+  k_update_norm<<<L.grid_k3, kThreads, 0, L.stream>>>(d, j, write ? 1 : 0, L.prefetch);
 }
 
 void launch_finalize(const KDev& d, int j, const Launch& L) { k_finalize<<<1, 32, 0, L.stream>>>(d, j); }

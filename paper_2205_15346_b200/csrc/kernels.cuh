@@ -45,6 +45,8 @@ struct Launch {
   cudaStream_t stream;
   int num_sms;
   int grid_k1, grid_k2, grid_k3;
+  int prefetch; // L2 bulk-prefetch distance in block iterations (0: off)
+  int variant;  // 0: register-streaming K1/K2 (default), 1: shared-memory / TMA-bulk staged K1/K2
 };
 
 // hot path (one Krylov step j = 3 launches; see kernels.cu)
@@ -65,6 +67,6 @@ void launch_csr_check(int64_t n, int64_t ncol_limit, const int64_t* rowptr, cons
 void launch_pack(const double2* x, const int32_t* idx, int64_t cnt, double2* out, cudaStream_t st);
 
 size_t k2_smem_bytes(int ncols, int* tile_rows);
-void configure_kernels();  // opt-in shared memory sizes (once per process/device)
+cudaError_t configure_kernels();  // opt-in shared memory sizes (once per process/device)
 
 }  // namespace te

@@ -102,6 +102,8 @@ struct te_handle {
   double2* h_coef = nullptr;  // pinned: omega~
   // profiling / bookkeeping
   bool profile = false;
+  int variant = 0;
+  int prefetch = 0;
   cudaEvent_t ev0[kEvPool], ev1[kEvPool];
   int ev_cls[kEvPool];
   double ev_bytes[kEvPool];
@@ -159,6 +161,8 @@ Launch make_launch(te_handle* h) {
   L.grid_k1 = (int)std::max<int64_t>(1, std::min<int64_t>(2 * h->num_sms, t256));
   L.grid_k2 = h->num_sms;
   L.grid_k3 = (int)std::max<int64_t>(1, std::min<int64_t>(8 * h->num_sms, t256));
+  L.variant = h->variant;
+  L.prefetch = h->prefetch;
   return L;
 }
 
@@ -466,7 +470,7 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
   if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(TE_ERR_CUDA, "cudaStreamCreate");
   h->stream = h->own_stream;
-  te::configure_kernels();
+  if (te::configure_kernels() != cudaSuccess) return fail(TE_ERR_CUDA, "kernel shared-memory configuration failed");
   const size_t vb = cplx ? 16 : 8;
   if (cudaMalloc(&h->d_rowptr, sizeof(int64_t) * (n + 1)) != cudaSuccess) return fail(TE_ERR_OOM, "rowptr alloc");
   if (cudaMalloc(&h->d_col, sizeof(int32_t) * std::max<int64_t>(1, h->nnz)) != cudaSuccess)
@@ -653,6 +657,14 @@ int te_set_option(te_handle* h, int option, double value) {
       return TE_OK;
     case TE_OPT_GRAPH:
       return TE_OK;  // launches are issued directly (graph replay: see DESIGN.md next steps)
+    case TE_OPT_KERNELS:
+      if (value != 0.0 && value != 1.0) return set_err(TE_ERR_ARG, "TE_OPT_KERNELS must be 0 or 1");
+      h->variant = (int)value;
+      return TE_OK;
+    case TE_OPT_PREFETCH:
+      if (value < 0 || value > 16) return set_err(TE_ERR_ARG, "TE_OPT_PREFETCH must be in [0, 16]");
+      h->prefetch = (int)value;
+      return TE_OK;
     default:
       return set_err(TE_ERR_ARG, "unknown option %d", option);
   }

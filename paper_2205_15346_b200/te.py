@@ -24,6 +24,8 @@ TE_WARN_ROUNDOFF = 1
 TE_WARN_QUADRATURE = 2
 TE_OPT_PROFILE = 1
 TE_OPT_GRAPH = 2
+TE_OPT_KERNELS = 3
+TE_OPT_PREFETCH = 4
 KERNELS = {0: "spmv_proj", 1: "update_proj", 2: "update_norm", 3: "combine", 4: "halo_pack"}
 
 

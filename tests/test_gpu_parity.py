@@ -35,10 +35,12 @@ def small_cases():
 CASES = small_cases()
 
 
+@pytest.mark.parametrize("variant", [0, 1], ids=["register", "staged"])
 @pytest.mark.parametrize("name,c", CASES, ids=[x[0] for x in CASES])
-def test_krylov_basis_matches_oracle(gpu_lib, name, c):
+def test_krylov_basis_matches_oracle(gpu_lib, name, c, variant):
     te = gpu_lib
     h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    te.te_set_option(h, te.TE_OPT_KERNELS, variant)
     m = min(c["m"], c["n"])
     tol_rate = c["tol"] / c["t"]
     g = te.te_krylov_basis(h, c["v0"], m, tol_rate, want_V=True)
@@ -70,8 +72,12 @@ def test_evolve_forced_and_adaptive(gpu_lib, name, c):
     ref = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], t, tol, m, schedule=[s[0] for s in sched])
     assert np.linalg.norm(v - ref["v"]) <= 1e-10
     assert [s[1] for s in ref["schedule"]] == [s[1] for s in sched]
+    # per-step bounds agree within the quadrature's own tolerance (rel. 1e-3) plus the
+    # absolute floor of the integrand: f = h |sum_k c_k e^{-i lam_k tau}| is a small matrix
+    # element formed with cancellation, accurate to ~ h m eps absolute (h <= ||H||_1)
     for (tg, _, eg), (to, _, eo) in zip(sched, ref["schedule"]):
-        assert abs(eg - eo) <= 1e-6 * max(eo, 1e-300) + 1e-300
+        floor = 10.0 * tg * st["one_norm"] * m * 2.0 ** -52
+        assert abs(eg - eo) <= 1e-3 * eo + floor
     # adaptive vs adaptive -> tol + 1e-12
     ada = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], t, tol, m)
     assert np.linalg.norm(v - ada["v"]) <= tol + 1e-12
