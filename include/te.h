@@ -127,15 +127,17 @@ int te_krylov_basis(te_handle* h, const te_c128* v1, int m, double tol_rate, dou
 enum {
   TE_OPT_PROFILE = 1,        /* 1: record CUDA events around every kernel launch (te_get_profile) */
   TE_OPT_GRAPH = 2,          /* 1 (default): replay each restart's launches as a CUDA graph      */
-  TE_OPT_KERNELS = 3,        /* 0 (default): register-streaming K1/K2; 1: shared-memory staged K1 and
-                                cp.async.bulk (TMA) staged K2 — same arithmetic, kept for comparison */
+  TE_OPT_KERNELS = 3,        /* 2 (default): standalone SpMV + TMA-tiled (2-D tensor boxes) warp-
+                                specialised projection kernels; 0: register-streaming fused K1/K2;
+                                1: shared-memory staged K1 + bulk-copy staged K2 — same arithmetic */
   TE_OPT_PREFETCH = 4        /* L2 bulk-prefetch distance (block iterations, 0..16; default 0)     */
 };
 int te_set_option(te_handle* h, int option, double value);
 
 /* Per-kernel-class profile accumulated while TE_OPT_PROFILE is on (reset by te_set_option):
- * kernel: 0 spmv_proj (K1), 1 update_proj (K2), 2 update_norm (K3), 3 combine V.omega (K4),
- * 4 halo pack (distributed).  launches, total device milliseconds (CUDA events on the
+ * kernel: 0 spmv (K1a; fused spmv_proj K1 in variants 0/1), 1 update_proj (K2), 2 update_norm (K3),
+ * 3 combine V.omega (K4), 4 halo pack (distributed), 5 proj_dots (K1b, variant 2), 6 host step
+ * search (eigensolve + quadrature + omega; wall-clock ms, alg_bytes 0).  launches, total device milliseconds (CUDA events on the
  * launching stream) and algorithmic bytes. */
 typedef struct { int64_t launches; double total_ms; double alg_bytes; } te_kernel_profile;
 int te_get_profile(const te_handle* h, int kernel, te_kernel_profile* out);
@@ -145,6 +147,10 @@ int64_t te_launch_count(const te_handle* h);
 
 /* ||H||_1 of the handle's matrix (global for distributed handles). */
 double te_one_norm(const te_handle* h);
+
+/* Diagnostics: compiled attributes of a hot-path kernel (which: 0 spmv, 1 proj_dots, 2 update_proj
+ * (TMA), 3 update_norm, 4 spmv_proj (register), 5 update_proj (register)). */
+int te_kernel_attributes(int which, int* regs, int* max_threads, int* static_smem, int* max_dyn_smem);
 
 /* Thread-local status / message of the last failing call (TE_OK / "" if none). */
 int te_last_status(void);

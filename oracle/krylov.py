@@ -179,7 +179,7 @@ def integrand(lam, U, h, tau):
     return h * np.abs(s)
 
 
-def tanh_sinh(f, a, b, rel=QUAD_REL, max_levels=QUAD_MAX_LEVELS, umax=QUAD_UMAX):
+def tanh_sinh(f, a, b, rel=QUAD_REL, max_levels=QUAD_MAX_LEVELS, umax=QUAD_UMAX, floor=0.0):
     """Adaptive tanh-sinh quadrature of f on [a, b].
 
     Textbook Takahasi-Mori form (reading O-5):
@@ -188,7 +188,12 @@ def tanh_sinh(f, a, b, rel=QUAD_REL, max_levels=QUAD_MAX_LEVELS, umax=QUAD_UMAX)
       w(u) = (b-a)/2 (pi/2) cosh u / cosh^2(pi/2 sinh u)
       I_k  = 2^-k sum_{|j 2^-k| <= umax} w(u_j) f(x(u_j)),  u_j = j 2^-k
     Level k adds the odd j.  Stop when I_k == 0, or k >= 2 and
-    |I_k - I_{k-1}| <= rel |I_k|.  Returns (I, converged).
+    |I_k - I_{k-1}| <= rel max(|I_k|, floor).  Returns (I, converged).
+
+    ``floor`` (reading O-5a): the step search passes tol_rate (b - a), the
+    size below which a piece of the error integral cannot change any decision
+    e <= tol_rate tau; without it, integrands at the roundoff floor (tiny tau,
+    f ~ h m eps noise) only converge after ~13 refinements.
     """
     if b == a:
         return 0.0, True
@@ -218,7 +223,7 @@ def tanh_sinh(f, a, b, rel=QUAD_REL, max_levels=QUAD_MAX_LEVELS, umax=QUAD_UMAX)
         cur = total * 2.0 ** -k
         if cur == 0.0:
             return cur, True
-        if k >= 2 and abs(cur - prev) <= rel * abs(cur):
+        if k >= 2 and abs(cur - prev) <= rel * max(abs(cur), floor):
             return cur, True
         prev = cur
     return cur, False
@@ -321,7 +326,7 @@ def evolve(rowptr, col, val, v0, t, tol, m, ortho="cgs2", schedule=None,
             return integrand(lam, U, h, tau)
 
         def integral(a, b):
-            v, conv = tanh_sinh(f, a, b)
+            v, conv = tanh_sinh(f, a, b, floor=tol_rate * (b - a))
             if not conv:
                 quad_ok[0] = False
             return v

@@ -94,36 +94,34 @@ struct Level {
   std::vector<double> d, w;
   std::vector<signed char> side;
 };
-std::vector<Level> g_levels;
-std::once_flag g_once;
+Level g_levels[kMaxLevels + 1];
+std::once_flag g_once[kMaxLevels + 1];
 
-void build_levels() {
-  g_levels.resize(kMaxLevels + 1);
+// level tables are built lazily (level 15 alone has 7 * 2^14 nodes)
+void build_level(int k) {
   const double half_pi = 0.5 * M_PI;
-  for (int k = 0; k <= kMaxLevels; ++k) {
-    const double step = std::ldexp(1.0, -k);
-    const long jmax = (long)std::floor(kUmax / step);
-    Level& L = g_levels[k];
-    for (long j = -jmax; j <= jmax; ++j) {
-      if (k > 0 && (j % 2 == 0)) continue;
-      const double u = (double)j * step;
-      const double s = half_pi * std::sinh(u);
-      const double cs = std::cosh(s);
-      L.d.push_back(2.0 / (1.0 + std::exp(2.0 * std::fabs(s))));
-      L.w.push_back(half_pi * std::cosh(u) / (cs * cs));
-      L.side.push_back(u < 0 ? -1 : (u > 0 ? 1 : 0));
-    }
+  const double step = std::ldexp(1.0, -k);
+  const long jmax = (long)std::floor(kUmax / step);
+  Level& L = g_levels[k];
+  for (long j = -jmax; j <= jmax; ++j) {
+    if (k > 0 && (j % 2 == 0)) continue;
+    const double u = (double)j * step;
+    const double s = half_pi * std::sinh(u);
+    const double cs = std::cosh(s);
+    L.d.push_back(2.0 / (1.0 + std::exp(2.0 * std::fabs(s))));
+    L.w.push_back(half_pi * std::cosh(u) / (cs * cs));
+    L.side.push_back(u < 0 ? -1 : (u > 0 ? 1 : 0));
   }
 }
 }  // namespace
 
-QuadResult tanh_sinh(const SmallEig& e, double a, double b, double rel, int max_levels) {
+QuadResult tanh_sinh(const SmallEig& e, double a, double b, double floor, double rel, int max_levels) {
   if (b == a) return {0.0, true};
-  std::call_once(g_once, build_levels);
   const double c = 0.5 * (a + b), hw = 0.5 * (b - a);
   double total = 0.0, prev = 0.0, cur = 0.0;
   if (max_levels > kMaxLevels) max_levels = kMaxLevels;
   for (int k = 0; k <= max_levels; ++k) {
+    std::call_once(g_once[k], build_level, k);
     const Level& L = g_levels[k];
     double s = 0.0;
     for (size_t q = 0; q < L.d.size(); ++q) {
@@ -133,7 +131,7 @@ QuadResult tanh_sinh(const SmallEig& e, double a, double b, double rel, int max_
     total += s;
     cur = total * std::ldexp(1.0, -k);
     if (cur == 0.0) return {cur, true};
-    if (k >= 2 && std::fabs(cur - prev) <= rel * std::fabs(cur)) return {cur, true};
+    if (k >= 2 && std::fabs(cur - prev) <= rel * std::fmax(std::fabs(cur), floor)) return {cur, true};
     prev = cur;
   }
   return {cur, false};
@@ -146,7 +144,7 @@ StepResult find_step(const SmallEig& e, bool breakdown, bool first, double tau_p
                      double tol_rate, double t_total) {
   bool qok = true;
   auto I = [&](double lo, double hi) {
-    QuadResult r = tanh_sinh(e, lo, hi);
+    QuadResult r = tanh_sinh(e, lo, hi, tol_rate * (hi - lo));
     if (!r.converged) qok = false;
     return r.value;
   };

@@ -25,11 +25,12 @@ double integrand(const SmallEig& e, double tau);
 
 struct QuadResult { double value; bool converged; };
 // tanh-sinh on [a,b]: level k uses u_j = j 2^-k, |u_j| <= 3.5; stop when I_k == 0 or
-// (k >= 2 and |I_k - I_{k-1}| <= rel |I_k|); at most 15 refinements.
-QuadResult tanh_sinh(const SmallEig& e, double a, double b, double rel = 1e-3, int max_levels = 15);
+// (k >= 2 and |I_k - I_{k-1}| <= rel max(|I_k|, floor)); at most 15 refinements.
+// floor = tol_rate (b - a) in the step search (reading O-5a).
+QuadResult tanh_sinh(const SmallEig& e, double a, double b, double floor, double rel = 1e-3, int max_levels = 15);
 
 struct StepResult { double tau, err; bool quad_ok; bool collapse; };
-// Largest admissible step: e <= tol_rate * tau (reading O-6).
+// Largest admissible step: e <= tol_rate * tau (reading O-6); integrals use floor tol_rate (b-a).
 StepResult find_step(const SmallEig& e, bool breakdown, bool first, double tau_prev, double rem,
                      double tol_rate, double t_total);
 

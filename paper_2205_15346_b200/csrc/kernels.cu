@@ -15,6 +15,7 @@
 // No floating-point atomics anywhere.
 #include "kernels.cuh"
 
+#include <cuda.h>
 #include <cstdio>
 
 namespace te {
@@ -640,6 +641,306 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_proj_r(KDev d, int j, in
 }
 
 // --------------------------------------------------------------------------------------
+// TMA-tiled projection kernel (default path), warp-specialised:
+//   warp S (producer, one elected lane) streams 32-row x ncols tiles of V with ONE 2-D TMA
+//   tensor load per tile (cp.async.bulk.tensor.2d; box = 64 doubles x ncols columns) plus the
+//   32-row slice of W (cp.async.bulk), into S shared-memory slots guarded by full/empty
+//   mbarriers;  consumer warp w owns slot w and every S-th tile of its CTA, with no CTA-wide
+//   barrier inside the loop.
+//   MODE 0 (sweep-1):  g1 = V^H p            (dots only)
+//   MODE 1 (sweep-2):  p' = p - V e1 -> W,  g2 = V^H p'   (update + dots on the same tile)
+// Lane = row for the update; the 32x32 column sums of a tile are formed by a butterfly
+// transpose-reduction (31 shuffles per 32 columns instead of 32 x 5), after which lane k owns
+// column k and accumulates it across tiles in one register pair.
+// --------------------------------------------------------------------------------------
+constexpr int kTileR = 32;          // rows per TMA tile
+constexpr int kMaxSlots = 7;  // 7 consumer warps + 1 producer warp = 256 threads
+constexpr int kProjThreads = (kMaxSlots + 1) * 32;
+constexpr size_t kProjSmemBudget = 200 * 1024;
+
+int proj_slots(int ncols) {
+  const size_t slot = (size_t)ncols * kTileR * 16 + kTileR * 16;
+  int s = (int)(kProjSmemBudget / slot);
+  return s > kMaxSlots ? kMaxSlots : (s < 1 ? 1 : s);
+}
+size_t proj_smem_bytes(int ncols) {
+  const size_t slot = (size_t)ncols * kTileR * 16 + kTileR * 16;
+  return (size_t)proj_slots(ncols) * slot + 1024;  // + alignment slack
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// re[c], im[c] (c < 32) per lane -> returns the sum over the 32 lanes of column c = lane
+__device__ __forceinline__ double2 butterfly_colsum(double (&re)[32], double (&im)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double sr = up ? re[i] : re[i + s];
+      const double si = up ? im[i] : im[i + s];
+      const double kr = up ? re[i + s] : re[i];
+      const double ki = up ? im[i + s] : im[i];
+      re[i] = kr + __shfl_xor_sync(0xffffffffu, sr, s);
+      im[i] = ki + __shfl_xor_sync(0xffffffffu, si, s);
+    }
+  }
+  return make_double2(re[0], im[0]);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kProjThreads, 1)
+    k_proj_tma(const __grid_constant__ CUtensorMap tmV, KDev d, int j, int S) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[kMaxSlots], empty[kMaxSlots];
+  __shared__ double2 coef[kMaxCols];
+  __shared__ double2 red[kMaxSlots][kMaxCols];
+  __shared__ int go_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ncols = j + 1;
+  if (tid == 0) go_s = (d.flag[0] == 0);
+  if (MODE == 1 && tid < ncols) {
+    const double sk = d.s[tid];
+    const double2 g = d.g1[tid];
+    coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);   // e1_k = s_k c1_k
+  }
+  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const size_t vbytes = (size_t)ncols * kTileR * 16;
+  const size_t slot_bytes = vbytes + kTileR * 16;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (!go_s) return;
+  const int64_t n = d.n;
+  const int64_t ntiles = (n + kTileR - 1) / kTileR;
+  const double2* srcW = d.W;
+
+  if (warp == S) {  // ---------------- producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
+      for (int64_t i = 0;; ++i) {
+        const int64_t tile = blockIdx.x + i * gridDim.x;
+        if (tile >= ntiles) break;
+        const int s = (int)(i % S);
+        const int64_t round = i / S;
+        if (round > 0) mbar_wait(&empty[s], (unsigned)((round - 1) & 1));
+        const int rows = (int)min((int64_t)kTileR, n - tile * kTileR);
+        unsigned char* base = smem + (size_t)s * slot_bytes;
+        mbar_expect_tx(&full[s], (unsigned)vbytes + (unsigned)rows * 16u);
+        tma_load_2d(base, &tmV, (int)(tile * kTileR * 2), 0, &full[s]);
+        bulk_g2s(base + vbytes, srcW + tile * kTileR, (unsigned)rows * 16u, &full[s], policy_evict_first());
+      }
+    }
+  } else if (warp < S) {  // ------- consumers
+    double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+    for (int64_t i = warp;; i += S) {
+      const int64_t tile = blockIdx.x + i * gridDim.x;
+      if (tile >= ntiles) break;
+      const int s = warp;
+      mbar_wait(&full[s], (unsigned)((i / S) & 1));
+      const double2* Vs = reinterpret_cast<const double2*>(smem + (size_t)s * slot_bytes);
+      const double2* Ws = reinterpret_cast<const double2*>(smem + (size_t)s * slot_bytes + vbytes);
+      const int64_t r0 = tile * kTileR;
+      const int rows = (int)min((int64_t)kTileR, n - r0);
+      double2 p = lane < rows ? Ws[lane] : make_double2(0.0, 0.0);
+      if (MODE == 1) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int k = 0; k < ncols; ++k) a = cfma(Vs[k * kTileR + lane], coef[k], a);
+        p = make_double2(p.x - a.x, p.y - a.y);
+        if (lane >= rows) p = make_double2(0.0, 0.0);
+        if (lane < rows) d.W[r0 + lane] = p;
+      }
+      // column sums of conj(V) p over the tile's 32 rows
+      for (int cb = 0; cb < ncols; cb += 32) {
+        double re[32], im[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int k = cb + c;
+          const double2 v = k < ncols ? Vs[k * kTileR + lane] : make_double2(0.0, 0.0);
+          re[c] = v.x * p.x + v.y * p.y;   // conj(v) * p
+          im[c] = v.x * p.y - v.y * p.x;
+        }
+        const double2 cs = butterfly_colsum(re, im);
+        if (cb == 0) acc0 = cadd(acc0, cs); else acc1 = cadd(acc1, cs);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    red[warp][lane] = acc0;
+    red[warp][lane + 32] = acc1;
+  }
+  __syncthreads();
+  // block partial in fixed warp order, then the last-CTA reduction
+  double2* out = MODE == 0 ? d.g1 : d.g2;
+  const int ctr = MODE;
+  if (tid < ncols) {
+    double2 t = red[0][tid];
+    for (int w = 1; w < S; ++w) t = cadd(t, red[w][tid]);
+    d.part[(size_t)blockIdx.x * kMaxCols + tid] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int last;
+  if (tid == 0) last = (atomicAdd(&d.counter[ctr], 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double2 seg[4][kMaxCols];
+  const int G = gridDim.x;
+  const int per = (G + 3) / 4;
+  if (tid < 256) {
+    const int c = tid & (kMaxCols - 1), sgi = tid >> 6;
+    double2 sm = make_double2(0.0, 0.0);
+    if (c < ncols) {
+      const int b0 = sgi * per, b1 = min(G, b0 + per);
+      for (int b = b0; b < b1; ++b) sm = cadd(sm, ld_cg(d.part + (size_t)b * kMaxCols + c));
+    }
+    seg[sgi][c] = sm;
+  }
+  __syncthreads();
+  if (tid < ncols) {
+    double2 t = seg[0][tid];
+    t = cadd(t, seg[1][tid]);
+    t = cadd(t, seg[2][tid]);
+    t = cadd(t, seg[3][tid]);
+    out[tid] = t;
+  }
+  if (tid == 0) d.counter[ctr] = 0u;
+}
+
+// Standalone SpMV, nnz-balanced tiles (default): tile t covers rows [tile_row[t], tile_row[t+1])
+// holding ~kSpmvTileNnz entries (built at create time).  Each thread issues all kSpmvE col/val
+// loads of a chunk at once, then all x gathers, products go to shared memory, and one thread
+// per row sums its entries left to right (deterministic).  3 dependent latencies per chunk.
+constexpr int kSpmvE = 4;
+constexpr int kChunk = kThreads * kSpmvE;  // 1024 entries per chunk
+template <bool CPLX>
+__global__ void __launch_bounds__(kThreads, 4) k_spmv_tile(KDev d, int j) {
+  using VT = typename ValT<CPLX>::T;
+  __shared__ double2 prod[kChunk];
+  __shared__ int64_t rps[kSpmvMaxTileRows + 1];
+  __shared__ double sj_s;
+  const int tid = threadIdx.x;
+  if (tid == 0) sj_s = step_gate(d, j, blockIdx.x == 0);
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+  const VT* __restrict__ val = static_cast<const VT*>(d.val);
+  const int32_t* __restrict__ col = d.col;
+  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  const double2* __restrict__ halo = d.halo;
+  const int64_t n = d.n;
+  constexpr int RPT = kSpmvMaxTileRows / kThreads;  // rows per thread (max)
+  for (int64_t t = blockIdx.x; t < d.ntiles; t += gridDim.x) {
+    const int64_t ra = __ldg(d.tile_row + t), rb = __ldg(d.tile_row + t + 1);
+    const int rows = (int)(rb - ra);
+    for (int i = tid; i <= rows; i += kThreads) rps[i] = __ldg(d.rowptr + ra + i);
+    __syncthreads();
+    const int64_t b = rps[0], e = rps[rows];
+    double2 acc[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) acc[u] = make_double2(0.0, 0.0);
+    for (int64_t cb = b; cb < e; cb += kChunk) {
+      const int cnt = (int)min((int64_t)kChunk, e - cb);
+      int cc[kSpmvE];
+      VT vv[kSpmvE];
+#pragma unroll
+      for (int u = 0; u < kSpmvE; ++u) {
+        const int q = tid + u * kThreads;
+        if (q < cnt) {
+          cc[u] = __ldg(col + cb + q);
+          vv[u] = __ldg(val + cb + q);
+        }
+      }
+      double2 xx[kSpmvE];
+#pragma unroll
+      for (int u = 0; u < kSpmvE; ++u) {
+        const int q = tid + u * kThreads;
+        if (q < cnt) xx[u] = (cc[u] < n) ? __ldg(x + cc[u]) : __ldg(halo + (cc[u] - n));
+      }
+#pragma unroll
+      for (int u = 0; u < kSpmvE; ++u) {
+        const int q = tid + u * kThreads;
+        if (q < cnt) prod[q] = ValT<CPLX>::mul(vv[u], xx[u]);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int i = tid + u * kThreads;
+        if (i < rows) {
+          const int64_t lo = max(rps[i], cb), hi = min(rps[i + 1], cb + cnt);
+          for (int64_t q = lo; q < hi; ++q) acc[u] = cadd(acc[u], prod[q - cb]);
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int i = tid + u * kThreads;
+      if (i < rows) __stcs(d.W + ra + i, make_double2(acc[u].x * sj, acc[u].y * sj));
+    }
+    __syncthreads();
+  }
+}
+
+// Standalone SpMV p = s_j H V_j -> W (CSR-vector, TPR lanes per row, high occupancy).
+template <bool CPLX, int TPR>
+__global__ void __launch_bounds__(kThreads) k_spmv(KDev d, int j) {
+  using VT = typename ValT<CPLX>::T;
+  __shared__ double sj_s;
+  const int tid = threadIdx.x, q = tid % TPR, grp = tid / TPR;
+  constexpr int RPB = kThreads / TPR;
+  if (tid == 0) sj_s = step_gate(d, j, blockIdx.x == 0);
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+  const VT* __restrict__ val = static_cast<const VT*>(d.val);
+  const int32_t* __restrict__ col = d.col;
+  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  const double2* __restrict__ halo = d.halo;
+  const int64_t n = d.n;
+  for (int64_t rb = (int64_t)blockIdx.x * RPB; rb < n; rb += (int64_t)gridDim.x * RPB) {
+    const int64_t r = rb + grp;
+    double2 sum = make_double2(0.0, 0.0);
+    if (r < n) {
+      const int64_t lo = __ldg(d.rowptr + r), hi = __ldg(d.rowptr + r + 1);
+      int64_t e = lo + q;
+      for (; e + TPR < hi; e += 2 * TPR) {  // two entries in flight per lane
+        const int c0 = __ldg(col + e), c1 = __ldg(col + e + TPR);
+        const VT w0 = __ldg(val + e), w1 = __ldg(val + e + TPR);
+        const double2 x0 = (c0 < n) ? __ldg(x + c0) : __ldg(halo + (c0 - n));
+        const double2 x1 = (c1 < n) ? __ldg(x + c1) : __ldg(halo + (c1 - n));
+        sum = cadd(sum, ValT<CPLX>::mul(w0, x0));
+        sum = cadd(sum, ValT<CPLX>::mul(w1, x1));
+      }
+      if (e < hi) {
+        const int c0 = __ldg(col + e);
+        const VT w0 = __ldg(val + e);
+        const double2 x0 = (c0 < n) ? __ldg(x + c0) : __ldg(halo + (c0 - n));
+        sum = cadd(sum, ValT<CPLX>::mul(w0, x0));
+      }
+    }
+    sum = group_sum<TPR>(sum);
+    if (r < n && q == 0) __stcs(d.W + r, make_double2(sum.x * sj, sum.y * sj));
+  }
+}
+
+// --------------------------------------------------------------------------------------
 // K3: sweep-2 update + norm; writes p'' as (unnormalised) column j+1
 // --------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_update_norm(KDev d, int j, int write, int pf) {
@@ -825,6 +1126,26 @@ __global__ void k_csr_check(int64_t n, int64_t ncl, const int64_t* __restrict__ 
     default: { constexpr int NCW = 8; __VA_ARGS__; } break; \
   }
 
+int kernel_attributes(int which, int* regs, int* max_threads, int* static_smem, int* max_dyn_smem) {
+  const void* f = nullptr;
+  switch (which) {
+    case 0: f = (const void*)k_spmv_tile<false>; break;
+    case 1: f = (const void*)k_proj_tma<0>; break;
+    case 2: f = (const void*)k_proj_tma<1>; break;
+    case 3: f = (const void*)k_update_norm; break;
+    case 4: f = (const void*)k_spmv_proj_r<false, 4>; break;
+    case 5: f = (const void*)k_update_proj_r<8>; break;
+    default: return -1;
+  }
+  cudaFuncAttributes a;
+  if (cudaFuncGetAttributes(&a, f) != cudaSuccess) return -2;
+  *regs = a.numRegs;
+  *max_threads = a.maxThreadsPerBlock;
+  *static_smem = (int)a.sharedSizeBytes;
+  *max_dyn_smem = a.maxDynamicSharedSizeBytes;
+  return 0;
+}
+
 cudaError_t configure_kernels() {
   static cudaError_t status = cudaErrorNotReady;
   if (status != cudaErrorNotReady) return status;
@@ -847,6 +1168,8 @@ cudaError_t configure_kernels() {
   set((const void*)k_update_proj<NCW>, k2_smem_bytes(kMaxCols, nullptr) + 64 * 1024);
   TE_SET(1) TE_SET(2) TE_SET(3) TE_SET(4) TE_SET(5) TE_SET(6) TE_SET(7) TE_SET(8)
 #undef TE_SET
+  set((const void*)k_proj_tma<0>, kProjSmemBudget + 1024);
+  set((const void*)k_proj_tma<1>, kProjSmemBudget + 1024);
   status = err;
   return status;
 }
@@ -865,8 +1188,40 @@ static int tpr_for(int ncols, int min_tpr) {
     default: { constexpr int TPR = 8; __VA_ARGS__; } break;    \
   }
 
+void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
+  if (L.spmv_tiled && d.ntiles > 0) {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(8 * L.num_sms, d.ntiles));
+    if (cplx) k_spmv_tile<true><<<grid, kThreads, 0, L.stream>>>(d, j);
+    else k_spmv_tile<false><<<grid, kThreads, 0, L.stream>>>(d, j);
+    return;
+  }
+  const int tpr = L.spmv_tpr;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(8 * L.num_sms, (d.n * tpr + kThreads - 1) / kThreads));
+    switch (tpr) {
+#define TE_SPMV(T)                                                                      \
+  case T:                                                                               \
+    if (cplx) k_spmv<true, T><<<grid, kThreads, 0, L.stream>>>(d, j);                   \
+    else k_spmv<false, T><<<grid, kThreads, 0, L.stream>>>(d, j);                       \
+    break;
+      TE_SPMV(1) TE_SPMV(2) TE_SPMV(4) TE_SPMV(8) TE_SPMV(16)
+      default: TE_SPMV(32)
+#undef TE_SPMV
+    }
+}
+
+void launch_proj_dots(const KDev& d, int j, const Launch& L) {
+  const int S = proj_slots(j + 1);
+  k_proj_tma<0><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S);
+}
+
 void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L) {
+  if (L.variant == 2) {
+    launch_spmv(d, cplx, j, L);
+    launch_proj_dots(d, j, L);
+    return;
+  }
   if (L.variant == 0) {
+
     const int tpr = tpr_for(j + 1, 4);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * L.num_sms, (d.n * tpr + kThreads - 1) / kThreads));
     TE_DISPATCH_TPR(tpr, {
@@ -887,6 +1242,11 @@ void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L) {
 }
 
 void launch_update_proj(const KDev& d, int j, const Launch& L) {
+  if (L.variant == 2) {
+    const int S = proj_slots(j + 1);
+    k_proj_tma<1><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S);
+    return;
+  }
   if (L.variant == 0) {
     const int tpr = tpr_for(j + 1, 1);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * L.num_sms, (d.n * tpr + kThreads - 1) / kThreads));

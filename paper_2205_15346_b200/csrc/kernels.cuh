@@ -8,6 +8,7 @@
 //         refer to the halo buffer in distributed handles), val double or double2.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace te {
@@ -17,6 +18,8 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMaxCols = 64;         // TE_M_MAX
 constexpr int kSpmvRows = 256;       // K1 row tile
 constexpr int kSpmvChunk = 4096;     // K1 products staged in shared memory per chunk
+constexpr int kSpmvTileNnz = 1024;   // nominal entries per nnz-balanced SpMV tile
+constexpr int kSpmvMaxTileRows = 512;   // rows per SpMV tile cap
 
 struct KDev {
   int64_t n;            // local rows
@@ -26,6 +29,8 @@ struct KDev {
   const int64_t* rowptr;
   const int32_t* col;
   const void* val;
+  const int64_t* tile_row;  // [ntiles+1] first row of each nnz-balanced SpMV tile
+  int64_t ntiles;
   const double2* halo;  // x entries for columns >= n (distributed); nullptr otherwise
   double* s;            // [m_cap+1] column scales
   double* alpha;        // [m_cap]
@@ -45,12 +50,18 @@ struct Launch {
   cudaStream_t stream;
   int num_sms;
   int grid_k1, grid_k2, grid_k3;
+  const CUtensorMap* tmaps;  // [kMaxCols] 2-D maps of V, box = 64 doubles x (k+1) columns
+  int spmv_tpr;  // lanes per row of the standalone CSR-vector SpMV
+  int spmv_tiled; // 1: nnz-balanced tiled SpMV (default), 0: CSR-vector
   int prefetch; // L2 bulk-prefetch distance in block iterations (0: off)
-  int variant;  // 0: register-streaming K1/K2 (default), 1: shared-memory / TMA-bulk staged K1/K2
+  int variant;  // 2: SpMV + TMA-tiled projections (default); 0: register-streaming K1/K2;
+                //    1: shared-memory / bulk-copy staged K1/K2
 };
 
 // hot path (one Krylov step j = 3 launches; see kernels.cu)
-void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L);   // K1
+void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L);   // K1 (variants 0/1; variant 2 = K1a+K1b)
+void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L);        // K1a: SpMV only
+void launch_proj_dots(const KDev& d, int j, const Launch& L);              // K1b: g1 = V^H p (TMA)
 void launch_update_proj(const KDev& d, int j, const Launch& L);            // K2
 void launch_update_norm(const KDev& d, int j, bool write, const Launch& L);// K3
 void launch_finalize(const KDev& d, int j, const Launch& L);               // beta_{m-1}
@@ -67,6 +78,9 @@ void launch_csr_check(int64_t n, int64_t ncol_limit, const int64_t* rowptr, cons
 void launch_pack(const double2* x, const int32_t* idx, int64_t cnt, double2* out, cudaStream_t st);
 
 size_t k2_smem_bytes(int ncols, int* tile_rows);
-cudaError_t configure_kernels();  // opt-in shared memory sizes (once per process/device)
+int proj_slots(int ncols);
+size_t proj_smem_bytes(int ncols);
+cudaError_t configure_kernels();
+int kernel_attributes(int which, int* regs, int* max_threads, int* static_smem, int* max_dyn_smem);  // opt-in shared memory sizes (once per process/device)
 
 }  // namespace te

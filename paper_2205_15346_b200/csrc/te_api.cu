@@ -18,6 +18,9 @@
 #include "kernels.cuh"
 #include "nccl_shim.h"
 
+#include <chrono>
+#include <cudaTypedefs.h>
+
 using te::KDev;
 using te::Launch;
 
@@ -66,7 +69,7 @@ struct te_dist {
 };
 
 namespace {
-constexpr int kProfKernels = 5;
+constexpr int kProfKernels = 7;  // 0 spmv(_proj) 1 update_proj 2 update_norm 3 combine 4 halo 5 proj_dots 6 host
 constexpr int kEvPool = 3 * te::kMaxCols + 16;
 struct Sched {
   double tau;
@@ -102,7 +105,12 @@ struct te_handle {
   double2* h_coef = nullptr;  // pinned: omega~
   // profiling / bookkeeping
   bool profile = false;
-  int variant = 0;
+  int variant = 2;
+  int spmv_tpr = 4;
+  int spmv_tiled = 1;
+  int64_t* d_tile_row = nullptr;
+  int64_t ntiles = 0;
+  std::vector<CUtensorMap> tmaps;
   int prefetch = 0;
   cudaEvent_t ev0[kEvPool], ev1[kEvPool];
   int ev_cls[kEvPool];
@@ -138,6 +146,8 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.col = h->d_col;
   d.val = h->d_val;
   d.halo = h->d_halo;
+  d.tile_row = h->d_tile_row;
+  d.ntiles = h->ntiles;
   d.alpha = h->d_small + kOffAlpha;
   d.beta = h->d_small + kOffBeta;
   d.flag = reinterpret_cast<int*>(h->d_small + kOffFlag);
@@ -162,6 +172,9 @@ Launch make_launch(te_handle* h) {
   L.grid_k2 = h->num_sms;
   L.grid_k3 = (int)std::max<int64_t>(1, std::min<int64_t>(8 * h->num_sms, t256));
   L.variant = h->variant;
+  L.tmaps = h->tmaps.data();
+  L.spmv_tpr = h->spmv_tpr;
+  L.spmv_tiled = h->spmv_tiled;
   L.prefetch = h->prefetch;
   return L;
 }
@@ -172,6 +185,33 @@ int free_workspace(te_handle* h) {
   h->d_V = nullptr;
   h->d_W = nullptr;
   h->m_cap = 0;
+  return TE_OK;
+}
+
+// 2-D TMA descriptors of V (dim0 = 2n doubles, contiguous; dim1 = columns, stride ldv*16 B),
+// one per column count: box = 64 doubles (32 complex rows) x ncols columns.
+int build_tensor_maps(te_handle* h) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return set_err(TE_ERR_CUDA, "cuTensorMapEncodeTiled not available");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const int nmaps = std::min(h->m_cap, te::kMaxCols);
+  h->tmaps.assign(te::kMaxCols, CUtensorMap{});
+  for (int c = 1; c <= nmaps; ++c) {
+    cuuint64_t gdim[2] = {(cuuint64_t)(2 * h->n), (cuuint64_t)h->m_cap};
+    cuuint64_t gstride[1] = {(cuuint64_t)(h->ldv * 16)};
+    cuuint32_t box[2] = {64u, (cuuint32_t)c};
+    cuuint32_t estr[2] = {1u, 1u};
+    CUresult r = encode(&h->tmaps[c - 1], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->d_V, gdim, gstride, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(TE_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for %d columns", (int)r, c);
+  }
   return TE_OK;
 }
 
@@ -200,7 +240,7 @@ int ensure_workspace(te_handle* h, int m) {
   }
   CK(cudaMalloc(&h->d_W, sizeof(double2) * (size_t)h->ldv));
   h->m_cap = m;
-  return TE_OK;
+  return build_tensor_maps(h);
 }
 
 // ---------------------------------------------------------------- profiling around launches
@@ -217,6 +257,12 @@ void prof_begin(te_handle* h) {
 }
 void prof_end(te_handle* h, int cls, double bytes) {
   ++h->launches;
+  static const bool dbg = getenv("TE_DEBUG_SYNC") != nullptr;
+  if (dbg) {
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) fprintf(stderr, "[te] kernel class %d failed: %s\n", cls, cudaGetErrorString(e));
+  }
   if (!h->profile || h->ev_used >= kEvPool) return;
   cudaEventRecord(h->ev1[h->ev_used], h->stream);
   h->ev_cls[h->ev_used] = cls;
@@ -280,9 +326,18 @@ int run_arnoldi(te_handle* h, int m, double tol_rate) {
     int rc = halo_exchange(h, j);
     if (rc) return rc;
     const double ncols = j + 1;
-    prof_begin(h);
-    te::launch_spmv_proj(d, h->cplx, j, L);
-    prof_end(h, 0, bh + 16.0 * n + 16.0 * n * ncols + 16.0 * n);
+    if (h->variant == 2) {
+      prof_begin(h);
+      te::launch_spmv(d, h->cplx, j, L);
+      prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
+      prof_begin(h);
+      te::launch_proj_dots(d, j, L);
+      prof_end(h, 5, 16.0 * n * ncols + 16.0 * n);
+    } else {
+      prof_begin(h);
+      te::launch_spmv_proj(d, h->cplx, j, L);
+      prof_end(h, 0, bh + 16.0 * n + 16.0 * n * ncols + 16.0 * n);
+    }
     if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g1), 2 * (size_t)(j + 1)))) return rc;
     prof_begin(h);
     te::launch_update_proj(d, j, L);
@@ -359,6 +414,7 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
     int m_eff;
     bool brk;
     if ((rc = read_flag(h, m, &m_eff, &brk))) { fill(); return rc; }
+    const auto host_t0 = std::chrono::steady_clock::now();
     const double* alpha = h->h_small + kOffAlpha;
     const double* beta = h->h_small + kOffBeta;
     te::SmallEig E;
@@ -372,7 +428,7 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
     bool qok = true;
     if (forced) {
       tau = std::min(forced[k], rem);
-      te::QuadResult q = te::tanh_sinh(E, 0.0, tau);
+      te::QuadResult q = te::tanh_sinh(E, 0.0, tau, tol_rate * tau);
       err = q.value;
       qok = q.converged;
     } else {
@@ -390,6 +446,11 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
     for (int q = 0; q < m_eff; ++q) {
       const double s = q == 0 ? 1.0 : 1.0 / beta[q - 1];
       h->h_coef[q] = make_double2(om[q].real() * s, om[q].imag() * s);
+    }
+    if (h->profile) {
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+      h->prof[6].launches += 1;
+      h->prof[6].total_ms += ms;
     }
     CK(cudaMemcpyAsync(h->d_g + 128, h->h_coef, sizeof(double2) * m_eff, cudaMemcpyHostToDevice, h->stream));
     {
@@ -482,6 +543,26 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     cudaMemcpyAsync(h->d_val, val, vb * h->nnz, cudaMemcpyHostToDevice, h->stream);
   }
   if (ensure_workspace(h, 1) != TE_OK) return fail(TE_ERR_OOM, "workspace");
+  {  // nnz-balanced SpMV tiles: close a tile before it would exceed kSpmvTileNnz entries or
+     // kSpmvMaxTileRows rows (a single longer row gets a tile of its own; the kernel chunks it)
+    std::vector<int64_t> tr;
+    tr.reserve((size_t)(h->nnz / te::kSpmvTileNnz + n / te::kSpmvMaxTileRows + 2));
+    int64_t start = 0;
+    tr.push_back(0);
+    for (int64_t r = 0; r < n; ++r) {
+      const bool over_rows = (r + 1 - start) > te::kSpmvMaxTileRows;
+      const bool over_nnz = (rowptr[r + 1] - rowptr[start]) > te::kSpmvTileNnz && r > start;
+      if (over_rows || over_nnz) {
+        tr.push_back(r);
+        start = r;
+      }
+    }
+    tr.push_back(n);
+    h->ntiles = (int64_t)tr.size() - 1;
+    if (cudaMalloc(&h->d_tile_row, sizeof(int64_t) * tr.size()) != cudaSuccess) return fail(TE_ERR_OOM, "tiles");
+    cudaMemcpyAsync(h->d_tile_row, tr.data(), sizeof(int64_t) * tr.size(), cudaMemcpyHostToDevice, h->stream);
+    cudaStreamSynchronize(h->stream);
+  }
   // validation + ||H||_1 on the device
   int* d_err = reinterpret_cast<int*>(h->d_counter + 4);
   unsigned long long* d_norm = reinterpret_cast<unsigned long long*>(h->d_small + kOffScalar);
@@ -506,6 +587,12 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
   double nrm;
   std::memcpy(&nrm, &nb, sizeof nrm);
   h->norm1 = nrm;
+  {  // lanes per row of the standalone SpMV ~ average row length / 3 (power of two, 2..32)
+    const double avg = (double)h->nnz / (double)n;
+    int t = 2;
+    while (t < 32 && 3.0 * t < avg) t <<= 1;
+    h->spmv_tpr = t;
+  }
   h->launches += 1;
   return h;
 }
@@ -516,6 +603,16 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
 // C ABI
 // ==========================================================================================
 extern "C" {
+
+int te_kernel_attributes(int which, int* regs, int* max_threads, int* static_smem, int* max_dyn_smem) {
+  clear_err();
+  if (!regs || !max_threads || !static_smem || !max_dyn_smem) return set_err(TE_ERR_ARG, "null");
+  te::configure_kernels();
+  const int r = te::kernel_attributes(which, regs, max_threads, static_smem, max_dyn_smem);
+  if (r == -1) return set_err(TE_ERR_ARG, "unknown kernel %d", which);
+  if (r != 0) return set_err(TE_ERR_CUDA, "cudaFuncGetAttributes failed");
+  return TE_OK;
+}
 
 int te_last_status(void) { return g_status; }
 const char* te_last_error(void) { return g_msg.c_str(); }
@@ -542,6 +639,7 @@ void te_destroy(te_handle* h) {
   cudaFree(h->d_partn);
   cudaFree(h->d_counter);
   cudaFree(h->d_halo);
+  cudaFree(h->d_tile_row);
   cudaFree(h->d_sendbuf);
   cudaFree(h->d_send_idx);
   if (h->h_small) cudaFreeHost(h->h_small);
@@ -658,7 +756,7 @@ int te_set_option(te_handle* h, int option, double value) {
     case TE_OPT_GRAPH:
       return TE_OK;  // launches are issued directly (graph replay: see DESIGN.md next steps)
     case TE_OPT_KERNELS:
-      if (value != 0.0 && value != 1.0) return set_err(TE_ERR_ARG, "TE_OPT_KERNELS must be 0 or 1");
+      if (value != 0.0 && value != 1.0 && value != 2.0) return set_err(TE_ERR_ARG, "TE_OPT_KERNELS must be 0, 1 or 2");
       h->variant = (int)value;
       return TE_OK;
     case TE_OPT_PREFETCH:
