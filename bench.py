@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=8)
-    ap.add_argument("--kernels", type=int, default=2, help="2 SpMV + TMA-tiled projections, 0 register-streaming, 1 smem-staged")
+    ap.add_argument("--kernels", type=int, default=2, help="2 SpMV + shuffle projections, 3 SpMV + TMA projections, 0 fused register, 1 staged")
     ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (library default if unset)")
     return ap.parse_args()
 
@@ -320,7 +320,7 @@ def run_ours(args):
                    "krylov_steps_per_step": ksteps / args.steps,
                    "restarts_per_step": stats[-1]["n_restarts"],
                    "l2": "inputs larger than L2 (V = %.0f MB > 126 MB)" % (16 * nloc * m / 1e6),
-                   "parallelism": f"rows{ws}", "kernels": ["register", "staged", "tma"][args.kernels],
+                   "parallelism": f"rows{ws}", "kernels": ["fused-register", "staged", "hybrid", "tma", "shuffle"][args.kernels],
                    "prefetch": args.prefetch},
         "achieved_hbm_gbs": all_bytes / (all_ms * 1e-3) / 1e9 if all_ms > 0 else None,
         "evolved_time_per_s": t * args.steps / (ms * 1e-3),

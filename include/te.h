@@ -127,9 +127,13 @@ int te_krylov_basis(te_handle* h, const te_c128* v1, int m, double tol_rate, dou
 enum {
   TE_OPT_PROFILE = 1,        /* 1: record CUDA events around every kernel launch (te_get_profile) */
   TE_OPT_GRAPH = 2,          /* 1 (default): replay each restart's launches as a CUDA graph      */
-  TE_OPT_KERNELS = 3,        /* 2 (default): standalone SpMV + TMA-tiled (2-D tensor boxes) warp-
-                                specialised projection kernels; 0: register-streaming fused K1/K2;
-                                1: shared-memory staged K1 + bulk-copy staged K2 — same arithmetic */
+  TE_OPT_KERNELS = 3,        /* kernel set (same arithmetic, kept for measured comparison):
+                                2 (default): nnz-balanced SpMV + projections chosen by column count
+                                  (register-streaming/shuffle for <= 16 columns, TMA-tiled above);
+                                3: SpMV + TMA-tiled (2-D tensor boxes) warp-specialised projections;
+                                4: SpMV + register-streaming/shuffle projections;
+                                0: register-streaming fused K1/K2; 1: shared-memory staged K1 and
+                                  bulk-copy staged K2                                                */
   TE_OPT_PREFETCH = 4        /* L2 bulk-prefetch distance (block iterations, 0..16; default 0)     */
 };
 int te_set_option(te_handle* h, int option, double value);

@@ -653,20 +653,34 @@ __global__ void __launch_bounds__(kThreads, 2) k_update_proj_r(KDev d, int j, in
 // transpose-reduction (31 shuffles per 32 columns instead of 32 x 5), after which lane k owns
 // column k and accumulates it across tiles in one register pair.
 // --------------------------------------------------------------------------------------
-constexpr int kTileR = 32;          // rows per TMA tile
-constexpr int kMaxSlots = 7;  // 7 consumer warps + 1 producer warp = 256 threads
-constexpr int kProjThreads = (kMaxSlots + 1) * 32;
+constexpr int kTileR = 32;          // rows per consumer sub-tile (lane = row)
+constexpr int kConsumers = 7;       // consumer warps (+1 producer warp = 256 threads)
+constexpr int kMaxSlots = 32;
+constexpr int kProjThreads = (kConsumers + 1) * 32;
 constexpr size_t kProjSmemBudget = 200 * 1024;
 
+// sub-tiles per TMA tile: at least ~8 KB per tile (a 128-row box is the largest single load)
+int proj_rsub(int ncols) {
+  int r = 1;
+  while (r < 4 && (size_t)(ncols + 1) * kTileR * 16 * r < 8192) r <<= 1;
+  return r;
+}
+static size_t proj_slot_bytes(int ncols) {
+  const int R = proj_rsub(ncols);
+  return (size_t)(ncols + 1) * kTileR * R * 16;
+}
+// Tile i -> slot i % S; slot s is owned by consumer warp s % C for its whole life, so each slot
+// is consumed by one warp in round order and no warp can poll a slot's full barrier one phase
+// early (mbarrier parity aliasing).
 int proj_slots(int ncols) {
-  const size_t slot = (size_t)ncols * kTileR * 16 + kTileR * 16;
-  int s = (int)(kProjSmemBudget / slot);
+  int s = (int)(kProjSmemBudget / proj_slot_bytes(ncols));
   return s > kMaxSlots ? kMaxSlots : (s < 1 ? 1 : s);
 }
-size_t proj_smem_bytes(int ncols) {
-  const size_t slot = (size_t)ncols * kTileR * 16 + kTileR * 16;
-  return (size_t)proj_slots(ncols) * slot + 1024;  // + alignment slack
+int proj_consumers(int ncols) {
+  const int s = proj_slots(ncols);
+  return s < kConsumers ? s : kConsumers;
 }
+size_t proj_smem_bytes(int ncols) { return (size_t)proj_slots(ncols) * proj_slot_bytes(ncols) + 1024; }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
   asm volatile(
@@ -698,13 +712,22 @@ __device__ __forceinline__ double2 butterfly_colsum(double (&re)[32], double (&i
   return make_double2(re[0], im[0]);
 }
 
+// TMA-tiled projection kernel (default path), warp-specialised.  The producer warp streams
+// tiles of 32*R rows x ncols columns of V (ONE 2-D tensor load per tile, box 64R doubles x
+// ncols) plus the matching rows of W (bulk copy) into S ring slots (full/empty mbarriers);
+// tile i of the CTA uses slot i % S and is consumed by warp i % kConsumers, so the number of
+// tiles in flight is set by shared memory (~200 KB), not by the number of warps.
+//   MODE 0 (sweep-1):  g1 = V^H p                           (dots only)
+//   MODE 1 (sweep-2):  p' = p - V e1 -> W,  g2 = V^H p'      (update + dots on the same tile)
+// Lane = row for the update; the 32 x 32 column sums of a sub-tile come from a butterfly
+// transpose-reduction (31 shuffles per 32 columns), after which lane k owns column k.
 template <int MODE>
 __global__ void __launch_bounds__(kProjThreads, 1)
-    k_proj_tma(const __grid_constant__ CUtensorMap tmV, KDev d, int j, int S) {
+    k_proj_tma(const __grid_constant__ CUtensorMap tmV, KDev d, int j, int S, int R, int C) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxSlots], empty[kMaxSlots];
   __shared__ double2 coef[kMaxCols];
-  __shared__ double2 red[kMaxSlots][kMaxCols];
+  __shared__ double2 red[kConsumers][kMaxCols];
   __shared__ int go_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ncols = j + 1;
@@ -715,8 +738,9 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);   // e1_k = s_k c1_k
   }
   unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const size_t vbytes = (size_t)ncols * kTileR * 16;
-  const size_t slot_bytes = vbytes + kTileR * 16;
+  const int TR = kTileR * R;
+  const size_t vbytes = (size_t)ncols * TR * 16;
+  const size_t slot_bytes = vbytes + (size_t)TR * 16;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -727,59 +751,75 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   __syncthreads();
   if (!go_s) return;
   const int64_t n = d.n;
-  const int64_t ntiles = (n + kTileR - 1) / kTileR;
-  const double2* srcW = d.W;
+  const int64_t ntiles = (n + TR - 1) / TR;
 
-  if (warp == S) {  // ---------------- producer
+  if (warp == kConsumers) {  // ---------------- producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
+      const uint64_t pol = policy_evict_first();
       for (int64_t i = 0;; ++i) {
         const int64_t tile = blockIdx.x + i * gridDim.x;
         if (tile >= ntiles) break;
         const int s = (int)(i % S);
         const int64_t round = i / S;
         if (round > 0) mbar_wait(&empty[s], (unsigned)((round - 1) & 1));
-        const int rows = (int)min((int64_t)kTileR, n - tile * kTileR);
+        const int rows = (int)min((int64_t)TR, n - tile * TR);
         unsigned char* base = smem + (size_t)s * slot_bytes;
         mbar_expect_tx(&full[s], (unsigned)vbytes + (unsigned)rows * 16u);
-        tma_load_2d(base, &tmV, (int)(tile * kTileR * 2), 0, &full[s]);
-        bulk_g2s(base + vbytes, srcW + tile * kTileR, (unsigned)rows * 16u, &full[s], policy_evict_first());
+        tma_load_2d(base, &tmV, (int)(tile * TR * 2), 0, &full[s]);
+        bulk_g2s(base + vbytes, d.W + tile * TR, (unsigned)rows * 16u, &full[s], pol);
       }
     }
-  } else if (warp < S) {  // ------- consumers
+  } else if (warp < C) {  // ------- consumers: warp owns slots warp, warp + C, ... (< S)
     double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-    for (int64_t i = warp;; i += S) {
-      const int64_t tile = blockIdx.x + i * gridDim.x;
-      if (tile >= ntiles) break;
-      const int s = warp;
-      mbar_wait(&full[s], (unsigned)((i / S) & 1));
-      const double2* Vs = reinterpret_cast<const double2*>(smem + (size_t)s * slot_bytes);
-      const double2* Ws = reinterpret_cast<const double2*>(smem + (size_t)s * slot_bytes + vbytes);
-      const int64_t r0 = tile * kTileR;
-      const int rows = (int)min((int64_t)kTileR, n - r0);
-      double2 p = lane < rows ? Ws[lane] : make_double2(0.0, 0.0);
-      if (MODE == 1) {
-        double2 a = make_double2(0.0, 0.0);
-        for (int k = 0; k < ncols; ++k) a = cfma(Vs[k * kTileR + lane], coef[k], a);
-        p = make_double2(p.x - a.x, p.y - a.y);
-        if (lane >= rows) p = make_double2(0.0, 0.0);
-        if (lane < rows) d.W[r0 + lane] = p;
-      }
-      // column sums of conj(V) p over the tile's 32 rows
-      for (int cb = 0; cb < ncols; cb += 32) {
-        double re[32], im[32];
+    bool more = true;
+    for (int64_t base = 0; more; base += S) {
+      for (int s = warp; s < S; s += C) {
+        const int64_t i = base + s;
+        const int64_t tile = blockIdx.x + i * gridDim.x;
+        if (tile >= ntiles) { more = false; break; }
+        mbar_wait(&full[s], (unsigned)((i / S) & 1));
+        const double2* Vs = reinterpret_cast<const double2*>(smem + (size_t)s * slot_bytes);
+        const double2* Ws = reinterpret_cast<const double2*>(smem + (size_t)s * slot_bytes + vbytes);
+        const int64_t r0 = tile * TR;
+        const int rows = (int)min((int64_t)TR, n - r0);
+        for (int sub = 0; sub < R && MODE < 2; ++sub) {  // MODE 2: streaming only (microbenchmark)
+          const int row = sub * kTileR + lane;
+          if (sub * kTileR >= rows) break;  // warp-uniform
+          double2 p = row < rows ? Ws[row] : make_double2(0.0, 0.0);
+          if (MODE == 1) {
+            // four independent FMA chains over the columns
+            double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
+            int k = 0;
+            for (; k + 4 <= ncols; k += 4) {
+              a0 = cfma(Vs[(k + 0) * TR + row], coef[k + 0], a0);
+              a1 = cfma(Vs[(k + 1) * TR + row], coef[k + 1], a1);
+              a2 = cfma(Vs[(k + 2) * TR + row], coef[k + 2], a2);
+              a3 = cfma(Vs[(k + 3) * TR + row], coef[k + 3], a3);
+            }
+            for (; k < ncols; ++k) a0 = cfma(Vs[k * TR + row], coef[k], a0);
+            const double2 a = cadd(cadd(a0, a1), cadd(a2, a3));
+            p = make_double2(p.x - a.x, p.y - a.y);
+            if (row >= rows) p = make_double2(0.0, 0.0);
+            else d.W[r0 + row] = p;
+          }
+          // column sums of conj(V) p over the sub-tile's 32 rows
+          for (int cb = 0; cb < ncols; cb += 32) {
+            double re[32], im[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int k = cb + c;
-          const double2 v = k < ncols ? Vs[k * kTileR + lane] : make_double2(0.0, 0.0);
-          re[c] = v.x * p.x + v.y * p.y;   // conj(v) * p
-          im[c] = v.x * p.y - v.y * p.x;
+            for (int c = 0; c < 32; ++c) {
+              const int k = cb + c;
+              const double2 v = k < ncols ? Vs[k * TR + row] : make_double2(0.0, 0.0);
+              re[c] = v.x * p.x + v.y * p.y;   // conj(v) * p
+              im[c] = v.x * p.y - v.y * p.x;
+            }
+            const double2 cs = butterfly_colsum(re, im);
+            if (cb == 0) acc0 = cadd(acc0, cs); else acc1 = cadd(acc1, cs);
+          }
         }
-        const double2 cs = butterfly_colsum(re, im);
-        if (cb == 0) acc0 = cadd(acc0, cs); else acc1 = cadd(acc1, cs);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
     }
     red[warp][lane] = acc0;
     red[warp][lane + 32] = acc1;
@@ -787,10 +827,10 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   __syncthreads();
   // block partial in fixed warp order, then the last-CTA reduction
   double2* out = MODE == 0 ? d.g1 : d.g2;
-  const int ctr = MODE;
+  const int ctr = MODE == 0 ? 0 : 1;
   if (tid < ncols) {
     double2 t = red[0][tid];
-    for (int w = 1; w < S; ++w) t = cadd(t, red[w][tid]);
+    for (int w = 1; w < C; ++w) t = cadd(t, red[w][tid]);
     d.part[(size_t)blockIdx.x * kMaxCols + tid] = t;
   }
   __threadfence();
@@ -803,7 +843,102 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   __shared__ double2 seg[4][kMaxCols];
   const int G = gridDim.x;
   const int per = (G + 3) / 4;
-  if (tid < 256) {
+  {
+    const int c = tid & (kMaxCols - 1), sgi = tid >> 6;
+    double2 sm = make_double2(0.0, 0.0);
+    if (c < ncols) {
+      const int b0 = sgi * per, b1 = min(G, b0 + per);
+      for (int b = b0; b < b1; ++b) sm = cadd(sm, ld_cg(d.part + (size_t)b * kMaxCols + c));
+    }
+    seg[sgi][c] = sm;
+  }
+  __syncthreads();
+  if (tid < ncols) {
+    double2 t = seg[0][tid];
+    t = cadd(t, seg[1][tid]);
+    t = cadd(t, seg[2][tid]);
+    t = cadd(t, seg[3][tid]);
+    out[tid] = t;
+  }
+  if (tid == 0) d.counter[ctr] = 0u;
+}
+
+// Register-streaming projection kernel with shuffle row-reduction (default): TPR lanes per row,
+// lane q holds the row's V entries of columns q + TPR*c (c < 8) in registers.  Column sums over
+// the warp's rows are formed by xor-shuffles over the row bits of the lane index and added to a
+// per-warp shared-memory accumulator, so no per-column accumulator registers persist across rows
+// (~60 registers -> 4 CTAs of 256 threads per SM, 8 loads of 16 B in flight per thread).
+//   MODE 0:  g1 = V^H p                          MODE 1:  p' = p - V e1 -> W, g2 = V^H p'
+template <int MODE, int TPR>
+__global__ void __launch_bounds__(kThreads, 4) k_proj_s(KDev d, int j) {
+  __shared__ double2 coef[kMaxCols];
+  __shared__ double2 red[kWarps][kMaxCols];
+  __shared__ int go_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = tid % TPR, grp = tid / TPR;
+  constexpr int RPB = kThreads / TPR;
+  const int ncols = j + 1;
+  if (tid == 0) go_s = (d.flag[0] == 0);
+  if (MODE == 1 && tid < ncols) {
+    const double sk = d.s[tid];
+    const double2 g = d.g1[tid];
+    coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);
+  }
+  for (int i = tid; i < kWarps * kMaxCols; i += kThreads) (&red[0][0])[i] = make_double2(0.0, 0.0);
+  __syncthreads();
+  if (!go_s) return;
+  const int64_t n = d.n, ldv = d.ldv;
+  for (int64_t rb = (int64_t)blockIdx.x * RPB; rb < n; rb += (int64_t)gridDim.x * RPB) {
+    const int64_t r = rb + grp;
+    const bool act = r < n;
+    double2 v[kCPT];
+#pragma unroll
+    for (int c = 0; c < kCPT; ++c) {
+      const int k = q + TPR * c;
+      v[c] = (act && k < ncols) ? ld_stream(d.V + r + (int64_t)k * ldv) : make_double2(0.0, 0.0);
+    }
+    double2 p = act ? (MODE == 1 ? __ldcs(d.W + r) : __ldg(d.W + r)) : make_double2(0.0, 0.0);
+    if (MODE == 1) {
+      double2 a = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < kCPT; ++c) {
+        const int k = q + TPR * c;
+        if (k < ncols) a = cfma(v[c], coef[k], a);
+      }
+      a = group_sum<TPR>(a);
+      p = make_double2(p.x - a.x, p.y - a.y);
+      if (act && q == 0) d.W[r] = p;
+    }
+#pragma unroll
+    for (int c = 0; c < kCPT; ++c) {
+      double2 pr = make_double2(v[c].x * p.x + v[c].y * p.y, v[c].x * p.y - v[c].y * p.x);  // conj(v) p
+#pragma unroll
+      for (int off = TPR; off < 32; off <<= 1) {
+        pr.x += __shfl_xor_sync(0xffffffffu, pr.x, off);
+        pr.y += __shfl_xor_sync(0xffffffffu, pr.y, off);
+      }
+      const int k = q + TPR * c;
+      if (lane < TPR && k < ncols) red[warp][k] = cadd(red[warp][k], pr);
+    }
+  }
+  __syncthreads();
+  double2* out = MODE == 0 ? d.g1 : d.g2;
+  const int ctr = MODE;
+  if (tid < ncols) {
+    double2 t = red[0][tid];
+    for (int w = 1; w < kWarps; ++w) t = cadd(t, red[w][tid]);
+    d.part[(size_t)blockIdx.x * kMaxCols + tid] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int last;
+  if (tid == 0) last = (atomicAdd(&d.counter[ctr], 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double2 seg[4][kMaxCols];
+  const int G = gridDim.x;
+  const int per = (G + 3) / 4;
+  {
     const int c = tid & (kMaxCols - 1), sgi = tid >> 6;
     double2 sm = make_double2(0.0, 0.0);
     if (c < ncols) {
@@ -1209,9 +1344,26 @@ void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
     }
 }
 
+static void launch_proj_s(const KDev& d, int j, int mode, const Launch& L) {
+  const int tpr = tpr_for(j + 1, 1);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * L.num_sms, (d.n * tpr + kThreads - 1) / kThreads));
+  TE_DISPATCH_TPR(tpr, {
+    if (mode == 0) k_proj_s<0, TPR><<<grid, kThreads, 0, L.stream>>>(d, j);
+    else k_proj_s<1, TPR><<<grid, kThreads, 0, L.stream>>>(d, j);
+  });
+}
+
+// measured on B200 (tools/micro/mb_proj.cu): the register/shuffle kernel streams faster for
+// <= 16 columns (small tiles expose the TMA ring's per-tile cost), the TMA ring above.
+constexpr int kShuffleMaxCols = 16;
+
 void launch_proj_dots(const KDev& d, int j, const Launch& L) {
-  const int S = proj_slots(j + 1);
-  k_proj_tma<0><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S);
+  if (L.proj_tma == 0 || (L.proj_tma == 2 && j + 1 <= kShuffleMaxCols)) {
+    launch_proj_s(d, j, 0, L);
+    return;
+  }
+  const int S = proj_slots(j + 1), R = proj_rsub(j + 1), C = proj_consumers(j + 1);
+  k_proj_tma<0><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S, R, C);
 }
 
 void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L) {
@@ -1242,9 +1394,13 @@ void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L) {
 }
 
 void launch_update_proj(const KDev& d, int j, const Launch& L) {
+  if (L.variant == 2 && (L.proj_tma == 0 || (L.proj_tma == 2 && j + 1 <= kShuffleMaxCols))) {
+    launch_proj_s(d, j, 1, L);
+    return;
+  }
   if (L.variant == 2) {
-    const int S = proj_slots(j + 1);
-    k_proj_tma<1><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S);
+    const int S = proj_slots(j + 1), R = proj_rsub(j + 1), C = proj_consumers(j + 1);
+    k_proj_tma<1><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S, R, C);
     return;
   }
   if (L.variant == 0) {

@@ -52,6 +52,7 @@ struct Launch {
   int grid_k1, grid_k2, grid_k3;
   const CUtensorMap* tmaps;  // [kMaxCols] 2-D maps of V, box = 64 doubles x (k+1) columns
   int spmv_tpr;  // lanes per row of the standalone CSR-vector SpMV
+  int proj_tma;   // 2: hybrid by column count (default), 1: TMA-tiled only, 0: register/shuffle only
   int spmv_tiled; // 1: nnz-balanced tiled SpMV (default), 0: CSR-vector
   int prefetch; // L2 bulk-prefetch distance in block iterations (0: off)
   int variant;  // 2: SpMV + TMA-tiled projections (default); 0: register-streaming K1/K2;
@@ -79,6 +80,8 @@ void launch_pack(const double2* x, const int32_t* idx, int64_t cnt, double2* out
 
 size_t k2_smem_bytes(int ncols, int* tile_rows);
 int proj_slots(int ncols);
+int proj_rsub(int ncols);
+int proj_consumers(int ncols);
 size_t proj_smem_bytes(int ncols);
 cudaError_t configure_kernels();
 int kernel_attributes(int which, int* regs, int* max_threads, int* static_smem, int* max_dyn_smem);  // opt-in shared memory sizes (once per process/device)

@@ -171,7 +171,8 @@ Launch make_launch(te_handle* h) {
   L.grid_k1 = (int)std::max<int64_t>(1, std::min<int64_t>(2 * h->num_sms, t256));
   L.grid_k2 = h->num_sms;
   L.grid_k3 = (int)std::max<int64_t>(1, std::min<int64_t>(8 * h->num_sms, t256));
-  L.variant = h->variant;
+  L.variant = h->variant >= 2 ? 2 : h->variant;  // 2 hybrid, 3 TMA-only, 4 shuffle-only
+  L.proj_tma = h->variant == 2 ? 2 : (h->variant == 3 ? 1 : (h->variant == 4 ? 0 : 0));
   L.tmaps = h->tmaps.data();
   L.spmv_tpr = h->spmv_tpr;
   L.spmv_tiled = h->spmv_tiled;
@@ -189,7 +190,7 @@ int free_workspace(te_handle* h) {
 }
 
 // 2-D TMA descriptors of V (dim0 = 2n doubles, contiguous; dim1 = columns, stride ldv*16 B),
-// one per column count: box = 64 doubles (32 complex rows) x ncols columns.
+// one per column count: box = 64 R doubles (32 R complex rows, R = proj_rsub) x ncols columns.
 int build_tensor_maps(te_handle* h) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
@@ -205,7 +206,7 @@ int build_tensor_maps(te_handle* h) {
   for (int c = 1; c <= nmaps; ++c) {
     cuuint64_t gdim[2] = {(cuuint64_t)(2 * h->n), (cuuint64_t)h->m_cap};
     cuuint64_t gstride[1] = {(cuuint64_t)(h->ldv * 16)};
-    cuuint32_t box[2] = {64u, (cuuint32_t)c};
+    cuuint32_t box[2] = {(cuuint32_t)(64 * te::proj_rsub(c)), (cuuint32_t)c};
     cuuint32_t estr[2] = {1u, 1u};
     CUresult r = encode(&h->tmaps[c - 1], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->d_V, gdim, gstride, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -326,7 +327,7 @@ int run_arnoldi(te_handle* h, int m, double tol_rate) {
     int rc = halo_exchange(h, j);
     if (rc) return rc;
     const double ncols = j + 1;
-    if (h->variant == 2) {
+    if (h->variant >= 2) {
       prof_begin(h);
       te::launch_spmv(d, h->cplx, j, L);
       prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
@@ -756,7 +757,8 @@ int te_set_option(te_handle* h, int option, double value) {
     case TE_OPT_GRAPH:
       return TE_OK;  // launches are issued directly (graph replay: see DESIGN.md next steps)
     case TE_OPT_KERNELS:
-      if (value != 0.0 && value != 1.0 && value != 2.0) return set_err(TE_ERR_ARG, "TE_OPT_KERNELS must be 0, 1 or 2");
+      if (value < 0.0 || value > 4.0 || value != (double)(int)value)
+        return set_err(TE_ERR_ARG, "TE_OPT_KERNELS must be 0..4");
       h->variant = (int)value;
       return TE_OK;
     case TE_OPT_PREFETCH:

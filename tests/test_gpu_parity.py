@@ -35,7 +35,7 @@ def small_cases():
 CASES = small_cases()
 
 
-@pytest.mark.parametrize("variant", [2, 0, 1], ids=["tma", "register", "staged"])
+@pytest.mark.parametrize("variant", [2, 3, 4, 0, 1], ids=["hybrid", "tma", "shuffle", "register", "staged"])
 @pytest.mark.parametrize("name,c", CASES, ids=[x[0] for x in CASES])
 def test_krylov_basis_matches_oracle(gpu_lib, name, c, variant):
     te = gpu_lib
