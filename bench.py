@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--cpu-sample-steps", type=int, default=8)
     ap.add_argument("--kernels", type=int, default=2, help="2 SpMV + shuffle projections, 3 SpMV + TMA projections, 0 fused register, 1 staged")
     ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (library default if unset)")
+    ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel: 2 TMA-fed, 1 tiled, 0 CSR-vector")
     return ap.parse_args()
 
 
@@ -231,6 +232,8 @@ def run_ours(args):
     te.te_set_option(h, te.TE_OPT_KERNELS, args.kernels)
     if args.prefetch is not None:
         te.te_set_option(h, te.TE_OPT_PREFETCH, args.prefetch)
+    if args.spmv is not None:
+        te.te_set_option(h, te.TE_OPT_SPMV, args.spmv)
     stream = torch.cuda.current_stream(dev)
     d_v0 = torch.from_numpy(np.ascontiguousarray(v0_loc)).to(dev)
     d_out = torch.empty_like(d_v0)
@@ -321,7 +324,7 @@ def run_ours(args):
                    "restarts_per_step": stats[-1]["n_restarts"],
                    "l2": "inputs larger than L2 (V = %.0f MB > 126 MB)" % (16 * nloc * m / 1e6),
                    "parallelism": f"rows{ws}", "kernels": ["fused-register", "staged", "hybrid", "tma", "shuffle"][args.kernels],
-                   "prefetch": args.prefetch},
+                   "prefetch": args.prefetch, "spmv": args.spmv},
         "achieved_hbm_gbs": all_bytes / (all_ms * 1e-3) / 1e9 if all_ms > 0 else None,
         "evolved_time_per_s": t * args.steps / (ms * 1e-3),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

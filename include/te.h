@@ -134,7 +134,12 @@ enum {
                                 4: SpMV + register-streaming/shuffle projections;
                                 0: register-streaming fused K1/K2; 1: shared-memory staged K1 and
                                   bulk-copy staged K2                                                */
-  TE_OPT_PREFETCH = 4        /* L2 bulk-prefetch distance (block iterations, 0..16; default 0)     */
+  TE_OPT_PREFETCH = 4,       /* L2 bulk-prefetch distance (block iterations, 0..16; default 0)     */
+  TE_OPT_SPMV = 5            /* SpMV kernel of kernel sets 2-4 (same arithmetic, measured choice):
+                                3 (default) nnz-balanced tiles, col/val staged in shared memory,
+                                thread-per-row gathers; 1 nnz-balanced tiles, entry-parallel products;
+                                2 TMA-fed (bulk copies of rowptr/col/val into a shared-memory ring,
+                                warp-specialised); 0 CSR-vector                                       */
 };
 int te_set_option(te_handle* h, int option, double value);
 

@@ -958,6 +958,165 @@ __global__ void __launch_bounds__(kThreads, 4) k_proj_s(KDev d, int j) {
   if (tid == 0) d.counter[ctr] = 0u;
 }
 
+// --------------------------------------------------------------------------------------
+// TMA-fed SpMV (default): p = s_j H V_j -> W.  Tiles of <= kSpmvTmaNnz entries / kSpmvTmaRows
+// rows (descriptors {first row, first entry} built at create).  The producer warp bulk-copies
+// (cp.async.bulk) each tile's rowptr, col and val ranges into a ring of shared-memory slots;
+// consumer warp (slot owner) gathers x (L2-resident) for 32 entries per instruction, 8 gathers
+// in flight per lane, stages the products in its scratch and sums each row left to right.
+// A single row longer than a tile is handled by its consumer straight from global memory.
+// --------------------------------------------------------------------------------------
+constexpr int kSpmvTmaNnz = kSpmvTmaNnzCap;
+constexpr int kSpmvTmaRows = kSpmvTmaRowCap;
+constexpr int kSmRp = ((kSpmvTmaRows + 4) * 8 + 15) / 16 * 16;
+constexpr int kSmCol = ((kSpmvTmaNnz + 4) * 4 + 15) / 16 * 16;
+size_t spmv_slot_bytes(bool cplx) { return kSmRp + kSmCol + (size_t)(kSpmvTmaNnz + 2) * (cplx ? 16 : 8) + 16; }
+constexpr size_t kSpmvScratch = 0;  // (no per-warp product scratch: lane-per-row sums)
+int spmv_slots(bool cplx) {
+  const size_t avail = kProjSmemBudget - kConsumers * kSpmvScratch;
+  int s = (int)(avail / spmv_slot_bytes(cplx));
+  return s > kMaxSlots ? kMaxSlots : (s < kConsumers ? kConsumers : s);
+}
+size_t spmv_smem_bytes(bool cplx) { return kConsumers * kSpmvScratch + spmv_slots(cplx) * spmv_slot_bytes(cplx) + 1024; }
+
+template <bool CPLX>
+__global__ void __launch_bounds__(kProjThreads, 1) k_spmv_tma(KDev d, int j, int S) {
+  using VT = typename ValT<CPLX>::T;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[kMaxSlots], empty[kMaxSlots];
+  __shared__ double sj_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int C = kConsumers;
+  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const size_t slot_bytes = kSmRp + kSmCol + (size_t)(kSpmvTmaNnz + 2) * sizeof(VT) + 16;
+  unsigned char* slots = smem + C * kSpmvScratch;
+  if (tid == 0) {
+    sj_s = step_gate(d, j, blockIdx.x == 0);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+  const int64_t n = d.n;
+  const int64_t ntiles = d.ntiles_desc;
+  const VT* __restrict__ val = static_cast<const VT*>(d.val);
+  const int32_t* __restrict__ col = d.col;
+  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  const double2* __restrict__ halo = d.halo;
+  const int64_t* __restrict__ tdesc = d.tile_desc;  // pairs {first row, first entry}, ntiles+1
+
+  if (warp == C) {  // ---------------- producer (whole warp loads descriptors, lane 0 issues)
+    const uint64_t pol = policy_evict_first();
+    for (int64_t base = 0;; base += 32) {
+      const int64_t ti = blockIdx.x + (base + lane) * gridDim.x;
+      int64_t ra = 0, ea = 0, rb = 0, eb = 0;
+      if (ti < ntiles) {
+        ra = __ldg(tdesc + 2 * ti);
+        ea = __ldg(tdesc + 2 * ti + 1);
+        rb = __ldg(tdesc + 2 * ti + 2);
+        eb = __ldg(tdesc + 2 * ti + 3);
+      }
+      bool done = false;
+      for (int l = 0; l < 32; ++l) {
+        const int64_t i = base + l;
+        const int64_t t = blockIdx.x + i * gridDim.x;
+        if (t >= ntiles) { done = true; break; }
+        const int64_t Ra = __shfl_sync(0xffffffffu, ra, l), Ea = __shfl_sync(0xffffffffu, ea, l);
+        const int64_t Rb = __shfl_sync(0xffffffffu, rb, l), Eb = __shfl_sync(0xffffffffu, eb, l);
+        if (lane == 0) {
+          const int s = (int)(i % S);
+          const int64_t round = i / S;
+          if (round > 0) mbar_wait(&empty[s], (unsigned)((round - 1) & 1));
+          unsigned char* sl = slots + (size_t)s * slot_bytes;
+          if (Eb - Ea > kSpmvTmaNnz) {  // long row: consumer reads global memory
+            mbar_expect_tx(&full[s], 0u);
+          } else {
+            const int64_t r0 = Ra & ~1LL, r1 = (Rb + 2) & ~1LL;          // rowptr[Ra..Rb], 16 B aligned
+            const int64_t c0 = Ea & ~3LL, c1 = (Eb + 3) & ~3LL;          // col[Ea..Eb)
+            constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
+            const int64_t v0 = Ea & ~(VA - 1), v1 = (Eb + VA - 1) & ~(VA - 1);
+            const unsigned br = (unsigned)((r1 - r0) * 8), bc = (unsigned)((c1 - c0) * 4),
+                           bv = (unsigned)((v1 - v0) * sizeof(VT));
+            mbar_expect_tx(&full[s], br + (bc ? bc : 0u) + (bv ? bv : 0u));
+            bulk_g2s(sl, d.rowptr + r0, br, &full[s], pol);
+            if (bc) bulk_g2s(sl + kSmRp, col + c0, bc, &full[s], pol);
+            if (bv) bulk_g2s(sl + kSmRp + kSmCol, val + v0, bv, &full[s], pol);
+          }
+        }
+        __syncwarp();
+      }
+      if (done) break;
+    }
+  } else if (warp < C) {  // ---------------- consumers: warp owns slots warp, warp + C, ...
+    bool more = true;
+    for (int64_t base = 0; more; base += S) {
+      for (int s = warp; s < S; s += C) {
+        const int64_t i = base + s;
+        const int64_t t = blockIdx.x + i * gridDim.x;
+        if (t >= ntiles) { more = false; break; }
+        const int64_t Ra = __ldg(tdesc + 2 * t), Ea = __ldg(tdesc + 2 * t + 1);
+        const int64_t Rb = __ldg(tdesc + 2 * t + 2), Eb = __ldg(tdesc + 2 * t + 3);
+        const int rows = (int)(Rb - Ra);
+        const int cnt = (int)(Eb - Ea);
+        mbar_wait(&full[s], (unsigned)((i / S) & 1));
+        if (cnt > kSpmvTmaNnz) {  // one long row (rows == 1), straight from global memory
+          double2 sum = make_double2(0.0, 0.0);
+          for (int64_t e = Ea + lane; e < Eb; e += 32) {
+            const int c = __ldg(col + e);
+            const double2 xv = (c < n) ? __ldg(x + c) : __ldg(halo + (c - n));
+            sum = cadd(sum, ValT<CPLX>::mul(__ldg(val + e), xv));
+          }
+          sum = warp_sum(sum);
+          if (lane == 0) __stcs(d.W + Ra, make_double2(sum.x * sj, sum.y * sj));
+        } else {
+          const unsigned char* sl = slots + (size_t)s * slot_bytes;
+          const int64_t* rp = reinterpret_cast<const int64_t*>(sl) + (Ra & 1);
+          const int32_t* cs = reinterpret_cast<const int32_t*>(sl + kSmRp) + (Ea & 3);
+          constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
+          const VT* vs = reinterpret_cast<const VT*>(sl + kSmRp + kSmCol) + (Ea & (VA - 1));
+          // lane = row: the k-th entries of 32 consecutive rows are gathered together (neighbouring
+          // rows have neighbouring columns in structured matrices -> few sectors per request);
+          // each lane sums its own row left to right, kG gathers in flight
+          constexpr int kG = 8;
+          for (int rr0 = 0; rr0 < rows; rr0 += 32) {
+            const int rr = rr0 + lane;
+            int lo = 0, len = 0;
+            if (rr < rows) {
+              lo = (int)(rp[rr] - Ea);
+              len = (int)(rp[rr + 1] - Ea) - lo;
+            }
+            int mlen = len;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) mlen = max(mlen, __shfl_xor_sync(0xffffffffu, mlen, off));
+            double2 sum = make_double2(0.0, 0.0);
+            for (int q0 = 0; q0 < mlen; q0 += kG) {
+              int cc[kG];
+              VT vv[kG];
+#pragma unroll
+              for (int u = 0; u < kG; ++u)
+                if (q0 + u < len) { cc[u] = cs[lo + q0 + u]; vv[u] = vs[lo + q0 + u]; }
+              double2 xx[kG];
+#pragma unroll
+              for (int u = 0; u < kG; ++u)
+                if (q0 + u < len) xx[u] = (cc[u] < n) ? __ldg(x + cc[u]) : __ldg(halo + (cc[u] - n));
+#pragma unroll
+              for (int u = 0; u < kG; ++u)
+                if (q0 + u < len) sum = cadd(sum, ValT<CPLX>::mul(vv[u], xx[u]));
+            }
+            if (rr < rows) __stcs(d.W + Ra + rr, make_double2(sum.x * sj, sum.y * sj));
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+    }
+  }
+}
+
 // Standalone SpMV, nnz-balanced tiles (default): tile t covers rows [tile_row[t], tile_row[t+1])
 // holding ~kSpmvTileNnz entries (built at create time).  Each thread issues all kSpmvE col/val
 // loads of a chunk at once, then all x gathers, products go to shared memory, and one thread
@@ -1020,6 +1179,74 @@ __global__ void __launch_bounds__(kThreads, 4) k_spmv_tile(KDev d, int j) {
         if (i < rows) {
           const int64_t lo = max(rps[i], cb), hi = min(rps[i + 1], cb + cnt);
           for (int64_t q = lo; q < hi; ++q) acc[u] = cadd(acc[u], prod[q - cb]);
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int i = tid + u * kThreads;
+      if (i < rows) __stcs(d.W + ra + i, make_double2(acc[u].x * sj, acc[u].y * sj));
+    }
+    __syncthreads();
+  }
+}
+
+// SpMV variant 3: nnz-balanced tiles, col/val staged coalesced into shared memory, then one
+// thread per row gathers x for its own entries (the k-th entries of neighbouring rows sit at
+// neighbouring columns in structured matrices) and sums them left to right.
+template <bool CPLX>
+__global__ void __launch_bounds__(kThreads, 4) k_spmv_rowtile(KDev d, int j) {
+  using VT = typename ValT<CPLX>::T;
+  __shared__ int32_t cs[kChunk];
+  __shared__ VT vs[kChunk];
+  __shared__ int64_t rps[kSpmvMaxTileRows + 1];
+  __shared__ double sj_s;
+  const int tid = threadIdx.x;
+  if (tid == 0) sj_s = step_gate(d, j, blockIdx.x == 0);
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+  const VT* __restrict__ val = static_cast<const VT*>(d.val);
+  const int32_t* __restrict__ col = d.col;
+  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  const double2* __restrict__ halo = d.halo;
+  const int64_t n = d.n;
+  constexpr int RPT = kSpmvMaxTileRows / kThreads;
+  for (int64_t t = blockIdx.x; t < d.ntiles; t += gridDim.x) {
+    const int64_t ra = __ldg(d.tile_row + t), rb = __ldg(d.tile_row + t + 1);
+    const int rows = (int)(rb - ra);
+    for (int i = tid; i <= rows; i += kThreads) rps[i] = __ldg(d.rowptr + ra + i);
+    __syncthreads();
+    const int64_t b = rps[0], e = rps[rows];
+    double2 acc[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) acc[u] = make_double2(0.0, 0.0);
+    for (int64_t cb = b; cb < e; cb += kChunk) {
+      const int cnt = (int)min((int64_t)kChunk, e - cb);
+#pragma unroll
+      for (int u = 0; u < kSpmvE; ++u) {
+        const int q = tid + u * kThreads;
+        if (q < cnt) { cs[q] = __ldg(col + cb + q); vs[q] = __ldg(val + cb + q); }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int i = tid + u * kThreads;
+        if (i < rows) {
+          const int lo = (int)(max(rps[i], cb) - cb), hi = (int)(min(rps[i + 1], cb + cnt) - cb);
+          int q = lo;
+          for (; q + 4 <= hi; q += 4) {
+            double2 xx[4];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) { const int c = cs[q + w]; xx[w] = (c < n) ? __ldg(x + c) : __ldg(halo + (c - n)); }
+#pragma unroll
+            for (int w = 0; w < 4; ++w) acc[u] = cadd(acc[u], ValT<CPLX>::mul(vs[q + w], xx[w]));
+          }
+          for (; q < hi; ++q) {
+            const int c = cs[q];
+            acc[u] = cadd(acc[u], ValT<CPLX>::mul(vs[q], (c < n) ? __ldg(x + c) : __ldg(halo + (c - n))));
+          }
         }
       }
       __syncthreads();
@@ -1304,6 +1531,8 @@ cudaError_t configure_kernels() {
   TE_SET(1) TE_SET(2) TE_SET(3) TE_SET(4) TE_SET(5) TE_SET(6) TE_SET(7) TE_SET(8)
 #undef TE_SET
   set((const void*)k_proj_tma<0>, kProjSmemBudget + 1024);
+  set((const void*)k_spmv_tma<false>, kProjSmemBudget + 1024);
+  set((const void*)k_spmv_tma<true>, kProjSmemBudget + 1024);
   set((const void*)k_proj_tma<1>, kProjSmemBudget + 1024);
   status = err;
   return status;
@@ -1324,6 +1553,18 @@ static int tpr_for(int ncols, int min_tpr) {
   }
 
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
+  if (L.spmv_tiled == 3 && d.ntiles > 0) {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(8 * L.num_sms, d.ntiles));
+    if (cplx) k_spmv_rowtile<true><<<grid, kThreads, 0, L.stream>>>(d, j);
+    else k_spmv_rowtile<false><<<grid, kThreads, 0, L.stream>>>(d, j);
+    return;
+  }
+  if (L.spmv_tiled == 2 && d.ntiles_desc > 0) {
+    const int S = spmv_slots(cplx);
+    if (cplx) k_spmv_tma<true><<<L.num_sms, kProjThreads, spmv_smem_bytes(true), L.stream>>>(d, j, S);
+    else k_spmv_tma<false><<<L.num_sms, kProjThreads, spmv_smem_bytes(false), L.stream>>>(d, j, S);
+    return;
+  }
   if (L.spmv_tiled && d.ntiles > 0) {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(8 * L.num_sms, d.ntiles));
     if (cplx) k_spmv_tile<true><<<grid, kThreads, 0, L.stream>>>(d, j);

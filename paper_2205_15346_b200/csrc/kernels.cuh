@@ -20,6 +20,8 @@ constexpr int kSpmvRows = 256;       // K1 row tile
 constexpr int kSpmvChunk = 4096;     // K1 products staged in shared memory per chunk
 constexpr int kSpmvTileNnz = 1024;   // nominal entries per nnz-balanced SpMV tile
 constexpr int kSpmvMaxTileRows = 512;   // rows per SpMV tile cap
+constexpr int kSpmvTmaNnzCap = 512;     // entries per TMA SpMV tile (== kSpmvTmaNnz)
+constexpr int kSpmvTmaRowCap = 128;     // rows per TMA SpMV tile
 
 struct KDev {
   int64_t n;            // local rows
@@ -31,6 +33,8 @@ struct KDev {
   const void* val;
   const int64_t* tile_row;  // [ntiles+1] first row of each nnz-balanced SpMV tile
   int64_t ntiles;
+  const int64_t* tile_desc;  // [2*(ntiles_desc+1)] {first row, first entry} of the TMA SpMV tiles
+  int64_t ntiles_desc;
   const double2* halo;  // x entries for columns >= n (distributed); nullptr otherwise
   double* s;            // [m_cap+1] column scales
   double* alpha;        // [m_cap]
@@ -53,7 +57,7 @@ struct Launch {
   const CUtensorMap* tmaps;  // [kMaxCols] 2-D maps of V, box = 64 doubles x (k+1) columns
   int spmv_tpr;  // lanes per row of the standalone CSR-vector SpMV
   int proj_tma;   // 2: hybrid by column count (default), 1: TMA-tiled only, 0: register/shuffle only
-  int spmv_tiled; // 1: nnz-balanced tiled SpMV (default), 0: CSR-vector
+  int spmv_tiled; // 2: TMA-fed SpMV (default), 1: nnz-balanced tiled SpMV, 0: CSR-vector
   int prefetch; // L2 bulk-prefetch distance in block iterations (0: off)
   int variant;  // 2: SpMV + TMA-tiled projections (default); 0: register-streaming K1/K2;
                 //    1: shared-memory / bulk-copy staged K1/K2

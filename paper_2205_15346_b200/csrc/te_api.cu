@@ -107,9 +107,11 @@ struct te_handle {
   bool profile = false;
   int variant = 2;
   int spmv_tpr = 4;
-  int spmv_tiled = 1;
+  int spmv_tiled = 3;
   int64_t* d_tile_row = nullptr;
   int64_t ntiles = 0;
+  int64_t* d_tile_desc = nullptr;
+  int64_t ntiles_desc = 0;
   std::vector<CUtensorMap> tmaps;
   int prefetch = 0;
   cudaEvent_t ev0[kEvPool], ev1[kEvPool];
@@ -148,6 +150,8 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.halo = h->d_halo;
   d.tile_row = h->d_tile_row;
   d.ntiles = h->ntiles;
+  d.tile_desc = h->d_tile_desc;
+  d.ntiles_desc = h->ntiles_desc;
   d.alpha = h->d_small + kOffAlpha;
   d.beta = h->d_small + kOffBeta;
   d.flag = reinterpret_cast<int*>(h->d_small + kOffFlag);
@@ -534,10 +538,13 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
   h->stream = h->own_stream;
   if (te::configure_kernels() != cudaSuccess) return fail(TE_ERR_CUDA, "kernel shared-memory configuration failed");
   const size_t vb = cplx ? 16 : 8;
-  if (cudaMalloc(&h->d_rowptr, sizeof(int64_t) * (n + 1)) != cudaSuccess) return fail(TE_ERR_OOM, "rowptr alloc");
-  if (cudaMalloc(&h->d_col, sizeof(int32_t) * std::max<int64_t>(1, h->nnz)) != cudaSuccess)
-    return fail(TE_ERR_OOM, "col alloc");
-  if (cudaMalloc(&h->d_val, vb * std::max<int64_t>(1, h->nnz)) != cudaSuccess) return fail(TE_ERR_OOM, "val alloc");
+  // padded by a few entries: the TMA SpMV's bulk copies round ranges out to 16-byte boundaries
+  if (cudaMalloc(&h->d_rowptr, sizeof(int64_t) * (n + 4)) != cudaSuccess) return fail(TE_ERR_OOM, "rowptr alloc");
+  if (cudaMalloc(&h->d_col, sizeof(int32_t) * (h->nnz + 8)) != cudaSuccess) return fail(TE_ERR_OOM, "col alloc");
+  if (cudaMalloc(&h->d_val, vb * (h->nnz + 4)) != cudaSuccess) return fail(TE_ERR_OOM, "val alloc");
+  cudaMemsetAsync(h->d_rowptr, 0, sizeof(int64_t) * (n + 4), h->stream);
+  cudaMemsetAsync(h->d_col, 0, sizeof(int32_t) * (h->nnz + 8), h->stream);
+  cudaMemsetAsync(h->d_val, 0, vb * (h->nnz + 4), h->stream);
   cudaMemcpyAsync(h->d_rowptr, rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, h->stream);
   if (h->nnz > 0) {
     cudaMemcpyAsync(h->d_col, col, sizeof(int32_t) * h->nnz, cudaMemcpyHostToDevice, h->stream);
@@ -562,6 +569,26 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     h->ntiles = (int64_t)tr.size() - 1;
     if (cudaMalloc(&h->d_tile_row, sizeof(int64_t) * tr.size()) != cudaSuccess) return fail(TE_ERR_OOM, "tiles");
     cudaMemcpyAsync(h->d_tile_row, tr.data(), sizeof(int64_t) * tr.size(), cudaMemcpyHostToDevice, h->stream);
+    // TMA SpMV tiles: <= kSpmvTmaNnzCap entries and <= kSpmvTmaRowCap rows; descriptors
+    // {first row, first entry} (a longer single row becomes a tile of its own)
+    std::vector<int64_t> td;
+    int64_t st = 0;
+    td.push_back(0);
+    td.push_back(0);
+    for (int64_t r = 0; r < n; ++r) {
+      const bool over_rows = (r + 1 - st) > te::kSpmvTmaRowCap;
+      const bool over_nnz = (rowptr[r + 1] - rowptr[st]) > te::kSpmvTmaNnzCap && r > st;
+      if (over_rows || over_nnz) {
+        td.push_back(r);
+        td.push_back(rowptr[r]);
+        st = r;
+      }
+    }
+    td.push_back(n);
+    td.push_back(rowptr[n]);
+    h->ntiles_desc = (int64_t)td.size() / 2 - 1;
+    if (cudaMalloc(&h->d_tile_desc, sizeof(int64_t) * td.size()) != cudaSuccess) return fail(TE_ERR_OOM, "tiles");
+    cudaMemcpyAsync(h->d_tile_desc, td.data(), sizeof(int64_t) * td.size(), cudaMemcpyHostToDevice, h->stream);
     cudaStreamSynchronize(h->stream);
   }
   // validation + ||H||_1 on the device
@@ -641,6 +668,7 @@ void te_destroy(te_handle* h) {
   cudaFree(h->d_counter);
   cudaFree(h->d_halo);
   cudaFree(h->d_tile_row);
+  cudaFree(h->d_tile_desc);
   cudaFree(h->d_sendbuf);
   cudaFree(h->d_send_idx);
   if (h->h_small) cudaFreeHost(h->h_small);
@@ -760,6 +788,11 @@ int te_set_option(te_handle* h, int option, double value) {
       if (value < 0.0 || value > 4.0 || value != (double)(int)value)
         return set_err(TE_ERR_ARG, "TE_OPT_KERNELS must be 0..4");
       h->variant = (int)value;
+      return TE_OK;
+    case TE_OPT_SPMV:
+      if (value != 0.0 && value != 1.0 && value != 2.0 && value != 3.0)
+        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 0..3");
+      h->spmv_tiled = (int)value;
       return TE_OK;
     case TE_OPT_PREFETCH:
       if (value < 0 || value > 16) return set_err(TE_ERR_ARG, "TE_OPT_PREFETCH must be in [0, 16]");

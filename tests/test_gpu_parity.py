@@ -35,12 +35,17 @@ def small_cases():
 CASES = small_cases()
 
 
-@pytest.mark.parametrize("variant", [2, 3, 4, 0, 1], ids=["hybrid", "tma", "shuffle", "register", "staged"])
+KERNEL_SETS = [(2, 3), (2, 1), (2, 2), (2, 0), (3, 3), (4, 3), (0, 3), (1, 3)]
+KERNEL_IDS = ["hybrid-spmvrow", "hybrid-spmvtile", "hybrid-spmvtma", "hybrid-spmvvec", "tma", "shuffle", "fused-register", "staged"]
+
+
+@pytest.mark.parametrize("kset", KERNEL_SETS, ids=KERNEL_IDS)
 @pytest.mark.parametrize("name,c", CASES, ids=[x[0] for x in CASES])
-def test_krylov_basis_matches_oracle(gpu_lib, name, c, variant):
+def test_krylov_basis_matches_oracle(gpu_lib, name, c, kset):
     te = gpu_lib
     h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
-    te.te_set_option(h, te.TE_OPT_KERNELS, variant)
+    te.te_set_option(h, te.TE_OPT_KERNELS, kset[0])
+    te.te_set_option(h, te.TE_OPT_SPMV, kset[1])
     m = min(c["m"], c["n"])
     tol_rate = c["tol"] / c["t"]
     g = te.te_krylov_basis(h, c["v0"], m, tol_rate, want_V=True)
