@@ -230,3 +230,20 @@ def test_full_size_xxz_L20_neel(gpu_lib):
     r1 = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], tau1, c["tol"], c["m"], schedule=[tau1])
     assert np.linalg.norm(v1 - r1["v"]) <= 1e-10
     h.close()
+
+
+def test_distributed_api_single_rank(gpu_lib):
+    """te_dist_init / te_create_csr_dist on one rank (global columns, halo plan, no NCCL
+    traffic) gives the same evolution as the plain handle."""
+    te = gpu_lib
+    c = configs.build(3, L=8, N=8)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    v1, s1 = te.te_evolve(h, c["v0"], 2.0, 1e-9, 30)
+    D = te.te_dist_init(1, 0, b"\0" * 128)
+    hd = te.te_create_csr_dist(D, c["n"], 0, c["n"], c["rowptr"], c["col"].astype(np.int64), c["val"])
+    v2, s2 = te.te_evolve(hd, c["v0"], 2.0, 1e-9, 30)
+    assert np.array_equal(v1, v2) and s1["n_restarts"] == s2["n_restarts"]
+    assert s1["one_norm"] == s2["one_norm"]
+    hd.close()
+    h.close()
+    D.close()
