@@ -43,6 +43,9 @@ static int set_err(int code, const char* fmt, ...) {
 static void clear_err() {
   g_status = TE_OK;
   g_msg.clear();
+  // the runtime's last-error slot is per thread and shared with every other CUDA user in it
+  // (e.g. torch): drop anything left there so only this call's own failures are reported
+  (void)cudaGetLastError();
 }
 
 #define CK(call)                                                                              \
@@ -70,7 +73,7 @@ struct te_dist {
 
 namespace {
 constexpr int kProfKernels = 7;  // 0 spmv(_proj) 1 update_proj 2 update_norm 3 combine 4 halo 5 proj_dots 6 host
-constexpr int kEvPool = 3 * te::kMaxCols + 16;
+constexpr int kEvPool = 4 * te::kMaxCols + 16;
 struct Sched {
   double tau;
   int32_t m_eff;
@@ -119,9 +122,24 @@ struct te_handle {
   double ev_bytes[kEvPool];
   int ev_used = 0;
   bool ev_ready = false;
+  cudaEvent_t evk0 = nullptr, evk1 = nullptr;  // V.omega (outside the per-restart graph)
+  bool evk_pending = false;
+  double evk_bytes = 0.0;
   te_kernel_profile prof[kProfKernels];
   int64_t launches = 0;
   std::vector<Sched> sched;
+  // CUDA graph of one restart's launches (replayed every restart)
+  bool use_graph = true;
+  bool capturing = false;
+  cudaGraphExec_t gexec = nullptr;
+  int g_m = -1, g_variant = -1, g_spmv = -1;
+  bool g_profile = false;
+  double g_tol_rate = -1.0;
+  const void* g_V = nullptr;
+  int64_t g_launches = 0;
+  int g_nev = 0;
+  int g_ev_cls[kEvPool];
+  double g_ev_bytes[kEvPool];
   // distributed
   te_dist* dist = nullptr;
   int64_t n_halo = 0;
@@ -243,6 +261,7 @@ int ensure_workspace(te_handle* h, int m) {
     h->d_V = nullptr;
     return set_err(TE_ERR_OOM, "cannot allocate the Krylov basis (%zu bytes)", bytes);
   }
+  CK(cudaMemset(h->d_V, 0, bytes));
   CK(cudaMalloc(&h->d_W, sizeof(double2) * (size_t)h->ldv));
   h->m_cap = m;
   return build_tensor_maps(h);
@@ -256,9 +275,13 @@ void prof_begin(te_handle* h) {
       cudaEventCreate(&h->ev0[i]);
       cudaEventCreate(&h->ev1[i]);
     }
+    cudaEventCreate(&h->evk0);
+    cudaEventCreate(&h->evk1);
     h->ev_ready = true;
   }
-  if (h->ev_used < kEvPool) cudaEventRecord(h->ev0[h->ev_used], h->stream);
+  // external record: inside stream capture this becomes a timing event-record node of the graph
+  if (h->ev_used < kEvPool)
+    cudaEventRecordWithFlags(h->ev0[h->ev_used], h->stream, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
 }
 void prof_end(te_handle* h, int cls, double bytes) {
   ++h->launches;
@@ -269,12 +292,20 @@ void prof_end(te_handle* h, int cls, double bytes) {
     if (e != cudaSuccess) fprintf(stderr, "[te] kernel class %d failed: %s\n", cls, cudaGetErrorString(e));
   }
   if (!h->profile || h->ev_used >= kEvPool) return;
-  cudaEventRecord(h->ev1[h->ev_used], h->stream);
+  cudaEventRecordWithFlags(h->ev1[h->ev_used], h->stream, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
   h->ev_cls[h->ev_used] = cls;
   h->ev_bytes[h->ev_used] = bytes;
   ++h->ev_used;
 }
 void prof_collect(te_handle* h) {
+  if (h->evk_pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->evk0, h->evk1);
+    h->prof[3].launches += 1;
+    h->prof[3].total_ms += ms;
+    h->prof[3].alg_bytes += h->evk_bytes;
+    h->evk_pending = false;
+  }
   for (int i = 0; i < h->ev_used; ++i) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, h->ev0[i], h->ev1[i]);
@@ -320,46 +351,125 @@ int halo_exchange(te_handle* h, int j) {
 // ---------------------------------------------------------------- one Krylov decomposition
 // Launch the whole restart (Alg. 1 step 1) without host synchronisation: the kernels gate
 // themselves on the device breakdown flag.  Then one D2H of alpha/beta/flag.
-int run_arnoldi(te_handle* h, int m, double tol_rate) {
+#define LCHECK(name)                                                                        \
+  do {                                                                                      \
+    cudaError_t e_ = cudaGetLastError();                                                    \
+    if (e_ != cudaSuccess) return set_err(TE_ERR_CUDA, "launch of %s (step j=%d): %s", name, \
+                                          (int)lj, cudaGetErrorString(e_));                 \
+  } while (0)
+
+int issue_arnoldi(te_handle* h, int m, double tol_rate) {
+  int lj = -1;
   KDev d = make_kdev(h, tol_rate, m);
   Launch L = make_launch(h);
   const double n = (double)h->n;
   const double bh = (double)h->nnz * ((h->cplx ? 16.0 : 8.0) + 4.0) + 8.0 * (n + 1.0);
-  te::launch_restart_init(d, L);
+  te::launch_restart_init(d, L); LCHECK("restart_init");
   ++h->launches;
   for (int j = 0; j < m; ++j) {
+    lj = j;
     int rc = halo_exchange(h, j);
     if (rc) return rc;
     const double ncols = j + 1;
     if (h->variant >= 2) {
       prof_begin(h);
-      te::launch_spmv(d, h->cplx, j, L);
+      te::launch_spmv(d, h->cplx, j, L); LCHECK("spmv");
       prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
       prof_begin(h);
-      te::launch_proj_dots(d, j, L);
+      te::launch_proj_dots(d, j, L); LCHECK("proj_dots");
       prof_end(h, 5, 16.0 * n * ncols + 16.0 * n);
     } else {
       prof_begin(h);
-      te::launch_spmv_proj(d, h->cplx, j, L);
+      te::launch_spmv_proj(d, h->cplx, j, L); LCHECK("spmv_proj");
       prof_end(h, 0, bh + 16.0 * n + 16.0 * n * ncols + 16.0 * n);
     }
     if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g1), 2 * (size_t)(j + 1)))) return rc;
     prof_begin(h);
-    te::launch_update_proj(d, j, L);
+    te::launch_update_proj(d, j, L); LCHECK("update_proj");
     prof_end(h, 1, 16.0 * n * ncols + 32.0 * n);
     if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g2), 2 * (size_t)(j + 1)))) return rc;
     const bool write = j + 1 < m;
     prof_begin(h);
-    te::launch_update_norm(d, j, write, L);
+    te::launch_update_norm(d, j, write, L); LCHECK("update_norm");
     prof_end(h, 2, 16.0 * n * ncols + 16.0 * n + (write ? 16.0 * n : 0.0));
     if ((rc = allreduce_sum(h, d.nrm2 + j, 1))) return rc;
   }
-  te::launch_finalize(d, m - 1, L);
+  te::launch_finalize(d, m - 1, L); LCHECK("finalize");
   ++h->launches;
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(h->h_small, h->d_small, sizeof(double) * (kOffFlag + 2), cudaMemcpyDeviceToHost, h->stream));
+  return TE_OK;
+}
+
+// One restart's Arnoldi decomposition.  With graphs on (default, single rank) the launch sequence
+// is captured once per (m, tol_rate, kernel set, basis allocation, profiling) and replayed; the
+// profiling events are captured as event-record nodes and read back after each replay.
+int run_arnoldi(te_handle* h, int m, double tol_rate) {
+  // profiling uses per-launch CUDA events, which graphs do not time: direct launches then
+  const bool graph = h->use_graph && !h->profile && (!h->dist || h->dist->nranks == 1);
+  if (!graph) {
+    int rc = issue_arnoldi(h, m, tol_rate);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(h->stream));
+    if (h->profile) prof_collect(h);
+    return TE_OK;
+  }
+  const bool hit = h->gexec && h->g_m == m && h->g_tol_rate == tol_rate && h->g_variant == h->variant &&
+                   h->g_spmv == h->spmv_tiled && h->g_profile == h->profile && h->g_V == (const void*)h->d_V;
+  if (!hit) {
+    if (h->gexec) {
+      cudaGraphExecDestroy(h->gexec);
+      h->gexec = nullptr;
+    }
+    if (h->profile && !h->ev_ready) prof_begin(h);  // make sure the event pool exists
+    cudaStream_t user = h->stream;
+    h->stream = h->own_stream;
+    const int64_t l0 = h->launches;
+    const int ev0 = h->ev_used;
+    CK(cudaStreamBeginCapture(h->own_stream, cudaStreamCaptureModeThreadLocal));
+    h->capturing = true;
+    int rc = issue_arnoldi(h, m, tol_rate);
+    h->capturing = false;
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(h->own_stream, &g);
+    h->stream = user;
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess) return set_err(TE_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+    ce = cudaGraphInstantiate(&h->gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) {
+      h->gexec = nullptr;
+      return set_err(TE_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+    }
+    h->g_launches = h->launches - l0;
+    h->launches = l0;
+    h->g_nev = h->ev_used - ev0;
+    for (int i = 0; i < h->g_nev; ++i) {
+      h->g_ev_cls[i] = h->ev_cls[ev0 + i];
+      h->g_ev_bytes[i] = h->ev_bytes[ev0 + i];
+    }
+    h->ev_used = ev0;
+    h->g_m = m;
+    h->g_tol_rate = tol_rate;
+    h->g_variant = h->variant;
+    h->g_spmv = h->spmv_tiled;
+    h->g_profile = h->profile;
+    h->g_V = h->d_V;
+  }
+  CK(cudaGraphLaunch(h->gexec, h->stream));
+  h->launches += h->g_launches;
   CK(cudaStreamSynchronize(h->stream));
-  if (h->profile) prof_collect(h);
+  if (h->profile) {
+    for (int i = 0; i < h->g_nev; ++i) {
+      h->ev_cls[i] = h->g_ev_cls[i];
+      h->ev_bytes[i] = h->g_ev_bytes[i];
+    }
+    h->ev_used = h->g_nev;
+    prof_collect(h);
+  }
   return TE_OK;
 }
 
@@ -461,9 +571,17 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
     {
       KDev d = make_kdev(h, tol_rate, m);
       Launch L = make_launch(h);
-      prof_begin(h);
+      if (h->profile) {
+        prof_begin(h);  // creates the event pool on first use
+        cudaEventRecord(h->evk0, h->stream);
+      }
       te::launch_combine(d, h->d_g + 128, m_eff, h->d_V, L);
-      prof_end(h, 3, 16.0 * (double)h->n * (m_eff + 1));
+      ++h->launches;
+      if (h->profile) {
+        cudaEventRecord(h->evk1, h->stream);
+        h->evk_pending = true;
+        h->evk_bytes = 16.0 * (double)h->n * (m_eff + 1);
+      }
     }
     t_now = (tau >= rem) ? t : t_now + tau;
     tau_prev = tau;
@@ -673,11 +791,15 @@ void te_destroy(te_handle* h) {
   cudaFree(h->d_send_idx);
   if (h->h_small) cudaFreeHost(h->h_small);
   if (h->h_coef) cudaFreeHost(h->h_coef);
-  if (h->ev_ready)
+  if (h->ev_ready) {
     for (int i = 0; i < kEvPool; ++i) {
       cudaEventDestroy(h->ev0[i]);
       cudaEventDestroy(h->ev1[i]);
     }
+    cudaEventDestroy(h->evk0);
+    cudaEventDestroy(h->evk1);
+  }
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }
@@ -783,7 +905,8 @@ int te_set_option(te_handle* h, int option, double value) {
       h->ev_used = 0;
       return TE_OK;
     case TE_OPT_GRAPH:
-      return TE_OK;  // launches are issued directly (graph replay: see DESIGN.md next steps)
+      h->use_graph = value != 0.0;
+      return TE_OK;
     case TE_OPT_KERNELS:
       if (value < 0.0 || value > 4.0 || value != (double)(int)value)
         return set_err(TE_ERR_ARG, "TE_OPT_KERNELS must be 0..4");

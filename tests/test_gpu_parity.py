@@ -179,6 +179,17 @@ def test_determinism_and_device_path(gpu_lib):
     v = c["v0"].copy()
     te.te_evolve(h, v, 3.0, 1e-10, 40, out=v)
     assert np.array_equal(v, v1)
+    # direct launches (no CUDA graph replay) and profiling events give the same bits
+    te.te_set_option(h, te.TE_OPT_GRAPH, 0)
+    v4, s4 = te.te_evolve(h, c["v0"], 3.0, 1e-10, 40)
+    assert np.array_equal(v4, v1) and s4 == s1
+    te.te_set_option(h, te.TE_OPT_GRAPH, 1)
+    te.te_set_option(h, te.TE_OPT_PROFILE, 1)
+    v5, s5 = te.te_evolve(h, c["v0"], 3.0, 1e-10, 40)
+    assert np.array_equal(v5, v1)
+    prof = te.te_get_profile(h)
+    assert prof["spmv"]["launches"] == s5["n_krylov_steps"] and prof["combine"]["launches"] == s5["n_restarts"]
+    assert all(p["total_ms"] > 0 for k, p in prof.items() if p["launches"] and k != "host_step")
     h.close()
 
 
