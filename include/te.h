@@ -136,8 +136,9 @@ enum {
                                   bulk-copy staged K2                                                */
   TE_OPT_PREFETCH = 4,       /* L2 bulk-prefetch distance (block iterations, 0..16; default 0)     */
   TE_OPT_SPMV = 5            /* SpMV kernel of kernel sets 2-4 (same arithmetic, measured choice):
-                                3 (default) nnz-balanced tiles, col/val staged in shared memory,
-                                thread-per-row gathers; 1 nnz-balanced tiles, entry-parallel products;
+                                4 (default) nnz-balanced tiles, rowptr/col/val of the next tile
+                                in flight by cp.async double buffering, thread-per-row gathers;
+                                3 as 4 without the pipeline; 1 nnz-balanced tiles, entry-parallel products;
                                 2 TMA-fed (bulk copies of rowptr/col/val into a shared-memory ring,
                                 warp-specialised); 0 CSR-vector                                       */
 };

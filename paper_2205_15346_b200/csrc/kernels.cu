@@ -1260,6 +1260,145 @@ __global__ void __launch_bounds__(kThreads, 4) k_spmv_rowtile(KDev d, int j) {
   }
 }
 
+// SpMV variant 4 (default): the row-tile SpMV software-pipelined with cp.async double buffering.
+// While the threads gather x for the rows of tile t (one thread per row, entries from shared
+// memory), the rowptr/col/val ranges of tile t+1 are already in flight into the other buffer and
+// the descriptors of tile t+2 are being loaded.  A tile whose single row exceeds the buffer is
+// summed straight from global memory by the whole block (fixed-order block reduction).
+__device__ __forceinline__ void cp_async4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+struct TileDesc { int64_t ra, rb, b, e; };
+
+template <bool CPLX>
+size_t spmv_pipe_smem() {
+  using VT = typename ValT<CPLX>::T;
+  return 2 * ((size_t)(kSpmvMaxTileRows + 2) * 8 + (size_t)kSpmvTileNnz * 4 + (size_t)kSpmvTileNnz * sizeof(VT));
+}
+
+template <bool CPLX>
+__global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
+  using VT = typename ValT<CPLX>::T;
+  extern __shared__ __align__(16) unsigned char smp[];
+  // buffer b at smp + b * kBuf: [val kChunk][rowptr kSpmvMaxTileRows+2][col kChunk]
+  constexpr size_t kVal = (size_t)kSpmvTileNnz * sizeof(VT), kRp = (size_t)(kSpmvMaxTileRows + 2) * 8;
+  constexpr size_t kBuf = kVal + kRp + (size_t)kSpmvTileNnz * 4;
+  auto vs_of = [&](int b) { return reinterpret_cast<VT*>(smp + b * kBuf); };
+  auto rp_of = [&](int b) { return reinterpret_cast<int64_t*>(smp + b * kBuf + kVal); };
+  auto cs_of = [&](int b) { return reinterpret_cast<int32_t*>(smp + b * kBuf + kVal + kRp); };
+  __shared__ double sj_s;
+  __shared__ double2 red[kWarps];
+  const int tid = threadIdx.x;
+  if (tid == 0) sj_s = step_gate(d, j, blockIdx.x == 0);
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+  const VT* __restrict__ val = static_cast<const VT*>(d.val);
+  const int32_t* __restrict__ col = d.col;
+  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  const double2* __restrict__ halo = d.halo;
+  const int64_t n = d.n;
+  const int64_t G = gridDim.x;
+  constexpr int RPT = kSpmvMaxTileRows / kThreads;
+
+  auto desc = [&](int64_t t) {
+    TileDesc td{0, 0, 0, 0};
+    if (t < d.ntiles) {
+      td.ra = __ldg(d.tile_row + t);
+      td.rb = __ldg(d.tile_row + t + 1);
+      td.b = __ldg(d.rowptr + td.ra);
+      td.e = __ldg(d.rowptr + td.rb);
+    }
+    return td;
+  };
+  auto issue = [&](const TileDesc& td, int bsel, int64_t t) {
+    if (t < d.ntiles) {
+      const int rows = (int)(td.rb - td.ra);
+      for (int i = tid; i <= rows; i += kThreads) cp_async8(rp_of(bsel) + i, d.rowptr + td.ra + i);
+      const int64_t cnt = td.e - td.b;
+      if (cnt <= kSpmvTileNnz) {
+        for (int q = tid; q < cnt; q += kThreads) {
+          cp_async4(cs_of(bsel) + q, col + td.b + q);
+          if constexpr (CPLX) cp_async16(vs_of(bsel) + q, val + td.b + q);
+          else cp_async8(vs_of(bsel) + q, val + td.b + q);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+
+  const int64_t t0 = blockIdx.x;
+  TileDesc cur = desc(t0);
+  TileDesc nxt = desc(t0 + G);
+  issue(cur, 0, t0);
+  for (int64_t it = 0;; ++it) {
+    const int64_t t = t0 + it * G;
+    if (t >= d.ntiles) break;
+    const int bsel = (int)(it & 1);
+    issue(nxt, bsel ^ 1, t + G);                // tile t+G in flight during this tile's gathers
+    const TileDesc nn = desc(t + 2 * G);        // descriptor loads in flight as well
+    cp_async_wait1();
+    __syncthreads();
+    const int rows = (int)(cur.rb - cur.ra);
+    const int64_t cnt = cur.e - cur.b;
+    if (cnt <= kSpmvTileNnz) {
+      const int64_t* rp = rp_of(bsel);
+      const int32_t* cc = cs_of(bsel);
+      const VT* vv = vs_of(bsel);
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int i = tid + u * kThreads;
+        if (i < rows) {
+          const int lo = (int)(rp[i] - cur.b), hi = (int)(rp[i + 1] - cur.b);
+          double2 acc = make_double2(0.0, 0.0);
+          for (int q0 = lo; q0 < hi; q0 += 8) {  // 8 gathers in flight, summed in row order
+            double2 xx[8];
+            VT ww[8];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+              if (q0 + w < hi) {
+                const int c = cc[q0 + w];
+                ww[w] = vv[q0 + w];
+                xx[w] = (c < n) ? __ldg(x + c) : __ldg(halo + (c - n));
+              }
+            }
+#pragma unroll
+            for (int w = 0; w < 8; ++w)
+              if (q0 + w < hi) acc = cadd(acc, ValT<CPLX>::mul(ww[w], xx[w]));
+          }
+          __stcs(d.W + cur.ra + i, make_double2(acc.x * sj, acc.y * sj));
+        }
+      }
+    } else {  // one long row, straight from global memory
+      double2 acc = make_double2(0.0, 0.0);
+      for (int64_t q = cur.b + tid; q < cur.e; q += kThreads) {
+        const int c = __ldg(col + q);
+        acc = cadd(acc, ValT<CPLX>::mul(__ldg(val + q), (c < n) ? __ldg(x + c) : __ldg(halo + (c - n))));
+      }
+      acc = warp_sum(acc);
+      if ((tid & 31) == 0) red[tid >> 5] = acc;
+      __syncthreads();
+      if (tid == 0) {
+        double2 s = red[0];
+        for (int w = 1; w < kWarps; ++w) s = cadd(s, red[w]);
+        __stcs(d.W + cur.ra, make_double2(s.x * sj, s.y * sj));
+      }
+    }
+    __syncthreads();                            // buffer bsel free for tile t+2G
+    cur = nxt;
+    nxt = nn;
+  }
+}
+
 // Standalone SpMV p = s_j H V_j -> W (CSR-vector, TPR lanes per row, high occupancy).
 template <bool CPLX, int TPR>
 __global__ void __launch_bounds__(kThreads) k_spmv(KDev d, int j) {
@@ -1532,6 +1671,8 @@ cudaError_t configure_kernels() {
 #undef TE_SET
   set((const void*)k_proj_tma<0>, kProjSmemBudget + 1024);
   set((const void*)k_spmv_tma<false>, kProjSmemBudget + 1024);
+  set((const void*)k_spmv_pipe<false>, spmv_pipe_smem<false>());
+  set((const void*)k_spmv_pipe<true>, spmv_pipe_smem<true>());
   set((const void*)k_spmv_tma<true>, kProjSmemBudget + 1024);
   set((const void*)k_proj_tma<1>, kProjSmemBudget + 1024);
   status = err;
@@ -1553,6 +1694,12 @@ static int tpr_for(int ncols, int min_tpr) {
   }
 
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
+  if (L.spmv_tiled == 4 && d.ntiles > 0) {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cplx ? 1 : 2) * L.num_sms, d.ntiles));
+    if (cplx) k_spmv_pipe<true><<<grid, kThreads, spmv_pipe_smem<true>(), L.stream>>>(d, j);
+    else k_spmv_pipe<false><<<grid, kThreads, spmv_pipe_smem<false>(), L.stream>>>(d, j);
+    return;
+  }
   if (L.spmv_tiled == 3 && d.ntiles > 0) {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(8 * L.num_sms, d.ntiles));
     if (cplx) k_spmv_rowtile<true><<<grid, kThreads, 0, L.stream>>>(d, j);

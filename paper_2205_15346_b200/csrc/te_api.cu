@@ -110,7 +110,7 @@ struct te_handle {
   bool profile = false;
   int variant = 2;
   int spmv_tpr = 4;
-  int spmv_tiled = 3;
+  int spmv_tiled = 4;
   int64_t* d_tile_row = nullptr;
   int64_t ntiles = 0;
   int64_t* d_tile_desc = nullptr;
@@ -913,8 +913,8 @@ int te_set_option(te_handle* h, int option, double value) {
       h->variant = (int)value;
       return TE_OK;
     case TE_OPT_SPMV:
-      if (value != 0.0 && value != 1.0 && value != 2.0 && value != 3.0)
-        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 0..3");
+      if (value < 0.0 || value > 4.0 || value != (double)(int)value)
+        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 0..4");
       h->spmv_tiled = (int)value;
       return TE_OK;
     case TE_OPT_PREFETCH:

@@ -35,8 +35,8 @@ def small_cases():
 CASES = small_cases()
 
 
-KERNEL_SETS = [(2, 3), (2, 1), (2, 2), (2, 0), (3, 3), (4, 3), (0, 3), (1, 3)]
-KERNEL_IDS = ["hybrid-spmvrow", "hybrid-spmvtile", "hybrid-spmvtma", "hybrid-spmvvec", "tma", "shuffle", "fused-register", "staged"]
+KERNEL_SETS = [(2, 4), (2, 3), (2, 1), (2, 2), (2, 0), (3, 4), (4, 4), (0, 4), (1, 4)]
+KERNEL_IDS = ["hybrid-spmvpipe", "hybrid-spmvrow", "hybrid-spmvtile", "hybrid-spmvtma", "hybrid-spmvvec", "tma", "shuffle", "fused-register", "staged"]
 
 
 @pytest.mark.parametrize("kset", KERNEL_SETS, ids=KERNEL_IDS)
