@@ -721,6 +721,31 @@ __device__ __forceinline__ double2 butterfly_colsum(double (&re)[32], double (&i
 //   MODE 1 (sweep-2):  p' = p - V e1 -> W,  g2 = V^H p'      (update + dots on the same tile)
 // Lane = row for the update; the 32 x 32 column sums of a sub-tile come from a butterfly
 // transpose-reduction (31 shuffles per 32 columns), after which lane k owns column k.
+// 16-column variant: re[c], im[c] (c < 16) per lane -> sum over the 32 lanes of column
+// c = lane & 15 (lanes l and l+16 hold the same value)
+__device__ __forceinline__ double2 butterfly_colsum16(double (&re)[16], double (&im)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    re[i] += __shfl_xor_sync(0xffffffffu, re[i], 16);
+    im[i] += __shfl_xor_sync(0xffffffffu, im[i], 16);
+  }
+#pragma unroll
+  for (int s = 8; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double sr = up ? re[i] : re[i + s];
+      const double si = up ? im[i] : im[i + s];
+      const double kr = up ? re[i + s] : re[i];
+      const double ki = up ? im[i + s] : im[i];
+      re[i] = kr + __shfl_xor_sync(0xffffffffu, sr, s);
+      im[i] = ki + __shfl_xor_sync(0xffffffffu, si, s);
+    }
+  }
+  return make_double2(re[0], im[0]);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kProjThreads, 1)
     k_proj_tma(const __grid_constant__ CUtensorMap tmV, KDev d, int j, int S, int R, int C) {
@@ -771,7 +796,12 @@ __global__ void __launch_bounds__(kProjThreads, 1)
       }
     }
   } else if (warp < C) {  // ------- consumers: warp owns slots warp, warp + C, ... (< S)
-    double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+    // columns 0..31: per-lane partial sums over all of this warp's rows, kept in registers and
+    // reduced across lanes once at the end; columns 32..: butterfly per 32-row sub-tile
+    double aR[32], aI[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) aR[c] = aI[c] = 0.0;
+    double2 acc1 = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
     bool more = true;
     for (int64_t base = 0; more; base += S) {
       for (int s = warp; s < S; s += C) {
@@ -803,26 +833,37 @@ __global__ void __launch_bounds__(kProjThreads, 1)
             if (row >= rows) p = make_double2(0.0, 0.0);
             else d.W[r0 + row] = p;
           }
-          // column sums of conj(V) p over the sub-tile's 32 rows
-          for (int cb = 0; cb < ncols; cb += 32) {
-            double re[32], im[32];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
+          for (int c = 0; c < 32; ++c) {
+            if (c < ncols) {
+              const double2 v = Vs[c * TR + row];
+              aR[c] = fma(v.x, p.x, fma(v.y, p.y, aR[c]));   // conj(v) * p
+              aI[c] = fma(v.x, p.y, fma(-v.y, p.x, aI[c]));
+            }
+          }
+          for (int cb = 32; cb < ncols; cb += 16) {  // columns 32..63 in 16-wide butterflies
+            double re[16], im[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
               const int k = cb + c;
               const double2 v = k < ncols ? Vs[k * TR + row] : make_double2(0.0, 0.0);
-              re[c] = v.x * p.x + v.y * p.y;   // conj(v) * p
+              re[c] = v.x * p.x + v.y * p.y;
               im[c] = v.x * p.y - v.y * p.x;
             }
-            const double2 cs = butterfly_colsum(re, im);
-            if (cb == 0) acc0 = cadd(acc0, cs); else acc1 = cadd(acc1, cs);
+            const double2 cs = butterfly_colsum16(re, im);
+            if (cb == 32) acc1 = cadd(acc1, cs); else acc2 = cadd(acc2, cs);
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
     }
+    const double2 acc0 = butterfly_colsum(aR, aI);
     red[warp][lane] = acc0;
-    red[warp][lane + 32] = acc1;
+    if (lane < 16) {
+      red[warp][32 + lane] = acc1;
+      red[warp][48 + lane] = acc2;
+    }
   }
   __syncthreads();
   // block partial in fixed warp order, then the last-CTA reduction
