@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import models
+from . import fast, models
 
 NAMES = {
     1: "random_herm_n4096",
@@ -66,7 +66,8 @@ def build(i: int, with_matrix: bool = True, **ov):
         h = models.xxz_fields(L, seed)
         out["fields"] = h
         if with_matrix:
-            out["rowptr"], out["col"], out["val"] = models.xxz_csr(L, p["J"], p["delta"], h)
+            build_xxz = fast.xxz_csr_fast if L > 22 else models.xxz_csr
+            out["rowptr"], out["col"], out["val"] = build_xxz(L, p["J"], p["delta"], h)
         v0 = np.zeros(n, dtype=np.complex128)
         v0[models.neel_index(L)] = 1.0
         out["v0"] = v0
@@ -76,7 +77,8 @@ def build(i: int, with_matrix: bool = True, **ov):
         h = models.xxz_fields(L, seed)
         out["fields"] = h
         if with_matrix:
-            out["rowptr"], out["col"], out["val"] = models.xxz_csr(L, p["J1"], p["delta"], h, J2=p["J2"])
+            build_xxz = fast.xxz_csr_fast if L > 20 else models.xxz_csr
+            out["rowptr"], out["col"], out["val"] = build_xxz(L, p["J1"], p["delta"], h, J2=p["J2"])
         out["v0"] = models.product_state(L, seed)
     elif i == 3:
         L, N = p["L"], p["N"]
