@@ -1326,7 +1326,7 @@ size_t spmv_pipe_smem() {
   return 2 * ((size_t)(kSpmvMaxTileRows + 2) * 8 + (size_t)kSpmvTileNnz * 4 + (size_t)kSpmvTileNnz * sizeof(VT));
 }
 
-template <bool CPLX>
+template <bool CPLX, int TPR>
 __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
   using VT = typename ValT<CPLX>::T;
   extern __shared__ __align__(16) unsigned char smp[];
@@ -1349,7 +1349,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
   const double2* __restrict__ halo = d.halo;
   const int64_t n = d.n;
   const int64_t G = gridDim.x;
-  constexpr int RPT = kSpmvMaxTileRows / kThreads;
+  const int q = tid % TPR, grp = tid / TPR;  // TPR lanes per row (tiles hold <= kThreads/TPR rows)
 
   auto desc = [&](int64_t t) {
     TileDesc td{0, 0, 0, 0};
@@ -1395,29 +1395,30 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
       const int64_t* rp = rp_of(bsel);
       const int32_t* cc = cs_of(bsel);
       const VT* vv = vs_of(bsel);
+      {  // group grp owns row grp of the tile (tiles hold <= kThreads/TPR rows); lane q takes
+         // entries lo+q, lo+q+TPR, ... (8 gathers in flight), then a fixed-order xor reduction
+        const int i = grp;
+        const bool act = i < rows;
+        const int lo = act ? (int)(rp[i] - cur.b) : 0, hi = act ? (int)(rp[i + 1] - cur.b) : 0;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int q0 = lo + q; q0 < hi; q0 += 8 * TPR) {
+          double2 xx[8];
+          VT ww[8];
 #pragma unroll
-      for (int u = 0; u < RPT; ++u) {
-        const int i = tid + u * kThreads;
-        if (i < rows) {
-          const int lo = (int)(rp[i] - cur.b), hi = (int)(rp[i + 1] - cur.b);
-          double2 acc = make_double2(0.0, 0.0);
-          for (int q0 = lo; q0 < hi; q0 += 8) {  // 8 gathers in flight, summed in row order
-            double2 xx[8];
-            VT ww[8];
-#pragma unroll
-            for (int w = 0; w < 8; ++w) {
-              if (q0 + w < hi) {
-                const int c = cc[q0 + w];
-                ww[w] = vv[q0 + w];
-                xx[w] = (c < n) ? __ldg(x + c) : __ldg(halo + (c - n));
-              }
+          for (int w = 0; w < 8; ++w) {
+            const int e = q0 + w * TPR;
+            if (e < hi) {
+              const int c = cc[e];
+              ww[w] = vv[e];
+              xx[w] = (c < n) ? __ldg(x + c) : __ldg(halo + (c - n));
             }
-#pragma unroll
-            for (int w = 0; w < 8; ++w)
-              if (q0 + w < hi) acc = cadd(acc, ValT<CPLX>::mul(ww[w], xx[w]));
           }
-          __stcs(d.W + cur.ra + i, make_double2(acc.x * sj, acc.y * sj));
+#pragma unroll
+          for (int w = 0; w < 8; ++w)
+            if (q0 + w * TPR < hi) acc = cadd(acc, ValT<CPLX>::mul(ww[w], xx[w]));
         }
+        if (TPR > 1) acc = group_sum<TPR>(acc);
+        if (act && q == 0) __stcs(d.W + cur.ra + i, make_double2(acc.x * sj, acc.y * sj));
       }
     } else {  // one long row, straight from global memory
       double2 acc = make_double2(0.0, 0.0);
@@ -1712,8 +1713,11 @@ cudaError_t configure_kernels() {
 #undef TE_SET
   set((const void*)k_proj_tma<0>, kProjSmemBudget + 1024);
   set((const void*)k_spmv_tma<false>, kProjSmemBudget + 1024);
-  set((const void*)k_spmv_pipe<false>, spmv_pipe_smem<false>());
-  set((const void*)k_spmv_pipe<true>, spmv_pipe_smem<true>());
+#define TE_SETP(T)                                                  \
+  set((const void*)k_spmv_pipe<false, T>, spmv_pipe_smem<false>()); \
+  set((const void*)k_spmv_pipe<true, T>, spmv_pipe_smem<true>());
+  TE_SETP(1) TE_SETP(2) TE_SETP(4) TE_SETP(8)
+#undef TE_SETP
   set((const void*)k_spmv_tma<true>, kProjSmemBudget + 1024);
   set((const void*)k_proj_tma<1>, kProjSmemBudget + 1024);
   status = err;
@@ -1737,8 +1741,16 @@ static int tpr_for(int ncols, int min_tpr) {
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
   if (L.spmv_tiled == 4 && d.ntiles > 0) {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cplx ? 1 : 2) * L.num_sms, d.ntiles));
-    if (cplx) k_spmv_pipe<true><<<grid, kThreads, spmv_pipe_smem<true>(), L.stream>>>(d, j);
-    else k_spmv_pipe<false><<<grid, kThreads, spmv_pipe_smem<false>(), L.stream>>>(d, j);
+    switch (L.spmv_pipe_tpr) {
+#define TE_PIPE(T)                                                                                  \
+  case T:                                                                                           \
+    if (cplx) k_spmv_pipe<true, T><<<grid, kThreads, spmv_pipe_smem<true>(), L.stream>>>(d, j);     \
+    else k_spmv_pipe<false, T><<<grid, kThreads, spmv_pipe_smem<false>(), L.stream>>>(d, j);        \
+    break;
+      TE_PIPE(1) TE_PIPE(2) TE_PIPE(4)
+      default: TE_PIPE(8)
+#undef TE_PIPE
+    }
     return;
   }
   if (L.spmv_tiled == 3 && d.ntiles > 0) {

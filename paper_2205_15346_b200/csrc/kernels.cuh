@@ -56,6 +56,7 @@ struct Launch {
   int grid_k1, grid_k2, grid_k3;
   const CUtensorMap* tmaps;  // [kMaxCols] 2-D maps of V, box = 64 doubles x (k+1) columns
   int spmv_tpr;  // lanes per row of the standalone CSR-vector SpMV
+  int spmv_pipe_tpr;  // lanes per row of the pipelined SpMV (tile row cap = kThreads / this)
   int proj_tma;   // 2: hybrid by column count (default), 1: TMA-tiled only, 0: register/shuffle only
   int spmv_tiled; // 2: TMA-fed SpMV (default), 1: nnz-balanced tiled SpMV, 0: CSR-vector
   int prefetch; // L2 bulk-prefetch distance in block iterations (0: off)

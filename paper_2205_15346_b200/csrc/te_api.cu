@@ -110,6 +110,7 @@ struct te_handle {
   bool profile = false;
   int variant = 2;
   int spmv_tpr = 4;
+  int spmv_pipe_tpr = 1;
   int spmv_tiled = 4;
   int64_t* d_tile_row = nullptr;
   int64_t ntiles = 0;
@@ -197,6 +198,7 @@ Launch make_launch(te_handle* h) {
   L.proj_tma = h->variant == 2 ? 2 : (h->variant == 3 ? 1 : (h->variant == 4 ? 0 : 0));
   L.tmaps = h->tmaps.data();
   L.spmv_tpr = h->spmv_tpr;
+  L.spmv_pipe_tpr = h->spmv_pipe_tpr;
   L.spmv_tiled = h->spmv_tiled;
   L.prefetch = h->prefetch;
   return L;
@@ -669,14 +671,26 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     cudaMemcpyAsync(h->d_val, val, vb * h->nnz, cudaMemcpyHostToDevice, h->stream);
   }
   if (ensure_workspace(h, 1) != TE_OK) return fail(TE_ERR_OOM, "workspace");
+  {  // lanes per row of the pipelined SpMV: <= ~16 gathers per lane per row (1, 2, 4 or 8);
+     // TE_SPMV_TPR overrides (measurement)
+    const double avg = n > 0 ? (double)h->nnz / (double)n : 0.0;
+    int t = 1;
+    while (t < 8 && 16.0 * t < avg) t <<= 1;
+    if (const char* e = getenv("TE_SPMV_TPR")) {
+      const int v = atoi(e);
+      if (v == 1 || v == 2 || v == 4 || v == 8) t = v;
+    }
+    h->spmv_pipe_tpr = t;
+  }
+  const int64_t tile_rows_cap = te::kSpmvMaxTileRows / h->spmv_pipe_tpr;
   {  // nnz-balanced SpMV tiles: close a tile before it would exceed kSpmvTileNnz entries or
-     // kSpmvMaxTileRows rows (a single longer row gets a tile of its own; the kernel chunks it)
+     // 256/tpr rows (a single longer row gets a tile of its own; the kernels chunk it)
     std::vector<int64_t> tr;
     tr.reserve((size_t)(h->nnz / te::kSpmvTileNnz + n / te::kSpmvMaxTileRows + 2));
     int64_t start = 0;
     tr.push_back(0);
     for (int64_t r = 0; r < n; ++r) {
-      const bool over_rows = (r + 1 - start) > te::kSpmvMaxTileRows;
+      const bool over_rows = (r + 1 - start) > tile_rows_cap;
       const bool over_nnz = (rowptr[r + 1] - rowptr[start]) > te::kSpmvTileNnz && r > start;
       if (over_rows || over_nnz) {
         tr.push_back(r);
