@@ -659,10 +659,12 @@ constexpr int kMaxSlots = 32;
 constexpr int kProjThreads = (kConsumers + 1) * 32;
 constexpr size_t kProjSmemBudget = 200 * 1024;
 
-// sub-tiles per TMA tile: at least ~8 KB per tile (a 128-row box is the largest single load)
+// sub-tiles per TMA tile: at least kProjMinTile bytes per tile (fewer, larger TMA operations;
+// a 128-row box is the largest single load).  Measured: tools/micro/mb_proj.cu.
+size_t g_proj_min_tile = 16384;
 int proj_rsub(int ncols) {
   int r = 1;
-  while (r < 4 && (size_t)(ncols + 1) * kTileR * 16 * r < 8192) r <<= 1;
+  while (r < 4 && (size_t)(ncols + 1) * kTileR * 16 * r < g_proj_min_tile) r <<= 1;
   return r;
 }
 static size_t proj_slot_bytes(int ncols) {
@@ -1794,12 +1796,13 @@ static void launch_proj_s(const KDev& d, int j, int mode, const Launch& L) {
   });
 }
 
-// measured on B200 (tools/micro/mb_proj.cu): the register/shuffle kernel streams faster for
-// <= 16 columns (small tiles expose the TMA ring's per-tile cost), the TMA ring above.
-constexpr int kShuffleMaxCols = 16;
+// measured on B200 (tools/micro/mb_proj.cu, 16 KB minimum TMA tiles): the TMA ring is faster
+// for the dots at every column count, the register/shuffle kernel for the update up to 8 columns.
+constexpr int kShuffleMaxColsDots = 0;
+constexpr int kShuffleMaxCols = 8;
 
 void launch_proj_dots(const KDev& d, int j, const Launch& L) {
-  if (L.proj_tma == 0 || (L.proj_tma == 2 && j + 1 <= kShuffleMaxCols)) {
+  if (L.proj_tma == 0 || (L.proj_tma == 2 && j + 1 <= kShuffleMaxColsDots)) {
     launch_proj_s(d, j, 0, L);
     return;
   }

@@ -8,6 +8,7 @@
 using namespace te;
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : (1 << 20);
+  if (argc > 3) g_proj_min_tile = atoll(argv[3]);
   const int mcap = 48;
   const int64_t ldv = (n + 31) / 32 * 32;
   double2 *V, *W, *g, *part; double *small, *partn; unsigned* ctr;
