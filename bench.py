@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--cpu-sample-steps", type=int, default=8)
     ap.add_argument("--kernels", type=int, default=2, help="2 SpMV + shuffle projections, 3 SpMV + TMA projections, 0 fused register, 1 staged")
     ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (library default if unset)")
-    ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel: 2 TMA-fed, 1 tiled, 0 CSR-vector")
+    ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel: 4 pipelined (default) .. 0 CSR-vector")
+    ap.add_argument("--ortho", type=int, default=0, help="0 CGS2 (north star), 1 paper-literal Lanczos (f1)")
     return ap.parse_args()
 
 
@@ -234,6 +235,7 @@ def run_ours(args):
         te.te_set_option(h, te.TE_OPT_PREFETCH, args.prefetch)
     if args.spmv is not None:
         te.te_set_option(h, te.TE_OPT_SPMV, args.spmv)
+    te.te_set_option(h, te.TE_OPT_ORTHO, args.ortho)
     stream = torch.cuda.current_stream(dev)
     d_v0 = torch.from_numpy(np.ascontiguousarray(v0_loc)).to(dev)
     d_out = torch.empty_like(d_v0)
@@ -336,7 +338,8 @@ def run_ours(args):
                    "restarts_per_step": stats[-1]["n_restarts"],
                    "l2": "inputs larger than L2 (V = %.0f MB > 126 MB)" % (16 * nloc * m / 1e6),
                    "parallelism": f"rows{ws}", "kernels": ["fused-register", "staged", "hybrid", "tma", "shuffle"][args.kernels],
-                   "prefetch": args.prefetch, "spmv": args.spmv},
+                   "prefetch": args.prefetch, "spmv": args.spmv,
+                   "ortho": ["cgs2", "lanczos3"][args.ortho]},
         "achieved_hbm_gbs": all_bytes / (all_ms * 1e-3) / 1e9 if all_ms > 0 else None,
         "step_hbm_gbs": all_bytes / (ms * 1e-3) / 1e9,
         "profiled_region_ms_per_step": ms_prof / args.steps,

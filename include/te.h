@@ -135,6 +135,9 @@ enum {
                                 0: register-streaming fused K1/K2; 1: shared-memory staged K1 and
                                   bulk-copy staged K2                                                */
   TE_OPT_PREFETCH = 4,       /* L2 bulk-prefetch distance (block iterations, 0..16; default 0)     */
+  TE_OPT_ORTHO = 6,          /* orthogonalisation: 0 (default) CGS2 against the full basis (reading
+                                C1, BASELINE north star); 1 the paper's 3-term Lanczos recurrence as
+                                printed (Eq. 8; Alg. 1), B_H + 144n bytes/step */
   TE_OPT_SPMV = 5            /* SpMV kernel of kernel sets 2-4 (same arithmetic, measured choice):
                                 4 (default) nnz-balanced tiles, rowptr/col/val of the next tile
                                 in flight by cp.async double buffering, thread-per-row gathers;

@@ -1542,6 +1542,116 @@ __global__ void __launch_bounds__(kThreads) k_update_norm(KDev d, int j, int wri
   finish_scalar(d, nrm, 2, d.nrm2 + j);
 }
 
+// --------------------------------------------------------------------------------------
+// Paper-literal 3-term Lanczos recurrence (Eq. 8; Alg. 1):
+//   p' = p - beta_{j-1} v_{j-1};  a = v_j^H p';  p'' = p' - a v_j;  alpha_j = Re(a)
+// with v_k = s_k V_k.  Two streaming kernels after the SpMV (p' is recomputed, not stored).
+// --------------------------------------------------------------------------------------
+__device__ __forceinline__ void finish_complex(const KDev& d, double2 v, int ctr, double2* out) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ double2 ws[kWarps];
+  v = warp_sum(v);
+  if (lane == 0) ws[warp] = v;
+  __syncthreads();
+  if (tid == 0) {
+    double2 t = ws[0];
+    for (int w = 1; w < kWarps; ++w) t = cadd(t, ws[w]);
+    d.part[(size_t)blockIdx.x * kMaxCols] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int last;
+  if (tid == 0) last = (atomicAdd(&d.counter[ctr], 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ double2 seg[kThreads];
+  const int G = gridDim.x;
+  const int per = (G + kThreads - 1) / kThreads;
+  double2 s = make_double2(0.0, 0.0);
+  const int b0 = tid * per, b1 = min(G, b0 + per);
+  for (int b = b0; b < b1; ++b) s = cadd(s, ld_cg(d.part + (size_t)b * kMaxCols));
+  seg[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    double2 t = make_double2(0.0, 0.0);
+    for (int i = 0; i < kThreads; ++i) t = cadd(t, seg[i]);
+    *out = t;
+    d.counter[ctr] = 0u;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_lanczos_dot(KDev d, int j) {
+  __shared__ int go_s;
+  __shared__ double cb_s, sj_s;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    go_s = (d.flag[0] == 0);
+    cb_s = j > 0 ? d.beta[j - 1] * d.s[j - 1] : 0.0;  // beta_{j-1} v_{j-1} = beta_{j-1} s_{j-1} V_{j-1}
+    sj_s = d.s[j];
+  }
+  __syncthreads();
+  if (!go_s) return;
+  const double cb = cb_s;
+  const int64_t n = d.n, ldv = d.ldv;
+  const double2* Vp = d.V + (int64_t)(j > 0 ? j - 1 : 0) * ldv;
+  const double2* Vj = d.V + (int64_t)j * ldv;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int64_t r = (int64_t)blockIdx.x * kThreads + tid; r < n; r += (int64_t)gridDim.x * kThreads) {
+    double2 p = __ldg(d.W + r);
+    if (j > 0) {
+      const double2 vp = ld_stream(Vp + r);
+      p = make_double2(p.x - cb * vp.x, p.y - cb * vp.y);
+    }
+    acc = cfma_conj(ld_stream(Vj + r), p, acc);
+  }
+  finish_complex(d, acc, 0, d.g1 + j);  // raw sum; a = s_j * g1[j]
+}
+
+__global__ void __launch_bounds__(kThreads) k_lanczos_update(KDev d, int j, int write) {
+  __shared__ int go_s;
+  __shared__ double cb_s;
+  __shared__ double2 ca_s;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    go_s = (d.flag[0] == 0);
+    const double sj = d.s[j];
+    const double2 g = d.g1[j];
+    cb_s = j > 0 ? d.beta[j - 1] * d.s[j - 1] : 0.0;
+    ca_s = make_double2(sj * sj * g.x, sj * sj * g.y);  // a v_j = (s_j g) (s_j V_j)
+    if (go_s && blockIdx.x == 0) d.alpha[j] = sj * g.x;  // alpha_j = Re(a)
+  }
+  __syncthreads();
+  if (!go_s) return;
+  const double cb = cb_s;
+  const double2 ca = ca_s;
+  const int64_t n = d.n, ldv = d.ldv;
+  const double2* Vp = d.V + (int64_t)(j > 0 ? j - 1 : 0) * ldv;
+  const double2* Vj = d.V + (int64_t)j * ldv;
+  double2* out = write ? d.V + (int64_t)(j + 1) * ldv : nullptr;
+  double nrm = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * kThreads + tid; r < n; r += (int64_t)gridDim.x * kThreads) {
+    double2 p = __ldcs(d.W + r);
+    if (j > 0) {
+      const double2 vp = ld_stream(Vp + r);
+      p = make_double2(p.x - cb * vp.x, p.y - cb * vp.y);
+    }
+    const double2 vj = ld_stream(Vj + r);
+    const double2 av = make_double2(ca.x * vj.x - ca.y * vj.y, ca.x * vj.y + ca.y * vj.x);
+    p = make_double2(p.x - av.x, p.y - av.y);
+    if (out) out[r] = p;
+    nrm = fma(p.x, p.x, fma(p.y, p.y, nrm));
+  }
+  finish_scalar(d, nrm, 2, d.nrm2 + j);
+}
+
+void launch_lanczos_dot(const KDev& d, int j, const Launch& L) {
+  k_lanczos_dot<<<L.grid_k3, kThreads, 0, L.stream>>>(d, j);
+}
+void launch_lanczos_update(const KDev& d, int j, bool write, const Launch& L) {
+  k_lanczos_update<<<L.grid_k3, kThreads, 0, L.stream>>>(d, j, write ? 1 : 0);
+}
+
 // ||p''_{m-1}||^2 -> beta_{m-1} = h_{m+1,m} and the final breakdown test (Alg. 1)
 __global__ void k_finalize(KDev d, int j) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;

@@ -70,7 +70,9 @@ void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L);        // K1
 void launch_proj_dots(const KDev& d, int j, const Launch& L);              // K1b: g1 = V^H p (TMA)
 void launch_update_proj(const KDev& d, int j, const Launch& L);            // K2
 void launch_update_norm(const KDev& d, int j, bool write, const Launch& L);// K3
-void launch_finalize(const KDev& d, int j, const Launch& L);               // beta_{m-1}
+void launch_finalize(const KDev& d, int j, const Launch& L);
+void launch_lanczos_dot(const KDev& d, int j, const Launch& L);                // f1: a = v_j^H (p - b v_{j-1})
+void launch_lanczos_update(const KDev& d, int j, bool write, const Launch& L); // f1: p'' and ||p''||^2               // beta_{m-1}
 void launch_combine(const KDev& d, const double2* coef, int m_eff, double2* out, const Launch& L); // K4
 void launch_restart_init(const KDev& d, const Launch& L);                  // flag=0, s[0]=1
 void launch_norm2(const KDev& d, const double2* x, double* out, const Launch& L);

@@ -109,6 +109,7 @@ struct te_handle {
   // profiling / bookkeeping
   bool profile = false;
   int variant = 2;
+  int ortho = 0;  // 0 CGS2 (default), 1 paper-literal 3-term Lanczos (f1)
   int spmv_tpr = 4;
   int spmv_pipe_tpr = 1;
   int spmv_tiled = 4;
@@ -133,7 +134,7 @@ struct te_handle {
   bool use_graph = true;
   bool capturing = false;
   cudaGraphExec_t gexec = nullptr;
-  int g_m = -1, g_variant = -1, g_spmv = -1;
+  int g_m = -1, g_variant = -1, g_spmv = -1, g_ortho = -1;
   bool g_profile = false;
   double g_tol_rate = -1.0;
   const void* g_V = nullptr;
@@ -373,6 +374,22 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
     int rc = halo_exchange(h, j);
     if (rc) return rc;
     const double ncols = j + 1;
+    if (h->ortho == 1) {  // paper-literal Lanczos (Eq. 8 as printed)
+      prof_begin(h);
+      te::launch_spmv(d, h->cplx, j, L); LCHECK("spmv");
+      prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
+      const double nv = j > 0 ? 2.0 : 1.0;
+      prof_begin(h);
+      te::launch_lanczos_dot(d, j, L); LCHECK("lanczos_dot");
+      prof_end(h, 5, 16.0 * n * nv + 16.0 * n);
+      if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g1 + j), 2))) return rc;
+      const bool wr = j + 1 < m;
+      prof_begin(h);
+      te::launch_lanczos_update(d, j, wr, L); LCHECK("lanczos_update");
+      prof_end(h, 2, 16.0 * n * nv + 16.0 * n + (wr ? 16.0 * n : 0.0));
+      if ((rc = allreduce_sum(h, d.nrm2 + j, 1))) return rc;
+      continue;
+    }
     if (h->variant >= 2) {
       prof_begin(h);
       te::launch_spmv(d, h->cplx, j, L); LCHECK("spmv");
@@ -417,6 +434,7 @@ int run_arnoldi(te_handle* h, int m, double tol_rate) {
     return TE_OK;
   }
   const bool hit = h->gexec && h->g_m == m && h->g_tol_rate == tol_rate && h->g_variant == h->variant &&
+                   h->g_ortho == h->ortho &&
                    h->g_spmv == h->spmv_tiled && h->g_profile == h->profile && h->g_V == (const void*)h->d_V;
   if (!hit) {
     if (h->gexec) {
@@ -458,6 +476,7 @@ int run_arnoldi(te_handle* h, int m, double tol_rate) {
     h->g_tol_rate = tol_rate;
     h->g_variant = h->variant;
     h->g_spmv = h->spmv_tiled;
+    h->g_ortho = h->ortho;
     h->g_profile = h->profile;
     h->g_V = h->d_V;
   }
@@ -925,6 +944,10 @@ int te_set_option(te_handle* h, int option, double value) {
       if (value < 0.0 || value > 4.0 || value != (double)(int)value)
         return set_err(TE_ERR_ARG, "TE_OPT_KERNELS must be 0..4");
       h->variant = (int)value;
+      return TE_OK;
+    case TE_OPT_ORTHO:
+      if (value != 0.0 && value != 1.0) return set_err(TE_ERR_ARG, "TE_OPT_ORTHO must be 0 (CGS2) or 1 (Lanczos)");
+      h->ortho = (int)value;
       return TE_OK;
     case TE_OPT_SPMV:
       if (value < 0.0 || value > 4.0 || value != (double)(int)value)

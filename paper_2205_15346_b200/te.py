@@ -27,6 +27,7 @@ TE_OPT_GRAPH = 2
 TE_OPT_KERNELS = 3
 TE_OPT_PREFETCH = 4
 TE_OPT_SPMV = 5
+TE_OPT_ORTHO = 6
 KERNELS = {0: "spmv", 1: "update_proj", 2: "update_norm", 3: "combine", 4: "halo_pack", 5: "proj_dots",
            6: "host_step"}
 

@@ -258,3 +258,29 @@ def test_distributed_api_single_rank(gpu_lib):
     hd.close()
     h.close()
     D.close()
+
+
+@pytest.mark.parametrize("name,c", CASES[:4], ids=[x[0] for x in CASES[:4]])
+def test_lanczos3_mode_matches_oracle(gpu_lib, name, c):
+    """the paper-literal 3-term recurrence (TE_OPT_ORTHO=1) against the oracle's
+    ortho='lanczos3' — same recurrence, same arithmetic up to summation order."""
+    te = gpu_lib
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    te.te_set_option(h, te.TE_OPT_ORTHO, 1)
+    m = min(20, c["n"])
+    tol_rate = c["tol"] / c["t"]
+    g = te.te_krylov_basis(h, c["v0"], m, tol_rate, want_V=True)
+    o = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), c["v0"], m, tol_rate, ortho="lanczos3")
+    assert g["m_eff"] == o["m_eff"]
+    scale = max(1.0, np.abs(o["alpha"]).max(), np.abs(o["beta"]).max())
+    assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-10 * scale
+    assert np.abs(g["beta"] - o["beta"]).max() <= 1e-10 * scale
+    assert np.linalg.norm(g["V"] - o["V"]) <= 1e-8
+    t, tol = min(c["t"], 2.0), c["tol"]
+    v, st = te.te_evolve(h, c["v0"], t, tol, c["m"])
+    sched = te.te_get_schedule(h)
+    ref = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], t, tol, c["m"], ortho="lanczos3",
+                   schedule=[s[0] for s in sched])
+    assert np.linalg.norm(v - ref["v"]) <= 1e-9
+    assert st["err_bound"] <= tol
+    h.close()
