@@ -58,3 +58,12 @@ def test_uniform_involution_is_matching():
     p, pair, ok = models.uniform_involution(n, 1, 100, rows)
     assert ok.all() and np.all(p != rows)
     assert np.array_equal(p[p], rows)
+
+
+def test_fast_xxz_row_range():
+    L, h = 11, models.xxz_fields(11, 3)
+    rp, col, val = models.xxz_csr(L, 1.0, 0.5, h, J2=0.5)
+    r0, r1 = 300, 1500
+    lrp, lcol, lval = fast.xxz_csr_fast(L, 1.0, 0.5, h, J2=0.5, r0=r0, r1=r1)
+    assert np.array_equal(lrp, rp[r0:r1 + 1] - rp[r0])
+    assert np.array_equal(lcol, col[rp[r0]:rp[r1]]) and np.array_equal(lval, val[rp[r0]:rp[r1]])

@@ -14,31 +14,31 @@ static int nbonds(int L, double J2, int* a, int* b, double* J, double J1) {
   return nb;
 }
 
-/* pass 1: row lengths -> rowptr (n+1) */
-void xxz_rowptr(int L, double J1, double J2, int64_t* rowptr) {
+/* pass 1: row lengths of rows [r0, r1) -> local rowptr (r1-r0+1, starting at 0) */
+void xxz_rowptr(int L, double J1, double J2, int64_t r0, int64_t r1, int64_t* rowptr) {
   int a[128], b[128];
   double J[128];
   const int nb = nbonds(L, J2, a, b, J, J1);
-  const int64_t n = (int64_t)1 << L;
+  const int64_t m = r1 - r0;
   rowptr[0] = 0;
 #pragma omp parallel for schedule(static)
-  for (int64_t r = 0; r < n; ++r) {
+  for (int64_t i = 0; i < m; ++i) {
+    const int64_t r = r0 + i;
     int cnt = 1;
     for (int k = 0; k < nb; ++k) cnt += (int)(((r >> a[k]) ^ (r >> b[k])) & 1);
-    rowptr[r + 1] = cnt;
+    rowptr[i + 1] = cnt;
   }
-  for (int64_t r = 0; r < n; ++r) rowptr[r + 1] += rowptr[r];
+  for (int64_t i = 0; i < m; ++i) rowptr[i + 1] += rowptr[i];
 }
 
-/* pass 2: fill col/val */
-void xxz_fill(int L, double J1, double J2, double delta, const double* h, const int64_t* rowptr, int32_t* col,
-              double* val) {
+/* pass 2: fill col (global indices) / val of rows [r0, r1) */
+void xxz_fill(int L, double J1, double J2, double delta, const double* h, int64_t r0, int64_t r1,
+              const int64_t* rowptr, int32_t* col, double* val) {
   int a[128], b[128];
   double J[128];
   const int nb = nbonds(L, J2, a, b, J, J1);
-  const int64_t n = (int64_t)1 << L;
 #pragma omp parallel for schedule(static)
-  for (int64_t r = 0; r < n; ++r) {
+  for (int64_t r = r0; r < r1; ++r) {
     int64_t cc[130];
     double vv[130];
     int m = 0;
@@ -69,7 +69,7 @@ void xxz_fill(int L, double J1, double J2, double delta, const double* h, const 
       cc[q + 1] = c;
       vv[q + 1] = v;
     }
-    int64_t o = rowptr[r];
+    int64_t o = rowptr[r - r0];
     for (int i = 0; i < m; ++i) { col[o + i] = (int32_t)cc[i]; val[o + i] = vv[i]; }
   }
 }

@@ -29,21 +29,23 @@ def _load():
     if _lib is None:
         build()
         _lib = C.CDLL(LIB)
-        _lib.xxz_rowptr.argtypes = [C.c_int, C.c_double, C.c_double, C.c_void_p]
-        _lib.xxz_fill.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
-                                  C.c_void_p]
+        _lib.xxz_rowptr.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_void_p]
+        _lib.xxz_fill.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_int64, C.c_int64,
+                                  C.c_void_p, C.c_void_p, C.c_void_p]
     return _lib
 
 
-def xxz_csr_fast(L, J1, delta, h, J2=0.0):
+def xxz_csr_fast(L, J1, delta, h, J2=0.0, r0=0, r1=None):
+    """CSR of rows [r0, r1) (default: all rows); rowptr local (starts at 0), columns global."""
     lib = _load()
     n = 1 << L
-    rowptr = np.empty(n + 1, dtype=np.int64)
-    lib.xxz_rowptr(L, float(J1), float(J2), rowptr.ctypes.data)
+    r1 = n if r1 is None else r1
+    rowptr = np.empty(r1 - r0 + 1, dtype=np.int64)
+    lib.xxz_rowptr(L, float(J1), float(J2), r0, r1, rowptr.ctypes.data)
     nnz = int(rowptr[-1])
     col = np.empty(nnz, dtype=np.int32)
     val = np.empty(nnz, dtype=np.float64)
     hh = np.ascontiguousarray(h, dtype=np.float64)
-    lib.xxz_fill(L, float(J1), float(J2), float(delta), hh.ctypes.data, rowptr.ctypes.data, col.ctypes.data,
-                 val.ctypes.data)
+    lib.xxz_fill(L, float(J1), float(J2), float(delta), hh.ctypes.data, r0, r1, rowptr.ctypes.data,
+                 col.ctypes.data, val.ctypes.data)
     return rowptr, col, val
