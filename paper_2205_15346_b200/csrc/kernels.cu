@@ -1325,7 +1325,7 @@ struct TileDesc { int64_t ra, rb, b, e; };
 template <bool CPLX>
 size_t spmv_pipe_smem() {
   using VT = typename ValT<CPLX>::T;
-  return 2 * ((size_t)(kSpmvMaxTileRows + 2) * 8 + (size_t)kSpmvTileNnz * 4 + (size_t)kSpmvTileNnz * sizeof(VT));
+  return 2 * ((size_t)(kSpmvMaxTileRows + 4) * 8 + (size_t)(kSpmvTileNnz + 4) * 4 + (size_t)(kSpmvTileNnz + 4) * sizeof(VT));
 }
 
 template <bool CPLX, int TPR>
@@ -1333,18 +1333,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
   using VT = typename ValT<CPLX>::T;
   extern __shared__ __align__(16) unsigned char smp[];
   // buffer b at smp + b * kBuf: [val kChunk][rowptr kSpmvMaxTileRows+2][col kChunk]
-  constexpr size_t kVal = (size_t)kSpmvTileNnz * sizeof(VT), kRp = (size_t)(kSpmvMaxTileRows + 2) * 8;
-  constexpr size_t kBuf = kVal + kRp + (size_t)kSpmvTileNnz * 4;
+  constexpr size_t kVal = (size_t)(kSpmvTileNnz + 4) * sizeof(VT), kRp = (size_t)(kSpmvMaxTileRows + 4) * 8;
+  constexpr size_t kBuf = kVal + kRp + (size_t)(kSpmvTileNnz + 4) * 4;
   auto vs_of = [&](int b) { return reinterpret_cast<VT*>(smp + b * kBuf); };
   auto rp_of = [&](int b) { return reinterpret_cast<int64_t*>(smp + b * kBuf + kVal); };
   auto cs_of = [&](int b) { return reinterpret_cast<int32_t*>(smp + b * kBuf + kVal + kRp); };
   __shared__ double sj_s;
   __shared__ double2 red[kWarps];
+  __shared__ __align__(8) uint64_t bar[2];
   const int tid = threadIdx.x;
-  if (tid == 0) sj_s = step_gate(d, j, blockIdx.x == 0);
+  if (tid == 0) {
+    sj_s = step_gate(d, j, blockIdx.x == 0);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
   const double sj = sj_s;
   if (sj == 0.0) return;
+  const uint64_t pol = policy_evict_first();
   const VT* __restrict__ val = static_cast<const VT*>(d.val);
   const int32_t* __restrict__ col = d.col;
   const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
@@ -1363,22 +1370,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
     }
     return td;
   };
+  // bulk copies (TMA engine, one thread) of the 16-byte-aligned supersets of the tile's rowptr /
+  // col / val ranges into buffer bsel; completion counted on bar[bsel]
   auto issue = [&](const TileDesc& td, int bsel, int64_t t) {
-    if (t < d.ntiles) {
-      const int rows = (int)(td.rb - td.ra);
-      for (int i = tid; i <= rows; i += kThreads) cp_async8(rp_of(bsel) + i, d.rowptr + td.ra + i);
+    if (tid == 0 && t < d.ntiles) {
       const int64_t cnt = td.e - td.b;
+      const int64_t r0 = td.ra & ~1LL, r1 = (td.rb + 2) & ~1LL;
+      unsigned br = (unsigned)((r1 - r0) * 8), bc = 0, bv = 0;
+      int64_t c0 = 0, v0 = 0;
       if (cnt <= kSpmvTileNnz) {
-        for (int q = tid; q < cnt; q += kThreads) {
-          cp_async4(cs_of(bsel) + q, col + td.b + q);
-          if constexpr (CPLX) cp_async16(vs_of(bsel) + q, val + td.b + q);
-          else cp_async8(vs_of(bsel) + q, val + td.b + q);
-        }
+        constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
+        c0 = td.b & ~3LL;
+        v0 = td.b & ~(VA - 1);
+        bc = (unsigned)((((td.e + 3) & ~3LL) - c0) * 4);
+        bv = (unsigned)((((td.e + VA - 1) & ~(VA - 1)) - v0) * sizeof(VT));
       }
+      mbar_expect_tx(&bar[bsel], br + bc + bv);
+      bulk_g2s(rp_of(bsel), d.rowptr + r0, br, &bar[bsel], pol);
+      if (bc) bulk_g2s(cs_of(bsel), col + c0, bc, &bar[bsel], pol);
+      if (bv) bulk_g2s(vs_of(bsel), val + v0, bv, &bar[bsel], pol);
     }
-    cp_async_commit();
   };
-
   const int64_t t0 = blockIdx.x;
   TileDesc cur = desc(t0);
   TileDesc nxt = desc(t0 + G);
@@ -1389,14 +1401,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
     const int bsel = (int)(it & 1);
     issue(nxt, bsel ^ 1, t + G);                // tile t+G in flight during this tile's gathers
     const TileDesc nn = desc(t + 2 * G);        // descriptor loads in flight as well
-    cp_async_wait1();
-    __syncthreads();
+    mbar_wait(&bar[bsel], (unsigned)((it >> 1) & 1));
     const int rows = (int)(cur.rb - cur.ra);
     const int64_t cnt = cur.e - cur.b;
     if (cnt <= kSpmvTileNnz) {
-      const int64_t* rp = rp_of(bsel);
-      const int32_t* cc = cs_of(bsel);
-      const VT* vv = vs_of(bsel);
+      constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
+      const int64_t* rp = rp_of(bsel) + (cur.ra & 1);
+      const int32_t* cc = cs_of(bsel) + (cur.b & 3);
+      const VT* vv = vs_of(bsel) + (cur.b & (VA - 1));
       {  // group grp owns row grp of the tile (tiles hold <= kThreads/TPR rows); lane q takes
          // entries lo+q, lo+q+TPR, ... (8 gathers in flight), then a fixed-order xor reduction
         const int i = grp;
@@ -1438,6 +1450,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
       }
     }
     __syncthreads();                            // buffer bsel free for tile t+2G
+    if (tid == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     cur = nxt;
     nxt = nn;
   }
