@@ -764,6 +764,9 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     const double2 g = d.g1[tid];
     coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);   // e1_k = s_k c1_k
   }
+  // 1024-B alignment through an integer cast: the consumers then read the tiles with generic
+  // LD.E.128 instead of LDS.128 — measured faster here (tools/micro/mb_proj.cu: dots at 23
+  // columns 6.0 vs 4.2 TB/s with the LDS build, which also spills), so kept deliberately
   unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int TR = kTileR * R;
   const size_t vbytes = (size_t)ncols * TR * 16;
@@ -1030,6 +1033,9 @@ __global__ void __launch_bounds__(kProjThreads, 1) k_spmv_tma(KDev d, int j, int
   __shared__ double sj_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int C = kConsumers;
+  // 1024-B alignment through an integer cast: the consumers then read the tiles with generic
+  // LD.E.128 instead of LDS.128 — measured faster here (tools/micro/mb_proj.cu: dots at 23
+  // columns 6.0 vs 4.2 TB/s with the LDS build, which also spills), so kept deliberately
   unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const size_t slot_bytes = kSmRp + kSmCol + (size_t)(kSpmvTmaNnz + 2) * sizeof(VT) + 16;
   unsigned char* slots = smem + C * kSpmvScratch;
