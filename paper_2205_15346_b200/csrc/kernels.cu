@@ -823,17 +823,25 @@ __global__ void __launch_bounds__(kProjThreads, 1)
           if (sub * kTileR >= rows) break;  // warp-uniform
           double2 p = row < rows ? Ws[row] : make_double2(0.0, 0.0);
           if (MODE == 1) {
-            // four independent FMA chains over the columns
-            double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
+            // eight independent FMA chains over the columns, 8 tile loads in flight
+            double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0, a4 = a0, a5 = a0, a6 = a0, a7 = a0;
             int k = 0;
-            for (; k + 4 <= ncols; k += 4) {
-              a0 = cfma(Vs[(k + 0) * TR + row], coef[k + 0], a0);
-              a1 = cfma(Vs[(k + 1) * TR + row], coef[k + 1], a1);
-              a2 = cfma(Vs[(k + 2) * TR + row], coef[k + 2], a2);
-              a3 = cfma(Vs[(k + 3) * TR + row], coef[k + 3], a3);
+            for (; k + 8 <= ncols; k += 8) {
+              const double2 v0 = Vs[(k + 0) * TR + row], v1 = Vs[(k + 1) * TR + row];
+              const double2 v2 = Vs[(k + 2) * TR + row], v3 = Vs[(k + 3) * TR + row];
+              const double2 v4 = Vs[(k + 4) * TR + row], v5 = Vs[(k + 5) * TR + row];
+              const double2 v6 = Vs[(k + 6) * TR + row], v7 = Vs[(k + 7) * TR + row];
+              a0 = cfma(v0, coef[k + 0], a0);
+              a1 = cfma(v1, coef[k + 1], a1);
+              a2 = cfma(v2, coef[k + 2], a2);
+              a3 = cfma(v3, coef[k + 3], a3);
+              a4 = cfma(v4, coef[k + 4], a4);
+              a5 = cfma(v5, coef[k + 5], a5);
+              a6 = cfma(v6, coef[k + 6], a6);
+              a7 = cfma(v7, coef[k + 7], a7);
             }
             for (; k < ncols; ++k) a0 = cfma(Vs[k * TR + row], coef[k], a0);
-            const double2 a = cadd(cadd(a0, a1), cadd(a2, a3));
+            const double2 a = cadd(cadd(cadd(a0, a1), cadd(a2, a3)), cadd(cadd(a4, a5), cadd(a6, a7)));
             p = make_double2(p.x - a.x, p.y - a.y);
             if (row >= rows) p = make_double2(0.0, 0.0);
             else d.W[r0 + row] = p;
