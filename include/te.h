@@ -112,6 +112,15 @@ int te_evolve_dev(te_handle* h, const void* d_v0, double t, double tol, int m_ma
 int te_evolve_schedule(te_handle* h, const te_c128* v0, int64_t k, const double* t_steps,
                        double tol, int m_max, te_c128* v_out, te_stats* stats);
 
+/* As te_evolve, also returning the states at the n_samples ascending times sample_times[] in
+ * [0, t] ("sample its values at intermediate points of time" from the Krylov space of the
+ * step that contains them).  samples_out: host, n_samples x n (sample-major); sample_bounds
+ * (nullable): the error bound of each sample (bound accumulated before its step + the integral
+ * of Eq. 16 up to the sample time). */
+int te_evolve_sampled(te_handle* h, const te_c128* v0, double t, double tol, int m_max, int64_t n_samples,
+                      const double* sample_times, te_c128* samples_out, double* sample_bounds,
+                      te_c128* v_out, te_stats* stats);
+
 /* Schedule of the most recent evolve call: up to cap entries of (tau_k, m_eff_k, e_k).
  * Any output pointer may be NULL.  Returns the number of restarts (may exceed cap). */
 int64_t te_get_schedule(const te_handle* h, int64_t cap, double* t_steps, int32_t* m_eff,
@@ -138,6 +147,9 @@ enum {
   TE_OPT_ORTHO = 6,          /* orthogonalisation: 0 (default) CGS2 against the full basis (reading
                                 C1, BASELINE north star); 1 the paper's 3-term Lanczos recurrence as
                                 printed (Eq. 8; Alg. 1), B_H + 144n bytes/step */
+  TE_OPT_INTEGRATOR = 7,     /* error integral: 0 (default) adaptive tanh-sinh;
+                                1 non-adaptive Gauss-Legendre of order 30 ("simpler and faster",
+                                for explorative runs)                                                 */
   TE_OPT_SPMV = 5            /* SpMV kernel of kernel sets 2-4 (same arithmetic, measured choice):
                                 4 (default) nnz-balanced tiles, rowptr/col/val of the next tile
                                 in flight by cp.async double buffering, thread-per-row gathers;

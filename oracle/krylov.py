@@ -229,6 +229,16 @@ def tanh_sinh(f, a, b, rel=QUAD_REL, max_levels=QUAD_MAX_LEVELS, umax=QUAD_UMAX,
     return cur, False
 
 
+def gauss_legendre(f, a, b, order=30):
+    """Non-adaptive Gauss-Legendre rule of the given order on [a, b] (the paper's optional
+    "non-adaptive Gauss-scheme"; order 30 per SPEC reading).  numpy.leggauss gives the nodes."""
+    if b == a:
+        return 0.0, True
+    x, w = np.polynomial.legendre.leggauss(order)
+    c, hw = 0.5 * (a + b), 0.5 * (b - a)
+    return float(hw * np.sum(w * f(c + hw * x))), True
+
+
 def find_step(integral, breakdown, first, tau_prev, rem, tol_rate, t_total):
     """Largest admissible step per Alg. 1 step 2, P:262, P:332-333,
     Eqs. 18-19; cleaned reading O-6 (C9, C11, C12, C16).
@@ -283,11 +293,15 @@ def omega(lam, U, tau):
 # ---------------------------------------------------------------------------
 
 def evolve(rowptr, col, val, v0, t, tol, m, ortho="cgs2", schedule=None,
-           max_restarts=1_000_000):
+           max_restarts=1_000_000, samples=None, integrator="tanh-sinh"):
     """v(t) ~= exp(-iHt) v0 with the rigorous bound (Alg. 1).
 
     ``schedule`` (optional list of step sizes) forces the step sequence
     (parity mode, reading C16): each step's bound is still integrated.
+    ``samples`` (ascending times in [0, t]): states at intermediate times from the restart
+    whose interval contains them, w_s = V exp(-iT (t_s - t_now)) e_1; returned in
+    res["samples"] with per-sample bounds res["sample_bounds"].
+    ``integrator``: "tanh-sinh" (default, P:222/P:406) or "gauss" (P:406).
     Returns dict(v, bound, restarts, krylov_steps, schedule=[(tau, m_eff, e)],
     warnings, roundoff_step, roundoff_total, breakdowns).
     """
@@ -300,6 +314,13 @@ def evolve(rowptr, col, val, v0, t, tol, m, ortho="cgs2", schedule=None,
     w = np.array(v0, dtype=np.complex128)
     res = dict(bound=0.0, restarts=0, krylov_steps=0, schedule=[], warnings=0,
                breakdowns=0)
+    samples = [] if samples is None else [float(x) for x in samples]
+    res["samples"] = [None] * len(samples)
+    res["sample_bounds"] = [0.0] * len(samples)
+    si = 0
+    while si < len(samples) and samples[si] <= 0.0:       # t_s = 0: the initial state
+        res["samples"][si] = w.copy()
+        si += 1
     norm1 = one_norm(rowptr, col, val, n)
     r_step = n * norm1 * EPS                       # Eq. 17
     res["roundoff_step"] = r_step
@@ -326,7 +347,10 @@ def evolve(rowptr, col, val, v0, t, tol, m, ortho="cgs2", schedule=None,
             return integrand(lam, U, h, tau)
 
         def integral(a, b):
-            v, conv = tanh_sinh(f, a, b, floor=tol_rate * (b - a))
+            if integrator == "gauss":
+                v, conv = gauss_legendre(f, a, b)
+            else:
+                v, conv = tanh_sinh(f, a, b, floor=tol_rate * (b - a))
             if not conv:
                 quad_ok[0] = False
             return v
@@ -337,6 +361,12 @@ def evolve(rowptr, col, val, v0, t, tol, m, ortho="cgs2", schedule=None,
             e = integral(0.0, tau)
         else:
             tau, e = find_step(integral, kr["breakdown"], k == 0, tau_prev, rem, tol_rate, t)
+        t_end = t if tau >= rem else t_now + tau
+        while si < len(samples) and samples[si] <= t_end:  # sample inside this step
+            ds = min(samples[si] - t_now, tau)
+            res["samples"][si] = kr["V"] @ omega(lam, U, ds)
+            res["sample_bounds"][si] = res["bound"] + integral(0.0, ds)
+            si += 1
         om = omega(lam, U, tau)
         w = kr["V"] @ om                           # Eq. 11 / Alg. 1
         t_now = t if tau >= rem else t_now + tau

@@ -138,13 +138,56 @@ QuadResult tanh_sinh(const SmallEig& e, double a, double b, double floor, double
 }
 
 // ------------------------------------------------------------------------------------------
+// Gauss-Legendre nodes of order 30 by Newton iteration on P_30 (Abramowitz-Stegun start values)
+// ------------------------------------------------------------------------------------------
+namespace {
+constexpr int kGaussOrder = 30;
+double g_gx[kGaussOrder], g_gw[kGaussOrder];
+std::once_flag g_gonce;
+void build_gauss() {
+  const int n = kGaussOrder;
+  for (int i = 0; i < n; ++i) {
+    double x = std::cos(M_PI * (i + 0.75) / (n + 0.5));
+    double dp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = x;
+      for (int k = 2; k <= n; ++k) {
+        const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (x * p1 - p0) / (x * x - 1.0);
+      const double dx = p1 / dp;
+      x -= dx;
+      if (std::fabs(dx) < 1e-16) break;
+    }
+    g_gx[i] = x;
+    g_gw[i] = 2.0 / ((1.0 - x * x) * dp * dp);
+  }
+}
+}  // namespace
+
+QuadResult gauss_legendre(const SmallEig& e, double a, double b) {
+  if (b == a) return {0.0, true};
+  std::call_once(g_gonce, build_gauss);
+  const double c = 0.5 * (a + b), hw = 0.5 * (b - a);
+  double s = 0.0;
+  for (int i = 0; i < kGaussOrder; ++i) s += g_gw[i] * integrand(e, c + hw * g_gx[i]);
+  return {hw * s, true};
+}
+
+QuadResult integrate(const SmallEig& e, double a, double b, double tol_rate, int integrator) {
+  return integrator == 1 ? gauss_legendre(e, a, b) : tanh_sinh(e, a, b, tol_rate * (b - a));
+}
+
+// ------------------------------------------------------------------------------------------
 // step search (Alg. 1 step 2, P:303-318 with P:262; reading O-6)
 // ------------------------------------------------------------------------------------------
 StepResult find_step(const SmallEig& e, bool breakdown, bool first, double tau_prev, double rem,
-                     double tol_rate, double t_total) {
+                     double tol_rate, double t_total, int integrator) {
   bool qok = true;
   auto I = [&](double lo, double hi) {
-    QuadResult r = tanh_sinh(e, lo, hi, tol_rate * (hi - lo));
+    QuadResult r = integrate(e, lo, hi, tol_rate, integrator);
     if (!r.converged) qok = false;
     return r.value;
   };

@@ -29,10 +29,16 @@ struct QuadResult { double value; bool converged; };
 // floor = tol_rate (b - a) in the step search (reading O-5a).
 QuadResult tanh_sinh(const SmallEig& e, double a, double b, double floor, double rel = 1e-3, int max_levels = 15);
 
+// Non-adaptive Gauss-Legendre rule of order 30 on [a,b] (the paper's optional fast scheme).
+QuadResult gauss_legendre(const SmallEig& e, double a, double b);
+
+// integrator: 0 adaptive tanh-sinh (default), 1 Gauss-Legendre
+QuadResult integrate(const SmallEig& e, double a, double b, double tol_rate, int integrator);
+
 struct StepResult { double tau, err; bool quad_ok; bool collapse; };
 // Largest admissible step: e <= tol_rate * tau (reading O-6); integrals use floor tol_rate (b-a).
 StepResult find_step(const SmallEig& e, bool breakdown, bool first, double tau_prev, double rem,
-                     double tol_rate, double t_total);
+                     double tol_rate, double t_total, int integrator = 0);
 
 // omega = U (e^{-i lam tau} .* U[0,:])  (Eq. 11)
 void omega(const SmallEig& e, double tau, std::complex<double>* out);

@@ -110,6 +110,7 @@ struct te_handle {
   bool profile = false;
   int variant = 2;
   int ortho = 0;  // 0 CGS2 (default), 1 paper-literal 3-term Lanczos (f1)
+  int integrator = 0;  // 0 adaptive tanh-sinh (default), 1 Gauss-Legendre
   int spmv_tpr = 4;
   int spmv_pipe_tpr = 1;
   int spmv_tiled = 4;
@@ -505,8 +506,15 @@ int read_flag(te_handle* h, int m, int* m_eff, bool* breakdown) {
 
 // ---------------------------------------------------------------- Algorithm 1
 // V[:,0] holds v0 on entry; on success V[:,0] holds v(t).
+struct Sampling {
+  int64_t n = 0;
+  const double* times = nullptr;  // ascending, in [0, t]
+  te_c128* out = nullptr;         // n x n_local host, row-major (sample-major)
+  double* bounds = nullptr;       // nullable
+};
+
 int evolve_core(te_handle* h, double t, double tol, int m_max, const double* forced, int64_t nforced,
-                te_stats* st) {
+                te_stats* st, const Sampling* smp = nullptr) {
   te_stats S{};
   S.one_norm = h->norm1;
   S.roundoff_step = (double)h->n_global * h->norm1 * std::ldexp(1.0, -52);  // Eq. 17
@@ -534,7 +542,16 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
       return set_err(TE_ERR_NOT_NORMALIZED, "| ||v0|| - 1 | = %.3e > 1e-8", std::fabs(nv - 1.0));
     }
   }
+  int64_t si = 0;
+  const size_t vbytes = sizeof(double2) * (size_t)h->n;
+  if (smp) {  // samples at t_s <= 0: the initial state
+    for (; si < smp->n && smp->times[si] <= 0.0; ++si) {
+      CK(cudaMemcpyAsync(smp->out + (size_t)si * h->n, h->d_V, vbytes, cudaMemcpyDeviceToHost, h->stream));
+      if (smp->bounds) smp->bounds[si] = 0.0;
+    }
+  }
   if (t == 0.0) {
+    CK(cudaStreamSynchronize(h->stream));
     fill();
     return TE_OK;
   }
@@ -564,11 +581,11 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
     bool qok = true;
     if (forced) {
       tau = std::min(forced[k], rem);
-      te::QuadResult q = te::tanh_sinh(E, 0.0, tau, tol_rate * tau);
+      te::QuadResult q = te::integrate(E, 0.0, tau, tol_rate, h->integrator);
       err = q.value;
       qok = q.converged;
     } else {
-      te::StepResult r = te::find_step(E, brk, k == 0, tau_prev, rem, tol_rate, t);
+      te::StepResult r = te::find_step(E, brk, k == 0, tau_prev, rem, tol_rate, t, h->integrator);
       if (r.collapse) {
         fill();
         return set_err(TE_ERR_STEP_COLLAPSE, "step size collapsed below 1e-13 t (m=%d too small for tol=%g)", m, tol);
@@ -576,6 +593,24 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
       tau = r.tau;
       err = r.err;
       qok = r.quad_ok;
+    }
+    // states at intermediate times inside this step: w_s = V exp(-iT(t_s - t_now)) e_1
+    const double t_end = (tau >= rem) ? t : t_now + tau;
+    for (; smp && si < smp->n && smp->times[si] <= t_end; ++si) {
+      const double ds = std::min(smp->times[si] - t_now, tau);
+      te::omega(E, ds, om.data());
+      for (int q = 0; q < m_eff; ++q) {
+        const double s = q == 0 ? 1.0 : 1.0 / beta[q - 1];
+        h->h_coef[q] = make_double2(om[q].real() * s, om[q].imag() * s);
+      }
+      CK(cudaMemcpyAsync(h->d_g + 128, h->h_coef, sizeof(double2) * m_eff, cudaMemcpyHostToDevice, h->stream));
+      KDev d = make_kdev(h, tol_rate, m);
+      Launch L = make_launch(h);
+      te::launch_combine(d, h->d_g + 128, m_eff, h->d_W, L);
+      ++h->launches;
+      CK(cudaMemcpyAsync(smp->out + (size_t)si * h->n, h->d_W, vbytes, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));  // h_coef is reused below
+      if (smp->bounds) smp->bounds[si] = S.err_bound + te::integrate(E, 0.0, ds, tol_rate, h->integrator).value;
     }
     // omega~_k = s_k omega_k with s_0 = 1, s_k = 1/beta_{k-1} (columns stored unnormalised)
     te::omega(E, tau, om.data());
@@ -838,7 +873,8 @@ void te_destroy(te_handle* h) {
 }
 
 static int evolve_entry(te_handle* h, const void* v0, bool v0_dev, double t, double tol, int m_max, void* vout,
-                        bool vout_dev, te_stats* st, cudaStream_t stream, const double* forced, int64_t nforced) {
+                        bool vout_dev, te_stats* st, cudaStream_t stream, const double* forced, int64_t nforced,
+                        const Sampling* smp = nullptr) {
   clear_err();
   int rc = check_evolve_args(h, t, tol, m_max);
   if (rc) return rc;
@@ -849,7 +885,7 @@ static int evolve_entry(te_handle* h, const void* v0, bool v0_dev, double t, dou
   if ((rc = ensure_workspace(h, std::max(m, 1)))) return rc;
   const size_t vbytes = sizeof(double2) * (size_t)h->n;
   CK(cudaMemcpyAsync(h->d_V, v0, vbytes, v0_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
-  rc = evolve_core(h, t, tol, m_max, forced, nforced, st);
+  rc = evolve_core(h, t, tol, m_max, forced, nforced, st, smp);
   if (rc) {
     cudaStreamSynchronize(h->stream);
     h->stream = h->own_stream;
@@ -880,6 +916,24 @@ int te_evolve_schedule(te_handle* h, const te_c128* v0, int64_t k, const double*
     t += t_steps[i];
   }
   return evolve_entry(h, v0, false, t, tol, m_max, v_out, false, stats, nullptr, t_steps, k);
+}
+
+int te_evolve_sampled(te_handle* h, const te_c128* v0, double t, double tol, int m_max, int64_t n_samples,
+                      const double* sample_times, te_c128* samples_out, double* sample_bounds, te_c128* v_out,
+                      te_stats* stats) {
+  clear_err();
+  if (n_samples < 0 || (n_samples > 0 && (!sample_times || !samples_out)))
+    return set_err(TE_ERR_ARG, "bad sampling arguments");
+  for (int64_t i = 0; i < n_samples; ++i) {
+    if (!(sample_times[i] >= 0.0) || sample_times[i] > t || (i > 0 && sample_times[i] < sample_times[i - 1]))
+      return set_err(TE_ERR_ARG, "sample times must be ascending and within [0, t]");
+  }
+  Sampling s;
+  s.n = n_samples;
+  s.times = sample_times;
+  s.out = samples_out;
+  s.bounds = sample_bounds;
+  return evolve_entry(h, v0, false, t, tol, m_max, v_out, false, stats, nullptr, nullptr, 0, &s);
 }
 
 int64_t te_get_schedule(const te_handle* h, int64_t cap, double* t_steps, int32_t* m_eff, double* err_steps) {
@@ -948,6 +1002,10 @@ int te_set_option(te_handle* h, int option, double value) {
     case TE_OPT_ORTHO:
       if (value != 0.0 && value != 1.0) return set_err(TE_ERR_ARG, "TE_OPT_ORTHO must be 0 (CGS2) or 1 (Lanczos)");
       h->ortho = (int)value;
+      return TE_OK;
+    case TE_OPT_INTEGRATOR:
+      if (value != 0.0 && value != 1.0) return set_err(TE_ERR_ARG, "TE_OPT_INTEGRATOR must be 0 or 1");
+      h->integrator = (int)value;
       return TE_OK;
     case TE_OPT_SPMV:
       if (value < 0.0 || value > 4.0 || value != (double)(int)value)

@@ -28,6 +28,7 @@ TE_OPT_KERNELS = 3
 TE_OPT_PREFETCH = 4
 TE_OPT_SPMV = 5
 TE_OPT_ORTHO = 6
+TE_OPT_INTEGRATOR = 7
 KERNELS = {0: "spmv", 1: "update_proj", 2: "update_norm", 3: "combine", 4: "halo_pack", 5: "proj_dots",
            6: "host_step"}
 
@@ -75,6 +76,8 @@ def load():
     L.te_evolve_dev.argtypes = [V, V, D, D, C.c_int, V, P(Stats), V]
     L.te_evolve_schedule.restype = C.c_int
     L.te_evolve_schedule.argtypes = [V, V, I64, V, D, C.c_int, V, P(Stats)]
+    L.te_evolve_sampled.restype = C.c_int
+    L.te_evolve_sampled.argtypes = [V, V, D, D, C.c_int, I64, V, V, V, V, P(Stats)]
     L.te_get_schedule.restype = I64
     L.te_get_schedule.argtypes = [V, I64, V, V, V]
     L.te_krylov_basis.restype = C.c_int
@@ -191,6 +194,20 @@ def te_evolve_schedule(h: Handle, v0, t_steps, tol, m_max):
     _check(L, L.te_evolve_schedule(h.ptr, _ptr(v0), ts.shape[0], _ptr(ts), float(tol), int(m_max), _ptr(vo),
                                    C.byref(st)))
     return vo, st.as_dict()
+
+
+def te_evolve_sampled(h: Handle, v0, t, tol, m_max, sample_times):
+    """Returns (v(t), samples [n_samples x n], sample_bounds, stats)."""
+    L = load()
+    v0 = np.ascontiguousarray(v0, dtype=np.complex128)
+    ts = np.ascontiguousarray(sample_times, dtype=np.float64)
+    out = np.zeros((ts.shape[0], v0.shape[0]), dtype=np.complex128)
+    sb = np.zeros(ts.shape[0])
+    vo = np.empty_like(v0)
+    st = Stats()
+    _check(L, L.te_evolve_sampled(h.ptr, _ptr(v0), float(t), float(tol), int(m_max), ts.shape[0], _ptr(ts),
+                                  _ptr(out), _ptr(sb), _ptr(vo), C.byref(st)))
+    return vo, out, sb, st.as_dict()
 
 
 def te_get_schedule(h: Handle):

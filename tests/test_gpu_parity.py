@@ -284,3 +284,28 @@ def test_lanczos3_mode_matches_oracle(gpu_lib, name, c):
     assert np.linalg.norm(v - ref["v"]) <= 1e-9
     assert st["err_bound"] <= tol
     h.close()
+
+
+def test_sampling_and_gauss_integrator(gpu_lib):
+    """P:335 intermediate-time sampling and the P:406 Gauss-Legendre option against the oracle."""
+    te = gpu_lib
+    c = configs.build(1, n=2000)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    ts = [0.0, 0.25, 0.8, 1.5, 2.0]
+    v, S, sb, st = te.te_evolve_sampled(h, c["v0"], 2.0, 1e-9, 30, ts)
+    sched = te.te_get_schedule(h)
+    ref = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], 2.0, 1e-9, 30, schedule=[s[0] for s in sched], samples=ts)
+    for i in range(len(ts)):
+        assert np.linalg.norm(S[i] - ref["samples"][i]) <= 1e-10
+        assert abs(sb[i] - ref["sample_bounds"][i]) <= 1e-3 * ref["sample_bounds"][i] + 1e-15
+    assert np.array_equal(S[0], c["v0"])
+    assert np.linalg.norm(S[-1] - v) <= 1e-13
+    te.te_set_option(h, te.TE_OPT_INTEGRATOR, 1)
+    vg, stg = te.te_evolve(h, c["v0"], 2.0, 1e-9, 30)
+    sg = te.te_get_schedule(h)
+    refg = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], 2.0, 1e-9, 30, schedule=[s[0] for s in sg], integrator="gauss")
+    assert np.linalg.norm(vg - refg["v"]) <= 1e-10
+    assert stg["err_bound"] == pytest.approx(refg["bound"], rel=1e-6)
+    ada = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], 2.0, 1e-9, 30, integrator="gauss")
+    assert np.linalg.norm(vg - ada["v"]) <= 1e-9 + 1e-12
+    h.close()

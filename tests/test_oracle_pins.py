@@ -427,3 +427,29 @@ def test_paper_dimensions_p527_p535():
         assert mb.dimension(p) == case["d"]
     occ, _, _ = mb.basis(mb.DEFAULTS)
     assert occ.shape[0] == 588
+
+
+def test_gauss_legendre_exactness():
+    """Order-30 Gauss-Legendre (P:406 option) is exact for polynomials of degree <= 59."""
+    v, ok = K.gauss_legendre(lambda x: x ** 59 + 3 * x ** 2, 0.0, 1.0)
+    assert abs(v - (1 / 60 + 1.0)) < 1e-13
+    v, _ = K.gauss_legendre(np.exp, 0.0, 1.0)
+    assert abs(v - (math.e - 1)) < 1e-13
+    assert K.gauss_legendre(np.sin, 2.0, 2.0) == (0.0, True)
+
+
+@pytest.mark.parametrize("integrator", ["tanh-sinh", "gauss"])
+def test_intermediate_samples_vs_dense(integrator):
+    """states sampled inside a step from that step's Krylov space; each sample is within
+    its own bound of the exact exp(-iH t_s) v0, and the sample at t equals the final state."""
+    A = rand_herm(120, 0.06, 31)
+    rp, c, v = csr_from_dense(A)
+    v0 = np.ones(120, complex) / math.sqrt(120)
+    ts = [0.0, 0.3, 1.1, 2.0, 2.9, 3.0]
+    r = K.evolve(rp, c, v, v0, 3.0, 1e-8, 10, samples=ts, integrator=integrator)
+    assert r["restarts"] > 1
+    assert np.array_equal(r["samples"][0], v0)
+    assert np.array_equal(r["samples"][-1], r["v"])
+    for tsi, s, b in zip(ts, r["samples"], r["sample_bounds"]):
+        assert np.linalg.norm(s - dense_evolve(A, v0, tsi)) <= b + 1e-12
+    assert r["sample_bounds"][-1] == pytest.approx(r["bound"], rel=1e-9)
