@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--kernels", type=int, default=2, help="2 SpMV + shuffle projections, 3 SpMV + TMA projections, 0 fused register, 1 staged")
     ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (library default if unset)")
     ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel: 4 pipelined (default) .. 0 CSR-vector")
-    ap.add_argument("--ortho", type=int, default=0, help="0 CGS2 (north star), 1 paper-literal Lanczos (f1)")
+    ap.add_argument("--ortho", type=int, default=0, help="0 CGS2 (north star), 1 paper-literal Lanczos (f1), 2 CGS2 with Gram second sweep (f2)")
     return ap.parse_args()
 
 
@@ -351,7 +351,7 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (V = %.0f MB > 126 MB)" % (16 * nloc * m / 1e6),
                    "parallelism": f"rows{ws}", "kernels": ["fused-register", "staged", "hybrid", "tma", "shuffle"][args.kernels],
                    "prefetch": args.prefetch, "spmv": args.spmv,
-                   "ortho": ["cgs2", "lanczos3"][args.ortho]},
+                   "ortho": ["cgs2", "lanczos3", "cgs2gram"][args.ortho]},
         "achieved_hbm_gbs": all_bytes / (all_ms * 1e-3) / 1e9 if all_ms > 0 else None,
         "step_hbm_gbs": all_bytes / (ms * 1e-3) / 1e9,
         "profiled_region_ms_per_step": ms_prof / args.steps,

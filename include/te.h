@@ -146,7 +146,9 @@ enum {
   TE_OPT_PREFETCH = 4,       /* L2 bulk-prefetch distance (block iterations, 0..16; default 0)     */
   TE_OPT_ORTHO = 6,          /* orthogonalisation: 0 (default) CGS2 against the full basis (reading
                                 C1, BASELINE north star); 1 the paper's 3-term Lanczos recurrence as
-                                printed (Eq. 8; Alg. 1), B_H + 144n bytes/step */
+                                printed (Eq. 8; Alg. 1), B_H + 144n bytes/step;
+                                2 CGS2 whose second sweep takes c2 = c1 - (V^H V) c1 from the Gram
+                                matrix built in the update pass: two V passes per step */
   TE_OPT_INTEGRATOR = 7,     /* error integral: 0 (default) adaptive tanh-sinh;
                                 1 non-adaptive Gauss-Legendre of order 30 ("simpler and faster",
                                 for explorative runs)                                                 */

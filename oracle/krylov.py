@@ -107,6 +107,15 @@ def arnoldi_step(matvec, V, beta, j, ortho="cgs2"):
         aa = np.vdot(V[:, j], p)
         p = p - aa * V[:, j]
         a = aa.real
+    elif ortho == "cgs2gram":
+        # SURVEY f2 (low-synchronisation CGS2): the second sweep's coefficients from the Gram
+        # matrix, c2 = V^H (p - V c1) = c1 - (V^H V) c1, then one update with c1 + c2
+        Vj = V[:, : j + 1]
+        c1 = Vj.conj().T @ p
+        G = Vj.conj().T @ Vj
+        c2 = c1 - G @ c1
+        p = p - Vj @ (c1 + c2)
+        a = (c1[j] + c2[j]).real
     else:
         raise ValueError(ortho)
     b = math.sqrt(np.vdot(p, p).real)
@@ -127,6 +136,8 @@ def arnoldi(matvec, v1, m, tol_rate, ortho="cgs2"):
                         alpha_j = Re(c1_j + c2_j)               (C2, C3)
     ortho="lanczos3" the paper's recurrence as printed:
                         p -= beta_{j-1} v_{j-1} ; a = v_j^H p ; p -= a v_j
+    ortho="cgs2gram" SURVEY f2: c1 = V^H p ; c2 = c1 - (V^H V) c1 ; p -= V (c1 + c2)
+                     (equal to CGS2 in exact arithmetic; one update pass instead of two)
 
     beta_j = ||p||_2 (Eq. 8 ``h_{j+1,j}``).  Lucky breakdown when
     beta_j < tol_rate (Alg. 1; reading C6/C7): stop with m_eff = j+1 and

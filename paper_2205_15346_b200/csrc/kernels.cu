@@ -104,7 +104,10 @@ __device__ __forceinline__ double warp_sum(double v) {
 // Returns the column scale s_j (0 => stop).  Only block 0 writes device state.
 __device__ __forceinline__ double step_gate(const KDev& d, int j, bool writer) {
   if (d.flag[0] != 0) return 0.0;
-  if (j == 0) return 1.0;
+  if (j == 0) {
+    if (writer && d.ortho == 2) d.G[0] = make_double2(1.0, 0.0);
+    return 1.0;
+  }
   const double b = sqrt(d.nrm2[j - 1]);
   if (!isfinite(b)) {
     if (writer) { d.beta[j - 1] = b; d.flag[1] = j; d.flag[0] = 2; }
@@ -115,7 +118,19 @@ __device__ __forceinline__ double step_gate(const KDev& d, int j, bool writer) {
     return 0.0;
   }
   const double sj = 1.0 / b;
-  if (writer) { d.beta[j - 1] = b; d.s[j] = sj; }
+  if (writer) {
+    d.beta[j - 1] = b;
+    d.s[j] = sj;
+    if (d.ortho == 2) {  // f2: Gram row j from the dots of the pass that produced V_j
+      for (int k = 0; k < j; ++k) {
+        const double sk = d.s[k] * sj;
+        const double2 g = d.g2[k];
+        d.G[k * kMaxCols + j] = make_double2(sk * g.x, sk * g.y);
+        d.G[j * kMaxCols + k] = make_double2(sk * g.x, -sk * g.y);
+      }
+      d.G[j * kMaxCols + j] = make_double2(1.0, 0.0);
+    }
+  }
   return sj;
 }
 
@@ -750,7 +765,7 @@ __device__ __forceinline__ double2 butterfly_colsum16(double (&re)[16], double (
 
 template <int MODE>
 __global__ void __launch_bounds__(kProjThreads, 1)
-    k_proj_tma(const __grid_constant__ CUtensorMap tmV, KDev d, int j, int S, int R, int C) {
+    k_proj_tma(const __grid_constant__ CUtensorMap tmV, KDev d, int j, int S, int R, int C, int write) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxSlots], empty[kMaxSlots];
   __shared__ double2 coef[kMaxCols];
@@ -758,11 +773,30 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   __shared__ int go_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ncols = j + 1;
+  __shared__ double2 c1s[kMaxCols];
+  __shared__ double nrm_s[kConsumers];
   if (tid == 0) go_s = (d.flag[0] == 0);
   if (MODE == 1 && tid < ncols) {
     const double sk = d.s[tid];
     const double2 g = d.g1[tid];
     coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);   // e1_k = s_k c1_k
+  }
+  if (MODE == 3) {  // f2: c1 = s g1, c2 = c1 - G c1, coefficient on raw V_k: s_k (c1_k + c2_k)
+    if (tid < ncols) {
+      const double sk = d.s[tid];
+      const double2 g = d.g1[tid];
+      c1s[tid] = make_double2(sk * g.x, sk * g.y);
+    }
+    __syncthreads();
+    if (tid < ncols) {
+      double2 gc = make_double2(0.0, 0.0);
+      for (int l = 0; l < ncols; ++l) gc = cfma(d.G[tid * kMaxCols + l], c1s[l], gc);
+      const double2 c1 = c1s[tid];
+      const double2 c = make_double2(c1.x + (c1.x - gc.x), c1.y + (c1.y - gc.y));
+      const double sk = d.s[tid];
+      coef[tid] = make_double2(sk * c.x, sk * c.y);
+      if (tid == j && blockIdx.x == 0 && d.flag[0] == 0) d.alpha[j] = c.x;  // Re(c1_j + c2_j)
+    }
   }
   // 1024-B alignment through an integer cast: the consumers then read the tiles with generic
   // LD.E.128 instead of LDS.128 — measured faster here (tools/micro/mb_proj.cu: dots at 23
@@ -807,6 +841,8 @@ __global__ void __launch_bounds__(kProjThreads, 1)
 #pragma unroll
     for (int c = 0; c < 32; ++c) aR[c] = aI[c] = 0.0;
     double2 acc1 = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+    double nrm = 0.0;
+    double2* outV = (MODE == 3 && write) ? d.V + (int64_t)(j + 1) * d.ldv : nullptr;
     bool more = true;
     for (int64_t base = 0; more; base += S) {
       for (int s = warp; s < S; s += C) {
@@ -818,11 +854,11 @@ __global__ void __launch_bounds__(kProjThreads, 1)
         const double2* Ws = reinterpret_cast<const double2*>(smem + (size_t)s * slot_bytes + vbytes);
         const int64_t r0 = tile * TR;
         const int rows = (int)min((int64_t)TR, n - r0);
-        for (int sub = 0; sub < R && MODE < 2; ++sub) {  // MODE 2: streaming only (microbenchmark)
+        for (int sub = 0; sub < R && MODE != 2; ++sub) {  // MODE 2: streaming only (microbenchmark)
           const int row = sub * kTileR + lane;
           if (sub * kTileR >= rows) break;  // warp-uniform
           double2 p = row < rows ? Ws[row] : make_double2(0.0, 0.0);
-          if (MODE == 1) {
+          if (MODE == 1 || MODE == 3) {
             // eight independent FMA chains over the columns, 8 tile loads in flight
             double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0, a4 = a0, a5 = a0, a6 = a0, a7 = a0;
             int k = 0;
@@ -844,7 +880,11 @@ __global__ void __launch_bounds__(kProjThreads, 1)
             const double2 a = cadd(cadd(cadd(a0, a1), cadd(a2, a3)), cadd(cadd(a4, a5), cadd(a6, a7)));
             p = make_double2(p.x - a.x, p.y - a.y);
             if (row >= rows) p = make_double2(0.0, 0.0);
-            else d.W[r0 + row] = p;
+            else if (MODE == 1) d.W[r0 + row] = p;
+            else {
+              if (outV) outV[r0 + row] = p;
+              nrm = fma(p.x, p.x, fma(p.y, p.y, nrm));
+            }
           }
 #pragma unroll
           for (int c = 0; c < 32; ++c) {
@@ -877,6 +917,10 @@ __global__ void __launch_bounds__(kProjThreads, 1)
       red[warp][32 + lane] = acc1;
       red[warp][48 + lane] = acc2;
     }
+    if (MODE == 3) {
+      nrm = warp_sum(nrm);
+      if (lane == 0) nrm_s[warp] = nrm;
+    }
   }
   __syncthreads();
   // block partial in fixed warp order, then the last-CTA reduction
@@ -886,6 +930,11 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     double2 t = red[0][tid];
     for (int w = 1; w < C; ++w) t = cadd(t, red[w][tid]);
     d.part[(size_t)blockIdx.x * kMaxCols + tid] = t;
+  }
+  if (MODE == 3 && tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < C; ++w) t += nrm_s[w];
+    d.partn[blockIdx.x] = t;
   }
   __threadfence();
   __syncthreads();
@@ -913,6 +962,11 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     t = cadd(t, seg[2][tid]);
     t = cadd(t, seg[3][tid]);
     out[tid] = t;
+  }
+  if (MODE == 3 && tid == 0) {  // ||p''||^2 in fixed block order
+    double t = 0.0;
+    for (int b = 0; b < G; ++b) t += __ldcg(d.partn + b);
+    d.nrm2[j] = t;
   }
   if (tid == 0) d.counter[ctr] = 0u;
 }
@@ -1851,6 +1905,7 @@ cudaError_t configure_kernels() {
   TE_SET(1) TE_SET(2) TE_SET(3) TE_SET(4) TE_SET(5) TE_SET(6) TE_SET(7) TE_SET(8)
 #undef TE_SET
   set((const void*)k_proj_tma<0>, kProjSmemBudget + 1024);
+  set((const void*)k_proj_tma<3>, kProjSmemBudget + 1024);
   set((const void*)k_spmv_tma<false>, kProjSmemBudget + 1024);
 #define TE_SETP(T)                                                  \
   set((const void*)k_spmv_pipe<false, T>, spmv_pipe_smem<false>()); \
@@ -1944,7 +1999,12 @@ void launch_proj_dots(const KDev& d, int j, const Launch& L) {
     return;
   }
   const int S = proj_slots(j + 1), R = proj_rsub(j + 1), C = proj_consumers(j + 1);
-  k_proj_tma<0><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S, R, C);
+  k_proj_tma<0><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S, R, C, 0);
+}
+
+void launch_gram_update(const KDev& d, int j, bool write, const Launch& L) {
+  const int S = proj_slots(j + 1), R = proj_rsub(j + 1), C = proj_consumers(j + 1);
+  k_proj_tma<3><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S, R, C, write ? 1 : 0);
 }
 
 void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L) {
@@ -1981,7 +2041,7 @@ void launch_update_proj(const KDev& d, int j, const Launch& L) {
   }
   if (L.variant == 2) {
     const int S = proj_slots(j + 1), R = proj_rsub(j + 1), C = proj_consumers(j + 1);
-    k_proj_tma<1><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S, R, C);
+    k_proj_tma<1><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S, R, C, 0);
     return;
   }
   if (L.variant == 0) {

@@ -48,6 +48,8 @@ struct KDev {
   int* flag;            // [0]: 0 running / 1 breakdown / 2 non-finite ; [1]: m_eff
   double tol_rate;
   int m;                // Krylov dimension of the current restart
+  int ortho;            // 0 CGS2, 1 Lanczos (f1), 2 CGS2 with Gram-matrix second sweep (f2)
+  double2* G;           // [kMaxCols x kMaxCols] Gram matrix <v_k, v_l> of the normalised basis (f2)
 };
 
 struct Launch {
@@ -69,6 +71,7 @@ void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L);   // K1
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L);        // K1a: SpMV only
 void launch_proj_dots(const KDev& d, int j, const Launch& L);              // K1b: g1 = V^H p (TMA)
 void launch_update_proj(const KDev& d, int j, const Launch& L);            // K2
+void launch_gram_update(const KDev& d, int j, bool write, const Launch& L); // f2: p'' = p - V(c1+c2) -> V_{j+1}, V^H p'', ||p''||^2
 void launch_update_norm(const KDev& d, int j, bool write, const Launch& L);// K3
 void launch_finalize(const KDev& d, int j, const Launch& L);
 void launch_lanczos_dot(const KDev& d, int j, const Launch& L);                // f1: a = v_j^H (p - b v_{j-1})

@@ -100,6 +100,7 @@ struct te_handle {
   double2* d_W = nullptr;
   double* d_small = nullptr;  // alpha[64] beta[64] | flag (2 ints) | s[65] nrm2[64] scalar
   double2* d_g = nullptr;     // g1[64] g2[64] coef[64]
+  double2* d_G = nullptr;     // Gram matrix 64 x 64 (f2)
   double2* d_part = nullptr;
   double* d_partn = nullptr;
   unsigned* d_counter = nullptr;
@@ -185,6 +186,8 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.counter = h->d_counter;
   d.tol_rate = tol_rate;
   d.m = m;
+  d.ortho = h->ortho;
+  d.G = h->d_G;
   return d;
 }
 
@@ -247,6 +250,8 @@ int ensure_workspace(te_handle* h, int m) {
     CK(cudaMalloc(&h->d_small, sizeof(double) * kSmallLen));
     CK(cudaMemset(h->d_small, 0, sizeof(double) * kSmallLen));
     CK(cudaMalloc(&h->d_g, sizeof(double2) * 3 * 64));
+    CK(cudaMalloc(&h->d_G, sizeof(double2) * te::kMaxCols * te::kMaxCols));
+    CK(cudaMemset(h->d_G, 0, sizeof(double2) * te::kMaxCols * te::kMaxCols));
     h->max_grid = 8 * h->num_sms;
     CK(cudaMalloc(&h->d_part, sizeof(double2) * te::kMaxCols * h->max_grid));
     CK(cudaMalloc(&h->d_partn, sizeof(double) * h->max_grid));
@@ -388,6 +393,22 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
       prof_begin(h);
       te::launch_lanczos_update(d, j, wr, L); LCHECK("lanczos_update");
       prof_end(h, 2, 16.0 * n * nv + 16.0 * n + (wr ? 16.0 * n : 0.0));
+      if ((rc = allreduce_sum(h, d.nrm2 + j, 1))) return rc;
+      continue;
+    }
+    if (h->ortho == 2) {  // f2: CGS2 with the Gram-matrix second sweep, two V passes per step
+      prof_begin(h);
+      te::launch_spmv(d, h->cplx, j, L); LCHECK("spmv");
+      prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
+      prof_begin(h);
+      te::launch_proj_dots(d, j, L); LCHECK("proj_dots");
+      prof_end(h, 5, 16.0 * n * ncols + 16.0 * n);
+      if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g1), 2 * (size_t)(j + 1)))) return rc;
+      const bool wr = j + 1 < m;
+      prof_begin(h);
+      te::launch_gram_update(d, j, wr, L); LCHECK("gram_update");
+      prof_end(h, 1, 16.0 * n * ncols + 16.0 * n + (wr ? 16.0 * n : 0.0));
+      if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g2), 2 * (size_t)(j + 1)))) return rc;
       if ((rc = allreduce_sum(h, d.nrm2 + j, 1))) return rc;
       continue;
     }
@@ -849,6 +870,7 @@ void te_destroy(te_handle* h) {
   free_workspace(h);
   cudaFree(h->d_small);
   cudaFree(h->d_g);
+  cudaFree(h->d_G);
   cudaFree(h->d_part);
   cudaFree(h->d_partn);
   cudaFree(h->d_counter);
@@ -1000,7 +1022,8 @@ int te_set_option(te_handle* h, int option, double value) {
       h->variant = (int)value;
       return TE_OK;
     case TE_OPT_ORTHO:
-      if (value != 0.0 && value != 1.0) return set_err(TE_ERR_ARG, "TE_OPT_ORTHO must be 0 (CGS2) or 1 (Lanczos)");
+      if (value != 0.0 && value != 1.0 && value != 2.0)
+        return set_err(TE_ERR_ARG, "TE_OPT_ORTHO must be 0 (CGS2), 1 (Lanczos) or 2 (CGS2, Gram second sweep)");
       h->ortho = (int)value;
       return TE_OK;
     case TE_OPT_INTEGRATOR:

@@ -309,3 +309,32 @@ def test_sampling_and_gauss_integrator(gpu_lib):
     ada = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], 2.0, 1e-9, 30, integrator="gauss")
     assert np.linalg.norm(vg - ada["v"]) <= 1e-9 + 1e-12
     h.close()
+
+
+@pytest.mark.parametrize("name,c", CASES, ids=[x[0] for x in CASES])
+def test_cgs2gram_mode_matches_oracle(gpu_lib, name, c):
+    """SURVEY f2 (TE_OPT_ORTHO=2): against the oracle's 'cgs2gram' (same recurrence) and its
+    plain CGS2 (equal in exact arithmetic): basis and the evolved state at 1e-10."""
+    te = gpu_lib
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    te.te_set_option(h, te.TE_OPT_ORTHO, 2)
+    m = min(c["m"], c["n"])
+    tol_rate = c["tol"] / c["t"]
+    g = te.te_krylov_basis(h, c["v0"], m, tol_rate, want_V=True)
+    mv = lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x)  # noqa: E731
+    for ortho in ("cgs2gram", "cgs2"):
+        o = K.arnoldi(mv, c["v0"], m, tol_rate, ortho=ortho)
+        assert g["m_eff"] == o["m_eff"]
+        scale = max(1.0, np.abs(o["alpha"]).max(), np.abs(o["beta"]).max())
+        assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-12 * scale
+        assert np.abs(g["beta"] - o["beta"]).max() <= 1e-12 * scale
+        assert np.linalg.norm(g["V"] - o["V"]) <= 1e-10
+    k = g["m_eff"]
+    assert np.abs(g["V"].conj().T @ g["V"] - np.eye(k)).max() <= 1e-13
+    t, tol = (min(c["t"], 2.0) if c["n"] > 5000 else c["t"]), c["tol"]
+    v, st = te.te_evolve(h, c["v0"], t, tol, c["m"])
+    sched = te.te_get_schedule(h)
+    ref = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], t, tol, c["m"], schedule=[s[0] for s in sched])
+    assert np.linalg.norm(v - ref["v"]) <= 1e-10
+    assert st["err_bound"] <= tol
+    h.close()

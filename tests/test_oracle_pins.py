@@ -70,7 +70,7 @@ def test_one_norm_hand_values():
 
 # ---------------------------------------------------------------- Arnoldi
 
-@pytest.mark.parametrize("ortho", ["cgs2", "lanczos3"])
+@pytest.mark.parametrize("ortho", ["cgs2", "lanczos3", "cgs2gram"])
 def test_arnoldi_relation_and_orthonormality(ortho):
     n, m = 120, 12
     A = rand_herm(n, 0.08, 4)
@@ -84,7 +84,7 @@ def test_arnoldi_relation_and_orthonormality(ortho):
     norm1 = np.abs(A).sum(axis=0).max()
     assert np.linalg.norm(R[:, :-1]) <= 32 * 2**-52 * n * norm1
     assert math.isclose(np.linalg.norm(R[:, -1]), kr["h"], rel_tol=1e-9)
-    if ortho == "cgs2":
+    if ortho in ("cgs2", "cgs2gram"):
         assert np.abs(V.conj().T @ V - np.eye(m)).max() <= 1e-13
 
 
@@ -453,3 +453,17 @@ def test_intermediate_samples_vs_dense(integrator):
     for tsi, s, b in zip(ts, r["samples"], r["sample_bounds"]):
         assert np.linalg.norm(s - dense_evolve(A, v0, tsi)) <= b + 1e-12
     assert r["sample_bounds"][-1] == pytest.approx(r["bound"], rel=1e-9)
+
+
+def test_cgs2gram_equals_cgs2_to_roundoff():
+    """f2: the Gram-corrected second sweep reproduces CGS2 (same T, same basis) to roundoff,
+    also deep into a restart where plain CGS would lose orthogonality."""
+    A = rand_herm(400, 0.02, 41)
+    v0 = np.random.default_rng(42).standard_normal(400) + 0j
+    v0 /= np.linalg.norm(v0)
+    a = K.arnoldi(lambda x: A @ x, v0, 40, 1e-14, "cgs2")
+    b = K.arnoldi(lambda x: A @ x, v0, 40, 1e-14, "cgs2gram")
+    assert np.abs(a["alpha"] - b["alpha"]).max() < 1e-12 * np.abs(a["alpha"]).max()
+    assert np.abs(a["beta"] - b["beta"]).max() < 1e-12 * np.abs(a["beta"]).max()
+    assert np.linalg.norm(a["V"] - b["V"]) < 1e-11
+    assert np.abs(b["V"].conj().T @ b["V"] - np.eye(40)).max() < 1e-13

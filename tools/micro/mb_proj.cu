@@ -41,9 +41,9 @@ int main(int argc, char** argv) {
     for (int mode = 0; mode < 6; ++mode) {
       for (int it = 0; it < 6; ++it) {
         if (it == 1) cudaEventRecord(e0);
-        if (mode == 0) k_proj_tma<0><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C);
-        if (mode == 1) k_proj_tma<1><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C);
-        if (mode == 2) k_proj_tma<2><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C);
+        if (mode == 0) k_proj_tma<0><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
+        if (mode == 1) k_proj_tma<1><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
+        if (mode == 2) k_proj_tma<2><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
         if (mode == 3) k_update_norm<<<8 * sms, kThreads>>>(d, j, 0, 0);
         if (mode == 4) { TE_DISPATCH_TPR(tpr, { k_proj_s<0, TPR><<<gs4, kThreads>>>(d, j); }); }
         if (mode == 5) { TE_DISPATCH_TPR(tpr, { k_proj_s<1, TPR><<<gs4, kThreads>>>(d, j); }); }
