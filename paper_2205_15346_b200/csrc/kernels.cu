@@ -1393,7 +1393,8 @@ struct TileDesc { int64_t ra, rb, b, e; };
 template <bool CPLX>
 size_t spmv_pipe_smem() {
   using VT = typename ValT<CPLX>::T;
-  return 2 * ((size_t)(kSpmvMaxTileRows + 4) * 8 + (size_t)(kSpmvTileNnz + 4) * 4 + (size_t)(kSpmvTileNnz + 4) * sizeof(VT));
+  constexpr int cap = CPLX ? kSpmvTileNnzC : kSpmvTileNnz;
+  return 2 * ((size_t)(kSpmvMaxTileRows + 4) * 8 + (size_t)(cap + 4) * 4 + (size_t)(cap + 4) * sizeof(VT));
 }
 
 template <bool CPLX, int TPR>
@@ -1401,8 +1402,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
   using VT = typename ValT<CPLX>::T;
   extern __shared__ __align__(16) unsigned char smp[];
   // buffer b at smp + b * kBuf: [val kChunk][rowptr kSpmvMaxTileRows+2][col kChunk]
-  constexpr size_t kVal = (size_t)(kSpmvTileNnz + 4) * sizeof(VT), kRp = (size_t)(kSpmvMaxTileRows + 4) * 8;
-  constexpr size_t kBuf = kVal + kRp + (size_t)(kSpmvTileNnz + 4) * 4;
+  constexpr int kCap = CPLX ? kSpmvTileNnzC : kSpmvTileNnz;
+  constexpr size_t kVal = (size_t)(kCap + 4) * sizeof(VT), kRp = (size_t)(kSpmvMaxTileRows + 4) * 8;
+  constexpr size_t kBuf = kVal + kRp + (size_t)(kCap + 4) * 4;
   auto vs_of = [&](int b) { return reinterpret_cast<VT*>(smp + b * kBuf); };
   auto rp_of = [&](int b) { return reinterpret_cast<int64_t*>(smp + b * kBuf + kVal); };
   auto cs_of = [&](int b) { return reinterpret_cast<int32_t*>(smp + b * kBuf + kVal + kRp); };
@@ -1446,7 +1448,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
       const int64_t r0 = td.ra & ~1LL, r1 = (td.rb + 2) & ~1LL;
       unsigned br = (unsigned)((r1 - r0) * 8), bc = 0, bv = 0;
       int64_t c0 = 0, v0 = 0;
-      if (cnt <= kSpmvTileNnz) {
+      if (cnt <= kCap) {
         constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
         c0 = td.b & ~3LL;
         v0 = td.b & ~(VA - 1);
@@ -1472,7 +1474,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
     mbar_wait(&bar[bsel], (unsigned)((it >> 1) & 1));
     const int rows = (int)(cur.rb - cur.ra);
     const int64_t cnt = cur.e - cur.b;
-    if (cnt <= kSpmvTileNnz) {
+    if (cnt <= kCap) {
       constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
       const int64_t* rp = rp_of(bsel) + (cur.ra & 1);
       const int32_t* cc = cs_of(bsel) + (cur.b & 3);
@@ -1934,7 +1936,7 @@ static int tpr_for(int ncols, int min_tpr) {
 
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
   if (L.spmv_tiled == 4 && d.ntiles > 0) {
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cplx ? 1 : 2) * L.num_sms, d.ntiles));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * L.num_sms, d.ntiles));
     switch (L.spmv_pipe_tpr) {
 #define TE_PIPE(T)                                                                                  \
   case T:                                                                                           \

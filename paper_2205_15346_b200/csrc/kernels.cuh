@@ -18,7 +18,8 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMaxCols = 64;         // TE_M_MAX
 constexpr int kSpmvRows = 256;       // K1 row tile
 constexpr int kSpmvChunk = 4096;     // K1 products staged in shared memory per chunk
-constexpr int kSpmvTileNnz = 4096;   // entries per nnz-balanced SpMV tile (cap)
+constexpr int kSpmvTileNnz = 4096;   // entries per nnz-balanced SpMV tile (cap), real values
+constexpr int kSpmvTileNnzC = 2048;  // complex values (two pipelined blocks per SM)
 constexpr int kSpmvMaxTileRows = 256;   // rows per SpMV tile cap (one thread per row)
 constexpr int kSpmvTmaNnzCap = 512;     // entries per TMA SpMV tile (== kSpmvTmaNnz)
 constexpr int kSpmvTmaRowCap = 128;     // rows per TMA SpMV tile

@@ -749,8 +749,9 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
   {  // lanes per row of the pipelined SpMV: <= ~16 gathers per lane per row (1, 2, 4 or 8);
      // TE_SPMV_TPR overrides (measurement)
     const double avg = n > 0 ? (double)h->nnz / (double)n : 0.0;
+    const double per_lane = cplx ? 8.0 : 16.0;  // complex tiles are half as large (kSpmvTileNnzC)
     int t = 1;
-    while (t < 8 && 16.0 * t < avg) t <<= 1;
+    while (t < 8 && per_lane * t < avg) t <<= 1;
     if (const char* e = getenv("TE_SPMV_TPR")) {
       const int v = atoi(e);
       if (v == 1 || v == 2 || v == 4 || v == 8) t = v;
@@ -766,7 +767,7 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     tr.push_back(0);
     for (int64_t r = 0; r < n; ++r) {
       const bool over_rows = (r + 1 - start) > tile_rows_cap;
-      const bool over_nnz = (rowptr[r + 1] - rowptr[start]) > te::kSpmvTileNnz && r > start;
+      const bool over_nnz = (rowptr[r + 1] - rowptr[start]) > (cplx ? te::kSpmvTileNnzC : te::kSpmvTileNnz) && r > start;
       if (over_rows || over_nnz) {
         tr.push_back(r);
         start = r;
