@@ -138,7 +138,7 @@ enum {
   TE_OPT_GRAPH = 2,          /* 1 (default): replay each restart's launches as a CUDA graph      */
   TE_OPT_KERNELS = 3,        /* kernel set (same arithmetic, kept for measured comparison):
                                 2 (default): nnz-balanced SpMV + projections chosen by column count
-                                  (TMA-tiled dots; update by the register-streaming/shuffle kernel for <= 8 columns, TMA above);
+                                  (register-streaming/shuffle kernel for <= 4 (dots) / <= 8 (update) columns, TMA-tiled above);
                                 3: SpMV + TMA-tiled (2-D tensor boxes) warp-specialised projections;
                                 4: SpMV + register-streaming/shuffle projections;
                                 0: register-streaming fused K1/K2; 1: shared-memory staged K1 and

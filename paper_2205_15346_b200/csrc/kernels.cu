@@ -995,6 +995,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_proj_s(KDev d, int j) {
   __syncthreads();
   if (!go_s) return;
   const int64_t n = d.n, ldv = d.ldv;
+  const int cmax = (ncols + TPR - 1) / TPR;  // live column slots per lane
   for (int64_t rb = (int64_t)blockIdx.x * RPB; rb < n; rb += (int64_t)gridDim.x * RPB) {
     const int64_t r = rb + grp;
     const bool act = r < n;
@@ -1018,6 +1019,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_proj_s(KDev d, int j) {
     }
 #pragma unroll
     for (int c = 0; c < kCPT; ++c) {
+      if (c >= cmax) break;  // warp-uniform: only the live column slots are reduced
       double2 pr = make_double2(v[c].x * p.x + v[c].y * p.y, v[c].x * p.y - v[c].y * p.x);  // conj(v) p
 #pragma unroll
       for (int off = TPR; off < 32; off <<= 1) {
@@ -1990,9 +1992,9 @@ static void launch_proj_s(const KDev& d, int j, int mode, const Launch& L) {
   });
 }
 
-// measured on B200 (tools/micro/mb_proj.cu, 16 KB minimum TMA tiles): the TMA ring is faster
-// for the dots at every column count, the register/shuffle kernel for the update up to 8 columns.
-constexpr int kShuffleMaxColsDots = 0;
+// measured on B200 (tools/micro/mb_proj.cu, 16 KB minimum TMA tiles): the register/shuffle kernel
+// is faster for the dots up to 4 columns and for the update up to 8 columns, the TMA ring above.
+constexpr int kShuffleMaxColsDots = 4;
 constexpr int kShuffleMaxCols = 8;
 
 void launch_proj_dots(const KDev& d, int j, const Launch& L) {
