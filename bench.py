@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--kernels", type=int, default=2, help="2 SpMV + shuffle projections, 3 SpMV + TMA projections, 0 fused register, 1 staged")
     ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (library default if unset)")
     ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel: 4 pipelined (default) .. 0 CSR-vector")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="single rank through the distributed API (te_dist_init/te_create_csr_dist), for testing")
     ap.add_argument("--ortho", type=int, default=0, help="0 CGS2 (north star), 1 paper-literal Lanczos (f1), 2 CGS2 with Gram second sweep (f2)")
     return ap.parse_args()
 
@@ -230,7 +232,12 @@ def run_ours(args):
     c, rb, re_ = build_workload(args.config, ws, rank)
     n_glob, nloc = c["n"], re_ - rb
     t, tol, m = c["t"], c["tol"], c["m"]
-    if ws == 1:
+    D = None
+    if ws == 1 and args.force_dist:
+        D = te.te_dist_init(1, 0, b"\0" * 128)
+        h = te.te_create_csr_dist(D, n_glob, 0, n_glob, c["rowptr"], c["col"].astype(np.int64), c["val"])
+        v0_loc = c["v0"]
+    elif ws == 1:
         h = te.te_create_csr(n_glob, c["rowptr"], c["col"], c["val"])
         v0_loc = c["v0"]
     else:
@@ -322,8 +329,9 @@ def run_ours(args):
 
     if rank != 0:
         h.close()
-        if ws > 1:
+        if D is not None:
             D.close()
+        if ws > 1:
             torch.distributed.destroy_process_group()
         return 0
 
@@ -379,8 +387,9 @@ def run_ours(args):
                                 "sample": sample}
     print(json.dumps(line))
     h.close()
-    if ws > 1:
+    if D is not None:
         D.close()
+    if ws > 1:
         torch.distributed.destroy_process_group()
     return 0
 

@@ -1,11 +1,5 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu1.log 2>&1
-python tools/profile_run.py --t 2.5 > gpurun_out/plain2.log 2>&1 && \
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:"k_proj|k_spmv|k_update_norm|k_combine" --csv --log-file gpurun_out/restart_metrics.csv python tools/profile_run.py --t 2.5 > gpurun_out/ncu2.log 2>&1
-python tools/profile_run.py --t 2.5 > gpurun_out/plain3.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_proj_tma|k_spmv_pipe|k_update_norm" -s 60 -c 4 -o gpurun_out/prof_r01d python tools/profile_run.py --t 2.5 > gpurun_out/ncu3.log 2>&1
-python tools/profile_run.py --config 5 --t 1.2 > gpurun_out/plain5.log 2>&1 && \
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:"k_proj|k_spmv|k_update_norm|k_combine" --csv --log-file gpurun_out/restart_metrics_c5.csv python tools/profile_run.py --config 5 --t 1.2 > gpurun_out/ncu5.log 2>&1
-echo done >> gpurun_out/ncu5.log
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --force-dist > gpurun_out/bench_fd.log 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_trun.log 2>&1
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1
