@@ -198,7 +198,7 @@ def run_reference(args):
         "impl": "reference", "metric": "Krylov steps/s", "value": rate, "unit": "krylov_steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
-        "data": "synthetic", "config": {"workload": f"{c['name']} (BASELINE configs[{args.config - 1}])",
+        "data": "synthetic", "config": {"workload": f"{c['name']} ({configs.LABELS[args.config]})",
                                         "n": c["n"], "nnz": int(c["rowptr"][-1]), "m": c["m"]},
         "cpu_baseline": {"value": rate, "unit": "krylov_steps/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": rate, "unit": "krylov_steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -214,6 +214,7 @@ def run_ours(args):
     import torch
     from paper_2205_15346_b200 import build as B
     from paper_2205_15346_b200 import te
+    from workloads import configs
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -352,7 +353,7 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic",
-        "config": {"workload": f"{c['name']} (BASELINE configs[{args.config - 1}])", "n": n_glob,
+        "config": {"workload": f"{c['name']} ({configs.LABELS[args.config]})", "n": n_glob,
                    "nnz": int(c["rowptr"][-1]) if "rowptr" in c else None, "m": m, "t": t, "tol": tol,
                    "krylov_steps_per_step": ksteps / args.steps,
                    "restarts_per_step": stats[-1]["n_restarts"],
@@ -364,6 +365,10 @@ def run_ours(args):
         "step_hbm_gbs": all_bytes / (ms * 1e-3) / 1e9,
         "profiled_region_ms_per_step": ms_prof / args.steps,
         "evolved_time_per_s": t * args.steps / (ms * 1e-3),
+        **({"paper_context": {"paper_wall_s": 353.0, "paper_hw": "i9-9900K, 1 thread (P:527-529)",
+                              "ours_wall_s": ms / args.steps * 1e-3,
+                              "err_bound": stats[-1]["err_bound"], "roundoff_total": stats[-1]["roundoff_total"]}}
+           if args.config == 6 else {}),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": p["alg_bytes"] / p["launches"],

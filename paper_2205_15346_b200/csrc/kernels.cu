@@ -1399,8 +1399,8 @@ size_t spmv_pipe_smem() {
   return 2 * ((size_t)(kSpmvMaxTileRows + 4) * 8 + (size_t)(cap + 4) * 4 + (size_t)(cap + 4) * sizeof(VT));
 }
 
-template <bool CPLX, int TPR>
-__global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
+template <bool CPLX, int TPR, bool HALO, int NF>
+__global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j, int pf) {
   using VT = typename ValT<CPLX>::T;
   extern __shared__ __align__(16) unsigned char smp[];
   // buffer b at smp + b * kBuf: [val kChunk][rowptr kSpmvMaxTileRows+2][col kChunk]
@@ -1427,6 +1427,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
   const VT* __restrict__ val = static_cast<const VT*>(d.val);
   const int32_t* __restrict__ col = d.col;
   const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  asm volatile("" : "+l"(x));  // keep the column base in a register (no per-gather recompute)
   const double2* __restrict__ halo = d.halo;
   const int64_t n = d.n;
   const int64_t G = gridDim.x;
@@ -1482,29 +1483,38 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j) {
       const int32_t* cc = cs_of(bsel) + (cur.b & 3);
       const VT* vv = vs_of(bsel) + (cur.b & (VA - 1));
       {  // group grp owns row grp of the tile (tiles hold <= kThreads/TPR rows); lane q takes
-         // entries lo+q, lo+q+TPR, ... (8 gathers in flight), then a fixed-order xor reduction
+         // entries lo+q, lo+q+TPR, ... (NF gathers in flight: 16 for real values, 8 for complex
+         // ones, whose registers are twice as wide), then a fixed-order xor reduction
         const int i = grp;
         const bool act = i < rows;
         const int lo = act ? (int)(rp[i] - cur.b) : 0, hi = act ? (int)(rp[i + 1] - cur.b) : 0;
         double2 acc = make_double2(0.0, 0.0);
-        for (int q0 = lo + q; q0 < hi; q0 += 8 * TPR) {
-          double2 xx[8];
-          VT ww[8];
+        for (int q0 = lo + q; q0 < hi; q0 += NF * TPR) {
+          double2 xx[NF];
 #pragma unroll
-          for (int w = 0; w < 8; ++w) {
+          for (int w = 0; w < NF; ++w) {
             const int e = q0 + w * TPR;
             if (e < hi) {
               const int c = cc[e];
-              ww[w] = vv[e];
-              xx[w] = (c < n) ? __ldg(x + c) : __ldg(halo + (c - n));
+              if (HALO) xx[w] = ((uint32_t)c < (uint32_t)n) ? __ldg(x + c) : __ldg(halo + (c - (int)n));
+              else xx[w] = __ldg(x + c);   // single rank: every column is local
             }
           }
+          // products accumulate from the LAST gather down, so the chain's first operand is the
+          // last load and the scheduler issues all NF gathers before any product; values are
+          // re-read from shared memory here rather than held in registers across the gathers
 #pragma unroll
-          for (int w = 0; w < 8; ++w)
-            if (q0 + w * TPR < hi) acc = cadd(acc, ValT<CPLX>::mul(ww[w], xx[w]));
+          for (int w = NF - 1; w >= 0; --w)
+            if (q0 + w * TPR < hi) acc = cadd(acc, ValT<CPLX>::mul(vv[q0 + w * TPR], xx[w]));
         }
         if (TPR > 1) acc = group_sum<TPR>(acc);
         if (act && q == 0) __stcs(d.W + cur.ra + i, make_double2(acc.x * sj, acc.y * sj));
+      }
+      // L2 prefetch of tile t+2G's entries (its descriptor arrived during this tile): one more
+      // tile of DRAM reads in flight per CTA without shared memory
+      if (pf && tid == 32 && t + 2 * G < d.ntiles) {
+        prefetch_range(col, (size_t)nn.b * 4, (size_t)nn.e * 4);
+        prefetch_range(val, (size_t)nn.b * sizeof(VT), (size_t)nn.e * sizeof(VT));
       }
     } else {  // one long row, straight from global memory
       double2 acc = make_double2(0.0, 0.0);
@@ -1912,8 +1922,14 @@ cudaError_t configure_kernels() {
   set((const void*)k_proj_tma<3>, kProjSmemBudget + 1024);
   set((const void*)k_spmv_tma<false>, kProjSmemBudget + 1024);
 #define TE_SETP(T)                                                  \
-  set((const void*)k_spmv_pipe<false, T>, spmv_pipe_smem<false>()); \
-  set((const void*)k_spmv_pipe<true, T>, spmv_pipe_smem<true>());
+  set((const void*)k_spmv_pipe<false, T, false, 12>, spmv_pipe_smem<false>()); \
+  set((const void*)k_spmv_pipe<true, T, false, 8>, spmv_pipe_smem<true>());    \
+  set((const void*)k_spmv_pipe<false, T, true, 12>, spmv_pipe_smem<false>());  \
+  set((const void*)k_spmv_pipe<true, T, true, 8>, spmv_pipe_smem<true>());     \
+  set((const void*)k_spmv_pipe<false, T, false, 16>, spmv_pipe_smem<false>()); \
+  set((const void*)k_spmv_pipe<true, T, false, 12>, spmv_pipe_smem<true>());   \
+  set((const void*)k_spmv_pipe<false, T, true, 16>, spmv_pipe_smem<false>());  \
+  set((const void*)k_spmv_pipe<true, T, true, 12>, spmv_pipe_smem<true>());
   TE_SETP(1) TE_SETP(2) TE_SETP(4) TE_SETP(8)
 #undef TE_SETP
   set((const void*)k_spmv_tma<true>, kProjSmemBudget + 1024);
@@ -1940,14 +1956,21 @@ void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
   if (L.spmv_tiled == 4 && d.ntiles > 0) {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * L.num_sms, d.ntiles));
     switch (L.spmv_pipe_tpr) {
+#define TE_PIPE_NF(T, H, NR, NC)                                                                     \
+  if (cplx) k_spmv_pipe<true, T, H, NC><<<grid, kThreads, spmv_pipe_smem<true>(), L.stream>>>(d, j, L.spmv_pf); \
+  else k_spmv_pipe<false, T, H, NR><<<grid, kThreads, spmv_pipe_smem<false>(), L.stream>>>(d, j, L.spmv_pf);
 #define TE_PIPE(T)                                                                                  \
   case T:                                                                                           \
-    if (cplx) k_spmv_pipe<true, T><<<grid, kThreads, spmv_pipe_smem<true>(), L.stream>>>(d, j);     \
-    else k_spmv_pipe<false, T><<<grid, kThreads, spmv_pipe_smem<false>(), L.stream>>>(d, j);        \
+    if (d.halo || L.spmv_force_halo) {                                                              \
+      if (L.spmv_nf_wide) { TE_PIPE_NF(T, true, 16, 12) } else { TE_PIPE_NF(T, true, 12, 8) }      \
+    } else {                                                                                        \
+      if (L.spmv_nf_wide) { TE_PIPE_NF(T, false, 16, 12) } else { TE_PIPE_NF(T, false, 12, 8) }    \
+    }                                                                                               \
     break;
       TE_PIPE(1) TE_PIPE(2) TE_PIPE(4)
       default: TE_PIPE(8)
 #undef TE_PIPE
+#undef TE_PIPE_NF
     }
     return;
   }

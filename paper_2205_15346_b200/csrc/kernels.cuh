@@ -60,6 +60,9 @@ struct Launch {
   const CUtensorMap* tmaps;  // [kMaxCols] 2-D maps of V, box = 64 doubles x (k+1) columns
   int spmv_tpr;  // lanes per row of the standalone CSR-vector SpMV
   int spmv_pipe_tpr;  // lanes per row of the pipelined SpMV (tile row cap = kThreads / this)
+  int spmv_pf;        // pipelined SpMV: L2 prefetch of tile t+2G (0 off, 1 on)
+  int spmv_force_halo;  // test hook: run the multi-rank (halo-aware) SpMV instantiation on one rank
+  int spmv_nf_wide;   // pipelined SpMV gathers in flight per lane: 0 -> 12 real / 8 complex, 1 -> 16 / 12
   int proj_tma;   // 2: hybrid by column count (default), 1: TMA-tiled only, 0: register/shuffle only
   int spmv_tiled; // 2: TMA-fed SpMV (default), 1: nnz-balanced tiled SpMV, 0: CSR-vector
   int prefetch; // L2 bulk-prefetch distance in block iterations (0: off)

@@ -114,6 +114,9 @@ struct te_handle {
   int integrator = 0;  // 0 adaptive tanh-sinh (default), 1 Gauss-Legendre
   int spmv_tpr = 4;
   int spmv_pipe_tpr = 1;
+  int spmv_pf = 0;
+  int spmv_nf_wide = 0;
+  int spmv_force_halo = 0;
   int spmv_tiled = 4;
   int64_t* d_tile_row = nullptr;
   int64_t ntiles = 0;
@@ -204,6 +207,9 @@ Launch make_launch(te_handle* h) {
   L.tmaps = h->tmaps.data();
   L.spmv_tpr = h->spmv_tpr;
   L.spmv_pipe_tpr = h->spmv_pipe_tpr;
+  L.spmv_pf = h->spmv_pf;
+  L.spmv_nf_wide = h->spmv_nf_wide;
+  L.spmv_force_halo = h->spmv_force_halo;
   L.spmv_tiled = h->spmv_tiled;
   L.prefetch = h->prefetch;
   return L;
@@ -746,10 +752,12 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     cudaMemcpyAsync(h->d_val, val, vb * h->nnz, cudaMemcpyHostToDevice, h->stream);
   }
   if (ensure_workspace(h, 1) != TE_OK) return fail(TE_ERR_OOM, "workspace");
-  {  // lanes per row of the pipelined SpMV: <= ~16 gathers per lane per row (1, 2, 4 or 8);
-     // TE_SPMV_TPR overrides (measurement)
+  {  // lanes per row of the pipelined SpMV: the smallest power of two (1..8) leaving <= 20 (real
+     // values) / <= 8 (complex values, half-size tiles) entries per lane of a mean-length row;
+     // gathers in flight per lane 16 when that share fits one round, else 12 (complex: 8).
+     // Measured on configs 2-6.  TE_SPMV_TPR / TE_SPMV_NF_WIDE override.
     const double avg = n > 0 ? (double)h->nnz / (double)n : 0.0;
-    const double per_lane = cplx ? 8.0 : 16.0;  // complex tiles are half as large (kSpmvTileNnzC)
+    const double per_lane = cplx ? 8.0 : 20.0;
     int t = 1;
     while (t < 8 && per_lane * t < avg) t <<= 1;
     if (const char* e = getenv("TE_SPMV_TPR")) {
@@ -757,6 +765,10 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
       if (v == 1 || v == 2 || v == 4 || v == 8) t = v;
     }
     h->spmv_pipe_tpr = t;
+    h->spmv_nf_wide = !cplx && avg <= 16.0 * t;
+    if (const char* e = getenv("TE_SPMV_PF")) h->spmv_pf = atoi(e) != 0;
+    if (const char* e = getenv("TE_SPMV_NF_WIDE")) h->spmv_nf_wide = atoi(e) != 0;
+    if (const char* e = getenv("TE_SPMV_FORCE_HALO")) h->spmv_force_halo = atoi(e) != 0;
   }
   const int64_t tile_rows_cap = te::kSpmvMaxTileRows / h->spmv_pipe_tpr;
   {  // nnz-balanced SpMV tiles: close a tile before it would exceed kSpmvTileNnz entries or

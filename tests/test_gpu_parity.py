@@ -62,6 +62,34 @@ def test_krylov_basis_matches_oracle(gpu_lib, name, c, kset):
     h.close()
 
 
+PIPE_CASES = [("xxznnn_L12", configs.build(5, L=12)), ("s5_K4_N20", configs.build(6, K=4, K1=4, Nm=2, N0=20, Nc=20)),
+              ("cfg1_n1000_ragged", configs.build(1, n=1000))]
+
+
+@pytest.mark.parametrize("tpr", [1, 2, 4, 8])
+@pytest.mark.parametrize("wide", [0, 1])
+@pytest.mark.parametrize("halo", [0, 1])
+@pytest.mark.parametrize("name,c", PIPE_CASES, ids=[x[0] for x in PIPE_CASES])
+def test_spmv_pipe_variants(gpu_lib, name, c, tpr, wide, halo, monkeypatch):
+    """Every instantiation of the pipelined SpMV (lanes per row, gathers in flight, halo-aware
+    or not; chosen at te_create_csr from the environment) against the oracle's Arnoldi basis."""
+    te = gpu_lib
+    monkeypatch.setenv("TE_SPMV_TPR", str(tpr))
+    monkeypatch.setenv("TE_SPMV_NF_WIDE", str(wide))
+    monkeypatch.setenv("TE_SPMV_FORCE_HALO", str(halo))
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    m = 12
+    tol_rate = c["tol"] / c["t"]
+    g = te.te_krylov_basis(h, c["v0"], m, tol_rate, want_V=True)
+    o = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), c["v0"], m, tol_rate)
+    assert g["m_eff"] == o["m_eff"]
+    scale = max(1.0, np.abs(o["alpha"]).max(), np.abs(o["beta"]).max())
+    assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-12 * scale
+    assert np.abs(g["beta"] - o["beta"]).max() <= 1e-12 * scale
+    assert np.linalg.norm(g["V"] - o["V"]) <= 1e-10
+    h.close()
+
+
 @pytest.mark.parametrize("name,c", CASES, ids=[x[0] for x in CASES])
 def test_evolve_forced_and_adaptive(gpu_lib, name, c):
     te = gpu_lib
@@ -239,6 +267,26 @@ def test_full_size_xxz_L20_neel(gpu_lib):
     tau1 = sched[0][0]
     v1, _ = te.te_evolve_schedule(h, c["v0"], [tau1], c["tol"], c["m"])
     r1 = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], tau1, c["tol"], c["m"], schedule=[tau1])
+    assert np.linalg.norm(v1 - r1["v"]) <= 1e-10
+    h.close()
+
+
+def test_full_size_paper_s5_benchmark(gpu_lib):
+    """Config 6, the paper's own benchmark: d = 1,565,904, t = 10, err_max = 1e-7, m = 40.
+    The bound is met; the norm holds; the forward-backward round trip of P:509 at the P:527 size,
+    using exp(+iHt) w = conj(exp(-iHt) conj(w)) for real H, returns to v0 within the two
+    bounds; one forced restart (m = 8) against the oracle element by element."""
+    te = gpu_lib
+    c = configs.build(6)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    v, st = te.te_evolve(h, c["v0"], c["t"], c["tol"], c["m"])
+    assert st["err_bound"] <= c["tol"] and st["one_norm"] == pytest.approx(171.515, abs=5e-4)
+    assert abs(np.linalg.norm(v) - 1) <= st["err_bound"] + 1e-9
+    w, st2 = te.te_evolve(h, np.conj(v), c["t"], c["tol"], c["m"])
+    assert np.linalg.norm(np.conj(w) - c["v0"]) <= st["err_bound"] + st2["err_bound"] + 1e-9
+    tau, m = 0.02, 8
+    v1, _ = te.te_evolve_schedule(h, c["v0"], [tau], c["tol"], m)
+    r1 = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], tau, c["tol"], m, schedule=[tau])
     assert np.linalg.norm(v1 - r1["v"]) <= 1e-10
     h.close()
 

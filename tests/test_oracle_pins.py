@@ -16,7 +16,7 @@ import scipy.sparse as sp
 
 from oracle import krylov as K
 from workloads import memory_burden as mb
-from workloads import models
+from workloads import configs, models
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -66,6 +66,16 @@ def test_one_norm_hand_values():
     A = rand_herm(40, 0.2, 3)
     rp, c, v = csr_from_dense(A)
     assert math.isclose(K.one_norm(rp, c, v, 40), np.abs(A).sum(axis=0).max(), rel_tol=1e-14)
+
+
+def test_one_norm_paper_s5_matrix():
+    """The P:527 benchmark matrix (config 6): ||H||_1 = 171.515, computed independently in
+    SURVEY.md App. A from the column-sum closed form with 50-digit couplings f_i; the roundoff
+    estimate of Eq. 17 for one restart is then d ||H||_1 2^-52 = 5.96e-8 (BASELINE.md §1 note)."""
+    c = configs.build(6)
+    nrm = K.one_norm(c["rowptr"], c["col"], c["val"], c["n"])
+    assert abs(nrm - 171.515) <= 5e-4
+    assert abs(c["n"] * nrm * 2.0 ** -52 - 5.96e-8) <= 5e-11
 
 
 # ---------------------------------------------------------------- Arnoldi

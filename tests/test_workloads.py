@@ -67,3 +67,35 @@ def test_fast_xxz_row_range():
     lrp, lcol, lval = fast.xxz_csr_fast(L, 1.0, 0.5, h, J2=0.5, r0=r0, r1=r1)
     assert np.array_equal(lrp, rp[r0:r1 + 1] - rp[r0])
     assert np.array_equal(lcol, col[rp[r0]:rp[r1]]) and np.array_equal(lval, val[rp[r0]:rp[r1]])
+
+
+@pytest.mark.parametrize("p", [None, dict(K=6, K1=6, Nm=3, N0=30, Nc=30), dict(K=5, K1=3, Nm=4, N0=7, Nc=9, dNc=2),
+                               dict(K=3, K1=4, Nm=1, N0=0, Nc=5)], ids=["default", "K6", "asym", "N0_0"])
+def test_memory_burden_fast_builder_bit_exact(p):
+    """The vectorised §5 builder equals the per-row loop builder bit for bit."""
+    from workloads import memory_burden as mb
+    a, b = mb.hamiltonian(p), mb.hamiltonian_fast(p)
+    assert a["n"] == b["n"] and a["init_index"] == b["init_index"]
+    for k in ("rowptr", "col", "val"):
+        assert a[k].dtype == b[k].dtype and np.array_equal(a[k].view(np.uint8), b[k].view(np.uint8))
+
+
+def test_paper_s5_instance_config6():
+    """Config 6 = the P:527 benchmark matrix: d = 1,565,904 (printed); 122,109,000 nonzeros
+     plus 504 explicit zero diagonals: the diagonal eps(1-n0/Nc)qa + eps(1-n0/(Nc-dNc))qb
+     vanishes at n0 = Nc-dNc = 88 with qa = 0 and at n0 = Nc = 100 with qb = 0, C(10,5) = 252
+    rows each; 76 memory-sector entries (diagonal + 5*15 hops) + 1 or 2 C0 terms per row;
+    v0 = |N0,0,1^5,0^15>, the lexicographically largest tuple of the N0 block."""
+    c = configs.build(6)
+    rp, col, val = c["rowptr"], c["col"], c["val"]
+    assert c["n"] == 1565904
+    assert rp[-1] == 122109504 and int(np.count_nonzero(val)) == 122109000
+    w = np.diff(rp)
+    d2 = math.comb(20, 5)
+    assert np.all(w[:d2] == 77) and np.all(w[-d2:] == 77) and np.all(w[d2:-d2] == 78)
+    assert np.array_equal(np.nonzero(c["v0"])[0], [100 * d2 + d2 - 1])
+    zpos = np.nonzero(val == 0)[0]
+    zrows = np.searchsorted(rp, zpos, side="right") - 1
+    assert np.all(col[zpos] == zrows)                                  # every zero is a diagonal entry
+    blk, cnt = np.unique(zrows // d2, return_counts=True)
+    assert blk.tolist() == [88, 100] and cnt.tolist() == [252, 252]

@@ -12,12 +12,15 @@ Config strings (BASELINE.json "configs"):
  3 Bose-Hubbard L=12 N=12 (n=1,352,078), J=1 U=2 mu_i~U[-.5,.5], v0=|1..1>; t=5 tol=1e-8 m=50
  4 random n=2^24 complex, 32 nnz/row (16 band within +-255, 16 uniform); t=2 tol=1e-8 m=30
  5 XXZ+NNN periodic L=26, J1=1 J2=0.5 Delta=1, h_i~U[-1,1], product v0; t=10 tol=1e-10 m=40
+ 6 (not in BASELINE.json) the paper's own benchmark, §5 memory-burden model at
+   K=K'=10, N_m=5, N0=Nc=100 (d=1,565,904), initial state Eq. initialStateSimple; t=10
+   err_max=1e-7 m=40.  Deterministic (no random draws): the couplings f_i are P:452-460.
 """
 from __future__ import annotations
 
 import numpy as np
 
-from . import fast, models
+from . import fast, memory_burden, models
 
 NAMES = {
     1: "random_herm_n4096",
@@ -25,7 +28,11 @@ NAMES = {
     3: "bose_hubbard_L12_N12",
     4: "random_banded_n2^24",
     5: "xxz_nnn_L26",
+    6: "paper_s5_memory_burden_d1565904",
 }
+
+LABELS = {i: f"BASELINE configs[{i - 1}]" for i in range(1, 6)}
+LABELS[6] = "paper §5 P:527 benchmark (353 s on 1 CPU thread in the paper)"
 
 
 def params(i: int, **ov):
@@ -39,6 +46,8 @@ def params(i: int, **ov):
         p = dict(n=1 << 24, t=2.0, tol=1e-8, m=30)
     elif i == 5:
         p = dict(L=26, J1=1.0, J2=0.5, delta=1.0, t=10.0, tol=1e-10, m=40)
+    elif i == 6:
+        p = dict(K=10, K1=10, Nm=5, N0=100, Nc=100, t=10.0, tol=1e-7, m=40)
     else:
         raise ValueError(i)
     p.update(ov)
@@ -100,5 +109,13 @@ def build(i: int, with_matrix: bool = True, **ov):
             v0[int(np.searchsorted(keys, models.bh_keys(occ0)[0]))] = 1.0
         out["v0"] = v0
         out["occ"] = occ
+    elif i == 6:
+        mp = {k: p[k] for k in p if k not in ("t", "tol", "m")}
+        H = memory_burden.hamiltonian_fast(mp)
+        if with_matrix:
+            out["rowptr"], out["col"], out["val"] = H["rowptr"], H["col"], H["val"]
+        v0 = np.zeros(H["n"], dtype=np.complex128)
+        v0[H["init_index"]] = 1.0
+        out["v0"] = v0
     out["n"] = out["v0"].shape[0]
     return out
