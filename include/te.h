@@ -153,8 +153,12 @@ enum {
                                 1 non-adaptive Gauss-Legendre of order 30 ("simpler and faster",
                                 for explorative runs)                                                 */
   TE_OPT_SPMV = 5            /* SpMV kernel of kernel sets 2-4 (same arithmetic, measured choice):
-                                4 (default) nnz-balanced tiles, rowptr/col/val of the next tile
-                                in flight by cp.async double buffering, thread-per-row gathers;
+                                4 (default) nnz-balanced tiles, rowptr/col/val of the next tile in
+                                flight by bulk copies (TMA engine) into a double buffer, TPR lanes
+                                per row with 12-16 register gathers in flight per lane;
+                                5 async gather: 1024-entry tiles, 3-stage bulk-copy ring, x gathers
+                                as cp.async copies into shared memory overlapping the previous
+                                tile's products;
                                 3 as 4 without the pipeline; 1 nnz-balanced tiles, entry-parallel products;
                                 2 TMA-fed (bulk copies of rowptr/col/val into a shared-memory ring,
                                 warp-specialised); 0 CSR-vector                                       */

@@ -17,6 +17,8 @@
 
 #include <cuda.h>
 #include <cstdio>
+#include <utility>
+#include <vector>
 
 namespace te {
 
@@ -1538,6 +1540,175 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j, int pf
   }
 }
 
+// SpMV variant 5 (async gather).  The x gathers of a tile are cp.async copies into shared
+// memory, so a whole tile's gathers (<= kAgCap) are in flight at once without holding registers,
+// and they overlap the products of the previous tile:
+//   iteration it:  bulk copy (TMA engine) of tile it+2's rowptr/col/val   [3-stage ring]
+//                  cp.async gathers x[col] of tile it+1                   [2-stage ring]
+//                  products + per-row sums of tile it from shared memory
+// Tile descriptors {ra, rb, b, e} come from a host-built table (te_api: kAgCap entries, <=
+// kThreads/TPR rows per tile) through a 4-slot shared ring that thread 0 fills one iteration
+// ahead.  Per row: TPR lanes, in-order partial sums, fixed xor reduction (deterministic).
+__device__ __forceinline__ void cp_async16_ca(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <bool CPLX>
+struct AgLayout {
+  using VT = typename ValT<CPLX>::T;
+  static constexpr size_t kVal = (size_t)(kAgCap + 4) * sizeof(VT);
+  static constexpr size_t kRp = (size_t)(kAgMaxRows + 4) * 8;
+  static constexpr size_t kCol = (size_t)(kAgCap + 4) * 4;
+  static constexpr size_t kStage = kVal + kRp + kCol;
+  static constexpr size_t kBytes = 3 * kStage + 2 * (size_t)kAgCap * 16;
+};
+
+template <bool CPLX>
+size_t spmv_ag_smem() { return AgLayout<CPLX>::kBytes; }
+
+template <bool CPLX, int TPR, bool HALO>
+__global__ void __launch_bounds__(kThreads, CPLX ? 2 : 3) k_spmv_ag(KDev d, int j) {
+  using VT = typename ValT<CPLX>::T;
+  using LY = AgLayout<CPLX>;
+  extern __shared__ __align__(16) unsigned char sm[];
+  auto vs_of = [&](int st) { return reinterpret_cast<const VT*>(sm + st * LY::kStage); };
+  auto rp_of = [&](int st) { return reinterpret_cast<const int64_t*>(sm + st * LY::kStage + LY::kVal); };
+  auto cs_of = [&](int st) { return reinterpret_cast<const int32_t*>(sm + st * LY::kStage + LY::kVal + LY::kRp); };
+  auto xg_of = [&](int b) { return reinterpret_cast<double2*>(sm + 3 * LY::kStage) + (size_t)b * kAgCap; };
+  __shared__ double sj_s;
+  __shared__ double2 red[kWarps];
+  __shared__ __align__(8) uint64_t bar[3];
+  __shared__ int64_t ring[4][4];  // descriptors of iterations it..it+3 (slot it & 3); ra < 0: none
+  const int tid = threadIdx.x;
+  const int64_t G = gridDim.x, t0 = blockIdx.x;
+  const int64_t* __restrict__ tab = d.tile_ag;
+  const uint64_t pol = policy_evict_first();
+  auto load_desc = [&](int64_t it, int64_t (&o)[4]) {
+    const int64_t t = t0 + it * G;
+    if (t < d.ntiles_ag) {
+      const longlong2 a = __ldg(reinterpret_cast<const longlong2*>(tab + 4 * t));
+      const longlong2 b = __ldg(reinterpret_cast<const longlong2*>(tab + 4 * t) + 1);
+      o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+    } else {
+      o[0] = -1; o[1] = -1; o[2] = 0; o[3] = 0;
+    }
+  };
+  // bulk copy of one tile's rowptr / col / val (16-byte-aligned supersets) into stage st
+  auto issue = [&](const int64_t* td, int st) {
+    if (td[0] < 0) return;
+    const int64_t cnt = td[3] - td[2];
+    const int64_t r0 = td[0] & ~1LL, r1 = (td[1] + 2) & ~1LL;
+    unsigned br = (unsigned)((r1 - r0) * 8), bc = 0, bv = 0;
+    int64_t c0 = 0, v0 = 0;
+    constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
+    if (cnt <= kAgCap) {
+      c0 = td[2] & ~3LL;
+      v0 = td[2] & ~(VA - 1);
+      bc = (unsigned)((((td[3] + 3) & ~3LL) - c0) * 4);
+      bv = (unsigned)((((td[3] + VA - 1) & ~(VA - 1)) - v0) * sizeof(VT));
+    }
+    unsigned char* base = sm + st * LY::kStage;
+    mbar_expect_tx(&bar[st], br + bc + bv);
+    bulk_g2s(base + LY::kVal, d.rowptr + r0, br, &bar[st], pol);
+    if (bc) bulk_g2s(base + LY::kVal + LY::kRp, d.col + c0, bc, &bar[st], pol);
+    if (bv) bulk_g2s(base, static_cast<const VT*>(d.val) + v0, bv, &bar[st], pol);
+  };
+  if (tid == 0) {
+    sj_s = step_gate(d, j, blockIdx.x == 0);
+    for (int k = 0; k < 3; ++k) mbar_init(&bar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int k = 0; k < 3; ++k) {
+      int64_t o[4];
+      load_desc(k, o);
+      for (int q = 0; q < 4; ++q) ring[k][q] = o[q];
+    }
+    if (sj_s != 0.0) {
+      issue(ring[0], 0);
+      issue(ring[1], 1);
+    }
+  }
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  asm volatile("" : "+l"(x));
+  const double2* __restrict__ halo = d.halo;
+  const int64_t n = d.n;
+  // gathers of iteration k's tile (stage k % 3 must have landed) into xg[k & 1]
+  auto gather = [&](int64_t k) {
+    const int64_t* td = ring[k & 3];
+    if (td[0] < 0) return;
+    const int64_t b = td[2], cnt = td[3] - b;
+    if (cnt > kAgCap) return;  // long row: summed from global memory in the compute phase
+    const int st = (int)(k % 3);
+    mbar_wait(&bar[st], (unsigned)((k / 3) & 1));
+    const int32_t* cc = cs_of(st) + (b & 3);
+    double2* xb = xg_of((int)(k & 1));
+    for (int e = tid; e < (int)cnt; e += kThreads) {
+      const int c = cc[e];
+      const double2* src;
+      if (HALO) src = ((uint32_t)c < (uint32_t)n) ? x + c : halo + (c - (int)n);
+      else src = x + c;
+      cp_async16_ca(xb + e, src);
+    }
+  };
+  gather(0);
+  cp_async_commit();
+  const int q = tid % TPR, grp = tid / TPR;
+  for (int64_t it = 0;; ++it) {
+    const int64_t ra = ring[it & 3][0];
+    if (ra < 0) break;
+    int64_t nd[4];
+    if (tid == 0) {
+      load_desc(it + 3, nd);               // lands during this iteration
+      issue(ring[(it + 2) & 3], (int)((it + 2) % 3));
+    }
+    gather(it + 1);
+    cp_async_commit();
+    cp_async_wait1();                      // this thread's gathers of tile it are complete
+    __syncthreads();                       // ... and every thread's
+    const int64_t rb = ring[it & 3][1], b = ring[it & 3][2], e = ring[it & 3][3];
+    const int64_t cnt = e - b;
+    const int st = (int)(it % 3);
+    if (cnt <= kAgCap) {
+      constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
+      const int64_t* rp = rp_of(st) + (ra & 1);
+      const VT* vv = vs_of(st) + (b & (VA - 1));
+      const double2* xb = xg_of((int)(it & 1));
+      const int rows = (int)(rb - ra);
+      const int i = grp;
+      const bool act = i < rows;
+      const int lo = act ? (int)(rp[i] - b) : 0, hi = act ? (int)(rp[i + 1] - b) : 0;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int k = lo + q; k < hi; k += TPR) acc = cadd(acc, ValT<CPLX>::mul(vv[k], xb[k]));
+      if (TPR > 1) acc = group_sum<TPR>(acc);
+      if (act && q == 0) __stcs(d.W + ra + i, make_double2(acc.x * sj, acc.y * sj));
+    } else {  // one long row, straight from global memory (its stage holds only rowptr)
+      const VT* __restrict__ val = static_cast<const VT*>(d.val);
+      double2 acc = make_double2(0.0, 0.0);
+      for (int64_t k = b + tid; k < e; k += kThreads) {
+        const int c = __ldg(d.col + k);
+        const double2 xv = (!HALO || (uint32_t)c < (uint32_t)n) ? __ldg(x + c) : __ldg(halo + (c - (int)n));
+        acc = cadd(acc, ValT<CPLX>::mul(__ldg(val + k), xv));
+      }
+      acc = warp_sum(acc);
+      if ((tid & 31) == 0) red[tid >> 5] = acc;
+      __syncthreads();
+      if (tid == 0) {
+        double2 s2 = red[0];
+        for (int w = 1; w < kWarps; ++w) s2 = cadd(s2, red[w]);
+        __stcs(d.W + ra, make_double2(s2.x * sj, s2.y * sj));
+      }
+    }
+    if (tid == 0)
+      for (int k = 0; k < 4; ++k) ring[(it + 3) & 3][k] = nd[k];
+    __syncthreads();                       // stage it % 3, xg[it & 1] and ring slot it & 3 free
+    if (tid == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  cp_async_wait0();
+}
+
 // Standalone SpMV p = s_j H V_j -> W (CSR-vector, TPR lanes per row, high occupancy).
 template <bool CPLX, int TPR>
 __global__ void __launch_bounds__(kThreads) k_spmv(KDev d, int j) {
@@ -1921,6 +2092,13 @@ cudaError_t configure_kernels() {
   set((const void*)k_proj_tma<0>, kProjSmemBudget + 1024);
   set((const void*)k_proj_tma<3>, kProjSmemBudget + 1024);
   set((const void*)k_spmv_tma<false>, kProjSmemBudget + 1024);
+#define TE_SETAG(T)                                                                      \
+  set((const void*)k_spmv_ag<false, T, false>, spmv_ag_smem<false>());                   \
+  set((const void*)k_spmv_ag<true, T, false>, spmv_ag_smem<true>());                     \
+  set((const void*)k_spmv_ag<false, T, true>, spmv_ag_smem<false>());                    \
+  set((const void*)k_spmv_ag<true, T, true>, spmv_ag_smem<true>());
+  TE_SETAG(1) TE_SETAG(2) TE_SETAG(4) TE_SETAG(8) TE_SETAG(16) TE_SETAG(32)
+#undef TE_SETAG
 #define TE_SETP(T)                                                  \
   set((const void*)k_spmv_pipe<false, T, false, 12>, spmv_pipe_smem<false>()); \
   set((const void*)k_spmv_pipe<true, T, false, 8>, spmv_pipe_smem<true>());    \
@@ -1953,6 +2131,41 @@ static int tpr_for(int ncols, int min_tpr) {
   }
 
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
+  if (L.spmv_tiled == 5 && d.ntiles_ag > 0) {
+    const bool hal = d.halo || L.spmv_force_halo;
+    // persistent grid = co-resident blocks (occupancy API, cached per instantiation)
+    auto grid_of = [&](const void* f, size_t smem) {
+      static std::vector<std::pair<const void*, int>> cache;
+      int per_sm = 0;
+      for (auto& c : cache)
+        if (c.first == f) per_sm = c.second;
+      if (per_sm == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kThreads, smem) != cudaSuccess || per_sm < 1)
+          per_sm = 1;
+        cache.emplace_back(f, per_sm);
+      }
+      return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * L.num_sms, d.ntiles_ag));
+    };
+#define TE_AG_H(T, H)                                                                                        \
+  if (cplx) {                                                                                                \
+    const int grid = grid_of((const void*)k_spmv_ag<true, T, H>, spmv_ag_smem<true>());                     \
+    k_spmv_ag<true, T, H><<<grid, kThreads, spmv_ag_smem<true>(), L.stream>>>(d, j);                         \
+  } else {                                                                                                   \
+    const int grid = grid_of((const void*)k_spmv_ag<false, T, H>, spmv_ag_smem<false>());                   \
+    k_spmv_ag<false, T, H><<<grid, kThreads, spmv_ag_smem<false>(), L.stream>>>(d, j);                       \
+  }
+#define TE_AG(T)                                            \
+  case T:                                                   \
+    if (hal) { TE_AG_H(T, true) } else { TE_AG_H(T, false) } \
+    break;
+    switch (L.spmv_ag_tpr) {
+      TE_AG(1) TE_AG(2) TE_AG(4) TE_AG(8) TE_AG(16)
+      default: TE_AG(32)
+    }
+#undef TE_AG
+#undef TE_AG_H
+    return;
+  }
   if (L.spmv_tiled == 4 && d.ntiles > 0) {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * L.num_sms, d.ntiles));
     switch (L.spmv_pipe_tpr) {

@@ -21,6 +21,8 @@ constexpr int kSpmvChunk = 4096;     // K1 products staged in shared memory per 
 constexpr int kSpmvTileNnz = 4096;   // entries per nnz-balanced SpMV tile (cap), real values
 constexpr int kSpmvTileNnzC = 2048;  // complex values (two pipelined blocks per SM)
 constexpr int kSpmvMaxTileRows = 256;   // rows per SpMV tile cap (one thread per row)
+constexpr int kAgCap = 1024;            // entries per async-gather SpMV tile (variant 5)
+constexpr int kAgMaxRows = 128;         // rows per async-gather tile cap (<= kThreads / TPR)
 constexpr int kSpmvTmaNnzCap = 512;     // entries per TMA SpMV tile (== kSpmvTmaNnz)
 constexpr int kSpmvTmaRowCap = 128;     // rows per TMA SpMV tile
 
@@ -34,6 +36,8 @@ struct KDev {
   const void* val;
   const int64_t* tile_row;  // [ntiles+1] first row of each nnz-balanced SpMV tile
   int64_t ntiles;
+  const int64_t* tile_ag;    // [4*ntiles_ag] {first row, end row, first entry, end entry} (variant 5)
+  int64_t ntiles_ag;
   const int64_t* tile_desc;  // [2*(ntiles_desc+1)] {first row, first entry} of the TMA SpMV tiles
   int64_t ntiles_desc;
   const double2* halo;  // x entries for columns >= n (distributed); nullptr otherwise
@@ -62,7 +66,8 @@ struct Launch {
   int spmv_pipe_tpr;  // lanes per row of the pipelined SpMV (tile row cap = kThreads / this)
   int spmv_pf;        // pipelined SpMV: L2 prefetch of tile t+2G (0 off, 1 on)
   int spmv_force_halo;  // test hook: run the multi-rank (halo-aware) SpMV instantiation on one rank
-  int spmv_nf_wide;   // pipelined SpMV gathers in flight per lane: 0 -> 12 real / 8 complex, 1 -> 16 / 12
+  int spmv_nf_wide;
+  int spmv_ag_tpr;    // lanes per row of the async-gather SpMV (1..32)   // pipelined SpMV gathers in flight per lane: 0 -> 12 real / 8 complex, 1 -> 16 / 12
   int proj_tma;   // 2: hybrid by column count (default), 1: TMA-tiled only, 0: register/shuffle only
   int spmv_tiled; // 2: TMA-fed SpMV (default), 1: nnz-balanced tiled SpMV, 0: CSR-vector
   int prefetch; // L2 bulk-prefetch distance in block iterations (0: off)

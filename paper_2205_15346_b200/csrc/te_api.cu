@@ -121,6 +121,9 @@ struct te_handle {
   int64_t* d_tile_row = nullptr;
   int64_t ntiles = 0;
   int64_t* d_tile_desc = nullptr;
+  int64_t* d_tile_ag = nullptr;
+  int64_t ntiles_ag = 0;
+  int spmv_ag_tpr = 1;
   int64_t ntiles_desc = 0;
   std::vector<CUtensorMap> tmaps;
   int prefetch = 0;
@@ -176,6 +179,8 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.tile_row = h->d_tile_row;
   d.ntiles = h->ntiles;
   d.tile_desc = h->d_tile_desc;
+  d.tile_ag = h->d_tile_ag;
+  d.ntiles_ag = h->ntiles_ag;
   d.ntiles_desc = h->ntiles_desc;
   d.alpha = h->d_small + kOffAlpha;
   d.beta = h->d_small + kOffBeta;
@@ -210,6 +215,7 @@ Launch make_launch(te_handle* h) {
   L.spmv_pf = h->spmv_pf;
   L.spmv_nf_wide = h->spmv_nf_wide;
   L.spmv_force_halo = h->spmv_force_halo;
+  L.spmv_ag_tpr = h->spmv_ag_tpr;
   L.spmv_tiled = h->spmv_tiled;
   L.prefetch = h->prefetch;
   return L;
@@ -811,6 +817,36 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     cudaMemcpyAsync(h->d_tile_desc, td.data(), sizeof(int64_t) * td.size(), cudaMemcpyHostToDevice, h->stream);
     cudaStreamSynchronize(h->stream);
   }
+  {  // async-gather SpMV (variant 5) tiles: <= kAgCap entries and <= kThreads/tpr rows, stored as
+     // {first row, end row, first entry, end entry}; lanes per row = the largest power of two
+     // <= mean row length / 4 (1..32), so a full tile keeps every row group busy
+    const double avg = n > 0 ? (double)h->nnz / (double)n : 0.0;
+    int ta = 1;
+    while (ta < 32 && 2.0 * ta * 4.0 <= avg) ta <<= 1;
+    if (const char* e = getenv("TE_SPMV_AG_TPR")) {
+      const int v = atoi(e);
+      if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) ta = v;
+    }
+    h->spmv_ag_tpr = ta;
+    const int64_t rcap = std::min<int64_t>(te::kAgMaxRows, te::kThreads / ta);
+    std::vector<int64_t> tg;
+    int64_t st = 0;
+    for (int64_t r = 0; r < n; ++r) {
+      const bool over_rows = (r + 1 - st) > rcap;
+      const bool over_nnz = (rowptr[r + 1] - rowptr[st]) > te::kAgCap && r > st;
+      if (over_rows || over_nnz) {
+        tg.insert(tg.end(), {st, r, rowptr[st], rowptr[r]});
+        st = r;
+      }
+    }
+    if (n > 0) tg.insert(tg.end(), {st, n, rowptr[st], rowptr[n]});
+    h->ntiles_ag = (int64_t)tg.size() / 4;
+    if (!tg.empty()) {
+      if (cudaMalloc(&h->d_tile_ag, sizeof(int64_t) * tg.size()) != cudaSuccess) return fail(TE_ERR_OOM, "tiles");
+      cudaMemcpyAsync(h->d_tile_ag, tg.data(), sizeof(int64_t) * tg.size(), cudaMemcpyHostToDevice, h->stream);
+      cudaStreamSynchronize(h->stream);
+    }
+  }
   // validation + ||H||_1 on the device
   int* d_err = reinterpret_cast<int*>(h->d_counter + 4);
   unsigned long long* d_norm = reinterpret_cast<unsigned long long*>(h->d_small + kOffScalar);
@@ -890,6 +926,7 @@ void te_destroy(te_handle* h) {
   cudaFree(h->d_halo);
   cudaFree(h->d_tile_row);
   cudaFree(h->d_tile_desc);
+  cudaFree(h->d_tile_ag);
   cudaFree(h->d_sendbuf);
   cudaFree(h->d_send_idx);
   if (h->h_small) cudaFreeHost(h->h_small);
@@ -1044,8 +1081,8 @@ int te_set_option(te_handle* h, int option, double value) {
       h->integrator = (int)value;
       return TE_OK;
     case TE_OPT_SPMV:
-      if (value < 0.0 || value > 4.0 || value != (double)(int)value)
-        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 0..4");
+      if (value < 0.0 || value > 5.0 || value != (double)(int)value)
+        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 0..5");
       h->spmv_tiled = (int)value;
       return TE_OK;
     case TE_OPT_PREFETCH:

@@ -35,8 +35,9 @@ def small_cases():
 CASES = small_cases()
 
 
-KERNEL_SETS = [(2, 4), (2, 3), (2, 1), (2, 2), (2, 0), (3, 4), (4, 4), (0, 4), (1, 4)]
-KERNEL_IDS = ["hybrid-spmvpipe", "hybrid-spmvrow", "hybrid-spmvtile", "hybrid-spmvtma", "hybrid-spmvvec", "tma", "shuffle", "fused-register", "staged"]
+KERNEL_SETS = [(2, 4), (2, 5), (2, 3), (2, 1), (2, 2), (2, 0), (3, 4), (4, 4), (0, 4), (1, 4)]
+KERNEL_IDS = ["hybrid-spmvpipe", "hybrid-spmvag", "hybrid-spmvrow", "hybrid-spmvtile", "hybrid-spmvtma", "hybrid-spmvvec",
+              "tma", "shuffle", "fused-register", "staged"]
 
 
 @pytest.mark.parametrize("kset", KERNEL_SETS, ids=KERNEL_IDS)
@@ -78,6 +79,49 @@ def test_spmv_pipe_variants(gpu_lib, name, c, tpr, wide, halo, monkeypatch):
     monkeypatch.setenv("TE_SPMV_NF_WIDE", str(wide))
     monkeypatch.setenv("TE_SPMV_FORCE_HALO", str(halo))
     h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    m = 12
+    tol_rate = c["tol"] / c["t"]
+    g = te.te_krylov_basis(h, c["v0"], m, tol_rate, want_V=True)
+    o = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), c["v0"], m, tol_rate)
+    assert g["m_eff"] == o["m_eff"]
+    scale = max(1.0, np.abs(o["alpha"]).max(), np.abs(o["beta"]).max())
+    assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-12 * scale
+    assert np.abs(g["beta"] - o["beta"]).max() <= 1e-12 * scale
+    assert np.linalg.norm(g["V"] - o["V"]) <= 1e-10
+    h.close()
+
+
+AG_CASES = PIPE_CASES + [("long_rows", None)]
+
+
+def _long_row_case():
+    """Rows longer than one async-gather tile (kAgCap = 1024 entries) next to short ones."""
+    n = 3000
+    g = np.random.default_rng(11)
+    A = np.zeros((n, n), complex)
+    A[np.arange(n), np.arange(n)] = g.standard_normal(n)
+    for r in (5, 1700):
+        cols = g.choice(n, 1500, replace=False)
+        A[r, cols] = g.standard_normal(1500) + 1j * g.standard_normal(1500)
+    A = (A + A.conj().T) / 2
+    rp, col, val = csr_from_dense(A)
+    v0 = g.standard_normal(n) + 1j * g.standard_normal(n)
+    return dict(n=n, rowptr=rp, col=col, val=val, v0=v0 / np.linalg.norm(v0), t=1.0, tol=1e-8, m=12)
+
+
+@pytest.mark.parametrize("tpr", [1, 4, 16, 32])
+@pytest.mark.parametrize("halo", [0, 1])
+@pytest.mark.parametrize("name,c", AG_CASES, ids=[x[0] for x in AG_CASES])
+def test_spmv_async_gather_variants(gpu_lib, name, c, tpr, halo, monkeypatch):
+    """The async-gather SpMV (TE_OPT_SPMV = 5) for several lanes-per-row choices, with and without
+    the halo-aware instantiation, including rows longer than a tile, against the oracle."""
+    te = gpu_lib
+    if c is None:
+        c = _long_row_case()
+    monkeypatch.setenv("TE_SPMV_AG_TPR", str(tpr))
+    monkeypatch.setenv("TE_SPMV_FORCE_HALO", str(halo))
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    te.te_set_option(h, te.TE_OPT_SPMV, 5)
     m = 12
     tol_rate = c["tol"] / c["t"]
     g = te.te_krylov_basis(h, c["v0"], m, tol_rate, want_V=True)

@@ -8,10 +8,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--t", type=float, default=None)
 ap.add_argument("--kernels", type=int, default=2)
+ap.add_argument("--spmv", type=int, default=None)
 a = ap.parse_args()
 c = configs.build(a.config)
 h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
 te.te_set_option(h, te.TE_OPT_KERNELS, a.kernels)
+if a.spmv is not None:
+    te.te_set_option(h, te.TE_OPT_SPMV, a.spmv)
 t = a.t if a.t is not None else c["t"] / 8
 v, st = te.te_evolve(h, c["v0"], t, c["tol"] * t / c["t"], c["m"])
 print("restarts", st["n_restarts"], "steps", st["n_krylov_steps"], "bound", st["err_bound"])
