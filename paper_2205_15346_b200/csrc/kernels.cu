@@ -765,8 +765,45 @@ __device__ __forceinline__ double2 butterfly_colsum16(double (&re)[16], double (
   return make_double2(re[0], im[0]);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kProjThreads, 1)
+// colsum for NREG register-accumulated columns: NREG = 32 -> lane k owns column k; NREG = 16 ->
+// lanes k and k + 16 own column k
+// 8-column variant: lanes l, l+8, l+16, l+24 end with the sum of column l & 7
+__device__ __forceinline__ double2 butterfly_colsum8(double (&re)[8], double (&im)[8]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    re[i] += __shfl_xor_sync(0xffffffffu, re[i], 16);
+    im[i] += __shfl_xor_sync(0xffffffffu, im[i], 16);
+    re[i] += __shfl_xor_sync(0xffffffffu, re[i], 8);
+    im[i] += __shfl_xor_sync(0xffffffffu, im[i], 8);
+  }
+#pragma unroll
+  for (int s = 4; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double sr = up ? re[i] : re[i + s];
+      const double si = up ? im[i] : im[i + s];
+      const double kr = up ? re[i + s] : re[i];
+      const double ki = up ? im[i + s] : im[i];
+      re[i] = kr + __shfl_xor_sync(0xffffffffu, sr, s);
+      im[i] = ki + __shfl_xor_sync(0xffffffffu, si, s);
+    }
+  }
+  return make_double2(re[0], im[0]);
+}
+template <int NREG>
+__device__ __forceinline__ double2 colsum_reg(double (&re)[NREG], double (&im)[NREG]) {
+  if constexpr (NREG == 32) return butterfly_colsum(re, im);
+  else if constexpr (NREG == 16) return butterfly_colsum16(re, im);
+  else return butterfly_colsum8(re, im);
+}
+
+// NREG: columns whose per-lane partial sums persist in registers across tiles (32 or 16; the
+// rest go through 16-wide butterflies per sub-tile).  MINB: resident CTAs per SM (the slot ring
+// shares the shared-memory budget between them).
+template <int MODE, int NREG = 32, int MINB = 1>
+__global__ void __launch_bounds__(kProjThreads, MINB)
     k_proj_tma(const __grid_constant__ CUtensorMap tmV, KDev d, int j, int S, int R, int C, int write) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxSlots], empty[kMaxSlots];
@@ -839,10 +876,11 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   } else if (warp < C) {  // ------- consumers: warp owns slots warp, warp + C, ... (< S)
     // columns 0..31: per-lane partial sums over all of this warp's rows, kept in registers and
     // reduced across lanes once at the end; columns 32..: butterfly per 32-row sub-tile
-    double aR[32], aI[32];
+    double aR[NREG], aI[NREG];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) aR[c] = aI[c] = 0.0;
-    double2 acc1 = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+    for (int c = 0; c < NREG; ++c) aR[c] = aI[c] = 0.0;
+    // 16-wide butterfly groups above NREG (<= 4): lane l & 15 owns column NREG + 16 g + (l & 15)
+    double2 accb0 = make_double2(0.0, 0.0), accb1 = accb0, accb2 = accb0, accb3 = accb0;
     double nrm = 0.0;
     double2* outV = (MODE == 3 && write) ? d.V + (int64_t)(j + 1) * d.ldv : nullptr;
     bool more = true;
@@ -889,14 +927,15 @@ __global__ void __launch_bounds__(kProjThreads, 1)
             }
           }
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
+          for (int c = 0; c < NREG; ++c) {
             if (c < ncols) {
               const double2 v = Vs[c * TR + row];
               aR[c] = fma(v.x, p.x, fma(v.y, p.y, aR[c]));   // conj(v) * p
               aI[c] = fma(v.x, p.y, fma(-v.y, p.x, aI[c]));
             }
           }
-          for (int cb = 32; cb < ncols; cb += 16) {  // columns 32..63 in 16-wide butterflies
+#pragma unroll 1
+          for (int cb = NREG; cb < ncols; cb += 16) {  // columns NREG.. in 16-wide butterflies
             double re[16], im[16];
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
@@ -906,18 +945,24 @@ __global__ void __launch_bounds__(kProjThreads, 1)
               im[c] = v.x * p.y - v.y * p.x;
             }
             const double2 cs = butterfly_colsum16(re, im);
-            if (cb == 32) acc1 = cadd(acc1, cs); else acc2 = cadd(acc2, cs);
+            const int g = (cb - NREG) >> 4;
+            if (g == 0) accb0 = cadd(accb0, cs);
+            else if (g == 1) accb1 = cadd(accb1, cs);
+            else if (g == 2) accb2 = cadd(accb2, cs);
+            else accb3 = cadd(accb3, cs);
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
     }
-    const double2 acc0 = butterfly_colsum(aR, aI);
-    red[warp][lane] = acc0;
+    const double2 acc0 = colsum_reg<NREG>(aR, aI);
+    if (lane < NREG) red[warp][lane] = acc0;
     if (lane < 16) {
-      red[warp][32 + lane] = acc1;
-      red[warp][48 + lane] = acc2;
+      const double2 ab[4] = {accb0, accb1, accb2, accb3};
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        if (NREG + 16 * g + lane < kMaxCols) red[warp][NREG + 16 * g + lane] = ab[g];
     }
     if (MODE == 3) {
       nrm = warp_sum(nrm);
@@ -2091,6 +2136,12 @@ cudaError_t configure_kernels() {
 #undef TE_SET
   set((const void*)k_proj_tma<0>, kProjSmemBudget + 1024);
   set((const void*)k_proj_tma<3>, kProjSmemBudget + 1024);
+  set((const void*)k_proj_tma<0, 8>, kProjSmemBudget + 1024);
+  set((const void*)k_proj_tma<3, 8>, kProjSmemBudget + 1024);
+  set((const void*)k_proj_tma<1, 8>, kProjSmemBudget + 1024);
+  set((const void*)k_proj_tma<0, 16>, kProjSmemBudget + 1024);
+  set((const void*)k_proj_tma<3, 16>, kProjSmemBudget + 1024);
+  set((const void*)k_proj_tma<1, 16>, kProjSmemBudget + 1024);
   set((const void*)k_spmv_tma<false>, kProjSmemBudget + 1024);
 #define TE_SETAG(T)                                                                      \
   set((const void*)k_spmv_ag<false, T, false>, spmv_ag_smem<false>());                   \
@@ -2229,9 +2280,18 @@ static void launch_proj_s(const KDev& d, int j, int mode, const Launch& L) {
 }
 
 // measured on B200 (tools/micro/mb_proj.cu, 16 KB minimum TMA tiles): the register/shuffle kernel
-// is faster for the dots up to 4 columns and for the update up to 8 columns, the TMA ring above.
+// is faster for the dots up to 4 columns and for the update up to 5 columns, the TMA ring above;
+// the TMA ring keeps per-lane register column sums for the smallest of 8 / 16 / 32 columns that
+// covers ncols (fewer live registers at small ncols: 8 columns, update 3.7 -> 4.7 TB/s)
 constexpr int kShuffleMaxColsDots = 4;
-constexpr int kShuffleMaxCols = 8;
+constexpr int kShuffleMaxCols = 5;
+
+#define TE_PROJ_TMA(MODE, ncols, ...)                                                                   \
+  do {                                                                                                  \
+    if ((ncols) <= 8) k_proj_tma<MODE, 8><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__);      \
+    else if ((ncols) <= 16) k_proj_tma<MODE, 16><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__); \
+    else k_proj_tma<MODE, 32><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__);                   \
+  } while (0)
 
 void launch_proj_dots(const KDev& d, int j, const Launch& L) {
   if (L.proj_tma == 0 || (L.proj_tma == 2 && j + 1 <= kShuffleMaxColsDots)) {
@@ -2239,12 +2299,12 @@ void launch_proj_dots(const KDev& d, int j, const Launch& L) {
     return;
   }
   const int S = proj_slots(j + 1), R = proj_rsub(j + 1), C = proj_consumers(j + 1);
-  k_proj_tma<0><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S, R, C, 0);
+  TE_PROJ_TMA(0, j + 1, L.tmaps[j], d, j, S, R, C, 0);
 }
 
 void launch_gram_update(const KDev& d, int j, bool write, const Launch& L) {
   const int S = proj_slots(j + 1), R = proj_rsub(j + 1), C = proj_consumers(j + 1);
-  k_proj_tma<3><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S, R, C, write ? 1 : 0);
+  TE_PROJ_TMA(3, j + 1, L.tmaps[j], d, j, S, R, C, write ? 1 : 0);
 }
 
 void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L) {
@@ -2281,7 +2341,7 @@ void launch_update_proj(const KDev& d, int j, const Launch& L) {
   }
   if (L.variant == 2) {
     const int S = proj_slots(j + 1), R = proj_rsub(j + 1), C = proj_consumers(j + 1);
-    k_proj_tma<1><<<L.num_sms, kProjThreads, proj_smem_bytes(j + 1), L.stream>>>(L.tmaps[j], d, j, S, R, C, 0);
+    TE_PROJ_TMA(1, j + 1, L.tmaps[j], d, j, S, R, C, 0);
     return;
   }
   if (L.variant == 0) {
