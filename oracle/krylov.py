@@ -13,6 +13,8 @@ listed in DESIGN.md "Readings".  Everything is complex128 / float64.
 Functions and what pins them (tests/test_oracle_pins.py):
   spmv            y = H x, row by row (Eq. 8 first line)
                   pinned: dense mat-vec, identity/permutation.
+  spmv_rows       the same definition for listed rows only (sampled full-size checks)
+                  pinned: dense mat-vec rows, empty rows.
   one_norm        ||H||_1 = max column abs sum (Eq. 17)
                   pinned: hand values, scaling.
   arnoldi         Eq. 8 / Alg. 1 step 1 with ortho
@@ -76,6 +78,17 @@ def spmv(rowptr, col, val, x):
     rows = np.repeat(np.arange(n), np.diff(rowptr))
     y = np.zeros(n, dtype=np.complex128)
     np.add.at(y, rows, val * x[col])
+    return y
+
+
+def spmv_rows(rowptr, col, val, x, rows):
+    """(H x)_r for the listed rows r only: the definition of ``spmv`` restricted to those rows
+    (sampled full-size checks, where the full product is too slow for the oracle)."""
+    rows = np.asarray(rows, dtype=np.int64)
+    y = np.zeros(rows.shape[0], dtype=np.complex128)
+    for i, r in enumerate(rows):
+        a, b = int(rowptr[r]), int(rowptr[r + 1])
+        y[i] = np.sum(val[a:b] * x[col[a:b]])
     return y
 
 

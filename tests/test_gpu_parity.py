@@ -335,6 +335,88 @@ def test_full_size_paper_s5_benchmark(gpu_lib):
     h.close()
 
 
+def _sampled_arnoldi_relation(te, c, m=4, nsample=300, seed=0):
+    """Full-size check of one Krylov decomposition in bench.py's launch configuration (default
+    kernels): orthonormal basis (all n rows) and the three-term Arnoldi relation of Eq. 8,
+    H V_k = beta_{k-1} V_{k-1} + alpha_k V_k + beta_k V_{k+1}, on sampled rows with (H V_k)_r
+    from the oracle's row-restricted product (reading C2: CGS2's off-tridiagonal coefficients
+    vanish for Hermitian H up to rounding)."""
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    g = te.te_krylov_basis(h, c["v0"], m, c["tol"] / c["t"], want_V=True)
+    nrm = te.te_one_norm(h) if hasattr(te, "te_one_norm") else None
+    h.close()
+    V, a, b, k = g["V"], g["alpha"], g["beta"], g["m_eff"]
+    assert k == m
+    G = V.conj().T @ V
+    assert np.abs(G - np.eye(k)).max() <= 1e-12
+    n = c["n"]
+    rows = np.unique(np.concatenate([[0, n - 1], np.random.default_rng(seed).integers(0, n, nsample)]))
+    scale = nrm if nrm else max(1.0, np.abs(a).max() + 2 * np.abs(b).max())
+    for j in range(k - 1):
+        hv = K.spmv_rows(c["rowptr"], c["col"], c["val"], V[:, j], rows)
+        rhs = a[j] * V[rows, j] + b[j] * V[rows, j + 1]
+        if j > 0:
+            rhs = rhs + b[j - 1] * V[rows, j - 1]
+        assert np.abs(hv - rhs).max() <= 1e-12 * scale
+    return g
+
+
+def test_full_size_config3_bose_hubbard(gpu_lib):
+    """Config 3 at full size (n = 1,352,078): one forced restart against the oracle element by
+    element; the adaptive evolution meets its bound, keeps the norm, and the forward-backward
+    round trip (real H: exp(+iHt) w = conj(exp(-iHt) conj(w))) returns to v0 within the bounds."""
+    te = gpu_lib
+    c = configs.build(3)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    v, st = te.te_evolve(h, c["v0"], c["t"], c["tol"], c["m"])
+    assert st["err_bound"] <= c["tol"]
+    assert abs(np.linalg.norm(v) - 1) <= st["err_bound"] + 1e-9
+    w, st2 = te.te_evolve(h, np.conj(v), c["t"], c["tol"], c["m"])
+    assert np.linalg.norm(np.conj(w) - c["v0"]) <= st["err_bound"] + st2["err_bound"] + 1e-9
+    tau, m = 0.05, 10
+    v1, _ = te.te_evolve_schedule(h, c["v0"], [tau], c["tol"], m)
+    r1 = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], tau, c["tol"], m, schedule=[tau])
+    assert np.linalg.norm(v1 - r1["v"]) <= 1e-10
+    h.close()
+    _sampled_arnoldi_relation(te, c)
+
+
+def test_full_size_config4_random_banded(gpu_lib):
+    """Config 4 at full size (n = 2^24, 5.4e8 complex entries): sampled Arnoldi relation and
+    orthonormality; the adaptive evolution meets its bound and keeps the norm."""
+    te = gpu_lib
+    c = configs.build(4)
+    _sampled_arnoldi_relation(te, c)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    v, st = te.te_evolve(h, c["v0"], c["t"], c["tol"], c["m"])
+    assert st["err_bound"] <= c["tol"]
+    assert abs(np.linalg.norm(v) - 1) <= st["err_bound"] + 1e-9
+    h.close()
+
+
+def test_full_size_config5_xxz_nnn_L26(gpu_lib):
+    """Config 5 at full size (n = 2^26, 1.8e9 entries): sampled Arnoldi relation and
+    orthonormality; the adaptive evolution meets its bound, keeps the norm and the total S^z
+    (the Hamiltonian conserves it; the product state's S^z distribution must not change)."""
+    te = gpu_lib
+    c = configs.build(5)
+    _sampled_arnoldi_relation(te, c, m=3, nsample=200)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    del c["rowptr"], c["col"], c["val"]
+    v, st = te.te_evolve(h, c["v0"], c["t"], c["tol"], c["m"])
+    h.close()
+    assert st["err_bound"] <= c["tol"]
+    assert abs(np.linalg.norm(v) - 1) <= st["err_bound"] + 1e-9
+    L = 26
+    pop = np.zeros(c["n"], dtype=np.int8)
+    idx = np.arange(c["n"], dtype=np.int64)
+    for b in range(L):
+        pop += ((idx >> b) & 1).astype(np.int8)
+    w0 = np.bincount(pop, weights=np.abs(c["v0"]) ** 2, minlength=L + 1)
+    w1 = np.bincount(pop, weights=np.abs(v) ** 2, minlength=L + 1)
+    assert np.abs(w1 - w0).max() <= 2 * st["err_bound"] + 1e-9
+
+
 def test_distributed_api_single_rank(gpu_lib):
     """te_dist_init / te_create_csr_dist on one rank (global columns, halo plan, no NCCL
     traffic) gives the same evolution as the plain handle."""

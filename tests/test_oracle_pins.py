@@ -58,6 +58,17 @@ def test_spmv_identity_and_permutation():
     assert np.array_equal(K.spmv(rp, c, v, np.array([1, 0], complex)), np.array([0, 1], complex))
 
 
+def test_spmv_rows_is_a_row_restriction():
+    """Dense mat-vec rows (the definition) on a ragged random matrix, including empty rows."""
+    A = rand_herm(50, 0.15, 9)
+    A[7, :] = 0
+    A[:, 7] = 0
+    rp, c, v = csr_from_dense(A)
+    x = np.random.default_rng(3).standard_normal(50) + 1j * np.random.default_rng(4).standard_normal(50)
+    rows = np.array([0, 7, 13, 49, 13])
+    assert np.allclose(K.spmv_rows(rp, c, v, x, rows), (A @ x)[rows], rtol=0, atol=1e-13)
+
+
 def test_one_norm_hand_values():
     rp, c, v = csr_from_dense(np.array([[0, 1], [1, 0]], dtype=float))
     assert K.one_norm(rp, c, v, 2) == 1.0

@@ -99,3 +99,14 @@ def test_paper_s5_instance_config6():
     assert np.all(col[zpos] == zrows)                                  # every zero is a diagonal entry
     blk, cnt = np.unique(zrows // d2, return_counts=True)
     assert blk.tolist() == [88, 100] and cnt.tolist() == [252, 252]
+
+
+@pytest.mark.parametrize("diag,band", [(True, 0), (False, 16)])
+def test_parallel_involution_builder_bit_exact(diag, band):
+    """Chunked process-pool build == single-process build, byte for byte (ragged last chunk)."""
+    from workloads import parallel_build
+    n = 70000
+    a = models.involution_csr(n, 4, n_uniform=16, n_band=band, diagonal=diag)
+    b = parallel_build.involution_csr_parallel(n, 4, n_uniform=16, n_band=band, diagonal=diag, nproc=3, chunk=1 << 14)
+    for x, y in zip(a, b):
+        assert x.dtype == y.dtype and np.array_equal(x.view(np.uint8), y.view(np.uint8))

@@ -20,7 +20,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import fast, memory_burden, models
+from . import fast, memory_burden, models, parallel_build
 
 NAMES = {
     1: "random_herm_n4096",
@@ -61,13 +61,14 @@ def build(i: int, with_matrix: bool = True, **ov):
     if i == 1:
         n = p["n"]
         if with_matrix:
-            out["rowptr"], out["col"], out["val"] = models.involution_csr(n, seed, n_uniform=16, diagonal=True)
+            build_inv = parallel_build.involution_csr_parallel if n >= (1 << 20) else models.involution_csr
+            out["rowptr"], out["col"], out["val"] = build_inv(n, seed, n_uniform=16, diagonal=True)
         out["v0"] = models.complex_gaussian_state(n, seed)
     elif i == 4:
         n = p["n"]
         if with_matrix:
-            out["rowptr"], out["col"], out["val"] = models.involution_csr(n, seed, n_uniform=16, n_band=16,
-                                                                          diagonal=False)
+            build_inv = parallel_build.involution_csr_parallel if n >= (1 << 20) else models.involution_csr
+            out["rowptr"], out["col"], out["val"] = build_inv(n, seed, n_uniform=16, n_band=16, diagonal=False)
         out["v0"] = models.complex_gaussian_state(n, seed)
     elif i == 2:
         L = p["L"]
