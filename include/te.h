@@ -156,6 +156,10 @@ enum {
                                 4 (default) nnz-balanced tiles, rowptr/col/val of the next tile in
                                 flight by bulk copies (TMA engine) into a double buffer, TPR lanes
                                 per row with 12-16 register gathers in flight per lane;
+                                6 SELL-32-sigma: rows sorted by length in 4096-row windows, 32-row
+                                slices stored column-major, one lane per row, software-pipelined
+                                loads (a padded copy of H is built on the device when selected;
+                                TE_ERR_ARG if padding would exceed the entry count);
                                 5 async gather: 1024-entry tiles, 3-stage bulk-copy ring, x gathers
                                 as cp.async copies into shared memory overlapping the previous
                                 tile's products;

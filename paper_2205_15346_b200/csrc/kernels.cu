@@ -220,6 +220,7 @@ template <>
 struct ValT<false> {
   using T = double;
   static __device__ __forceinline__ double2 mul(double v, double2 x) { return make_double2(v * x.x, v * x.y); }
+  static __device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }
 };
 template <>
 struct ValT<true> {
@@ -227,6 +228,7 @@ struct ValT<true> {
   static __device__ __forceinline__ double2 mul(double2 v, double2 x) {
     return make_double2(v.x * x.x - v.y * x.y, v.x * x.y + v.y * x.x);
   }
+  static __device__ __forceinline__ double2 ldcs(const double2* p) { return __ldcs(p); }
 };
 
 constexpr size_t kK1Smem = sizeof(double2) * (kSpmvChunk + kSpmvRows) + sizeof(int64_t) * (kSpmvRows + 1);
@@ -1754,6 +1756,134 @@ __global__ void __launch_bounds__(kThreads, CPLX ? 2 : 3) k_spmv_ag(KDev d, int 
   cp_async_wait0();
 }
 
+// SpMV variant 6: SELL-C-sigma (C = 32).  Rows sorted by length (descending, stable) inside
+// windows of kSellSigma rows, cut into slices of 32; a slice stores its entries column-major
+// (entry k of lane l at sptr[s] + 32 k + l, zero-padded to the slice width with the lane's own
+// row as column), so a warp streams its slice with fully coalesced loads and no shared-memory
+// staging or block barriers.  One lane per row, entries in CSR order: each row's sum is the
+// sequential sum of its products.  Built on the device from the CSR (te_api: build_sell).
+template <bool CPLX>
+__global__ void k_sell_build(int64_t npos, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                             const void* __restrict__ val_, const int32_t* __restrict__ perm,
+                             const int64_t* __restrict__ sptr, const int32_t* __restrict__ slen,
+                             int32_t* __restrict__ scol, void* __restrict__ sval_) {
+  using VT = typename ValT<CPLX>::T;
+  const VT* val = static_cast<const VT*>(val_);
+  VT* sval = static_cast<VT*>(sval_);
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npos; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = p >> 5;
+    const int l = (int)(p & 31);
+    const int r = perm[p];
+    const int w = slen[s];
+    const int64_t base = sptr[s] + l;
+    int64_t a = 0, len = 0;
+    if (r >= 0) {
+      a = rowptr[r];
+      len = rowptr[r + 1] - a;
+    }
+    const int pc = r >= 0 ? r : 0;
+    for (int k = 0; k < w; ++k) {
+      const int64_t o = base + (int64_t)k * 32;
+      if (k < len) {
+        scol[o] = col[a + k];
+        sval[o] = val[a + k];
+      } else {
+        scol[o] = pc;
+        sval[o] = VT{};
+      }
+    }
+  }
+}
+
+template <bool CPLX>
+void launch_sell_build(int64_t npos, const int64_t* rowptr, const int32_t* col, const void* val, const int32_t* perm,
+                       const int64_t* sptr, const int32_t* slen, int32_t* scol, void* sval, cudaStream_t st) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(65535, (npos + kThreads - 1) / kThreads));
+  k_sell_build<CPLX><<<grid, kThreads, 0, st>>>(npos, rowptr, col, val, perm, sptr, slen, scol, sval);
+}
+void launch_sell_build(bool cplx, int64_t npos, const int64_t* rowptr, const int32_t* col, const void* val,
+                       const int32_t* perm, const int64_t* sptr, const int32_t* slen, int32_t* scol, void* sval,
+                       cudaStream_t st) {
+  if (cplx) launch_sell_build<true>(npos, rowptr, col, val, perm, sptr, slen, scol, sval, st);
+  else launch_sell_build<false>(npos, rowptr, col, val, perm, sptr, slen, scol, sval, st);
+}
+
+template <bool CPLX, bool HALO, int U>
+__global__ void __launch_bounds__(kThreads, 2) k_spmv_sell(KDev d, int j) {
+  using VT = typename ValT<CPLX>::T;
+  __shared__ double sj_s;
+  if (threadIdx.x == 0) sj_s = step_gate(d, j, blockIdx.x == 0);
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  asm volatile("" : "+l"(x));
+  const double2* __restrict__ halo = d.halo;
+  const int n = (int)d.n;
+  const int32_t* __restrict__ scol = d.scol;
+  const VT* __restrict__ sval = static_cast<const VT*>(d.sval);
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  auto gx = [&](int c) -> double2 {
+    if (HALO) return __ldg(((uint32_t)c < (uint32_t)n) ? x + c : halo + (c - n));
+    return __ldg(x + c);
+  };
+  // software pipeline over batches of U entries per lane: in iteration b the gathers of batch
+  // b+1 and the column/value loads of batch b+2 are issued before batch b's products, so both
+  // latencies stay hidden across the loop back-edge; entries past the slice width read column 0
+  // with value 0 (predicated, no padding to a multiple of U)
+  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < d.nslices; s += nw) {
+    const int64_t base = __ldg(d.sptr + s) + lane;
+    const int w = __ldg(d.slen + s);
+    const int r = __ldg(d.sperm + s * 32 + lane);
+    const int nb = (w + U - 1) / U;
+    auto ldcv = [&](int b, int (&c)[U], VT (&v)[U]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = b * U + u;
+        if (k < w) {
+          c[u] = __ldg(scol + base + (int64_t)k * 32);
+          v[u] = __ldg(sval + base + (int64_t)k * 32);
+        } else {
+          c[u] = 0;
+          v[u] = VT{};
+        }
+      }
+    };
+    int cB[U];
+    VT vA[U], vB[U];
+    double2 xA[U];
+    if (nb > 0) {
+      int cA[U];
+      ldcv(0, cA, vA);
+#pragma unroll
+      for (int u = 0; u < U; ++u) xA[u] = gx(cA[u]);
+    }
+    if (nb > 1) ldcv(1, cB, vB);
+    double2 acc = make_double2(0.0, 0.0);
+    for (int b = 0; b < nb; ++b) {
+      double2 xB[U];
+      int cC[U];
+      VT vC[U];
+      if (b + 1 < nb) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) xB[u] = gx(cB[u]);
+      }
+      if (b + 2 < nb) ldcv(b + 2, cC, vC);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = cadd(acc, ValT<CPLX>::mul(vA[u], xA[u]));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        xA[u] = xB[u];
+        vA[u] = vB[u];
+        cB[u] = cC[u];
+        vB[u] = vC[u];
+      }
+    }
+    if (r >= 0) __stcs(d.W + r, make_double2(acc.x * sj, acc.y * sj));
+  }
+}
+
 // Standalone SpMV p = s_j H V_j -> W (CSR-vector, TPR lanes per row, high occupancy).
 template <bool CPLX, int TPR>
 __global__ void __launch_bounds__(kThreads) k_spmv(KDev d, int j) {
@@ -2182,6 +2312,18 @@ static int tpr_for(int ncols, int min_tpr) {
   }
 
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
+  if (L.spmv_tiled == 6 && d.nslices > 0) {
+    const bool hal = d.halo || L.spmv_force_halo;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)8 * L.num_sms, (d.nslices + kWarps - 1) / kWarps));
+    if (cplx) {
+      if (hal) k_spmv_sell<true, true, 4><<<grid, kThreads, 0, L.stream>>>(d, j);
+      else k_spmv_sell<true, false, 4><<<grid, kThreads, 0, L.stream>>>(d, j);
+    } else {
+      if (hal) k_spmv_sell<false, true, 4><<<grid, kThreads, 0, L.stream>>>(d, j);
+      else k_spmv_sell<false, false, 4><<<grid, kThreads, 0, L.stream>>>(d, j);
+    }
+    return;
+  }
   if (L.spmv_tiled == 5 && d.ntiles_ag > 0) {
     const bool hal = d.halo || L.spmv_force_halo;
     // persistent grid = co-resident blocks (occupancy API, cached per instantiation)

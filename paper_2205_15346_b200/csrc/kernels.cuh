@@ -21,6 +21,7 @@ constexpr int kSpmvChunk = 4096;     // K1 products staged in shared memory per 
 constexpr int kSpmvTileNnz = 4096;   // entries per nnz-balanced SpMV tile (cap), real values
 constexpr int kSpmvTileNnzC = 2048;  // complex values (two pipelined blocks per SM)
 constexpr int kSpmvMaxTileRows = 256;   // rows per SpMV tile cap (one thread per row)
+constexpr int kSellSigma = 4096;       // SELL-32-sigma sorting window (rows)
 constexpr int kAgCap = 1024;            // entries per async-gather SpMV tile (variant 5)
 constexpr int kAgMaxRows = 128;         // rows per async-gather tile cap (<= kThreads / TPR)
 constexpr int kSpmvTmaNnzCap = 512;     // entries per TMA SpMV tile (== kSpmvTmaNnz)
@@ -36,6 +37,12 @@ struct KDev {
   const void* val;
   const int64_t* tile_row;  // [ntiles+1] first row of each nnz-balanced SpMV tile
   int64_t ntiles;
+  const int32_t* scol;       // SELL-32-sigma (variant 6): padded column-major slices
+  const void* sval;
+  const int64_t* sptr;       // [nslices+1] slice offsets (entries)
+  const int32_t* slen;       // [nslices] slice widths
+  const int32_t* sperm;      // [32*nslices] slice position -> row (-1: padding lane)
+  int64_t nslices;
   const int64_t* tile_ag;    // [4*ntiles_ag] {first row, end row, first entry, end entry} (variant 5)
   int64_t ntiles_ag;
   const int64_t* tile_desc;  // [2*(ntiles_desc+1)] {first row, first entry} of the TMA SpMV tiles
@@ -77,6 +84,9 @@ struct Launch {
 
 // hot path (one Krylov step j = 3 launches; see kernels.cu)
 void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L);   // K1 (variants 0/1; variant 2 = K1a+K1b)
+void launch_sell_build(bool cplx, int64_t npos, const int64_t* rowptr, const int32_t* col, const void* val,
+                       const int32_t* perm, const int64_t* sptr, const int32_t* slen, int32_t* scol, void* sval,
+                       cudaStream_t st);
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L);        // K1a: SpMV only
 void launch_proj_dots(const KDev& d, int j, const Launch& L);              // K1b: g1 = V^H p (TMA)
 void launch_update_proj(const KDev& d, int j, const Launch& L);            // K2

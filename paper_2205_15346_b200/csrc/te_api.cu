@@ -122,6 +122,13 @@ struct te_handle {
   int64_t ntiles = 0;
   int64_t* d_tile_desc = nullptr;
   int64_t* d_tile_ag = nullptr;
+  // SELL-32-sigma copy of H (SpMV variant 6), built on first selection
+  int32_t* d_scol = nullptr;
+  void* d_sval = nullptr;
+  int64_t* d_sptr = nullptr;
+  int32_t* d_slen = nullptr;
+  int32_t* d_sperm = nullptr;
+  int64_t nslices = 0;
   int64_t ntiles_ag = 0;
   int spmv_ag_tpr = 1;
   int64_t ntiles_desc = 0;
@@ -180,6 +187,12 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.ntiles = h->ntiles;
   d.tile_desc = h->d_tile_desc;
   d.tile_ag = h->d_tile_ag;
+  d.scol = h->d_scol;
+  d.sval = h->d_sval;
+  d.sptr = h->d_sptr;
+  d.slen = h->d_slen;
+  d.sperm = h->d_sperm;
+  d.nslices = h->nslices;
   d.ntiles_ag = h->ntiles_ag;
   d.ntiles_desc = h->ntiles_desc;
   d.alpha = h->d_small + kOffAlpha;
@@ -927,6 +940,11 @@ void te_destroy(te_handle* h) {
   cudaFree(h->d_tile_row);
   cudaFree(h->d_tile_desc);
   cudaFree(h->d_tile_ag);
+  cudaFree(h->d_scol);
+  cudaFree(h->d_sval);
+  cudaFree(h->d_sptr);
+  cudaFree(h->d_slen);
+  cudaFree(h->d_sperm);
   cudaFree(h->d_sendbuf);
   cudaFree(h->d_send_idx);
   if (h->h_small) cudaFreeHost(h->h_small);
@@ -1054,6 +1072,65 @@ int te_krylov_basis(te_handle* h, const te_c128* v1, int m, double tol_rate, dou
   return TE_OK;
 }
 
+// SELL-32-sigma copy of the (local) CSR for SpMV variant 6: rows sorted by length (descending,
+// stable) inside windows of kSellSigma rows, slices of 32 rows padded to the slice width and
+// stored column-major; built by a device scatter from the device CSR.  Refused (TE_ERR_ARG) when
+// padding would exceed the CSR's entry count (a few very long rows).
+static int build_sell(te_handle* h) {
+  if (h->nslices > 0 || h->n == 0) return TE_OK;
+  const int64_t n = h->n;
+  std::vector<int64_t> rp((size_t)n + 1);
+  if (cudaMemcpy(rp.data(), h->d_rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return set_err(TE_ERR_CUDA, "SELL: rowptr copy");
+  const int64_t nsl = (n + 31) / 32;
+  std::vector<int32_t> perm((size_t)nsl * 32, -1);
+  std::vector<int32_t> idx;
+  for (int64_t w0 = 0; w0 < n; w0 += te::kSellSigma) {
+    const int64_t w1 = std::min<int64_t>(n, w0 + te::kSellSigma);
+    idx.resize((size_t)(w1 - w0));
+    for (int64_t r = w0; r < w1; ++r) idx[(size_t)(r - w0)] = (int32_t)r;
+    std::stable_sort(idx.begin(), idx.end(),
+                     [&](int32_t x, int32_t y) { return rp[x + 1] - rp[x] > rp[y + 1] - rp[y]; });
+    std::copy(idx.begin(), idx.end(), perm.begin() + w0);
+  }
+  std::vector<int64_t> sptr((size_t)nsl + 1, 0);
+  std::vector<int32_t> slen((size_t)nsl, 0);
+  for (int64_t s = 0; s < nsl; ++s) {
+    int64_t w = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int32_t r = perm[(size_t)(s * 32 + l)];
+      if (r >= 0) w = std::max<int64_t>(w, rp[r + 1] - rp[r]);
+    }
+    if (w > INT32_MAX) return set_err(TE_ERR_ARG, "SELL: row too long");
+    slen[(size_t)s] = (int32_t)w;
+    sptr[(size_t)s + 1] = sptr[(size_t)s] + 32 * w;
+  }
+  const int64_t total = sptr[(size_t)nsl];
+  if (total > 2 * h->nnz + 32 * 64)
+    return set_err(TE_ERR_ARG, "SELL: padding %lld entries for %lld nonzeros (rows too uneven)", (long long)total,
+                   (long long)h->nnz);
+  const size_t vb = h->cplx ? 16 : 8;
+  auto fail = [&](const char* what) {
+    cudaFree(h->d_scol); cudaFree(h->d_sval); cudaFree(h->d_sptr); cudaFree(h->d_slen); cudaFree(h->d_sperm);
+    h->d_scol = nullptr; h->d_sval = nullptr; h->d_sptr = nullptr; h->d_slen = nullptr; h->d_sperm = nullptr;
+    return set_err(TE_ERR_OOM, "SELL: %s", what);
+  };
+  if (cudaMalloc(&h->d_scol, sizeof(int32_t) * std::max<int64_t>(1, total)) != cudaSuccess) return fail("col");
+  if (cudaMalloc(&h->d_sval, vb * std::max<int64_t>(1, total)) != cudaSuccess) return fail("val");
+  if (cudaMalloc(&h->d_sptr, sizeof(int64_t) * (nsl + 1)) != cudaSuccess) return fail("ptr");
+  if (cudaMalloc(&h->d_slen, sizeof(int32_t) * nsl) != cudaSuccess) return fail("len");
+  if (cudaMalloc(&h->d_sperm, sizeof(int32_t) * nsl * 32) != cudaSuccess) return fail("perm");
+  cudaMemcpyAsync(h->d_sptr, sptr.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice, h->stream);
+  cudaMemcpyAsync(h->d_slen, slen.data(), sizeof(int32_t) * nsl, cudaMemcpyHostToDevice, h->stream);
+  cudaMemcpyAsync(h->d_sperm, perm.data(), sizeof(int32_t) * nsl * 32, cudaMemcpyHostToDevice, h->stream);
+  te::launch_sell_build(h->cplx, nsl * 32, h->d_rowptr, h->d_col, h->d_val, h->d_sperm, h->d_sptr, h->d_slen,
+                        h->d_scol, h->d_sval, h->stream);
+  const cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return fail(cudaGetErrorString(e));
+  h->nslices = nsl;
+  return TE_OK;
+}
+
 int te_set_option(te_handle* h, int option, double value) {
   clear_err();
   if (!h) return set_err(TE_ERR_ARG, "null handle");
@@ -1081,8 +1158,12 @@ int te_set_option(te_handle* h, int option, double value) {
       h->integrator = (int)value;
       return TE_OK;
     case TE_OPT_SPMV:
-      if (value < 0.0 || value > 5.0 || value != (double)(int)value)
-        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 0..5");
+      if (value < 0.0 || value > 6.0 || value != (double)(int)value)
+        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 0..6");
+      if (value == 6.0) {
+        const int rc = build_sell(h);
+        if (rc != TE_OK) return rc;
+      }
       h->spmv_tiled = (int)value;
       return TE_OK;
     case TE_OPT_PREFETCH:

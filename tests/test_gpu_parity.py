@@ -35,8 +35,8 @@ def small_cases():
 CASES = small_cases()
 
 
-KERNEL_SETS = [(2, 4), (2, 5), (2, 3), (2, 1), (2, 2), (2, 0), (3, 4), (4, 4), (0, 4), (1, 4)]
-KERNEL_IDS = ["hybrid-spmvpipe", "hybrid-spmvag", "hybrid-spmvrow", "hybrid-spmvtile", "hybrid-spmvtma", "hybrid-spmvvec",
+KERNEL_SETS = [(2, 4), (2, 5), (2, 6), (2, 3), (2, 1), (2, 2), (2, 0), (3, 4), (4, 4), (0, 4), (1, 4)]
+KERNEL_IDS = ["hybrid-spmvpipe", "hybrid-spmvag", "hybrid-spmvsell", "hybrid-spmvrow", "hybrid-spmvtile", "hybrid-spmvtma", "hybrid-spmvvec",
               "tma", "shuffle", "fused-register", "staged"]
 
 
@@ -131,6 +131,36 @@ def test_spmv_async_gather_variants(gpu_lib, name, c, tpr, halo, monkeypatch):
     assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-12 * scale
     assert np.abs(g["beta"] - o["beta"]).max() <= 1e-12 * scale
     assert np.linalg.norm(g["V"] - o["V"]) <= 1e-10
+    h.close()
+
+
+@pytest.mark.parametrize("halo", [0, 1])
+@pytest.mark.parametrize("name,c", PIPE_CASES, ids=[x[0] for x in PIPE_CASES])
+def test_spmv_sell_halo_variants(gpu_lib, name, c, halo, monkeypatch):
+    """SELL-32-sigma SpMV (TE_OPT_SPMV = 6), plain and halo-aware instantiation, vs the oracle."""
+    te = gpu_lib
+    monkeypatch.setenv("TE_SPMV_FORCE_HALO", str(halo))
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    te.te_set_option(h, te.TE_OPT_SPMV, 6)
+    g = te.te_krylov_basis(h, c["v0"], 12, c["tol"] / c["t"], want_V=True)
+    o = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), c["v0"], 12, c["tol"] / c["t"])
+    scale = max(1.0, np.abs(o["alpha"]).max(), np.abs(o["beta"]).max())
+    assert g["m_eff"] == o["m_eff"]
+    assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-12 * scale
+    assert np.linalg.norm(g["V"] - o["V"]) <= 1e-10
+    h.close()
+
+
+def test_spmv_sell_refuses_uneven_rows(gpu_lib):
+    """A few rows much longer than the rest would make the padded SELL copy several times the
+    CSR: selecting it fails with TE_ERR_ARG and the handle keeps working on its previous SpMV."""
+    te = gpu_lib
+    c = _long_row_case()
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    with pytest.raises(te.TEError):
+        te.te_set_option(h, te.TE_OPT_SPMV, 6)
+    v, st = te.te_evolve(h, c["v0"], 0.5, 1e-8, 12)
+    assert st["err_bound"] <= 1e-8
     h.close()
 
 
