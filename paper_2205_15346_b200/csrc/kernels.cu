@@ -918,7 +918,14 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
               a6 = cfma(v6, coef[k + 6], a6);
               a7 = cfma(v7, coef[k + 7], a7);
             }
-            for (; k < ncols; ++k) a0 = cfma(Vs[k * TR + row], coef[k], a0);
+            // remainder (< 8 columns) on independent chains as well
+            if (k + 0 < ncols) a0 = cfma(Vs[(k + 0) * TR + row], coef[k + 0], a0);
+            if (k + 1 < ncols) a1 = cfma(Vs[(k + 1) * TR + row], coef[k + 1], a1);
+            if (k + 2 < ncols) a2 = cfma(Vs[(k + 2) * TR + row], coef[k + 2], a2);
+            if (k + 3 < ncols) a3 = cfma(Vs[(k + 3) * TR + row], coef[k + 3], a3);
+            if (k + 4 < ncols) a4 = cfma(Vs[(k + 4) * TR + row], coef[k + 4], a4);
+            if (k + 5 < ncols) a5 = cfma(Vs[(k + 5) * TR + row], coef[k + 5], a5);
+            if (k + 6 < ncols) a6 = cfma(Vs[(k + 6) * TR + row], coef[k + 6], a6);
             const double2 a = cadd(cadd(cadd(a0, a1), cadd(a2, a3)), cadd(cadd(a4, a5), cadd(a6, a7)));
             p = make_double2(p.x - a.x, p.y - a.y);
             if (row >= rows) p = make_double2(0.0, 0.0);

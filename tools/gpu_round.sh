@@ -1,11 +1,7 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/b_plain.log 2>&1 || exit 1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu1.log 2>&1
-timeout 300 python tools/profile_run.py --t 2.5 > gpurun_out/pr2.log 2>&1 || exit 1
-timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:"k_proj|k_spmv|k_update_norm|k_combine" --csv --log-file gpurun_out/restart_metrics.csv python tools/profile_run.py --t 2.5 > gpurun_out/ncu2.log 2>&1
-timeout 300 python tools/profile_run.py --config 6 --t 0.3 > gpurun_out/pr6.log 2>&1 || exit 1
-timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:"k_proj|k_spmv|k_update_norm|k_combine" --csv --log-file gpurun_out/restart_metrics_c6.csv python tools/profile_run.py --config 6 --t 0.3 > gpurun_out/ncu3.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_proj_tma" -s 60 -c 2 -o gpurun_out/full_c2 python tools/profile_run.py --t 2.5 > gpurun_out/ncu4.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_spmv_pipe" -s 20 -c 1 -o gpurun_out/full_c6_spmv python tools/profile_run.py --config 6 --t 0.3 > gpurun_out/ncu5.log 2>&1
-echo done >> gpurun_out/ncu5.log
+B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline"
+timeout 600 $B --config 2 > gpurun_out/sw_rem_c2a.log 2>&1
+timeout 600 $B --config 3 > gpurun_out/sw_rem_c3.log 2>&1
+timeout 600 $B --config 2 > gpurun_out/sw_rem_c2b.log 2>&1
+timeout 600 $B --config 2 --ortho 2 > gpurun_out/sw_rem_c2f2.log 2>&1
