@@ -207,7 +207,11 @@ void te_dist_destroy(te_dist* d);
  * GLOBAL column indices (int64).  All ranks call collectively with contiguous, ordered,
  * non-overlapping row blocks covering [0, n_global).  val is complex (te_c128) if
  * val_is_complex else double.  Builds the halo plan (te_halo_plan) and exchanges the
- * per-peer need lists once.  v0/v_out of evolve calls are the local row slices. */
+ * per-peer need lists once.  v0/v_out of evolve calls are the local row slices.
+ * Each rank's global columns must lie in [0, n_global) and increase strictly within a row
+ * (checked on the host); the local columns keep that entry order (so each row's sum has the
+ * single-GPU order).  Errors are agreed collectively: if any rank's input is invalid or its
+ * local create fails, every rank returns NULL (TE_ERR_CSR / TE_ERR_ARG) instead of blocking. */
 te_handle* te_create_csr_dist(te_dist* d, int64_t n_global, int64_t row_begin, int64_t row_end,
                               const int64_t* rowptr_local, const int64_t* col_global,
                               const void* val, int val_is_complex);

@@ -102,25 +102,48 @@ extern "C" te_handle* te_create_csr_dist(te_dist* d, int64_t n_global, int64_t r
   int64_t* dbuf = nullptr;
   cudaStream_t st = nullptr;
   ncclComm_t comm = te_internal_comm(d);
+  // 0. local structure check of the caller's global CSR (rowptr non-decreasing from 0, columns in
+  //    [0, n_global) and strictly increasing per row); the verdict travels with the row partition
+  //    so that every rank fails together instead of leaving peers inside a collective
+  int64_t local_bad = (rowptr_local[0] != 0) ? 1 : 0;
+  for (int64_t r = 0; r < n_loc && !local_bad; ++r) {
+    if (rowptr_local[r + 1] < rowptr_local[r]) { local_bad = 1; break; }
+    int64_t prev = -1;
+    for (int64_t q = rowptr_local[r]; q < rowptr_local[r + 1]; ++q) {
+      const int64_t c = col_global[q];
+      if (c < 0 || c >= n_global || c <= prev) { local_bad = 1; break; }
+      prev = c;
+    }
+  }
+  if (P == 1 && local_bad) {
+    te_internal_set_error(TE_ERR_CSR, "te_create_csr_dist: columns out of range or not strictly increasing");
+    return nullptr;
+  }
   DCK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   if (P > 1) {
-    // 1. row partition
-    DCK(cudaMalloc(&dbuf, sizeof(int64_t) * (2 * P + 2 * P * P + 8)));
+    // 1. row partition (+ every rank's structure verdict)
+    DCK(cudaMalloc(&dbuf, sizeof(int64_t) * (16 + 4 * P + P * P)));
     {
-      int64_t mine[2] = {row_begin, row_end};
-      std::vector<int64_t> all(2 * P);
+      int64_t mine[3] = {row_begin, row_end, local_bad};
+      std::vector<int64_t> all(3 * P);
       DCK(cudaMemcpy(dbuf, mine, sizeof mine, cudaMemcpyHostToDevice));
-      DNK(te::nccl().AllGather(dbuf, dbuf + 2, 2, ncclInt64, comm, st));
+      DNK(te::nccl().AllGather(dbuf, dbuf + 3, 3, ncclInt64, comm, st));
       DCK(cudaStreamSynchronize(st));
-      DCK(cudaMemcpy(all.data(), dbuf + 2, sizeof(int64_t) * 2 * P, cudaMemcpyDeviceToHost));
+      DCK(cudaMemcpy(all.data(), dbuf + 3, sizeof(int64_t) * 3 * P, cudaMemcpyDeviceToHost));
+      for (int q = 0; q < P; ++q)
+        if (all[3 * q + 2]) {
+          te_internal_set_error(TE_ERR_CSR, q == me ? "te_create_csr_dist: columns out of range or not strictly increasing"
+                                                    : "te_create_csr_dist: invalid CSR on another rank");
+          goto fail;
+        }
       for (int q = 0; q < P; ++q) {
-        if (all[2 * q] != (q == 0 ? 0 : all[2 * q - 1])) {
+        if (all[3 * q] != (q == 0 ? 0 : all[3 * q - 2])) {
           te_internal_set_error(TE_ERR_ARG, "row blocks must be contiguous and ordered by rank");
           goto fail;
         }
-        row_starts[q] = all[2 * q];
+        row_starts[q] = all[3 * q];
       }
-      row_starts[P] = all[2 * P - 1];
+      row_starts[P] = all[3 * (P - 1) + 1];
       if (row_starts[P] != n_global) {
         te_internal_set_error(TE_ERR_ARG, "row blocks do not cover [0, n_global)");
         goto fail;
@@ -184,18 +207,24 @@ extern "C" te_handle* te_create_csr_dist(te_dist* d, int64_t n_global, int64_t r
   // 5. local handle with local column indices (Hermiticity needs the global matrix: not checked)
   h = te_internal_create_local(n_loc, n_global, row_begin, rowptr_local, col_local.data(), val, val_is_complex != 0,
                                d, n_loc + n_halo);
-  if (!h) goto fail;
+  if (!h && P == 1) goto fail;
   {
-    // 6. ||H||_1 = max over all rows of the row abs sums (allreduce max)
-    double nrm = te_internal_local_norm1(h);
+    // 6. ||H||_1 = max over all rows of the row abs sums (allreduce max), together with a
+    //    "local create failed" flag so that a failure on one rank fails every rank
+    double nv[2] = {h ? te_internal_local_norm1(h) : 0.0, h ? 0.0 : 1.0};
     if (P > 1) {
       double* dn = reinterpret_cast<double*>(dbuf);
-      DCK(cudaMemcpy(dn, &nrm, sizeof nrm, cudaMemcpyHostToDevice));
-      DNK(te::nccl().AllReduce(dn, dn, 1, ncclDouble, ncclMax, comm, st));
+      DCK(cudaMemcpy(dn, nv, sizeof nv, cudaMemcpyHostToDevice));
+      DNK(te::nccl().AllReduce(dn, dn, 2, ncclDouble, ncclMax, comm, st));
       DCK(cudaStreamSynchronize(st));
-      DCK(cudaMemcpy(&nrm, dn, sizeof nrm, cudaMemcpyDeviceToHost));
+      DCK(cudaMemcpy(nv, dn, sizeof nv, cudaMemcpyDeviceToHost));
     }
-    if (te_internal_setup_halo(h, n_halo, recv_counts, send_counts, send_idx, nrm) != TE_OK) goto fail;
+    if (!h) goto fail;  // own error already set by te_internal_create_local
+    if (nv[1] != 0.0) {
+      te_internal_set_error(TE_ERR_CSR, "te_create_csr_dist: local handle creation failed on another rank");
+      goto fail;
+    }
+    if (te_internal_setup_halo(h, n_halo, recv_counts, send_counts, send_idx, nv[0]) != TE_OK) goto fail;
   }
   cudaFree(dbuf);
   cudaStreamDestroy(st);

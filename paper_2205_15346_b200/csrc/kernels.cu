@@ -2179,7 +2179,10 @@ __global__ void k_csr_check(int64_t n, int64_t ncl, const int64_t* __restrict__ 
     int e = 0;
     for (int64_t q = lo; q < hi; ++q) {
       const int64_t c = col[q];
-      if (c < 0 || c >= ncl || c <= prev) { e |= 1; prev = c; continue; }
+      // strictly increasing columns are required of single-rank handles (the Hermiticity search
+      // needs them); a distributed handle's local columns keep the caller's global order, which
+      // the halo remap does not preserve (validated on the host before the remap, dist.cpp)
+      if (c < 0 || c >= ncl || (herm && c <= prev)) { e |= 1; prev = c; continue; }
       prev = c;
       double2 v;
       if constexpr (CPLX) v = val[q]; else v = make_double2(val[q], 0.0);

@@ -2,6 +2,7 @@
 // so that single-GPU use of the library needs no NCCL at all.
 #pragma once
 #include <dlfcn.h>
+#include <stdlib.h>
 #include <nccl.h>
 
 #include <string>
@@ -26,7 +27,11 @@ struct NcclApi {
 inline NcclApi& nccl() {
   static NcclApi api = [] {
     NcclApi a;
+    // TE_NCCL_LIB: an alternative NCCL-compatible library (tests: tests/support/fake_nccl.cu runs
+    // several ranks as threads on one GPU)
+    const char* over = getenv("TE_NCCL_LIB");
     const char* cands[] = {
+        over && *over ? over : "libnccl.so.2",
         "libnccl.so.2",
         "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2",
         "libnccl.so",
