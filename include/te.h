@@ -152,6 +152,11 @@ enum {
   TE_OPT_INTEGRATOR = 7,     /* error integral: 0 (default) adaptive tanh-sinh;
                                 1 non-adaptive Gauss-Legendre of order 30 ("simpler and faster",
                                 for explorative runs)                                                 */
+  TE_OPT_HALO = 8,           /* distributed handles: 0 (default) halo staged by an NCCL send/recv
+                                exchange before each SpMV; 1 the SpMV reads halo columns straight
+                                from the owning rank's V column (peer memory: CUDA IPC over NVLink,
+                                or the same address space) — SURVEY f4, the exchange fused into
+                                the SpMV.  Used with the default SpMV (TE_OPT_SPMV 4).       */
   TE_OPT_SPMV = 5            /* SpMV kernel of kernel sets 2-4 (same arithmetic, measured choice):
                                 4 (default) nnz-balanced tiles, rowptr/col/val of the next tile in
                                 flight by bulk copies (TMA engine) into a double buffer, TPR lanes

@@ -16,7 +16,8 @@ te_handle* te_internal_create_local(int64_t n_loc, int64_t n_global, int64_t row
                                     int64_t ncol_limit);
 int te_internal_setup_halo(te_handle* h, int64_t n_halo, const std::vector<int64_t>& recv_counts,
                            const std::vector<int64_t>& send_counts, const std::vector<int32_t>& send_idx,
-                           double norm1_global);
+                           double norm1_global, const std::vector<int64_t>& halo_global,
+                           const std::vector<int64_t>& row_starts);
 int te_internal_set_error(int code, const char* msg);
 cudaStream_t te_internal_stream(te_handle* h);
 double te_internal_local_norm1(te_handle* h);
@@ -224,7 +225,8 @@ extern "C" te_handle* te_create_csr_dist(te_dist* d, int64_t n_global, int64_t r
       te_internal_set_error(TE_ERR_CSR, "te_create_csr_dist: local handle creation failed on another rank");
       goto fail;
     }
-    if (te_internal_setup_halo(h, n_halo, recv_counts, send_counts, send_idx, nv[0]) != TE_OK) goto fail;
+    if (te_internal_setup_halo(h, n_halo, recv_counts, send_counts, send_idx, nv[0], halo, row_starts) != TE_OK)
+      goto fail;
   }
   cudaFree(dbuf);
   cudaStreamDestroy(st);

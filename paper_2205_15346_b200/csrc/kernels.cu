@@ -1455,7 +1455,17 @@ size_t spmv_pipe_smem() {
   return 2 * ((size_t)(kSpmvMaxTileRows + 4) * 8 + (size_t)(cap + 4) * 4 + (size_t)(cap + 4) * sizeof(VT));
 }
 
-template <bool CPLX, int TPR, bool HALO, int NF>
+// halo entry hi of step j from the owning rank's V column (uncached: written by another GPU)
+__device__ __forceinline__ double2 peer_x(const KDev& d, int j, int hi) {
+  const int q = __ldg(d.halo_owner + hi);
+  const double2* base = d.peer_base[q];
+  return __ldcv(base + (int64_t)j * __ldg(d.peer_ldv + q) + __ldg(d.halo_lidx + hi));
+}
+
+// HM: 0 single rank (every column local), 1 multi-rank with the halo staged by the NCCL exchange,
+// 2 multi-rank reading halo columns straight from the owning rank's V column (peer memory over
+// NVLink; the exchange fused into the SpMV)
+template <bool CPLX, int TPR, int HM, int NF>
 __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j, int pf) {
   using VT = typename ValT<CPLX>::T;
   extern __shared__ __align__(16) unsigned char smp[];
@@ -1552,7 +1562,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j, int pf
             const int e = q0 + w * TPR;
             if (e < hi) {
               const int c = cc[e];
-              if (HALO) xx[w] = ((uint32_t)c < (uint32_t)n) ? __ldg(x + c) : __ldg(halo + (c - (int)n));
+              if (HM == 1) xx[w] = ((uint32_t)c < (uint32_t)n) ? __ldg(x + c) : __ldg(halo + (c - (int)n));
+              else if (HM == 2) xx[w] = ((uint32_t)c < (uint32_t)n) ? __ldg(x + c) : peer_x(d, j, c - (int)n);
               else xx[w] = __ldg(x + c);   // single rank: every column is local
             }
           }
@@ -1576,7 +1587,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j, int pf
       double2 acc = make_double2(0.0, 0.0);
       for (int64_t q = cur.b + tid; q < cur.e; q += kThreads) {
         const int c = __ldg(col + q);
-        acc = cadd(acc, ValT<CPLX>::mul(__ldg(val + q), (c < n) ? __ldg(x + c) : __ldg(halo + (c - n))));
+        const double2 xv = (c < n) ? __ldg(x + c) : (HM == 2 ? peer_x(d, j, (int)(c - n)) : __ldg(halo + (c - n)));
+        acc = cadd(acc, ValT<CPLX>::mul(__ldg(val + q), xv));
       }
       acc = warp_sum(acc);
       if ((tid & 31) == 0) red[tid >> 5] = acc;
@@ -2290,15 +2302,19 @@ cudaError_t configure_kernels() {
   set((const void*)k_spmv_ag<true, T, true>, spmv_ag_smem<true>());
   TE_SETAG(1) TE_SETAG(2) TE_SETAG(4) TE_SETAG(8) TE_SETAG(16) TE_SETAG(32)
 #undef TE_SETAG
-#define TE_SETP(T)                                                  \
-  set((const void*)k_spmv_pipe<false, T, false, 12>, spmv_pipe_smem<false>()); \
-  set((const void*)k_spmv_pipe<true, T, false, 8>, spmv_pipe_smem<true>());    \
-  set((const void*)k_spmv_pipe<false, T, true, 12>, spmv_pipe_smem<false>());  \
-  set((const void*)k_spmv_pipe<true, T, true, 8>, spmv_pipe_smem<true>());     \
-  set((const void*)k_spmv_pipe<false, T, false, 16>, spmv_pipe_smem<false>()); \
-  set((const void*)k_spmv_pipe<true, T, false, 12>, spmv_pipe_smem<true>());   \
-  set((const void*)k_spmv_pipe<false, T, true, 16>, spmv_pipe_smem<false>());  \
-  set((const void*)k_spmv_pipe<true, T, true, 12>, spmv_pipe_smem<true>());
+#define TE_SETP(T)                                                                   \
+  set((const void*)k_spmv_pipe<false, T, 0, 12>, spmv_pipe_smem<false>());           \
+  set((const void*)k_spmv_pipe<true, T, 0, 8>, spmv_pipe_smem<true>());              \
+  set((const void*)k_spmv_pipe<false, T, 1, 12>, spmv_pipe_smem<false>());           \
+  set((const void*)k_spmv_pipe<true, T, 1, 8>, spmv_pipe_smem<true>());              \
+  set((const void*)k_spmv_pipe<false, T, 2, 12>, spmv_pipe_smem<false>());           \
+  set((const void*)k_spmv_pipe<true, T, 2, 8>, spmv_pipe_smem<true>());              \
+  set((const void*)k_spmv_pipe<false, T, 0, 16>, spmv_pipe_smem<false>());           \
+  set((const void*)k_spmv_pipe<true, T, 0, 12>, spmv_pipe_smem<true>());             \
+  set((const void*)k_spmv_pipe<false, T, 1, 16>, spmv_pipe_smem<false>());           \
+  set((const void*)k_spmv_pipe<true, T, 1, 12>, spmv_pipe_smem<true>());             \
+  set((const void*)k_spmv_pipe<false, T, 2, 16>, spmv_pipe_smem<false>());           \
+  set((const void*)k_spmv_pipe<true, T, 2, 12>, spmv_pipe_smem<true>());
   TE_SETP(1) TE_SETP(2) TE_SETP(4) TE_SETP(8)
 #undef TE_SETP
   set((const void*)k_spmv_tma<true>, kProjSmemBudget + 1024);
@@ -2377,10 +2393,12 @@ void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
   else k_spmv_pipe<false, T, H, NR><<<grid, kThreads, spmv_pipe_smem<false>(), L.stream>>>(d, j, L.spmv_pf);
 #define TE_PIPE(T)                                                                                  \
   case T:                                                                                           \
-    if (d.halo || L.spmv_force_halo) {                                                              \
-      if (L.spmv_nf_wide) { TE_PIPE_NF(T, true, 16, 12) } else { TE_PIPE_NF(T, true, 12, 8) }      \
+    if (L.halo_peer) {                                                                              \
+      if (L.spmv_nf_wide) { TE_PIPE_NF(T, 2, 16, 12) } else { TE_PIPE_NF(T, 2, 12, 8) }            \
+    } else if (d.halo || L.spmv_force_halo) {                                                       \
+      if (L.spmv_nf_wide) { TE_PIPE_NF(T, 1, 16, 12) } else { TE_PIPE_NF(T, 1, 12, 8) }            \
     } else {                                                                                        \
-      if (L.spmv_nf_wide) { TE_PIPE_NF(T, false, 16, 12) } else { TE_PIPE_NF(T, false, 12, 8) }    \
+      if (L.spmv_nf_wide) { TE_PIPE_NF(T, 0, 16, 12) } else { TE_PIPE_NF(T, 0, 12, 8) }            \
     }                                                                                               \
     break;
       TE_PIPE(1) TE_PIPE(2) TE_PIPE(4)

@@ -37,6 +37,10 @@ struct KDev {
   const void* val;
   const int64_t* tile_row;  // [ntiles+1] first row of each nnz-balanced SpMV tile
   int64_t ntiles;
+  const double2* const* peer_base;  // [nranks] V base of every rank in this address space (halo mode 1)
+  const int64_t* peer_ldv;          // [nranks] their column strides
+  const int32_t* halo_owner;        // [n_halo] owning rank of each halo entry
+  const int32_t* halo_lidx;         // [n_halo] row index of the entry at its owner
   const int32_t* scol;       // SELL-32-sigma (variant 6): padded column-major slices
   const void* sval;
   const int64_t* sptr;       // [nslices+1] slice offsets (entries)
@@ -74,6 +78,7 @@ struct Launch {
   int spmv_pf;        // pipelined SpMV: L2 prefetch of tile t+2G (0 off, 1 on)
   int spmv_force_halo;  // test hook: run the multi-rank (halo-aware) SpMV instantiation on one rank
   int spmv_nf_wide;
+  int halo_peer;      // SpMV reads halo columns from peer memory (no staged exchange)
   int spmv_ag_tpr;    // lanes per row of the async-gather SpMV (1..32)   // pipelined SpMV gathers in flight per lane: 0 -> 12 real / 8 complex, 1 -> 16 / 12
   int proj_tma;   // 2: hybrid by column count (default), 1: TMA-tiled only, 0: register/shuffle only
   int spmv_tiled; // 2: TMA-fed SpMV (default), 1: nnz-balanced tiled SpMV, 0: CSR-vector

@@ -5,6 +5,8 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstring>
+#include <unistd.h>
 #include <cmath>
 #include <complex>
 #include <cstdarg>
@@ -163,6 +165,14 @@ struct te_handle {
   double2* d_halo = nullptr;
   double2* d_sendbuf = nullptr;
   int32_t* d_send_idx = nullptr;
+  // halo mode 1 (TE_OPT_HALO): halo columns read from peer memory inside the SpMV
+  int halo_mode = 0;
+  int32_t* d_halo_owner = nullptr;
+  int32_t* d_halo_lidx = nullptr;
+  const double2** d_peer_base = nullptr;
+  int64_t* d_peer_ldv = nullptr;
+  std::vector<void*> ipc_open;          // peer V mappings opened through CUDA IPC (closed on reset)
+  const double2* peer_for_V = nullptr;  // the V allocation the peer table describes
   std::vector<int64_t> send_counts, recv_counts;
   int64_t n_send = 0;
 };
@@ -183,6 +193,10 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.col = h->d_col;
   d.val = h->d_val;
   d.halo = h->d_halo;
+  d.peer_base = h->d_peer_base;
+  d.peer_ldv = h->d_peer_ldv;
+  d.halo_owner = h->d_halo_owner;
+  d.halo_lidx = h->d_halo_lidx;
   d.tile_row = h->d_tile_row;
   d.ntiles = h->ntiles;
   d.tile_desc = h->d_tile_desc;
@@ -212,6 +226,13 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   return d;
 }
 
+// halo mode 1 is used by the pipelined SpMV of the projection-kernel sets (and f1/f2); the other
+// SpMV variants keep the staged exchange
+bool peer_active(const te_handle* h) {
+  return h->dist && h->dist->nranks > 1 && h->halo_mode == 1 && h->spmv_tiled == 4 &&
+         (h->variant >= 2 || h->ortho != 0);
+}
+
 Launch make_launch(te_handle* h) {
   Launch L;
   L.stream = h->stream;
@@ -228,6 +249,7 @@ Launch make_launch(te_handle* h) {
   L.spmv_pf = h->spmv_pf;
   L.spmv_nf_wide = h->spmv_nf_wide;
   L.spmv_force_halo = h->spmv_force_halo;
+  L.halo_peer = peer_active(h) ? 1 : 0;
   L.spmv_ag_tpr = h->spmv_ag_tpr;
   L.spmv_tiled = h->spmv_tiled;
   L.prefetch = h->prefetch;
@@ -359,7 +381,7 @@ int allreduce_sum(te_handle* h, double* buf, size_t count) {
 }
 
 int halo_exchange(te_handle* h, int j) {
-  if (!h->dist || h->dist->nranks == 1) return TE_OK;
+  if (!h->dist || h->dist->nranks == 1 || peer_active(h)) return TE_OK;
   const double2* x = h->d_V + (int64_t)j * h->ldv;
   if (h->n_send > 0) {
     prof_begin(h);
@@ -382,6 +404,67 @@ int halo_exchange(te_handle* h, int j) {
   return TE_OK;
 }
 
+// Halo mode 1: every rank learns every rank's V base and column stride (collective, once per V
+// allocation).  A peer in the same address space (several ranks as threads of one process) is
+// addressed directly; another process's V is mapped through CUDA IPC (NVLink peer access).
+int setup_peers(te_handle* h) {
+  struct Rec {
+    cudaIpcMemHandle_t hdl;
+    uint64_t ptr;
+    int64_t ldv;
+    int64_t pid;
+  };
+  const int P = h->dist->nranks, me = h->dist->rank;
+  Rec mine{};
+  if (cudaIpcGetMemHandle(&mine.hdl, h->d_V) != cudaSuccess) {
+    cudaGetLastError();  // not exportable: peers in this process still work through the pointer
+    std::memset(&mine.hdl, 0, sizeof(mine.hdl));
+  }
+  mine.ptr = reinterpret_cast<uint64_t>(h->d_V);
+  mine.ldv = h->ldv;
+  mine.pid = (int64_t)getpid();
+  std::vector<Rec> all(P);
+  char* dbuf = nullptr;
+  CK(cudaMalloc(&dbuf, sizeof(Rec) * (P + 1)));
+  CK(cudaMemcpyAsync(dbuf, &mine, sizeof(Rec), cudaMemcpyHostToDevice, h->stream));
+  {
+    const ncclResult_t r = te::nccl().AllGather(dbuf, dbuf + sizeof(Rec), sizeof(Rec), ncclChar, h->dist->comm, h->stream);
+    if (r != ncclSuccess) {
+      cudaFree(dbuf);
+      return set_err(TE_ERR_NCCL, "peer table allgather: %s", te::nccl().GetErrorString(r));
+    }
+  }
+  CK(cudaMemcpyAsync(all.data(), dbuf + sizeof(Rec), sizeof(Rec) * P, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  cudaFree(dbuf);
+  for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
+  h->ipc_open.clear();
+  std::vector<const double2*> base(P);
+  std::vector<int64_t> ldv(P);
+  for (int q = 0; q < P; ++q) {
+    ldv[q] = all[q].ldv;
+    if (q == me || all[q].pid == mine.pid) {
+      base[q] = reinterpret_cast<const double2*>(all[q].ptr);
+    } else {
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, all[q].hdl, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(TE_ERR_CUDA, "cannot map rank %d's Krylov basis (CUDA IPC / peer access)", q);
+      }
+      h->ipc_open.push_back(p);
+      base[q] = static_cast<const double2*>(p);
+    }
+  }
+  if (!h->d_peer_base) {
+    CK(cudaMalloc(&h->d_peer_base, sizeof(double2*) * P));
+    CK(cudaMalloc(&h->d_peer_ldv, sizeof(int64_t) * P));
+  }
+  CK(cudaMemcpy(h->d_peer_base, base.data(), sizeof(double2*) * P, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->d_peer_ldv, ldv.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice));
+  h->peer_for_V = h->d_V;
+  return TE_OK;
+}
+
 // ---------------------------------------------------------------- one Krylov decomposition
 // Launch the whole restart (Alg. 1 step 1) without host synchronisation: the kernels gate
 // themselves on the device breakdown flag.  Then one D2H of alpha/beta/flag.
@@ -394,6 +477,10 @@ int halo_exchange(te_handle* h, int j) {
 
 int issue_arnoldi(te_handle* h, int m, double tol_rate) {
   int lj = -1;
+  if (peer_active(h) && h->peer_for_V != h->d_V) {
+    const int rc = setup_peers(h);
+    if (rc) return rc;
+  }
   KDev d = make_kdev(h, tol_rate, m);
   Launch L = make_launch(h);
   const double n = (double)h->n;
@@ -679,6 +766,10 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
       }
       te::launch_combine(d, h->d_g + 128, m_eff, h->d_V, L);
       ++h->launches;
+      if (peer_active(h)) {  // peers read the new V_0 directly in the next SpMV: barrier
+        const int rc = allreduce_sum(h, h->d_small + kOffScalar, 1);
+        if (rc) return rc;
+      }
       if (h->profile) {
         cudaEventRecord(h->evk1, h->stream);
         h->evk_pending = true;
@@ -937,6 +1028,11 @@ void te_destroy(te_handle* h) {
   cudaFree(h->d_partn);
   cudaFree(h->d_counter);
   cudaFree(h->d_halo);
+  cudaFree(h->d_halo_owner);
+  cudaFree(h->d_halo_lidx);
+  cudaFree(h->d_peer_base);
+  cudaFree(h->d_peer_ldv);
+  for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
   cudaFree(h->d_tile_row);
   cudaFree(h->d_tile_desc);
   cudaFree(h->d_tile_ag);
@@ -1153,6 +1249,10 @@ int te_set_option(te_handle* h, int option, double value) {
         return set_err(TE_ERR_ARG, "TE_OPT_ORTHO must be 0 (CGS2), 1 (Lanczos) or 2 (CGS2, Gram second sweep)");
       h->ortho = (int)value;
       return TE_OK;
+    case TE_OPT_HALO:
+      if (value != 0.0 && value != 1.0) return set_err(TE_ERR_ARG, "TE_OPT_HALO must be 0 (NCCL exchange) or 1 (peer loads)");
+      h->halo_mode = (int)value;
+      return TE_OK;
     case TE_OPT_INTEGRATOR:
       if (value != 0.0 && value != 1.0) return set_err(TE_ERR_ARG, "TE_OPT_INTEGRATOR must be 0 or 1");
       h->integrator = (int)value;
@@ -1244,8 +1344,22 @@ int te_internal_rank(te_dist* d) { return d->rank; }
 
 int te_internal_setup_halo(te_handle* h, int64_t n_halo, const std::vector<int64_t>& recv_counts,
                            const std::vector<int64_t>& send_counts, const std::vector<int32_t>& send_idx,
-                           double norm1_global) {
+                           double norm1_global, const std::vector<int64_t>& halo_global,
+                           const std::vector<int64_t>& row_starts) {
   h->n_halo = n_halo;
+  if (n_halo > 0) {  // owner rank and owner-local row of every halo entry (halo mode 1)
+    std::vector<int32_t> own((size_t)n_halo), lidx((size_t)n_halo);
+    int64_t k = 0;
+    for (int q = 0; q < (int)recv_counts.size(); ++q)
+      for (int64_t i = 0; i < recv_counts[q]; ++i, ++k) {
+        own[(size_t)k] = q;
+        lidx[(size_t)k] = (int32_t)(halo_global[(size_t)k] - row_starts[(size_t)q]);
+      }
+    CK(cudaMalloc(&h->d_halo_owner, sizeof(int32_t) * n_halo));
+    CK(cudaMalloc(&h->d_halo_lidx, sizeof(int32_t) * n_halo));
+    CK(cudaMemcpy(h->d_halo_owner, own.data(), sizeof(int32_t) * n_halo, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_halo_lidx, lidx.data(), sizeof(int32_t) * n_halo, cudaMemcpyHostToDevice));
+  }
   h->recv_counts = recv_counts;
   h->send_counts = send_counts;
   h->n_send = (int64_t)send_idx.size();

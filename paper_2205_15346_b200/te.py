@@ -29,6 +29,7 @@ TE_OPT_PREFETCH = 4
 TE_OPT_SPMV = 5
 TE_OPT_ORTHO = 6
 TE_OPT_INTEGRATOR = 7
+TE_OPT_HALO = 8
 KERNELS = {0: "spmv", 1: "update_proj", 2: "update_norm", 3: "combine", 4: "halo_pack", 5: "proj_dots",
            6: "host_step"}
 

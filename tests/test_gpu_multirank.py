@@ -24,7 +24,7 @@ sys.path.insert(0, sys.argv[3])
 from paper_2205_15346_b200 import te
 from oracle import krylov as K
 from workloads import configs
-ws, case = int(sys.argv[1]), sys.argv[2]
+ws, case, halo_mode = int(sys.argv[1]), sys.argv[2], int(sys.argv[4])
 c = {"xxz": lambda: configs.build(5, L=12), "bh": lambda: configs.build(3, L=7, N=7),
      "random": lambda: configs.build(1, n=3001)}[case]()
 n, m, t, tol = c["n"], 16, 1.0, 1e-9
@@ -43,6 +43,7 @@ def worker(r):
         rb, re_ = rs[r], rs[r + 1]
         h = te.te_create_csr_dist(D, n, rb, re_, (rp[rb:re_ + 1] - rp[rb]).astype(np.int64),
                                   col[rp[rb]:rp[re_]].astype(np.int64), val[rp[rb]:rp[re_]])
+        te.te_set_option(h, te.TE_OPT_HALO, halo_mode)
         g = te.te_krylov_basis(h, v0[rb:re_], m, tol_rate, want_V=True)
         vf = None
         if sched is not None:
@@ -91,12 +92,15 @@ def fake_nccl(tmp_path_factory):
     return lib
 
 
+@pytest.mark.parametrize("halo", [0, 1], ids=["nccl_exchange", "peer_loads"])
 @pytest.mark.parametrize("ws", [2, 3])
 @pytest.mark.parametrize("case", ["xxz", "bh", "random"])
-def test_multirank_device_path_on_one_gpu(gpu_lib, fake_nccl, ws, case):
+def test_multirank_device_path_on_one_gpu(gpu_lib, fake_nccl, ws, case, halo):
+    """halo 0: staged NCCL send/recv exchange before each SpMV; halo 1 (TE_OPT_HALO): the
+    SpMV reads halo columns directly from the owning rank's V column (same address space here)."""
     env = dict(os.environ, TE_NCCL_LIB=fake_nccl)
-    p = subprocess.run([sys.executable, "-c", SCRIPT, str(ws), case, ROOT], env=env, capture_output=True, text=True,
-                       timeout=300)
+    p = subprocess.run([sys.executable, "-c", SCRIPT, str(ws), case, ROOT, str(halo)], env=env, capture_output=True,
+                       text=True, timeout=300)
     line = [l for l in p.stdout.splitlines() if l.startswith("RESULT ")]
     assert p.returncode == 0 and line, p.stdout[-2000:] + p.stderr[-4000:]
     r = json.loads(line[0][7:])
