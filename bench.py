@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel: 4 pipelined (default) .. 0 CSR-vector")
     ap.add_argument("--force-dist", action="store_true",
                     help="single rank through the distributed API (te_dist_init/te_create_csr_dist), for testing")
+    ap.add_argument("--halo", type=int, default=0, help="N>1: 0 NCCL halo exchange (default), 1 SpMV reads peer memory (f4)")
     ap.add_argument("--ortho", type=int, default=0, help="0 CGS2 (north star), 1 paper-literal Lanczos (f1), 2 CGS2 with Gram second sweep (f2)")
     return ap.parse_args()
 
@@ -254,6 +255,7 @@ def run_ours(args):
     if args.spmv is not None:
         te.te_set_option(h, te.TE_OPT_SPMV, args.spmv)
     te.te_set_option(h, te.TE_OPT_ORTHO, args.ortho)
+    te.te_set_option(h, te.TE_OPT_HALO, args.halo)
     stream = torch.cuda.current_stream(dev)
     d_v0 = torch.from_numpy(np.ascontiguousarray(v0_loc)).to(dev)
     d_out = torch.empty_like(d_v0)
@@ -360,7 +362,8 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (V = %.0f MB > 126 MB)" % (16 * nloc * m / 1e6),
                    "parallelism": f"rows{ws}", "kernels": ["fused-register", "staged", "hybrid", "tma", "shuffle"][args.kernels],
                    "prefetch": args.prefetch, "spmv": args.spmv,
-                   "ortho": ["cgs2", "lanczos3", "cgs2gram"][args.ortho]},
+                   "ortho": ["cgs2", "lanczos3", "cgs2gram"][args.ortho],
+                   "halo": ["nccl_exchange", "peer_loads"][args.halo] if ws > 1 else None},
         "achieved_hbm_gbs": all_bytes / (all_ms * 1e-3) / 1e9 if all_ms > 0 else None,
         "step_hbm_gbs": all_bytes / (ms * 1e-3) / 1e9,
         "profiled_region_ms_per_step": ms_prof / args.steps,
