@@ -1,3 +1,13 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests/test_gpu_multirank.py tests/test_gpu_parity.py -q -x -k "multirank or distributed or krylov_basis or pipe_variants" > gpurun_out/pytest_mr.log 2>&1
+B="python bench.py --steps 5 --warmup 3"
+timeout 900 $B --config 2 > gpurun_out/fin_c2.log 2>&1
+timeout 900 $B --config 1 --no-cpu-baseline > gpurun_out/fin_c1.log 2>&1
+timeout 900 $B --config 3 > gpurun_out/fin_c3.log 2>&1
+timeout 900 $B --config 6 > gpurun_out/fin_c6.log 2>&1
+timeout 900 python bench.py --steps 3 --warmup 3 --config 4 --no-cpu-baseline > gpurun_out/fin_c4.log 2>&1
+timeout 1200 python bench.py --steps 3 --warmup 3 --config 5 --no-cpu-baseline > gpurun_out/fin_c5.log 2>&1
+for c in 2 3 6; do timeout 900 $B --config $c --ortho 2 --no-cpu-baseline > gpurun_out/fin_c${c}_f2.log 2>&1; done
+for c in 2 6; do timeout 900 $B --config $c --ortho 1 --no-cpu-baseline > gpurun_out/fin_c${c}_f1.log 2>&1; done
+timeout 1200 python bench.py --steps 3 --warmup 3 --config 5 --ortho 2 --no-cpu-baseline > gpurun_out/fin_c5_f2.log 2>&1
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/fin_ref_c2.log 2>&1
