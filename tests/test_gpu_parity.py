@@ -210,6 +210,23 @@ def test_dense_exponential_and_bound(gpu_lib):
     assert st["err_bound"] <= c["tol"]
 
 
+def test_option_validation(gpu_lib):
+    """Out-of-range option values are rejected (TE_ERR_ARG) and leave the handle usable; the halo
+    mode is accepted on a single-rank handle and has no effect there."""
+    te = gpu_lib
+    c = configs.build(1, n=600)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    v_ref, _ = te.te_evolve(h, c["v0"], 0.5, 1e-9, 20)
+    for opt, bad in ((te.TE_OPT_SPMV, 7), (te.TE_OPT_SPMV, -1), (te.TE_OPT_HALO, 2), (te.TE_OPT_ORTHO, 3),
+                     (te.TE_OPT_KERNELS, 5), (te.TE_OPT_INTEGRATOR, 2), (te.TE_OPT_SPMV, 4.5)):
+        with pytest.raises(te.TEError):
+            te.te_set_option(h, opt, bad)
+    te.te_set_option(h, te.TE_OPT_HALO, 1)
+    v, _ = te.te_evolve(h, c["v0"], 0.5, 1e-9, 20)
+    assert np.array_equal(v, v_ref)
+    h.close()
+
+
 def test_edge_cases(gpu_lib):
     te = gpu_lib
     # Pauli X, t = pi -> -e1 (exp(-i X pi) = -I); breakdown at j = 1 (m_eff = 2)
