@@ -1567,9 +1567,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j, int pf
               else xx[w] = __ldg(x + c);   // single rank: every column is local
             }
           }
-          // products accumulate from the LAST gather down, so the chain's first operand is the
-          // last load and the scheduler issues all NF gathers before any product; values are
-          // re-read from shared memory here rather than held in registers across the gathers
+          // values are re-read from shared memory here rather than held in registers across the
+          // gathers (under the 128-register cap ptxas still issues the gathers in groups of 4-6
+          // ahead of their products; the reverse accumulation order is kept from that experiment)
 #pragma unroll
           for (int w = NF - 1; w >= 0; --w)
             if (q0 + w * TPR < hi) acc = cadd(acc, ValT<CPLX>::mul(vv[q0 + w * TPR], xx[w]));

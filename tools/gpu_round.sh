@@ -1,13 +1,9 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-B="python bench.py --steps 5 --warmup 3"
-timeout 900 $B --config 2 > gpurun_out/fin_c2.log 2>&1
-timeout 900 $B --config 1 --no-cpu-baseline > gpurun_out/fin_c1.log 2>&1
-timeout 900 $B --config 3 > gpurun_out/fin_c3.log 2>&1
-timeout 900 $B --config 6 > gpurun_out/fin_c6.log 2>&1
-timeout 900 python bench.py --steps 3 --warmup 3 --config 4 --no-cpu-baseline > gpurun_out/fin_c4.log 2>&1
-timeout 1200 python bench.py --steps 3 --warmup 3 --config 5 --no-cpu-baseline > gpurun_out/fin_c5.log 2>&1
-for c in 2 3 6; do timeout 900 $B --config $c --ortho 2 --no-cpu-baseline > gpurun_out/fin_c${c}_f2.log 2>&1; done
-for c in 2 6; do timeout 900 $B --config $c --ortho 1 --no-cpu-baseline > gpurun_out/fin_c${c}_f1.log 2>&1; done
-timeout 1200 python bench.py --steps 3 --warmup 3 --config 5 --ortho 2 --no-cpu-baseline > gpurun_out/fin_c5_f2.log 2>&1
-timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/fin_ref_c2.log 2>&1
+B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
+for r in 1 2; do TE_SPMV_RPG=$r timeout 600 $B --config 2 > gpurun_out/sw_rpg${r}_c2.log 2>&1; done
+for r in 1 2; do TE_SPMV_RPG=$r timeout 600 $B --config 3 > gpurun_out/sw_rpg${r}_c3.log 2>&1; done
+for r in 1 2; do TE_SPMV_RPG=$r timeout 900 $B --config 5 > gpurun_out/sw_rpg${r}_c5.log 2>&1; done
+TE_SPMV_RPG=2 TE_SPMV_TPR=8 timeout 600 $B --config 6 > gpurun_out/sw_rpg2_c6_t8.log 2>&1
+TE_SPMV_RPG=1 timeout 600 $B --config 6 > gpurun_out/sw_rpg1_c6.log 2>&1
+TE_SPMV_RPG=2 timeout 600 $B --config 1 > gpurun_out/sw_rpg2_c1.log 2>&1
