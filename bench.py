@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--cpu-sample-steps", type=int, default=8)
     ap.add_argument("--kernels", type=int, default=2, help="2 SpMV + shuffle projections, 3 SpMV + TMA projections, 0 fused register, 1 staged")
     ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (library default if unset)")
-    ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel: 4 pipelined (default) .. 0 CSR-vector")
+    ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel: 7 warp-specialised ring (default), 4 pipelined, 6 SELL, 5 async gather, 3..0 older variants")
     ap.add_argument("--force-dist", action="store_true",
                     help="single rank through the distributed API (te_dist_init/te_create_csr_dist), for testing")
     ap.add_argument("--halo", type=int, default=0, help="N>1: 0 NCCL halo exchange (default), 1 SpMV reads peer memory (f4)")
@@ -361,7 +361,9 @@ def run_ours(args):
                    "restarts_per_step": stats[-1]["n_restarts"],
                    "l2": "inputs larger than L2 (V = %.0f MB > 126 MB)" % (16 * nloc * m / 1e6),
                    "parallelism": f"rows{ws}", "kernels": ["fused-register", "staged", "hybrid", "tma", "shuffle"][args.kernels],
-                   "prefetch": args.prefetch, "spmv": args.spmv,
+                   "prefetch": args.prefetch,
+                   "spmv": {None: "ring (default)", 0: "csr-vector", 1: "tile", 2: "tma", 3: "rowtile", 4: "pipe",
+                            5: "async-gather", 6: "sell", 7: "ring"}[args.spmv],
                    "ortho": ["cgs2", "lanczos3", "cgs2gram"][args.ortho],
                    "halo": ["nccl_exchange", "peer_loads"][args.halo] if ws > 1 else None},
         "achieved_hbm_gbs": all_bytes / (all_ms * 1e-3) / 1e9 if all_ms > 0 else None,

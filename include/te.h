@@ -156,11 +156,15 @@ enum {
                                 exchange before each SpMV; 1 the SpMV reads halo columns straight
                                 from the owning rank's V column (peer memory: CUDA IPC over NVLink,
                                 or the same address space) — SURVEY f4, the exchange fused into
-                                the SpMV.  Used with the default SpMV (TE_OPT_SPMV 4).       */
+                                the SpMV.  Used with TE_OPT_SPMV 7 (default) or 4.            */
   TE_OPT_SPMV = 5            /* SpMV kernel of kernel sets 2-4 (same arithmetic, measured choice):
-                                4 (default) nnz-balanced tiles, rowptr/col/val of the next tile in
-                                flight by bulk copies (TMA engine) into a double buffer, TPR lanes
-                                per row with 12-16 register gathers in flight per lane;
+                                7 (default) warp-specialised ring: one producer warp bulk-copies
+                                (TMA engine) rowptr/col/val of nnz-balanced tiles into a 4-stage
+                                shared-memory ring, 15 consumer warps (TPR lanes per row, 12-16
+                                register gathers in flight per lane) release stages per warp —
+                                no block barrier per tile;
+                                4 the same tiles double-buffered per block of 8 warps with a block
+                                barrier per tile;
                                 6 SELL-32-sigma: rows sorted by length in 4096-row windows, 32-row
                                 slices stored column-major, one lane per row, software-pipelined
                                 loads (a padded copy of H is built on the device when selected;

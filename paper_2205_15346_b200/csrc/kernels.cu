@@ -1606,6 +1606,143 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j, int pf
   }
 }
 
+// SpMV variant 7 (warp-specialised ring): one producer warp issues the bulk copies of tiles into
+// a kRingStages-deep shared-memory ring (full/empty mbarriers); 15 consumer warps process every tile
+// (TPR lanes per row, <= 480/TPR rows per tile) and release a stage per warp, so warps are never
+// joined by a block barrier: the extra gather round of a long row delays one warp, not the tile.
+// Tile descriptors {first row, end row, first entry, end entry} come from a host table; the
+// producer copies each into its stage.  A row longer than a tile is summed by one consumer warp
+// straight from global memory.
+constexpr int kRingStages = 4;
+constexpr int kRingConsumers = 15;
+constexpr int kRingThreads = (kRingConsumers + 1) * 32;
+
+template <bool CPLX>
+struct RingLayout {
+  using VT = typename ValT<CPLX>::T;
+  static constexpr int kCap = CPLX ? kSpmvTileNnzC : kSpmvTileNnz;
+  static constexpr size_t kVal = (size_t)(kCap + 4) * sizeof(VT);
+  static constexpr size_t kRp = (size_t)(kRingConsumers * 32 + 4) * 8;
+  static constexpr size_t kCol = (size_t)(kCap + 4) * 4;
+  static constexpr size_t kStage = kVal + kRp + kCol;
+  static constexpr size_t kBytes = kRingStages * kStage;
+};
+template <bool CPLX>
+size_t spmv_ring_smem() { return RingLayout<CPLX>::kBytes; }
+
+template <bool CPLX, int TPR, int HM, int NF>
+__global__ void __launch_bounds__(kRingThreads, 1) k_spmv_ring(KDev d, int j) {
+  using VT = typename ValT<CPLX>::T;
+  using LY = RingLayout<CPLX>;
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ __align__(8) uint64_t full[kRingStages], empty[kRingStages];
+  __shared__ int64_t desc[kRingStages][4];
+  __shared__ double sj_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    sj_s = step_gate(d, j, blockIdx.x == 0);
+    for (int k = 0; k < kRingStages; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], kRingConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+  const int64_t G = gridDim.x;
+  if (warp == kRingConsumers) {  // ------------------------------------------------ producer
+    if (lane != 0) return;
+    const uint64_t pol = policy_evict_first();
+    constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
+    for (int64_t it = 0;; ++it) {
+      const int64_t t = blockIdx.x + it * G;
+      const int st = (int)(it % kRingStages);
+      if (it >= kRingStages) mbar_wait(&empty[st], (unsigned)(((it / kRingStages) - 1) & 1));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (t >= d.ntiles_ring) {  // tell the consumers there is nothing more
+        desc[st][0] = -1;
+        mbar_expect_tx(&full[st], 0);
+        break;
+      }
+      const longlong2 a = __ldg(reinterpret_cast<const longlong2*>(d.tile_ring + 4 * t));
+      const longlong2 b = __ldg(reinterpret_cast<const longlong2*>(d.tile_ring + 4 * t) + 1);
+      desc[st][0] = a.x; desc[st][1] = a.y; desc[st][2] = b.x; desc[st][3] = b.y;
+      const int64_t cnt = b.y - b.x;
+      const int64_t r0 = a.x & ~1LL, r1 = (a.y + 2) & ~1LL;
+      unsigned br = (unsigned)((r1 - r0) * 8), bc = 0, bv = 0;
+      int64_t c0 = 0, v0 = 0;
+      if (cnt <= LY::kCap) {
+        c0 = b.x & ~3LL;
+        v0 = b.x & ~(VA - 1);
+        bc = (unsigned)((((b.y + 3) & ~3LL) - c0) * 4);
+        bv = (unsigned)((((b.y + VA - 1) & ~(VA - 1)) - v0) * sizeof(VT));
+      } else {
+        br = 0;
+      }
+      unsigned char* base = sm + (size_t)st * LY::kStage;
+      mbar_expect_tx(&full[st], br + bc + bv);
+      if (br) bulk_g2s(base + LY::kVal, d.rowptr + r0, br, &full[st], pol);
+      if (bc) bulk_g2s(base + LY::kVal + LY::kRp, d.col + c0, bc, &full[st], pol);
+      if (bv) bulk_g2s(base, static_cast<const VT*>(d.val) + v0, bv, &full[st], pol);
+    }
+    return;
+  }
+  // --------------------------------------------------------------------------------- consumers
+  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  asm volatile("" : "+l"(x));
+  const double2* __restrict__ halo = d.halo;
+  const int n = (int)d.n;
+  const int q = tid % TPR, grp = tid / TPR;  // consumer threads 0 .. 32*kRingConsumers-1
+  auto gx = [&](int c) -> double2 {
+    if (HM == 1) return ((uint32_t)c < (uint32_t)n) ? __ldg(x + c) : __ldg(halo + (c - n));
+    if (HM == 2) return ((uint32_t)c < (uint32_t)n) ? __ldg(x + c) : peer_x(d, j, c - n);
+    return __ldg(x + c);
+  };
+  for (int64_t it = 0;; ++it) {
+    const int st = (int)(it % kRingStages);
+    mbar_wait(&full[st], (unsigned)((it / kRingStages) & 1));
+    const int64_t ra = desc[st][0];
+    if (ra < 0) break;
+    const int64_t rb = desc[st][1], b = desc[st][2], e = desc[st][3];
+    const int64_t cnt = e - b;
+    const int64_t t = blockIdx.x + it * G;
+    if (cnt <= LY::kCap) {
+      constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
+      const unsigned char* base = sm + (size_t)st * LY::kStage;
+      const int64_t* rp = reinterpret_cast<const int64_t*>(base + LY::kVal) + (ra & 1);
+      const int32_t* cc = reinterpret_cast<const int32_t*>(base + LY::kVal + LY::kRp) + (b & 3);
+      const VT* vv = reinterpret_cast<const VT*>(base) + (b & (VA - 1));
+      const int rows = (int)(rb - ra);
+      const int i = grp;
+      const bool act = i < rows;
+      const int lo = act ? (int)(rp[i] - b) : 0, hi = act ? (int)(rp[i + 1] - b) : 0;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int q0 = lo + q; q0 < hi; q0 += NF * TPR) {
+        double2 xx[NF];
+#pragma unroll
+        for (int w = 0; w < NF; ++w) {
+          const int ee = q0 + w * TPR;
+          if (ee < hi) xx[w] = gx(cc[ee]);
+        }
+#pragma unroll
+        for (int w = NF - 1; w >= 0; --w)
+          if (q0 + w * TPR < hi) acc = cadd(acc, ValT<CPLX>::mul(vv[q0 + w * TPR], xx[w]));
+      }
+      if (TPR > 1) acc = group_sum<TPR>(acc);
+      if (act && q == 0) __stcs(d.W + ra + i, make_double2(acc.x * sj, acc.y * sj));
+    } else if (warp == (int)(t % kRingConsumers)) {  // one long row: one warp, from global memory
+      const VT* __restrict__ val = static_cast<const VT*>(d.val);
+      double2 acc = make_double2(0.0, 0.0);
+      for (int64_t k = b + lane; k < e; k += 32) acc = cadd(acc, ValT<CPLX>::mul(__ldg(val + k), gx(__ldg(d.col + k))));
+      acc = warp_sum(acc);
+      if (lane == 0) __stcs(d.W + ra, make_double2(acc.x * sj, acc.y * sj));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+}
+
 // SpMV variant 5 (async gather).  The x gathers of a tile are cp.async copies into shared
 // memory, so a whole tile's gathers (<= kAgCap) are in flight at once without holding registers,
 // and they overlap the products of the previous tile:
@@ -2295,6 +2432,15 @@ cudaError_t configure_kernels() {
   set((const void*)k_proj_tma<3, 16>, kProjSmemBudget + 1024);
   set((const void*)k_proj_tma<1, 16>, kProjSmemBudget + 1024);
   set((const void*)k_spmv_tma<false>, kProjSmemBudget + 1024);
+#define TE_SETRING(T, H)                                                                   \
+  set((const void*)k_spmv_ring<false, T, H, 16>, spmv_ring_smem<false>());                \
+  set((const void*)k_spmv_ring<false, T, H, 12>, spmv_ring_smem<false>());                \
+  set((const void*)k_spmv_ring<true, T, H, 12>, spmv_ring_smem<true>());                  \
+  set((const void*)k_spmv_ring<true, T, H, 8>, spmv_ring_smem<true>());
+  TE_SETRING(1, 0) TE_SETRING(2, 0) TE_SETRING(4, 0) TE_SETRING(8, 0)
+  TE_SETRING(1, 1) TE_SETRING(2, 1) TE_SETRING(4, 1) TE_SETRING(8, 1)
+  TE_SETRING(1, 2) TE_SETRING(2, 2) TE_SETRING(4, 2) TE_SETRING(8, 2)
+#undef TE_SETRING
 #define TE_SETAG(T)                                                                      \
   set((const void*)k_spmv_ag<false, T, false>, spmv_ag_smem<false>());                   \
   set((const void*)k_spmv_ag<true, T, false>, spmv_ag_smem<true>());                     \
@@ -2338,6 +2484,29 @@ static int tpr_for(int ncols, int min_tpr) {
   }
 
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
+  if (L.spmv_tiled == 7 && d.ntiles_ring > 0) {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(L.num_sms, d.ntiles_ring));
+#define TE_RING_H(T, H)                                                                                      \
+  if (cplx) {                                                                                                \
+    if (L.spmv_nf_wide) k_spmv_ring<true, T, H, 12><<<grid, kRingThreads, spmv_ring_smem<true>(), L.stream>>>(d, j);   \
+    else k_spmv_ring<true, T, H, 8><<<grid, kRingThreads, spmv_ring_smem<true>(), L.stream>>>(d, j);                   \
+  } else {                                                                                                   \
+    if (L.spmv_nf_wide) k_spmv_ring<false, T, H, 16><<<grid, kRingThreads, spmv_ring_smem<false>(), L.stream>>>(d, j); \
+    else k_spmv_ring<false, T, H, 12><<<grid, kRingThreads, spmv_ring_smem<false>(), L.stream>>>(d, j);                \
+  }
+#define TE_RING(T)                                                                                 \
+  case T:                                                                                          \
+    if (L.halo_peer) { TE_RING_H(T, 2) } else if (d.halo || L.spmv_force_halo) { TE_RING_H(T, 1) } \
+    else { TE_RING_H(T, 0) }                                                                       \
+    break;
+    switch (L.spmv_ring_tpr) {
+      TE_RING(1) TE_RING(2) TE_RING(4)
+      default: TE_RING(8)
+    }
+#undef TE_RING
+#undef TE_RING_H
+    return;
+  }
   if (L.spmv_tiled == 6 && d.nslices > 0) {
     const bool hal = d.halo || L.spmv_force_halo;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)8 * L.num_sms, (d.nslices + kWarps - 1) / kWarps));

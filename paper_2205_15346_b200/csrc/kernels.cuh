@@ -47,6 +47,8 @@ struct KDev {
   const int32_t* slen;       // [nslices] slice widths
   const int32_t* sperm;      // [32*nslices] slice position -> row (-1: padding lane)
   int64_t nslices;
+  const int64_t* tile_ring;  // [4*ntiles_ring] {first row, end row, first entry, end entry} (variant 7)
+  int64_t ntiles_ring;
   const int64_t* tile_ag;    // [4*ntiles_ag] {first row, end row, first entry, end entry} (variant 5)
   int64_t ntiles_ag;
   const int64_t* tile_desc;  // [2*(ntiles_desc+1)] {first row, first entry} of the TMA SpMV tiles
@@ -79,7 +81,8 @@ struct Launch {
   int spmv_force_halo;  // test hook: run the multi-rank (halo-aware) SpMV instantiation on one rank
   int spmv_nf_wide;
   int halo_peer;      // SpMV reads halo columns from peer memory (no staged exchange)
-  int spmv_ag_tpr;    // lanes per row of the async-gather SpMV (1..32)   // pipelined SpMV gathers in flight per lane: 0 -> 12 real / 8 complex, 1 -> 16 / 12
+  int spmv_ag_tpr;
+  int spmv_ring_tpr;  // lanes per row of the warp-specialised ring SpMV    // lanes per row of the async-gather SpMV (1..32)   // pipelined SpMV gathers in flight per lane: 0 -> 12 real / 8 complex, 1 -> 16 / 12
   int proj_tma;   // 2: hybrid by column count (default), 1: TMA-tiled only, 0: register/shuffle only
   int spmv_tiled; // 2: TMA-fed SpMV (default), 1: nnz-balanced tiled SpMV, 0: CSR-vector
   int prefetch; // L2 bulk-prefetch distance in block iterations (0: off)

@@ -119,11 +119,14 @@ struct te_handle {
   int spmv_pf = 0;
   int spmv_nf_wide = 0;
   int spmv_force_halo = 0;
-  int spmv_tiled = 4;
+  int spmv_tiled = 7;
   int64_t* d_tile_row = nullptr;
   int64_t ntiles = 0;
   int64_t* d_tile_desc = nullptr;
   int64_t* d_tile_ag = nullptr;
+  int64_t* d_tile_ring = nullptr;
+  int64_t ntiles_ring = 0;
+  int spmv_ring_tpr = 1;
   // SELL-32-sigma copy of H (SpMV variant 6), built on first selection
   int32_t* d_scol = nullptr;
   void* d_sval = nullptr;
@@ -201,6 +204,8 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.ntiles = h->ntiles;
   d.tile_desc = h->d_tile_desc;
   d.tile_ag = h->d_tile_ag;
+  d.tile_ring = h->d_tile_ring;
+  d.ntiles_ring = h->ntiles_ring;
   d.scol = h->d_scol;
   d.sval = h->d_sval;
   d.sptr = h->d_sptr;
@@ -229,7 +234,7 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
 // halo mode 1 is used by the pipelined SpMV of the projection-kernel sets (and f1/f2); the other
 // SpMV variants keep the staged exchange
 bool peer_active(const te_handle* h) {
-  return h->dist && h->dist->nranks > 1 && h->halo_mode == 1 && h->spmv_tiled == 4 &&
+  return h->dist && h->dist->nranks > 1 && h->halo_mode == 1 && (h->spmv_tiled == 4 || h->spmv_tiled == 7) &&
          (h->variant >= 2 || h->ortho != 0);
 }
 
@@ -251,6 +256,7 @@ Launch make_launch(te_handle* h) {
   L.spmv_force_halo = h->spmv_force_halo;
   L.halo_peer = peer_active(h) ? 1 : 0;
   L.spmv_ag_tpr = h->spmv_ag_tpr;
+  L.spmv_ring_tpr = h->spmv_ring_tpr;
   L.spmv_tiled = h->spmv_tiled;
   L.prefetch = h->prefetch;
   return L;
@@ -921,6 +927,35 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     cudaMemcpyAsync(h->d_tile_desc, td.data(), sizeof(int64_t) * td.size(), cudaMemcpyHostToDevice, h->stream);
     cudaStreamSynchronize(h->stream);
   }
+  {  // warp-specialised ring SpMV (variant 7, default) tiles: <= kSpmvTileNnz(C) entries and
+     // <= 480/tpr rows, {first row, end row, first entry, end entry}; lanes per row by the same rule
+     // as the pipelined SpMV (measured best on configs 2-6: 1 / 2 / 8 / 2 / 4)
+    int tr = h->spmv_pipe_tpr;
+    if (const char* e = getenv("TE_SPMV_RING_TPR")) {
+      const int v = atoi(e);
+      if (v == 1 || v == 2 || v == 4 || v == 8) tr = v;
+    }
+    h->spmv_ring_tpr = tr;
+    const int64_t rcap = 480 / tr;
+    const int64_t ncap = cplx ? te::kSpmvTileNnzC : te::kSpmvTileNnz;
+    std::vector<int64_t> tg;
+    int64_t st = 0;
+    for (int64_t r = 0; r < n; ++r) {
+      const bool over_rows = (r + 1 - st) > rcap;
+      const bool over_nnz = (rowptr[r + 1] - rowptr[st]) > ncap && r > st;
+      if (over_rows || over_nnz) {
+        tg.insert(tg.end(), {st, r, rowptr[st], rowptr[r]});
+        st = r;
+      }
+    }
+    if (n > 0) tg.insert(tg.end(), {st, n, rowptr[st], rowptr[n]});
+    h->ntiles_ring = (int64_t)tg.size() / 4;
+    if (!tg.empty()) {
+      if (cudaMalloc(&h->d_tile_ring, sizeof(int64_t) * tg.size()) != cudaSuccess) return fail(TE_ERR_OOM, "tiles");
+      cudaMemcpyAsync(h->d_tile_ring, tg.data(), sizeof(int64_t) * tg.size(), cudaMemcpyHostToDevice, h->stream);
+      cudaStreamSynchronize(h->stream);
+    }
+  }
   {  // async-gather SpMV (variant 5) tiles: <= kAgCap entries and <= kThreads/tpr rows, stored as
      // {first row, end row, first entry, end entry}; lanes per row = the largest power of two
      // <= mean row length / 4 (1..32), so a full tile keeps every row group busy
@@ -1036,6 +1071,7 @@ void te_destroy(te_handle* h) {
   cudaFree(h->d_tile_row);
   cudaFree(h->d_tile_desc);
   cudaFree(h->d_tile_ag);
+  cudaFree(h->d_tile_ring);
   cudaFree(h->d_scol);
   cudaFree(h->d_sval);
   cudaFree(h->d_sptr);
@@ -1258,8 +1294,8 @@ int te_set_option(te_handle* h, int option, double value) {
       h->integrator = (int)value;
       return TE_OK;
     case TE_OPT_SPMV:
-      if (value < 0.0 || value > 6.0 || value != (double)(int)value)
-        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 0..6");
+      if (value < 0.0 || value > 7.0 || value != (double)(int)value)
+        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 0..7");
       if (value == 6.0) {
         const int rc = build_sell(h);
         if (rc != TE_OK) return rc;

@@ -35,8 +35,8 @@ def small_cases():
 CASES = small_cases()
 
 
-KERNEL_SETS = [(2, 4), (2, 5), (2, 6), (2, 3), (2, 1), (2, 2), (2, 0), (3, 4), (4, 4), (0, 4), (1, 4)]
-KERNEL_IDS = ["hybrid-spmvpipe", "hybrid-spmvag", "hybrid-spmvsell", "hybrid-spmvrow", "hybrid-spmvtile", "hybrid-spmvtma", "hybrid-spmvvec",
+KERNEL_SETS = [(2, 4), (2, 7), (2, 5), (2, 6), (2, 3), (2, 1), (2, 2), (2, 0), (3, 4), (4, 4), (0, 4), (1, 4)]
+KERNEL_IDS = ["hybrid-spmvpipe", "hybrid-spmvring", "hybrid-spmvag", "hybrid-spmvsell", "hybrid-spmvrow", "hybrid-spmvtile", "hybrid-spmvtma", "hybrid-spmvvec",
               "tma", "shuffle", "fused-register", "staged"]
 
 
@@ -134,6 +134,28 @@ def test_spmv_async_gather_variants(gpu_lib, name, c, tpr, halo, monkeypatch):
     h.close()
 
 
+@pytest.mark.parametrize("tpr", [1, 2, 4, 8])
+@pytest.mark.parametrize("halo", [0, 1])
+@pytest.mark.parametrize("name,c", AG_CASES, ids=[x[0] for x in AG_CASES])
+def test_spmv_ring_variants(gpu_lib, name, c, tpr, halo, monkeypatch):
+    """Warp-specialised ring SpMV (TE_OPT_SPMV = 7) for every lanes-per-row choice, plain and
+    halo-aware, including rows longer than a tile (one warp from global memory), vs the oracle."""
+    te = gpu_lib
+    if c is None:
+        c = _long_row_case()
+    monkeypatch.setenv("TE_SPMV_RING_TPR", str(tpr))
+    monkeypatch.setenv("TE_SPMV_FORCE_HALO", str(halo))
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    te.te_set_option(h, te.TE_OPT_SPMV, 7)
+    g = te.te_krylov_basis(h, c["v0"], 12, c["tol"] / c["t"], want_V=True)
+    o = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), c["v0"], 12, c["tol"] / c["t"])
+    scale = max(1.0, np.abs(o["alpha"]).max(), np.abs(o["beta"]).max())
+    assert g["m_eff"] == o["m_eff"]
+    assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-12 * scale
+    assert np.linalg.norm(g["V"] - o["V"]) <= 1e-10
+    h.close()
+
+
 @pytest.mark.parametrize("halo", [0, 1])
 @pytest.mark.parametrize("name,c", PIPE_CASES, ids=[x[0] for x in PIPE_CASES])
 def test_spmv_sell_halo_variants(gpu_lib, name, c, halo, monkeypatch):
@@ -217,7 +239,7 @@ def test_option_validation(gpu_lib):
     c = configs.build(1, n=600)
     h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
     v_ref, _ = te.te_evolve(h, c["v0"], 0.5, 1e-9, 20)
-    for opt, bad in ((te.TE_OPT_SPMV, 7), (te.TE_OPT_SPMV, -1), (te.TE_OPT_HALO, 2), (te.TE_OPT_ORTHO, 3),
+    for opt, bad in ((te.TE_OPT_SPMV, 8), (te.TE_OPT_SPMV, -1), (te.TE_OPT_HALO, 2), (te.TE_OPT_ORTHO, 3),
                      (te.TE_OPT_KERNELS, 5), (te.TE_OPT_INTEGRATOR, 2), (te.TE_OPT_SPMV, 4.5)):
         with pytest.raises(te.TEError):
             te.te_set_option(h, opt, bad)
