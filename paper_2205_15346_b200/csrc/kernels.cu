@@ -1613,27 +1613,29 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_pipe(KDev d, int j, int pf
 // Tile descriptors {first row, end row, first entry, end entry} come from a host table; the
 // producer copies each into its stage.  A row longer than a tile is summed by one consumer warp
 // straight from global memory.
-constexpr int kRingStages = 4;
+// STG stages of kCap entries: 4 x 4096 (real) / 2048 (complex), or 3 x 5632 / 2816 (te_api picks
+// per matrix: the deeper ring for short real rows, the larger tiles otherwise)
 constexpr int kRingConsumers = 15;
 constexpr int kRingThreads = (kRingConsumers + 1) * 32;
 
-template <bool CPLX>
+template <bool CPLX, int STG>
 struct RingLayout {
   using VT = typename ValT<CPLX>::T;
-  static constexpr int kCap = CPLX ? kSpmvTileNnzC : kSpmvTileNnz;
+  static constexpr int kCap = STG == 3 ? (CPLX ? kRingNnzC3 : kRingNnz3) : (CPLX ? kRingNnzC4 : kRingNnz4);
   static constexpr size_t kVal = (size_t)(kCap + 4) * sizeof(VT);
   static constexpr size_t kRp = (size_t)(kRingConsumers * 32 + 4) * 8;
   static constexpr size_t kCol = (size_t)(kCap + 4) * 4;
   static constexpr size_t kStage = kVal + kRp + kCol;
-  static constexpr size_t kBytes = kRingStages * kStage;
+  static constexpr size_t kBytes = STG * kStage;
 };
-template <bool CPLX>
-size_t spmv_ring_smem() { return RingLayout<CPLX>::kBytes; }
+template <bool CPLX, int STG>
+size_t spmv_ring_smem() { return RingLayout<CPLX, STG>::kBytes; }
 
-template <bool CPLX, int TPR, int HM, int NF>
+template <bool CPLX, int TPR, int HM, int NF, int STG>
 __global__ void __launch_bounds__(kRingThreads, 1) k_spmv_ring(KDev d, int j) {
   using VT = typename ValT<CPLX>::T;
-  using LY = RingLayout<CPLX>;
+  using LY = RingLayout<CPLX, STG>;
+  constexpr int kRingStages = STG;
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ __align__(8) uint64_t full[kRingStages], empty[kRingStages];
   __shared__ int64_t desc[kRingStages][4];
@@ -2432,15 +2434,17 @@ cudaError_t configure_kernels() {
   set((const void*)k_proj_tma<3, 16>, kProjSmemBudget + 1024);
   set((const void*)k_proj_tma<1, 16>, kProjSmemBudget + 1024);
   set((const void*)k_spmv_tma<false>, kProjSmemBudget + 1024);
-#define TE_SETRING(T, H)                                                                   \
-  set((const void*)k_spmv_ring<false, T, H, 16>, spmv_ring_smem<false>());                \
-  set((const void*)k_spmv_ring<false, T, H, 12>, spmv_ring_smem<false>());                \
-  set((const void*)k_spmv_ring<true, T, H, 12>, spmv_ring_smem<true>());                  \
-  set((const void*)k_spmv_ring<true, T, H, 8>, spmv_ring_smem<true>());
+#define TE_SETRING_S(T, H, S)                                                              \
+  set((const void*)k_spmv_ring<false, T, H, 16, S>, spmv_ring_smem<false, S>());          \
+  set((const void*)k_spmv_ring<false, T, H, 12, S>, spmv_ring_smem<false, S>());          \
+  set((const void*)k_spmv_ring<true, T, H, 12, S>, spmv_ring_smem<true, S>());            \
+  set((const void*)k_spmv_ring<true, T, H, 8, S>, spmv_ring_smem<true, S>());
+#define TE_SETRING(T, H) TE_SETRING_S(T, H, 3) TE_SETRING_S(T, H, 4)
   TE_SETRING(1, 0) TE_SETRING(2, 0) TE_SETRING(4, 0) TE_SETRING(8, 0)
   TE_SETRING(1, 1) TE_SETRING(2, 1) TE_SETRING(4, 1) TE_SETRING(8, 1)
   TE_SETRING(1, 2) TE_SETRING(2, 2) TE_SETRING(4, 2) TE_SETRING(8, 2)
 #undef TE_SETRING
+#undef TE_SETRING_S
 #define TE_SETAG(T)                                                                      \
   set((const void*)k_spmv_ag<false, T, false>, spmv_ag_smem<false>());                   \
   set((const void*)k_spmv_ag<true, T, false>, spmv_ag_smem<true>());                     \
@@ -2486,14 +2490,16 @@ static int tpr_for(int ncols, int min_tpr) {
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
   if (L.spmv_tiled == 7 && d.ntiles_ring > 0) {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(L.num_sms, d.ntiles_ring));
-#define TE_RING_H(T, H)                                                                                      \
-  if (cplx) {                                                                                                \
-    if (L.spmv_nf_wide) k_spmv_ring<true, T, H, 12><<<grid, kRingThreads, spmv_ring_smem<true>(), L.stream>>>(d, j);   \
-    else k_spmv_ring<true, T, H, 8><<<grid, kRingThreads, spmv_ring_smem<true>(), L.stream>>>(d, j);                   \
-  } else {                                                                                                   \
-    if (L.spmv_nf_wide) k_spmv_ring<false, T, H, 16><<<grid, kRingThreads, spmv_ring_smem<false>(), L.stream>>>(d, j); \
-    else k_spmv_ring<false, T, H, 12><<<grid, kRingThreads, spmv_ring_smem<false>(), L.stream>>>(d, j);                \
+#define TE_RING_S(T, H, S)                                                                                      \
+  if (cplx) {                                                                                                   \
+    if (L.spmv_nf_wide) k_spmv_ring<true, T, H, 12, S><<<grid, kRingThreads, spmv_ring_smem<true, S>(), L.stream>>>(d, j);   \
+    else k_spmv_ring<true, T, H, 8, S><<<grid, kRingThreads, spmv_ring_smem<true, S>(), L.stream>>>(d, j);                   \
+  } else {                                                                                                      \
+    if (L.spmv_nf_wide) k_spmv_ring<false, T, H, 16, S><<<grid, kRingThreads, spmv_ring_smem<false, S>(), L.stream>>>(d, j); \
+    else k_spmv_ring<false, T, H, 12, S><<<grid, kRingThreads, spmv_ring_smem<false, S>(), L.stream>>>(d, j);                \
   }
+#define TE_RING_H(T, H) \
+  if (L.ring_stages == 3) { TE_RING_S(T, H, 3) } else { TE_RING_S(T, H, 4) }
 #define TE_RING(T)                                                                                 \
   case T:                                                                                          \
     if (L.halo_peer) { TE_RING_H(T, 2) } else if (d.halo || L.spmv_force_halo) { TE_RING_H(T, 1) } \
@@ -2505,6 +2511,7 @@ void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
     }
 #undef TE_RING
 #undef TE_RING_H
+#undef TE_RING_S
     return;
   }
   if (L.spmv_tiled == 6 && d.nslices > 0) {

@@ -20,7 +20,10 @@ constexpr int kSpmvRows = 256;       // K1 row tile
 constexpr int kSpmvChunk = 4096;     // K1 products staged in shared memory per chunk
 constexpr int kSpmvTileNnz = 4096;   // entries per nnz-balanced SpMV tile (cap), real values
 constexpr int kSpmvTileNnzC = 2048;  // complex values (two pipelined blocks per SM)
-constexpr int kSpmvMaxTileRows = 256;   // rows per SpMV tile cap (one thread per row)
+constexpr int kSpmvMaxTileRows = 256;
+// warp-specialised ring SpMV tile capacities (entries) for its 4-stage and 3-stage layouts
+constexpr int kRingNnz4 = 4096, kRingNnzC4 = 2048;
+constexpr int kRingNnz3 = 5632, kRingNnzC3 = 2816;   // rows per SpMV tile cap (one thread per row)
 constexpr int kSellSigma = 4096;       // SELL-32-sigma sorting window (rows)
 constexpr int kAgCap = 1024;            // entries per async-gather SpMV tile (variant 5)
 constexpr int kAgMaxRows = 128;         // rows per async-gather tile cap (<= kThreads / TPR)
@@ -82,7 +85,8 @@ struct Launch {
   int spmv_nf_wide;
   int halo_peer;      // SpMV reads halo columns from peer memory (no staged exchange)
   int spmv_ag_tpr;
-  int spmv_ring_tpr;  // lanes per row of the warp-specialised ring SpMV    // lanes per row of the async-gather SpMV (1..32)   // pipelined SpMV gathers in flight per lane: 0 -> 12 real / 8 complex, 1 -> 16 / 12
+  int spmv_ring_tpr;  // lanes per row of the warp-specialised ring SpMV
+  int ring_stages;    // its ring depth: 4 (short real rows) or 3 (larger tiles)    // lanes per row of the async-gather SpMV (1..32)   // pipelined SpMV gathers in flight per lane: 0 -> 12 real / 8 complex, 1 -> 16 / 12
   int proj_tma;   // 2: hybrid by column count (default), 1: TMA-tiled only, 0: register/shuffle only
   int spmv_tiled; // 2: TMA-fed SpMV (default), 1: nnz-balanced tiled SpMV, 0: CSR-vector
   int prefetch; // L2 bulk-prefetch distance in block iterations (0: off)

@@ -134,15 +134,18 @@ def test_spmv_async_gather_variants(gpu_lib, name, c, tpr, halo, monkeypatch):
     h.close()
 
 
+@pytest.mark.parametrize("stages", [3, 4])
 @pytest.mark.parametrize("tpr", [1, 2, 4, 8])
 @pytest.mark.parametrize("halo", [0, 1])
 @pytest.mark.parametrize("name,c", AG_CASES, ids=[x[0] for x in AG_CASES])
-def test_spmv_ring_variants(gpu_lib, name, c, tpr, halo, monkeypatch):
-    """Warp-specialised ring SpMV (TE_OPT_SPMV = 7) for every lanes-per-row choice, plain and
-    halo-aware, including rows longer than a tile (one warp from global memory), vs the oracle."""
+def test_spmv_ring_variants(gpu_lib, name, c, tpr, halo, stages, monkeypatch):
+    """Warp-specialised ring SpMV (TE_OPT_SPMV = 7) for every lanes-per-row choice and both ring
+    depths, plain and halo-aware, including rows longer than a tile (one warp from global memory),
+    vs the oracle."""
     te = gpu_lib
     if c is None:
         c = _long_row_case()
+    monkeypatch.setenv("TE_SPMV_RING_STAGES", str(stages))
     monkeypatch.setenv("TE_SPMV_RING_TPR", str(tpr))
     monkeypatch.setenv("TE_SPMV_FORCE_HALO", str(halo))
     h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
