@@ -1,8 +1,8 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
-export TE_SPMV_NF_WIDE=0
-for t in 1 2; do TE_SPMV_RING_TPR=$t timeout 600 $B --config 2 > gpurun_out/sw_r23_c2_t$t.log 2>&1; done
-for t in 4 8; do TE_SPMV_RING_TPR=$t timeout 600 $B --config 6 > gpurun_out/sw_r23_c6_t$t.log 2>&1; done
-for t in 2 4; do TE_SPMV_RING_TPR=$t timeout 900 $B --config 5 > gpurun_out/sw_r23_c5_t$t.log 2>&1; done
-for t in 2 4; do TE_SPMV_RING_TPR=$t timeout 600 $B --config 3 > gpurun_out/sw_r23_c3_t$t.log 2>&1; done
+timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/b_plain.log 2>&1 || exit 1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu1.log 2>&1
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none -k regex:"k_proj|k_spmv|k_update_norm|k_combine" --csv --log-file gpurun_out/restart_metrics.csv python tools/profile_run.py --t 2.5 > gpurun_out/ncu2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_spmv_ring" -s 60 -c 1 -o gpurun_out/full_c2_spmv python tools/profile_run.py --t 2.5 > gpurun_out/ncu6.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_proj_tma" -s 60 -c 2 -o gpurun_out/full_c2 python tools/profile_run.py --t 2.5 > gpurun_out/ncu4.log 2>&1
+echo done >> gpurun_out/ncu4.log
