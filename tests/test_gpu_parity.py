@@ -235,6 +235,37 @@ def test_dense_exponential_and_bound(gpu_lib):
     assert st["err_bound"] <= c["tol"]
 
 
+@pytest.mark.parametrize("kset,ortho", [((2, 7), 0), ((3, 4), 0), ((4, 4), 0), ((0, 4), 0), ((2, 7), 2), ((2, 7), 1)],
+                         ids=["hybrid-ring", "tma", "shuffle", "fused-register", "cgs2gram", "lanczos3"])
+def test_maximum_krylov_dimension(gpu_lib, kset, ortho):
+    """m = TE_M_MAX = 64: every column group of the projection kernels (register partials and the
+    16-wide butterflies up to column 63, the 64 x 64 Gram matrix of f2) against the oracle; one
+    adaptive evolution at m = 64; m = 65 is rejected."""
+    te = gpu_lib
+    c = configs.build(1)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    te.te_set_option(h, te.TE_OPT_KERNELS, kset[0])
+    te.te_set_option(h, te.TE_OPT_SPMV, kset[1])
+    te.te_set_option(h, te.TE_OPT_ORTHO, ortho)
+    mode = ["cgs2", "lanczos3", "cgs2gram"][ortho]
+    g = te.te_krylov_basis(h, c["v0"], 64, 1e-14, want_V=True)
+    o = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), c["v0"], 64, 1e-14, ortho=mode)
+    assert g["m_eff"] == o["m_eff"] == 64
+    scale = max(1.0, np.abs(o["alpha"]).max(), np.abs(o["beta"]).max())
+    # the paper-literal recurrence loses orthogonality over 64 steps; both sides follow it alike
+    tolr = 1e-12 if ortho != 1 else 1e-9
+    assert np.abs(g["alpha"] - o["alpha"]).max() <= tolr * scale
+    assert np.abs(g["beta"] - o["beta"]).max() <= tolr * scale
+    if ortho != 1:
+        assert np.linalg.norm(g["V"] - o["V"]) <= 1e-10
+    v, st = te.te_evolve(h, c["v0"], 2.0, 1e-8, 64)
+    r = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], 2.0, 1e-8, 64, ortho=mode)
+    assert st["err_bound"] <= 1e-8 and np.linalg.norm(v - r["v"]) <= 1e-8 + 1e-12
+    with pytest.raises(te.TEError):
+        te.te_evolve(h, c["v0"], 2.0, 1e-8, 65)
+    h.close()
+
+
 def test_option_validation(gpu_lib):
     """Out-of-range option values are rejected (TE_ERR_ARG) and leave the handle usable; the halo
     mode is accepted on a single-rank handle and has no effect there."""
