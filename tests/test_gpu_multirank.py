@@ -25,8 +25,15 @@ from paper_2205_15346_b200 import te
 from oracle import krylov as K
 from workloads import configs
 ws, case, halo_mode = int(sys.argv[1]), sys.argv[2], int(sys.argv[4])
+def blockdiag():
+    # two independent Hermitian blocks of 1000 rows: split at 1000 (2 ranks) there is no halo at all
+    a, b = configs.build(1, n=1000), configs.build(1, n=1000)
+    rp = np.concatenate([a["rowptr"], b["rowptr"][1:] + a["rowptr"][-1]])
+    col = np.concatenate([a["col"], b["col"] + 1000]).astype(np.int32)
+    v0 = np.concatenate([a["v0"], b["v0"]]) / np.sqrt(2.0)
+    return dict(n=2000, rowptr=rp, col=col, val=np.concatenate([a["val"], b["val"]]), v0=v0)
 c = {"xxz": lambda: configs.build(5, L=12), "bh": lambda: configs.build(3, L=7, N=7),
-     "random": lambda: configs.build(1, n=3001)}[case]()
+     "random": lambda: configs.build(1, n=3001), "blockdiag": blockdiag}[case]()
 n, m, t, tol = c["n"], 16, 1.0, 1e-9
 rp, col, val, v0 = c["rowptr"], c["col"], c["val"], c["v0"]
 tol_rate = tol / t
@@ -94,7 +101,7 @@ def fake_nccl(tmp_path_factory):
 
 @pytest.mark.parametrize("halo", [0, 1], ids=["nccl_exchange", "peer_loads"])
 @pytest.mark.parametrize("ws", [2, 3])
-@pytest.mark.parametrize("case", ["xxz", "bh", "random"])
+@pytest.mark.parametrize("case", ["xxz", "bh", "random", "blockdiag"])
 def test_multirank_device_path_on_one_gpu(gpu_lib, fake_nccl, ws, case, halo):
     """halo 0: staged NCCL send/recv exchange before each SpMV; halo 1 (TE_OPT_HALO): the
     SpMV reads halo columns directly from the owning rank's V column (same address space here)."""
