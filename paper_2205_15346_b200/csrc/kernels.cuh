@@ -99,6 +99,15 @@ void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L);   // K1
 void launch_sell_build(bool cplx, int64_t npos, const int64_t* rowptr, const int32_t* col, const void* val,
                        const int32_t* perm, const int64_t* sptr, const int32_t* slen, int32_t* scol, void* sval,
                        cudaStream_t st);
+// kernel attribute setup: configure_kernels() (kernels.cu) sets the dynamic shared memory limits
+// of every kernel; the SpMV kernels' part lives in spmv.cu
+struct AttrState {
+  int optin;
+  cudaError_t err;
+};
+void set_attr(const void* f, size_t want, void* ctx);
+void configure_spmv_kernels(void (*set_attr)(const void*, size_t, void*), void* ctx);
+const void* spmv_attr_kernel();  // the SpMV kernel reported by kernel_attributes(0)
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L);        // K1a: SpMV only
 void launch_proj_dots(const KDev& d, int j, const Launch& L);              // K1b: g1 = V^H p (TMA)
 void launch_update_proj(const KDev& d, int j, const Launch& L);            // K2

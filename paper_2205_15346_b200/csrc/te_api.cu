@@ -300,18 +300,23 @@ int build_tensor_maps(te_handle* h) {
   return TE_OK;
 }
 
+// All initialisation is stream-ordered on the handle's current stream: the handle's own stream is
+// non-blocking, so a plain cudaMemset (legacy default stream, asynchronous for device memory) could
+// land after the v0 upload or the first kernels of that stream (an intermittent wrong first SpMV
+// and corrupted reduction tickets, seen as rare parity failures in the GPU tests)
 int ensure_workspace(te_handle* h, int m) {
+  cudaStream_t s = h->stream ? h->stream : h->own_stream;
   if (h->d_small == nullptr) {
     CK(cudaMalloc(&h->d_small, sizeof(double) * kSmallLen));
-    CK(cudaMemset(h->d_small, 0, sizeof(double) * kSmallLen));
+    CK(cudaMemsetAsync(h->d_small, 0, sizeof(double) * kSmallLen, s));
     CK(cudaMalloc(&h->d_g, sizeof(double2) * 3 * 64));
     CK(cudaMalloc(&h->d_G, sizeof(double2) * te::kMaxCols * te::kMaxCols));
-    CK(cudaMemset(h->d_G, 0, sizeof(double2) * te::kMaxCols * te::kMaxCols));
+    CK(cudaMemsetAsync(h->d_G, 0, sizeof(double2) * te::kMaxCols * te::kMaxCols, s));
     h->max_grid = 8 * h->num_sms;
     CK(cudaMalloc(&h->d_part, sizeof(double2) * te::kMaxCols * h->max_grid));
     CK(cudaMalloc(&h->d_partn, sizeof(double) * h->max_grid));
     CK(cudaMalloc(&h->d_counter, sizeof(unsigned) * 8));
-    CK(cudaMemset(h->d_counter, 0, sizeof(unsigned) * 8));
+    CK(cudaMemsetAsync(h->d_counter, 0, sizeof(unsigned) * 8, s));
     CK(cudaMallocHost(&h->h_small, sizeof(double) * kSmallLen));
     CK(cudaMallocHost(&h->h_coef, sizeof(double2) * 64));
   }
@@ -325,7 +330,7 @@ int ensure_workspace(te_handle* h, int m) {
     h->d_V = nullptr;
     return set_err(TE_ERR_OOM, "cannot allocate the Krylov basis (%zu bytes)", bytes);
   }
-  CK(cudaMemset(h->d_V, 0, bytes));
+  CK(cudaMemsetAsync(h->d_V, 0, bytes, s));
   CK(cudaMalloc(&h->d_W, sizeof(double2) * (size_t)h->ldv));
   h->m_cap = m;
   return build_tensor_maps(h);

@@ -2,6 +2,7 @@
 // projection kernel in its three modes (0 dots, 1 update+dots, 2 streaming only) and the
 // register update_norm kernel for a range of column counts, n = 2^20 rows.
 #include "../../paper_2205_15346_b200/csrc/kernels.cu"
+#include "../../paper_2205_15346_b200/csrc/spmv.cu"
 #include <cudaTypedefs.h>
 #include <cstdio>
 #include <vector>
