@@ -100,8 +100,9 @@ void te_destroy(te_handle* h);
 te_handle* te_create_csr_real(int64_t n, const int64_t* rowptr, const int32_t* col, const double* val);
 
 /* As te_evolve with DEVICE pointers (n complex128 each, 16-byte aligned, may alias) on the
- * CUDA stream `stream` (cudaStream_t; NULL = the handle's own stream).  The call returns
- * after the result is complete on that stream. */
+ * CUDA stream `stream` (cudaStream_t; NULL = the handle's own stream, a blocking stream, i.e.
+ * ordered with work the caller issued on the legacy default stream).  The call returns after the
+ * result is complete on that stream. */
 int te_evolve_dev(te_handle* h, const void* d_v0, double t, double tol, int m_max,
                   void* d_vout, te_stats* stats, void* stream);
 

@@ -857,7 +857,9 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
   };
   if (cudaGetDevice(&h->device) != cudaSuccess) return fail(TE_ERR_CUDA, "cudaGetDevice");
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
-  if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess)
+  // a blocking stream: work on it is ordered with the legacy default stream, so device vectors a
+  // caller produced there (stream argument 0) are complete before the library reads them
+  if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamDefault) != cudaSuccess)
     return fail(TE_ERR_CUDA, "cudaStreamCreate");
   h->stream = h->own_stream;
   if (te::configure_kernels() != cudaSuccess) return fail(TE_ERR_CUDA, "kernel shared-memory configuration failed");
