@@ -984,12 +984,11 @@ __device__ __forceinline__ void finish_complex(const KDev& d, double2 v, int ctr
 
 __global__ void __launch_bounds__(kThreads) k_lanczos_dot(KDev d, int j) {
   __shared__ int go_s;
-  __shared__ double cb_s, sj_s;
+  __shared__ double cb_s;
   const int tid = threadIdx.x;
   if (tid == 0) {
     go_s = (d.flag[0] == 0);
     cb_s = j > 0 ? d.beta[j - 1] * d.s[j - 1] : 0.0;  // beta_{j-1} v_{j-1} = beta_{j-1} s_{j-1} V_{j-1}
-    sj_s = d.s[j];
   }
   __syncthreads();
   if (!go_s) return;

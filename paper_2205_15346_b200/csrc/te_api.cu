@@ -710,8 +710,8 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
     if (forced && k >= nforced) break;
     int rc = run_arnoldi(h, m, tol_rate);
     if (rc) { fill(); return rc; }
-    int m_eff;
-    bool brk;
+    int m_eff = 0;
+    bool brk = false;
     if ((rc = read_flag(h, m, &m_eff, &brk))) { fill(); return rc; }
     const auto host_t0 = std::chrono::steady_clock::now();
     const double* alpha = h->h_small + kOffAlpha;
@@ -1197,8 +1197,8 @@ int te_krylov_basis(te_handle* h, const te_c128* v1, int m, double tol_rate, dou
   if (rc) return rc;
   CK(cudaMemcpyAsync(h->d_V, v1, sizeof(double2) * h->n, cudaMemcpyHostToDevice, h->stream));
   if ((rc = run_arnoldi(h, m, tol_rate))) return rc;
-  bool brk;
-  int me;
+  bool brk = false;
+  int me = 0;
   if ((rc = read_flag(h, m, &me, &brk))) return rc;
   *m_eff = me;
   if (breakdown) *breakdown = brk ? 1 : 0;
