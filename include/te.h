@@ -193,8 +193,9 @@ int64_t te_launch_count(const te_handle* h);
 /* ||H||_1 of the handle's matrix (global for distributed handles). */
 double te_one_norm(const te_handle* h);
 
-/* Diagnostics: compiled attributes of a hot-path kernel (which: 0 spmv, 1 proj_dots, 2 update_proj
- * (TMA), 3 update_norm, 4 spmv_proj (register), 5 update_proj (register)). */
+/* Diagnostics: compiled attributes of a hot-path kernel (which: 0 spmv (the default ring kernel,
+ * real values, one lane per row), 1 proj_dots, 2 update_proj (TMA), 3 update_norm, 4 spmv_proj
+ * (register), 5 update_proj (register)). */
 int te_kernel_attributes(int which, int* regs, int* max_threads, int* static_smem, int* max_dyn_smem);
 
 /* Thread-local status / message of the last failing call (TE_OK / "" if none). */

@@ -1136,6 +1136,7 @@ void configure_spmv_kernels(void (*set_attr)(const void*, size_t, void*), void* 
   set((const void*)k_spmv_tma<true>, kProjSmemBudget + 1024);
 }
 
-const void* spmv_attr_kernel() { return (const void*)k_spmv_tile<false>; }
+// the default SpMV as launched for a real matrix with one lane per row (config 2)
+const void* spmv_attr_kernel() { return (const void*)k_spmv_ring<false, 1, 0, 16, 4>; }
 
 }  // namespace te
