@@ -1,3 +1,5 @@
+"""Print the compiled attributes (registers, threads, shared memory) of the hot-path kernels
+(te_kernel_attributes); needs a GPU."""
 import ctypes as C, sys
 sys.path.insert(0, '.')
 from paper_2205_15346_b200 import te
