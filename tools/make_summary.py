@@ -1,5 +1,5 @@
 """Collect bench.py JSON lines (gpurun_out/fin_*.log) into profiles/r01_bench_*.json and
-profiles/r01_summary.md.  Usage: python tools/make_summary.py [glob]"""
+profiles/r01_summary.md.  Usage: python tools/make_summary.py [glob | --from-profiles]"""
 import glob
 import json
 import os
@@ -21,7 +21,16 @@ def line_of(path):
 
 rows = {"cgs2": [], "lanczos3": [], "cgs2gram": []}
 ref = None
-for f in sorted(glob.glob(pat)):
+if pat == "--from-profiles":  # rebuild the summary from the committed bench lines
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r01_bench_*.json"))):
+        d = json.load(open(f))
+        if d.get("impl") == "reference":
+            ref = d
+            continue
+        cfg = int(os.path.basename(f).split("config")[1].split("_")[0].split(".")[0])
+        rows[d["config"]["ortho"]].append((cfg, d))
+else:
+  for f in sorted(glob.glob(pat)):
     d = line_of(f)
     if d is None:
         continue
