@@ -20,10 +20,10 @@ constexpr int kSpmvRows = 256;       // K1 row tile
 constexpr int kSpmvChunk = 4096;     // K1 products staged in shared memory per chunk
 constexpr int kSpmvTileNnz = 4096;   // entries per nnz-balanced SpMV tile (cap), real values
 constexpr int kSpmvTileNnzC = 2048;  // complex values (two pipelined blocks per SM)
-constexpr int kSpmvMaxTileRows = 256;
+constexpr int kSpmvMaxTileRows = 256;  // rows per pipelined-SpMV tile cap (kThreads / TPR)
 // warp-specialised ring SpMV tile capacities (entries) for its 4-stage and 3-stage layouts
 constexpr int kRingNnz4 = 4096, kRingNnzC4 = 2048;
-constexpr int kRingNnz3 = 5632, kRingNnzC3 = 2816;   // rows per SpMV tile cap (one thread per row)
+constexpr int kRingNnz3 = 5632, kRingNnzC3 = 2816;
 constexpr int kSellSigma = 4096;       // SELL-32-sigma sorting window (rows)
 constexpr int kAgCap = 1024;            // entries per async-gather SpMV tile (variant 5)
 constexpr int kAgMaxRows = 128;         // rows per async-gather tile cap (<= kThreads / TPR)
