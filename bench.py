@@ -36,11 +36,12 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=WORKLOAD_DEFAULT)
+    ap.add_argument("--config", type=int, default=WORKLOAD_DEFAULT,
+                    help="workload: 1-5 BASELINE.json configs (default 2, XXZ L=20), 6 the paper's P:527 benchmark")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=8)
-    ap.add_argument("--kernels", type=int, default=2, help="2 SpMV + shuffle projections, 3 SpMV + TMA projections, 0 fused register, 1 staged")
+    ap.add_argument("--kernels", type=int, default=2, help="projection kernels: 2 hybrid (shuffle up to 4-5 columns, TMA ring above; default), 3 TMA only, 4 shuffle only, 0 fused register, 1 staged")
     ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (library default if unset)")
     ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel: 7 warp-specialised ring (default), 4 pipelined, 6 SELL, 5 async gather, 3..0 older variants")
     ap.add_argument("--force-dist", action="store_true",
