@@ -8,8 +8,13 @@ value = Krylov steps (Arnoldi iterations of the global problem) / device time, m
 ranks, inputs resident in HBM (te_evolve_dev).  e2e = the same through te_evolve with host
 buffers (pinned), H2D of v0 and D2H of v(t) inside the timed region.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
   N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+         (run without WORLD_SIZE in the environment, bench.py re-launches itself that way)
+
+Default workload: BASELINE configs[4] (XXZ+NNN, L = 26, n = 2^26, 1.8e9 nnz), the largest
+configuration that fits one B200 and the one the north star's targets are stated on; configs[0]
+is the oracle-size case and the other configs are parity-test / --config cases.
 """
 from __future__ import annotations
 
@@ -28,7 +33,7 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-WORKLOAD_DEFAULT = 2  # BASELINE.json configs[1] (XXZ L=20); configs[0] is the oracle-size case
+WORKLOAD_DEFAULT = 5  # BASELINE.json configs[4] (XXZ+NNN L=26, n=2^26): largest single-GPU config
 
 
 def parse():
@@ -37,10 +42,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=WORKLOAD_DEFAULT,
-                    help="workload: 1-5 BASELINE.json configs (default 2, XXZ L=20), 6 the paper's P:527 benchmark")
+                    help="workload: 1-5 BASELINE.json configs (default 5, XXZ+NNN L=26), 6 the paper's P:527 benchmark")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-steps", type=int, default=8)
+    ap.add_argument("--cpu-sample-steps", type=int, default=None,
+                    help="oracle Krylov steps timed for cpu_baseline (default: 1 for n >= 2^24, else 8)")
+    ap.add_argument("--prof-steps", type=int, default=3, help="evolutions in the per-kernel (roofline) pass")
+    ap.add_argument("--e2e-steps", type=int, default=5, help="evolutions in the e2e (host buffers) pass")
     ap.add_argument("--kernels", type=int, default=2, help="projection kernels: 2 hybrid (shuffle up to 4-5 columns, TMA ring above; default), 3 TMA only, 4 shuffle only, 0 fused register, 1 staged")
     ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (library default if unset)")
     ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel: 7 warp-specialised ring (default), 4 pipelined, 6 SELL, 5 async gather, 3..0 older variants")
@@ -149,22 +157,44 @@ def build_workload(cfg, ws, rank):
 # ------------------------------------------------------------------------------------------
 # CPU baseline: the oracle as it stands, single thread, bounded sample
 # ------------------------------------------------------------------------------------------
-def oracle_sample(c, steps, warmup=0):
-    """Oracle Krylov steps at the mean basis size j = m/2 of the workload (cost per step is
-    linear in j, so this is the average restart step).  Setup (building the first j columns
-    with the oracle's own arnoldi) is untimed.  Returns (steps/s, seconds per step, sample)."""
+def step_bytes(n, nnz, val_bytes, j):
+    """SURVEY.md §8(d) analytic bytes of one Krylov step at basis size j: B_H + n (96 + 48 j)."""
+    return nnz * (val_bytes + 4) + 8 * (n + 1) + n * (96 + 48 * j)
+
+
+BIG = 1 << 24  # n at and above which the oracle's basis is a stand-in (configs 4, 5)
+
+
+def oracle_sample(c, steps, warmup=0, standin=None):
+    """The oracle as it stands (oracle.krylov.arnoldi_step, CGS2, 1 thread) timed for `steps` Krylov
+    steps at the mean basis size j = m/2 of the workload (the step cost is linear in j).  Setup is
+    untimed: for n < 2^24 the first j columns come from the oracle's own arnoldi; for the 2^24 and
+    2^26 configs the basis is a stand-in (every column = v0; the timing does not depend on the
+    values) because building it with the oracle would take j times the timed step.
+    Returns (steps/s, seconds per step, sample description, per-step times)."""
     from oracle import krylov as K
     m = c["m"]
     j = m // 2
+    n = c["n"]
     tol_rate = c["tol"] / c["t"]
 
     def mv(x):
         return K.spmv(c["rowptr"], c["col"], c["val"], x)
 
-    kr = K.arnoldi(mv, c["v0"], j + 1, tol_rate)
-    V = np.zeros((c["n"], j + 1), dtype=np.complex128)
-    V[:, : kr["V"].shape[1]] = kr["V"]
-    beta = kr["beta"]
+    if standin is None:
+        standin = n >= BIG
+    if standin:
+        V = np.empty((n, j + 1), dtype=np.complex128)
+        for k in range(j + 1):
+            V[:, k] = c["v0"]
+        beta = np.ones(j + 1)
+        basis = "stand-in basis (every column = v0)"
+    else:
+        kr = K.arnoldi(mv, c["v0"], j + 1, tol_rate)
+        V = np.zeros((n, j + 1), dtype=np.complex128)
+        V[:, : kr["V"].shape[1]] = kr["V"]
+        beta = kr["beta"]
+        basis = "basis from the oracle's arnoldi"
     times = []
     for it in range(warmup + steps):
         t0 = time.perf_counter()
@@ -172,10 +202,37 @@ def oracle_sample(c, steps, warmup=0):
         dt = time.perf_counter() - t0
         if it >= warmup:
             times.append(dt)
+    del V
     per = sum(times) / len(times)
-    sample = (f"{len(times)} oracle Arnoldi/CGS2 steps (oracle.krylov.arnoldi_step) at j={j} "
-              f"(mean basis size of an m={m} restart) on the full workload, 1 thread")
+    sample = (f"{len(times)} oracle Arnoldi/CGS2 step(s) (oracle.krylov.arnoldi_step) at j={j} (mean basis size "
+              f"of an m={m} restart) on the {c['name']} model at n={n}, nnz={int(c['rowptr'][-1])}, {basis}, 1 thread")
     return 1.0 / per, per, sample, times
+
+
+def oracle_ram_ok(c):
+    """The oracle's step at j = m/2 holds V (n (j+1) complex), its conjugate copy and the SpMV's
+    temporaries (rows int64, x[col] and the products, complex: 40 B per entry).  Returns
+    (fits, bytes needed, bytes available)."""
+    j = c["m"] // 2
+    need = 2 * 16 * c["n"] * (j + 1) + 40 * int(c["rowptr"][-1]) + 64 * c["n"]
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 0
+    return avail > 1.15 * need, need, avail
+
+
+def reduced_for_reference(cfg):
+    """The --impl reference arm times K oracle steps; at 2^24 / 2^26 rows one oracle step takes
+    minutes, so each step runs on the same model at 1/16 of the rows (config 4: n = 2^20; config 5:
+    L = 22) and the rate is scaled to the full workload by the §8(d) analytic bytes per step."""
+    from workloads import configs
+    if cfg == 5:
+        return configs.build(5, L=22)
+    if cfg == 4:
+        return configs.build(4, n=1 << 20)
+    return None
 
 
 def set_single_thread():
@@ -188,25 +245,63 @@ def set_single_thread():
         pass
 
 
+def config_dict(c, args, ws, nloc):
+    """The workload description shared by both arms (the driver compares them)."""
+    from workloads import configs
+    return {"workload": f"{c['name']} ({configs.LABELS[args.config]})", "n": c["n"],
+            "nnz": int(c["nnz"]), "m": c["m"], "t": c["t"], "tol": c["tol"],
+            "l2": "inputs larger than L2 (V = %.0f MB > 126 MB)" % (16 * nloc * c["m"] / 1e6),
+            "parallelism": f"rows{ws}", "kernels": ["fused-register", "staged", "hybrid", "tma", "shuffle"][args.kernels],
+            "spmv": {None: "ring (default)", 0: "csr-vector", 1: "tile", 2: "tma", 3: "rowtile", 4: "pipe",
+                     5: "async-gather", 6: "sell", 7: "ring"}[args.spmv],
+            "ortho": ["cgs2", "lanczos3", "cgs2gram"][args.ortho],
+            "halo": (["nccl_exchange", "peer_loads"][args.halo] if ws > 1 else None)}
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if ws > 1 and rank != 0:
         return 0
     set_single_thread()
     from workloads import configs
-    c = configs.build(args.config)
-    rate, per, sample, times = oracle_sample(c, args.steps, args.warmup)
+    c = configs.build(args.config, with_matrix=False)
+    c["nnz"] = full_nnz(args.config, c)
+    small = reduced_for_reference(args.config)
+    if small is None:
+        src = configs.build(args.config)
+        rate, per, sample, times = oracle_sample(src, args.steps, args.warmup)
+    else:
+        r_small, per_small, sample, times = oracle_sample(small, args.steps, args.warmup, standin=True)
+        j = c["m"] // 2
+        vb = 16 if np.iscomplexobj(small["val"]) else 8
+        ratio = step_bytes(small["n"], int(small["rowptr"][-1]), vb, j) / step_bytes(c["n"], c["nnz"], vb, j)
+        rate = r_small * ratio
+        per = 1.0 / rate
+        sample += (f"; scaled to the full workload (n={c['n']}) by the SURVEY §8(d) analytic bytes per step "
+                   f"(x{ratio:.4f}); extrapolated, the oracle at the full size needs minutes per step")
     line = {
         "impl": "reference", "metric": "Krylov steps/s", "value": rate, "unit": "krylov_steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
-        "data": "synthetic", "config": {"workload": f"{c['name']} ({configs.LABELS[args.config]})",
-                                        "n": c["n"], "nnz": int(c["rowptr"][-1]), "m": c["m"]},
+        "data": "synthetic", "config": config_dict(c, args, args.gpus, c["n"] // max(1, args.gpus)),
         "cpu_baseline": {"value": rate, "unit": "krylov_steps/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": rate, "unit": "krylov_steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
     return 0
+
+
+def full_nnz(cfg, c):
+    """nnz of the full workload without building it where a closed form exists."""
+    if "rowptr" in c:
+        return int(c["rowptr"][-1])
+    p = c["params"]
+    if cfg == 5:
+        return (1 << p["L"]) * (1 + p["L"])
+    if cfg == 2:
+        return (1 << p["L"]) * (1 + p["L"] // 2)
+    from workloads import configs
+    return int(configs.build(cfg)["rowptr"][-1])
 
 
 # ------------------------------------------------------------------------------------------
@@ -233,6 +328,7 @@ def run_ours(args):
     dev = torch.device("cuda", local if ws > 1 else 0)
 
     c, rb, re_ = build_workload(args.config, ws, rank)
+    c["nnz"] = full_nnz(args.config, c)
     n_glob, nloc = c["n"], re_ - rb
     t, tol, m = c["t"], c["tol"], c["m"]
     D = None
@@ -304,8 +400,9 @@ def run_ours(args):
     torch.cuda.synchronize()
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
+    prof_steps = max(1, min(args.steps, args.prof_steps))
     p0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(prof_steps):
         one_step()
     p1.record(stream)
     torch.cuda.synchronize()
@@ -319,9 +416,10 @@ def run_ours(args):
     v0n, outn = hv0.numpy(), hout.numpy()
     te.te_evolve(h, v0n, t, tol, m, out=outn)
     barrier()
+    e2e_n = max(1, min(args.steps, args.e2e_steps))
     w0 = time.perf_counter()
     e2e_steps = 0
-    for _ in range(args.steps):
+    for _ in range(e2e_n):
         _, st2 = te.te_evolve(h, v0n, t, tol, m, out=outn)
         e2e_steps += st2["n_krylov_steps"]
     w1 = time.perf_counter()
@@ -356,20 +454,12 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic",
-        "config": {"workload": f"{c['name']} ({configs.LABELS[args.config]})", "n": n_glob,
-                   "nnz": int(c["rowptr"][-1]) if "rowptr" in c else None, "m": m, "t": t, "tol": tol,
-                   "krylov_steps_per_step": ksteps / args.steps,
-                   "restarts_per_step": stats[-1]["n_restarts"],
-                   "l2": "inputs larger than L2 (V = %.0f MB > 126 MB)" % (16 * nloc * m / 1e6),
-                   "parallelism": f"rows{ws}", "kernels": ["fused-register", "staged", "hybrid", "tma", "shuffle"][args.kernels],
-                   "prefetch": args.prefetch,
-                   "spmv": {None: "ring (default)", 0: "csr-vector", 1: "tile", 2: "tma", 3: "rowtile", 4: "pipe",
-                            5: "async-gather", 6: "sell", 7: "ring"}[args.spmv],
-                   "ortho": ["cgs2", "lanczos3", "cgs2gram"][args.ortho],
-                   "halo": ["nccl_exchange", "peer_loads"][args.halo] if ws > 1 else None},
+        "config": config_dict(c, args, ws, nloc),
+        "krylov_steps_per_step": ksteps / args.steps,
+        "restarts_per_step": stats[-1]["n_restarts"],
         "achieved_hbm_gbs": all_bytes / (all_ms * 1e-3) / 1e9 if all_ms > 0 else None,
         "step_hbm_gbs": all_bytes / (ms * 1e-3) / 1e9,
-        "profiled_region_ms_per_step": ms_prof / args.steps,
+        "profiled_region_ms_per_step": ms_prof / prof_steps,
         "evolved_time_per_s": t * args.steps / (ms * 1e-3),
         **({"paper_context": {"paper_wall_s": 353.0, "paper_hw": "i9-9900K, 1 thread (P:527-529)",
                               "ours_wall_s": ms / args.steps * 1e-3,
@@ -380,20 +470,36 @@ def run_ours(args):
                      "alg_bytes_per_launch": p["alg_bytes"] / p["launches"],
                      "avg_launch_ms": p["total_ms"] / p["launches"],
                      "share_of_kernel_time": p["total_ms"] / all_ms if all_ms else None,
-                     "timing": "CUDA events around every launch of a second timed pass of the same K steps "
-                               "(direct launches; the headline pass replays CUDA graphs)"},
+                     "timing": f"CUDA events on the launching stream around every launch of a second timed pass "
+                               f"of {prof_steps} of the same steps (direct launches; the headline pass replays CUDA "
+                               f"graphs)"},
         "kernels": {k: {"launches": prof[k]["launches"], "ms": prof[k]["total_ms"],
                         "gbs": (prof[k]["alg_bytes"] / (prof[k]["total_ms"] * 1e-3) / 1e9) if prof[k]["total_ms"] else None}
                     for k in prof if prof[k]["launches"]},
         "e2e": {"value": e2e_steps / e2e_s, "unit": "krylov_steps/s", "h2d_bytes_per_step": 16 * nloc,
-                "d2h_bytes_per_step": 16 * nloc, "timing": "wall clock around te_evolve (host buffers, pinned)"},
+                "d2h_bytes_per_step": 16 * nloc, "steps": e2e_n,
+                "timing": "wall clock around te_evolve (host buffers, pinned), max over ranks"},
         "gpu_launches": launches,
         "clocks": clocks,
         "err_bound": stats[-1]["err_bound"],
     }
     if not args.no_cpu_baseline and ws == 1:
         set_single_thread()
-        rate, per, sample, _ = oracle_sample(c, args.cpu_sample_steps)
+        h.close()
+        torch.cuda.empty_cache()
+        steps = args.cpu_sample_steps or (1 if c["n"] >= BIG else 8)
+        fits, need, avail = oracle_ram_ok(c)
+        if fits:
+            rate, per, sample, _ = oracle_sample(c, steps)
+        else:  # not enough host RAM for the oracle's temporaries at this size: same model, 1/16 rows
+            small = reduced_for_reference(args.config)
+            r_small, _, sample, _ = oracle_sample(small, steps, standin=True)
+            j = c["m"] // 2
+            vb = 16 if np.iscomplexobj(small["val"]) else 8
+            ratio = step_bytes(small["n"], int(small["rowptr"][-1]), vb, j) / step_bytes(c["n"], c["nnz"], vb, j)
+            rate = r_small * ratio
+            sample += (f"; scaled to n={c['n']} by the §8(d) bytes per step (x{ratio:.4f}): host RAM "
+                       f"{avail / 1e9:.0f} GB < {need / 1e9:.0f} GB the full-size oracle step needs")
         line["cpu_baseline"] = {"value": rate, "unit": "krylov_steps/s", "cores": 1, "kind": "oracle",
                                 "sample": sample}
     print(json.dumps(line))
@@ -405,10 +511,37 @@ def run_ours(args):
     return 0
 
 
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args):
+    """--gpus N > 1 without a torch.distributed environment: re-run this command as N ranks (one
+    process per GPU) under torch.distributed.run on this node; rank 0 prints the JSON line.  Fails
+    loudly when fewer than N GPUs are visible (a 1-GPU timing must never pass as N GPUs)."""
+    import torch
+    have = torch.cuda.device_count() if args.impl == "ours" else args.gpus
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) visible\n")
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
+    ws = dist_env()[0]
+    if ws != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}\n")
+        return 2
     return run_ours(args)
 
 

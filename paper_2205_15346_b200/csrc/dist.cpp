@@ -21,6 +21,7 @@ int te_internal_setup_halo(te_handle* h, int64_t n_halo, const std::vector<int64
 int te_internal_set_error(int code, const char* msg);
 cudaStream_t te_internal_stream(te_handle* h);
 double te_internal_local_norm1(te_handle* h);
+void te_internal_set_norm1(te_handle* h, double v);
 ncclComm_t te_internal_comm(te_dist* d);
 int te_internal_nranks(te_dist* d);
 int te_internal_rank(te_dist* d);
@@ -210,9 +211,15 @@ extern "C" te_handle* te_create_csr_dist(te_dist* d, int64_t n_global, int64_t r
                                d, n_loc + n_halo);
   if (!h && P == 1) goto fail;
   {
-    // 6. ||H||_1 = max over all rows of the row abs sums (allreduce max), together with a
-    //    "local create failed" flag so that a failure on one rank fails every rank
-    double nv[2] = {h ? te_internal_local_norm1(h) : 0.0, h ? 0.0 : 1.0};
+    // 6. halo buffers and peer tables first (their allocations can fail too), then
+    //    ||H||_1 = max over all rows of the row abs sums (allreduce max), together with a
+    //    "local setup failed" flag, so that a failure on one rank fails every rank
+    bool local_ok = h != nullptr;
+    const double norm_loc = h ? te_internal_local_norm1(h) : 0.0;
+    if (local_ok &&
+        te_internal_setup_halo(h, n_halo, recv_counts, send_counts, send_idx, norm_loc, halo, row_starts) != TE_OK)
+      local_ok = false;
+    double nv[2] = {norm_loc, local_ok ? 0.0 : 1.0};
     if (P > 1) {
       double* dn = reinterpret_cast<double*>(dbuf);
       DCK(cudaMemcpy(dn, nv, sizeof nv, cudaMemcpyHostToDevice));
@@ -220,13 +227,12 @@ extern "C" te_handle* te_create_csr_dist(te_dist* d, int64_t n_global, int64_t r
       DCK(cudaStreamSynchronize(st));
       DCK(cudaMemcpy(nv, dn, sizeof nv, cudaMemcpyDeviceToHost));
     }
-    if (!h) goto fail;  // own error already set by te_internal_create_local
+    if (!local_ok) goto fail;  // own error already set by te_internal_create_local / setup_halo
     if (nv[1] != 0.0) {
-      te_internal_set_error(TE_ERR_CSR, "te_create_csr_dist: local handle creation failed on another rank");
+      te_internal_set_error(TE_ERR_CSR, "te_create_csr_dist: local handle setup failed on another rank");
       goto fail;
     }
-    if (te_internal_setup_halo(h, n_halo, recv_counts, send_counts, send_idx, nv[0], halo, row_starts) != TE_OK)
-      goto fail;
+    te_internal_set_norm1(h, nv[0]);
   }
   cudaFree(dbuf);
   cudaStreamDestroy(st);

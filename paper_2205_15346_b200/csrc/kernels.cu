@@ -1074,7 +1074,9 @@ __global__ void k_restart_init(KDev d) {
 // --------------------------------------------------------------------------------------
 // K4: w = sum_k V_k coef_k (coef_k = s_k omega_k), in place into column 0 (Eq. 11)
 // --------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_combine(const double2* __restrict__ Vbase, int64_t n, int64_t ldv,
+// out may alias column 0 of V (in place): no __restrict__ on either pointer; each thread reads its
+// row of every column before it writes that row
+__global__ void __launch_bounds__(kThreads) k_combine(const double2* Vbase, int64_t n, int64_t ldv,
                                                       const double2* __restrict__ coefg, int m_eff, double2* out) {
   __shared__ double2 coef[kMaxCols];
   if (threadIdx.x < m_eff) coef[threadIdx.x] = coefg[threadIdx.x];

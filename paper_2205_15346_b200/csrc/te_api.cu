@@ -155,7 +155,7 @@ struct te_handle {
   bool use_graph = true;
   bool capturing = false;
   cudaGraphExec_t gexec = nullptr;
-  int g_m = -1, g_variant = -1, g_spmv = -1, g_ortho = -1;
+  int g_m = -1, g_variant = -1, g_spmv = -1, g_ortho = -1, g_prefetch = -1, g_halo = -1;
   bool g_profile = false;
   double g_tol_rate = -1.0;
   const void* g_V = nullptr;
@@ -270,6 +270,10 @@ int free_workspace(te_handle* h) {
   h->d_V = nullptr;
   h->d_W = nullptr;
   h->m_cap = 0;
+  // the peer table described the freed V: every rank reallocates V at the same call (same m_max,
+  // collective evolve), so every rank re-runs the collective setup_peers before its next restart,
+  // even when cudaMalloc hands back the same address
+  h->peer_for_V = nullptr;
   return TE_OK;
 }
 
@@ -581,7 +585,7 @@ int run_arnoldi(te_handle* h, int m, double tol_rate) {
     return TE_OK;
   }
   const bool hit = h->gexec && h->g_m == m && h->g_tol_rate == tol_rate && h->g_variant == h->variant &&
-                   h->g_ortho == h->ortho &&
+                   h->g_ortho == h->ortho && h->g_prefetch == h->prefetch && h->g_halo == h->halo_mode &&
                    h->g_spmv == h->spmv_tiled && h->g_profile == h->profile && h->g_V == (const void*)h->d_V;
   if (!hit) {
     if (h->gexec) {
@@ -624,6 +628,8 @@ int run_arnoldi(te_handle* h, int m, double tol_rate) {
     h->g_variant = h->variant;
     h->g_spmv = h->spmv_tiled;
     h->g_ortho = h->ortho;
+    h->g_prefetch = h->prefetch;
+    h->g_halo = h->halo_mode;
     h->g_profile = h->profile;
     h->g_V = h->d_V;
   }
@@ -1428,3 +1434,4 @@ int te_internal_setup_halo(te_handle* h, int64_t n_halo, const std::vector<int64
 int te_internal_set_error(int code, const char* msg) { return set_err(code, "%s", msg); }
 cudaStream_t te_internal_stream(te_handle* h) { return h->own_stream; }
 double te_internal_local_norm1(te_handle* h) { return h->norm1; }
+void te_internal_set_norm1(te_handle* h, double v) { h->norm1 = v; }

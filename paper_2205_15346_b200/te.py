@@ -123,6 +123,47 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
 
+def _vec_in(v, n: int, what: str) -> np.ndarray:
+    """Host input vector: converted to contiguous complex128; must hold exactly n entries."""
+    v = np.ascontiguousarray(v, dtype=np.complex128)
+    if v.shape != (n,):
+        raise ValueError(f"{what}: expected shape ({n},), got {v.shape}")
+    return v
+
+
+def _vec_out(out, n: int, what: str) -> np.ndarray:
+    """Caller-supplied host output: must be a writeable C-contiguous complex128 array of n entries
+    (the library writes exactly n * 16 bytes into it)."""
+    if out is None:
+        return np.empty(n, dtype=np.complex128)
+    if not isinstance(out, np.ndarray) or out.dtype != np.complex128 or out.shape != (n,) \
+            or not out.flags.c_contiguous or not out.flags.writeable:
+        raise ValueError(f"{what}: expected a writeable C-contiguous complex128 array of shape ({n},)")
+    return out
+
+
+def _dev_ptr(t, n: int, what: str) -> int:
+    """Device vector: a CUDA tensor (complex128, contiguous, n entries) or a raw device pointer
+    (unchecked: the caller guarantees n complex128 entries)."""
+    if hasattr(t, "data_ptr"):
+        import torch
+        if not t.is_cuda or t.dtype != torch.complex128 or t.numel() != n or not t.is_contiguous():
+            raise ValueError(f"{what}: expected a contiguous complex128 CUDA tensor of {n} entries, got "
+                             f"{t.dtype} numel={t.numel()} cuda={t.is_cuda} contiguous={t.is_contiguous()}")
+        return t.data_ptr()
+    return int(t)
+
+
+def _csr_in(n: int, rowptr, col, val):
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    if rowptr.shape != (int(n) + 1,):
+        raise ValueError(f"rowptr: expected shape ({int(n) + 1},), got {rowptr.shape}")
+    nnz = int(rowptr[-1]) if rowptr.shape[0] else 0
+    if np.shape(col)[0] < nnz or np.shape(val)[0] < nnz:
+        raise ValueError(f"col/val hold fewer than rowptr[-1] = {nnz} entries")
+    return rowptr
+
+
 class Handle:
     """Owns a te_handle*; te_destroy on close()/GC."""
 
@@ -146,7 +187,7 @@ class Handle:
 
 def te_create_csr(n, rowptr, col, val) -> Handle:
     L = load()
-    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    rowptr = _csr_in(n, rowptr, col, val)
     col = np.ascontiguousarray(col, dtype=np.int32)
     if np.iscomplexobj(val):
         val = np.ascontiguousarray(val, dtype=np.complex128)
@@ -165,8 +206,8 @@ def te_destroy(h: Handle):
 
 def te_evolve(h: Handle, v0, t, tol, m_max, out=None):
     L = load()
-    v0 = np.ascontiguousarray(v0, dtype=np.complex128)
-    vo = np.empty_like(v0) if out is None else out
+    v0 = _vec_in(v0, h.n, "v0")
+    vo = _vec_out(out, h.n, "out")
     st = Stats()
     _check(L, L.te_evolve(h.ptr, _ptr(v0), float(t), float(tol), int(m_max), _ptr(vo), C.byref(st)))
     return vo, st.as_dict()
@@ -175,8 +216,8 @@ def te_evolve(h: Handle, v0, t, tol, m_max, out=None):
 def te_evolve_dev(h: Handle, d_v0, t, tol, m_max, d_vout, stream=None):
     """d_v0 / d_vout: CUDA tensors (complex128, contiguous) or raw device pointers."""
     L = load()
-    p0 = d_v0.data_ptr() if hasattr(d_v0, "data_ptr") else int(d_v0)
-    p1 = d_vout.data_ptr() if hasattr(d_vout, "data_ptr") else int(d_vout)
+    p0 = _dev_ptr(d_v0, h.n, "d_v0")
+    p1 = _dev_ptr(d_vout, h.n, "d_vout")
     s = None
     if stream is not None:
         s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
@@ -188,7 +229,7 @@ def te_evolve_dev(h: Handle, d_v0, t, tol, m_max, d_vout, stream=None):
 
 def te_evolve_schedule(h: Handle, v0, t_steps, tol, m_max):
     L = load()
-    v0 = np.ascontiguousarray(v0, dtype=np.complex128)
+    v0 = _vec_in(v0, h.n, "v0")
     ts = np.ascontiguousarray(t_steps, dtype=np.float64)
     vo = np.empty_like(v0)
     st = Stats()
@@ -200,7 +241,7 @@ def te_evolve_schedule(h: Handle, v0, t_steps, tol, m_max):
 def te_evolve_sampled(h: Handle, v0, t, tol, m_max, sample_times):
     """Returns (v(t), samples [n_samples x n], sample_bounds, stats)."""
     L = load()
-    v0 = np.ascontiguousarray(v0, dtype=np.complex128)
+    v0 = _vec_in(v0, h.n, "v0")
     ts = np.ascontiguousarray(sample_times, dtype=np.float64)
     out = np.zeros((ts.shape[0], v0.shape[0]), dtype=np.complex128)
     sb = np.zeros(ts.shape[0])
@@ -223,7 +264,7 @@ def te_get_schedule(h: Handle):
 
 def te_krylov_basis(h: Handle, v1, m, tol_rate, want_V=True):
     L = load()
-    v1 = np.ascontiguousarray(v1, dtype=np.complex128)
+    v1 = _vec_in(v1, h.n, "v1")
     a = np.zeros(m)
     b = np.zeros(m)
     me = C.c_int(0)
@@ -295,7 +336,7 @@ def te_dist_init(nranks: int, rank: int, uid: bytes) -> Dist:
 
 def te_create_csr_dist(d: Dist, n_global, row_begin, row_end, rowptr_local, col_global, val) -> Handle:
     L = load()
-    rp = np.ascontiguousarray(rowptr_local, dtype=np.int64)
+    rp = _csr_in(int(row_end) - int(row_begin), rowptr_local, col_global, val)
     cg = np.ascontiguousarray(col_global, dtype=np.int64)
     cplx = np.iscomplexobj(val)
     v = np.ascontiguousarray(val, dtype=np.complex128 if cplx else np.float64)

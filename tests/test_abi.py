@@ -86,3 +86,36 @@ def test_halo_plan_bit_exact(lib, P):
 def test_halo_plan_rejects_out_of_range(lib):
     with pytest.raises(te.TEError):
         te.te_halo_plan(2, 0, np.array([0, 4, 8]), np.array([0, 9], dtype=np.int64))
+
+
+def test_binding_rejects_bad_buffers_before_the_c_call(lib):
+    """The binding checks every buffer it hands to C (the library copies n * 16 bytes each way):
+    wrong length, dtype, strides or a read-only output raise ValueError before any C call, so a
+    short vector can never be read or written past its end."""
+    h = te.Handle(None, 4, True)  # never reaches C: validation comes first
+    good = np.zeros(4, dtype=np.complex128)
+    good[0] = 1
+    with pytest.raises(ValueError):
+        te.te_evolve(h, np.zeros(3, complex), 1.0, 1e-8, 4)
+    for out in (np.zeros(4), np.zeros(3, complex), np.zeros(8, complex)[::2], np.zeros((2, 2), complex)):
+        with pytest.raises(ValueError):
+            te.te_evolve(h, good, 1.0, 1e-8, 4, out=out)
+    ro = np.zeros(4, complex)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        te.te_evolve(h, good, 1.0, 1e-8, 4, out=ro)
+    with pytest.raises(ValueError):
+        te.te_evolve_schedule(h, np.zeros(5, complex), [0.1], 1e-8, 4)
+    with pytest.raises(ValueError):
+        te.te_evolve_sampled(h, np.zeros(2, complex), 1.0, 1e-8, 4, [0.5])
+    with pytest.raises(ValueError):
+        te.te_krylov_basis(h, np.zeros(6, complex), 3, 1e-9)
+    import torch
+    for bad in (torch.zeros(4, dtype=torch.complex64), torch.zeros(4, dtype=torch.complex128),  # not on CUDA
+                torch.zeros(5, dtype=torch.complex128)):
+        with pytest.raises(ValueError):
+            te.te_evolve_dev(h, bad, 1.0, 1e-8, 4, bad)
+    with pytest.raises(ValueError):
+        te.te_create_csr(2, np.array([0, 1]), np.array([1, 0]), np.array([1.0, 1.0]))      # rowptr too short
+    with pytest.raises(ValueError):
+        te.te_create_csr(2, np.array([0, 1, 3]), np.array([1, 0]), np.array([1.0, 1.0]))   # col shorter than nnz

@@ -51,6 +51,9 @@ def worker(r):
         h = te.te_create_csr_dist(D, n, rb, re_, (rp[rb:re_ + 1] - rp[rb]).astype(np.int64),
                                   col[rp[rb]:rp[re_]].astype(np.int64), val[rp[rb]:rp[re_]])
         te.te_set_option(h, te.TE_OPT_HALO, halo_mode)
+        # a first evolution with a smaller basis: the m = 16 calls below reallocate V, and every
+        # rank must rebuild its peer table (halo mode 1) even if cudaMalloc returns the same address
+        te.te_evolve(h, v0[rb:re_], 0.2, tol, 8)
         g = te.te_krylov_basis(h, v0[rb:re_], m, tol_rate, want_V=True)
         vf = None
         if sched is not None:

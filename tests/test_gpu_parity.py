@@ -541,6 +541,40 @@ def test_full_size_config5_xxz_nnn_L26(gpu_lib):
     assert np.abs(w1 - w0).max() <= 2 * st["err_bound"] + 1e-9
 
 
+def _forced_wrap_parity(te, c, sched, m, ring_min_wraps=4):
+    """Forced-schedule evolution vs the oracle element by element (<= 1e-10, north star) at a
+    size where every CTA of the ring SpMV takes many tiles (the ring wraps, the mbarrier phase
+    flips many times).  The SpMV instantiation (value type, lanes per row, ring depth) depends only
+    on the value type and the mean row length, so it is the one the full-size config launches."""
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    v, st = te.te_evolve_schedule(h, c["v0"], sched, c["tol"], m)
+    h.close()
+    ref = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], float(sum(sched)), c["tol"], m, schedule=sched)
+    tiles_per_cta = c["rowptr"][-1] / (5632 if c["val"].dtype == np.float64 else 2816) / 148
+    assert tiles_per_cta >= ring_min_wraps * 4
+    assert [s[1] for s in ref["schedule"]] == [m] * len(sched)
+    err = np.linalg.norm(v - ref["v"])
+    assert err <= 1e-10, err
+    assert st["n_krylov_steps"] == ref["krylov_steps"]
+    return err
+
+
+def test_forced_parity_complex_ring_wraps_config4_n2e20(gpu_lib):
+    """Complex H through the ring SpMV at a wrapping size: config 4's model at n = 2^20 (32
+    complex entries per row, the k_spmv_ring<complex, TPR 4, 3 stages> instantiation of the full
+    2^24 config), m = 8, two forced restarts, element by element against the oracle."""
+    c = configs.build(4, n=1 << 20)
+    _forced_wrap_parity(gpu_lib, c, [0.05, 0.05], 8)
+
+
+def test_forced_parity_config5_instantiation_L22(gpu_lib):
+    """Config 5's model at L = 22 (n = 4,194,304, 23 entries per row on average: the TPR 2 /
+    3-stage real ring instantiation of the full L = 26 config), m = 10, one forced restart,
+    element by element against the oracle."""
+    c = configs.build(5, L=22)
+    _forced_wrap_parity(gpu_lib, c, [0.1], 10)
+
+
 def test_distributed_api_single_rank(gpu_lib):
     """te_dist_init / te_create_csr_dist on one rank (global columns, halo plan, no NCCL
     traffic) gives the same evolution as the plain handle."""

@@ -224,6 +224,107 @@ def test_error_integral_2x2_closed_form():
     assert abs(v - exact) <= 1e-12
 
 
+def _count_calls(f):
+    calls = [0]
+
+    def g(x):
+        calls[0] += np.size(x)
+        return f(x)
+    return g, calls
+
+
+def test_error_integral_floor_o5a_2x2_closed_form():
+    """Reading O-5a: the stop test |I_k - I_{k-1}| <= 1e-3 max(|I_k|, floor) with
+    floor = tol_rate (b - a).  Pinned on the closed-form 2x2 error integral
+    h |b| (1 - cos Om tau) / Om^2 (Eq. 16; P:406's relative 1e-3 test):
+      * floor active (tol_rate tau >> exact): |I - exact| <= 1e-3 tol_rate tau, and the rule stops
+        at level 2 (29 nodes: 7 + 8 + 14), where the pure relative test refines further;
+      * floor inactive (tol_rate tau << exact): the relative 1e-3 accuracy of P:406 is kept;
+      * the floor scales with (b - a): the same tol_rate on a 100x longer interval is inactive
+        again for an integral that grows like tau^2."""
+    a, b, c, h = 0.1, 0.9, 0.4, 0.6
+    lam, U = K.small_eig(np.array([a, c]), np.array([b, 0.0]))
+    Om = math.sqrt(((a - c) / 2) ** 2 + b ** 2)
+
+    def exact(t):
+        return h * abs(b) * (1 - math.cos(Om * t)) / Om ** 2
+
+    f = lambda x: K.integrand(lam, U, h, x)  # noqa: E731
+    # floor active
+    tau, tol_rate = 1e-4, 1e-3
+    assert tol_rate * tau > 10 * exact(tau)
+    g, calls = _count_calls(f)
+    v, ok = K.tanh_sinh(g, 0.0, tau, floor=tol_rate * tau)
+    assert ok and abs(v - exact(tau)) <= 1e-3 * max(exact(tau), tol_rate * tau)
+    assert calls[0] == 29
+    g0, calls0 = _count_calls(f)
+    v0, ok0 = K.tanh_sinh(g0, 0.0, tau)
+    assert ok0 and abs(v0 - exact(tau)) <= 1e-3 * exact(tau)
+    assert calls0[0] >= calls[0]
+    # floor inactive: same result as the plain relative test
+    tau2, tol_rate2 = 0.9 * math.pi / Om, 1e-9
+    assert tol_rate2 * tau2 < 1e-3 * exact(tau2)
+    v2, ok2 = K.tanh_sinh(f, 0.0, tau2, floor=tol_rate2 * tau2)
+    v2r, _ = K.tanh_sinh(f, 0.0, tau2)
+    assert ok2 and abs(v2 - exact(tau2)) <= 1e-3 * exact(tau2) and v2 == v2r
+    # sub-interval [tau, tau + s] (the step search's substep pieces): floor tol_rate * s
+    t0, s = 0.5, 0.05
+    piece = exact(t0 + s) - exact(t0)
+    v3, ok3 = K.tanh_sinh(f, t0, t0 + s, floor=1e-2 * s)
+    assert ok3 and abs(v3 - piece) <= 1e-3 * max(piece, 1e-2 * s)
+
+
+def test_error_integral_floor_o5a_roundoff_regime():
+    """The regime O-5a exists for: for m = 10 and small tau the true integrand is
+    h prod(beta) tau^(m-1)/(m-1)! + O(tau^m) (leading Taylor term of e_m^T exp(-iT tau) e_1 for a
+    tridiagonal T), far below the roundoff noise h m eps of the eigendecomposition formula.  With
+    the floor the rule converges at level 2 and returns the integral within 1e-3 tol_rate tau of
+    the true value h prod(beta) tau^m / m!; the evolution's own calls (evolve -> find_step) pass
+    the same floor, checked through the 29-node count of a first-restart integral."""
+    g = np.random.default_rng(5)
+    m = 10
+    alpha = g.standard_normal(m)
+    beta = np.abs(g.standard_normal(m)) + 0.5
+    lam, U = K.small_eig(alpha, beta[: m - 1])
+    h = beta[m - 1]
+    tau, tol_rate = 1e-3, 1e-11
+    true = h * float(np.prod(beta[: m - 1])) * tau ** m / math.factorial(m)
+    assert true < 1e-30
+    f = lambda x: K.integrand(lam, U, h, x)  # noqa: E731
+    gf, calls = _count_calls(f)
+    v, ok = K.tanh_sinh(gf, 0.0, tau, floor=tol_rate * tau)
+    assert ok and calls[0] == 29
+    assert abs(v - true) <= 1e-3 * max(true, tol_rate * tau)
+    # without the floor the relative test chases the noise through many more levels
+    gf0, calls0 = _count_calls(f)
+    K.tanh_sinh(gf0, 0.0, tau)
+    assert calls0[0] > 4 * calls[0]
+
+
+def test_evolve_first_step_error_matches_closed_form():
+    """The ledger entry of the first restart of an m = 2 evolution on a 3x3 Hermitian H from e_1
+    equals the closed-form 2x2 error integral (Eq. 16; T = [[a, b], [b, c]] built by hand from H:
+    a = H_00, b = ||H e_0 - a e_0||, v_1 = (H e_0 - a e_0)/b, c = v_1^H H v_1, h = ||H v_1 - c v_1
+    - b e_0||) within the O-5a tolerance 1e-3 max(e, tol_rate tau) — so evolve passes the floor as
+    tol_rate (b - a) and integrates [0, tau] (a wrong floor scale or interval shows here)."""
+    H = np.array([[0.3, 0.5 - 0.2j, 0.1j], [0.5 + 0.2j, -0.4, 0.25], [-0.1j, 0.25, 0.7]])
+    e0 = np.array([1.0, 0.0, 0.0], dtype=np.complex128)
+    a = H[0, 0].real
+    r = H @ e0 - a * e0
+    b = np.linalg.norm(r)
+    v1 = r / b
+    c = np.vdot(v1, H @ v1).real
+    hh = np.linalg.norm(H @ v1 - c * v1 - b * e0)
+    Om = math.sqrt(((a - c) / 2) ** 2 + b ** 2)
+    rp, col, val = csr_from_dense(H)
+    for t, tol in [(0.5, 1e-3), (0.5, 1e-6), (2.0, 1e-2)]:
+        res = K.evolve(rp, col, val, e0, t, tol, 2)
+        tau, m_eff, e = res["schedule"][0]
+        assert m_eff == 2 and Om * tau <= math.pi
+        ex = hh * abs(b) * (1 - math.cos(Om * tau)) / Om ** 2
+        assert abs(e - ex) <= 1e-3 * max(ex, tol / t * tau)
+
+
 def test_error_integral_against_mpmath_quad():
     g = np.random.default_rng(13)
     a, b = g.standard_normal(10), np.abs(g.standard_normal(10)) + 0.1

@@ -29,6 +29,48 @@ def test_closed_form_sizes():
     assert int(np.nonzero(c["v0"])[0][0]) == int(np.searchsorted(models.bh_keys(occ), models.bh_keys(np.ones((1, 6), np.uint8))[0]))
 
 
+def test_full_size_closed_forms():
+    """BASELINE sizes, integer setup bit-exact against closed forms (SURVEY.md App. A,
+    north_star "Integer setup ... must be bit-exact"):
+      config 2  XXZ L=20:     nnz = 2^L (1 + L/2) = 11,534,336;  Neel (even sites up) -> 349,525
+      config 5  XXZ+NNN L=26: nnz = 2^L (1 + L)   = 1,811,939,328 (C rowptr builder, all rows)
+      config 3  BH L=N=12:    d = C(23,12) = 1,352,078;  nnz = d (1 + 2 (L-1) N/(N+L-1)) =
+                              16,871,582;  |1,...,1> -> 873,885;  first (0,..,0,12), last (12,0,..,0)."""
+    assert models.neel_index(20) == 349525 == sum(1 << i for i in range(0, 20, 2))
+    lib = fast._load()
+    for L, J2, nnz in [(20, 0.0, 11534336), (26, 0.5, 1811939328)]:
+        n = 1 << L
+        rp = np.empty(n + 1, dtype=np.int64)
+        lib.xxz_rowptr(L, 1.0, J2, 0, n, rp.ctypes.data)
+        assert rp[0] == 0 and int(rp[-1]) == nnz
+        assert nnz == (1 << L) * (1 + (L if J2 else L // 2))
+        del rp
+    c = configs.build(3)
+    d = math.comb(23, 12)
+    assert c["n"] == d == 1352078
+    assert int(c["rowptr"][-1]) == 16871582 == d * (23 + 2 * 11 * 12) // 23
+    assert int(np.nonzero(c["v0"])[0][0]) == 873885
+    assert tuple(c["occ"][0]) == (0,) * 11 + (12,) and tuple(c["occ"][-1]) == (12,) + (0,) * 11
+
+
+def test_bh_hash_index_map_bit_exact():
+    """The hash-table ind^-1 and the sorted-key search give bit-identical Bose-Hubbard CSR
+    arrays at the full config-3 size, and the table round-trips every basis key (exhaustive,
+    SURVEY §8(c) BH pin) and rejects keys outside the sector."""
+    L, N = 12, 12
+    mu = models.bh_mu(L, 3)
+    a = models.bose_hubbard_csr(L, N, 1.0, 2.0, mu, index="search")
+    b = models.bose_hubbard_csr(L, N, 1.0, 2.0, mu, index="hash")
+    for x, y in zip(a, b):
+        assert x.dtype == y.dtype and np.array_equal(x.view(np.uint8), y.view(np.uint8))
+    keys = models.bh_keys(a[0])
+    T = models.BHIndexHash(keys)
+    assert T.slot_key.shape[0] == 1 << 22
+    assert np.array_equal(T.lookup(keys), np.arange(keys.shape[0]))
+    bad = keys[:1000] + 1  # sum of occupations N+1: not in the fixed-N sector
+    assert np.all(T.lookup(bad) == -1)
+
+
 def test_hermitian_and_sorted():
     import scipy.sparse as sp
     for c in (configs.build(1, n=512), configs.build(4, n=4096), configs.build(3, L=5, N=5), configs.build(5, L=9)):

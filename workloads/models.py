@@ -178,23 +178,81 @@ def bh_keys(occ: np.ndarray) -> np.ndarray:
     return k
 
 
+class BHIndexHash:
+    """ind^-1 of the Bose-Hubbard basis as an open-addressing hash table (TimeEvolver
+    indexes its basis with a hash map): slot = splitmix64 finaliser of
+    the 48-bit occupation key, masked to a power-of-two capacity (2^22 for d = 1,352,078, load
+    0.32), linear probing.  Built and queried with vectorised probe rounds (every still-unplaced
+    key tries its next slot; the lowest basis index wins a contested empty slot, so the layout is
+    deterministic).  Independent of ``searchsorted``;
+    tests/test_workloads.py checks the two give bit-identical CSR arrays."""
+
+    EMPTY = np.int64(-1)
+
+    def __init__(self, keys: np.ndarray, capacity: int | None = None):
+        d = keys.shape[0]
+        cap = capacity or (1 << max(4, int(math.ceil(math.log2(max(2, 3 * d))))))
+        assert cap & (cap - 1) == 0 and cap > d
+        self.mask = np.uint64(cap - 1)
+        self.slot_key = np.full(cap, -1, dtype=np.int64)
+        self.slot_idx = np.full(cap, -1, dtype=np.int64)
+        pend = np.arange(d, dtype=np.int64)
+        pos = self._home(keys)
+        while pend.size:
+            s = pos[pend].astype(np.int64)
+            free = self.slot_key[s] < 0
+            # one winner per free slot: the smallest pending basis index (pend is ascending)
+            cand = pend[free]
+            cs = s[free]
+            _, first = np.unique(cs, return_index=True)
+            win = cand[first]
+            self.slot_key[cs[first]] = keys[win]
+            self.slot_idx[cs[first]] = win
+            placed = np.zeros(d, dtype=bool)
+            placed[win] = True
+            pend = pend[~placed[pend]]
+            pos[pend] = (pos[pend] + np.uint64(1)) & self.mask
+        self.d = d
+
+    def _home(self, keys):
+        return rng.mix64(np.asarray(keys, dtype=np.int64).astype(np.uint64)) & self.mask
+
+    def lookup(self, q: np.ndarray) -> np.ndarray:
+        """Basis index of every key in q (-1 where the key is not in the basis)."""
+        q = np.asarray(q, dtype=np.int64)
+        out = np.full(q.shape[0], -1, dtype=np.int64)
+        pend = np.arange(q.shape[0], dtype=np.int64)
+        pos = self._home(q)
+        while pend.size:
+            s = pos[pend].astype(np.int64)
+            k = self.slot_key[s]
+            hit = k == q[pend]
+            out[pend[hit]] = self.slot_idx[s[hit]]
+            go = (~hit) & (k >= 0)            # occupied by another key: probe on
+            pend = pend[go]
+            pos[pend] = (pos[pend] + np.uint64(1)) & self.mask
+        return out
+
+
 def bh_mu(L: int, seed: int) -> np.ndarray:
     """mu_i ~ U[-0.5, 0.5] as u - 0.5 (exact) from tag 30."""
     return rng.uniform(seed, 30, np.arange(L)) - 0.5
 
 
 def bose_hubbard_csr(L: int, N: int, J: float, U: float, mu: np.ndarray,
-                     periodic: bool = False):
+                     periodic: bool = False, index: str = "search"):
     """Real CSR of the Bose-Hubbard chain in the fixed-N sector.
 
     Diagonal order: 0.0, += (U/2) n_i (n_i - 1) for i ascending, then
     -= mu_i n_i for i ascending.  Hop amplitudes -J sqrt(n_s (n_t + 1)).
-    Row/column index = position in ``bh_basis`` (the inverse map ind^-1 is
-    a sorted-key search here; the library uses a hash table).
+    Row/column index = position in ``bh_basis``; the inverse map ind^-1 is a
+    sorted-key search (``index="search"``) or the open-addressing hash table of
+    P:412 (``index="hash"``, ``BHIndexHash``) — bit-identical results.
     """
     occ = bh_basis(L, N)
     d = occ.shape[0]
     keys = bh_keys(occ)
+    table = BHIndexHash(keys) if index == "hash" else None
     o = occ.astype(np.int64)
     diag = np.zeros(d, dtype=np.float64)
     for i in range(L):
@@ -218,7 +276,11 @@ def bose_hubbard_csr(L: int, N: int, J: float, U: float, mu: np.ndarray,
         for (a, b, sa, sb) in ((i, j, si, sj), (j, i, sj, si)):
             ok = o[:, b] > 0
             newkey = keys + (np.int64(1) << sa) - (np.int64(1) << sb)
-            tgt = np.searchsorted(keys, np.where(ok, newkey, keys))
+            if table is None:
+                tgt = np.searchsorted(keys, np.where(ok, newkey, keys))
+            else:
+                tgt = table.lookup(np.where(ok, newkey, keys))
+                assert np.all(tgt >= 0)
             amp = -J * np.sqrt((o[:, b] * (o[:, a] + 1)).astype(np.float64))
             cols[:, q] = tgt
             vals[:, q] = amp
