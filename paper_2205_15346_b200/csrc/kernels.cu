@@ -5,8 +5,8 @@
 //   update_proj p' = p - V e1, g2 = V^H p'         k_proj_tma<1> / k_proj_s<1>
 //   update_norm p'' = p' - V e2 -> column j+1, ||p''||^2      k_update_norm
 //   combine     w = V (s omega), in place into column 0          k_combine
-// plus the f1 (paper-literal Lanczos) and f2 (Gram second sweep, k_proj_tma<3>) kernels, the older
-// fused kernel sets 0/1, validation and small helpers.  e_k = s_k^2 g_k (s_k = 1/||V_k||: columns
+// plus the f1 (paper-literal Lanczos) and f2 (Gram second sweep, k_proj_tma<3>) kernels,
+// validation and small helpers (round 1's fused kernel sets 0/1 measured slower and were removed).  e_k = s_k^2 g_k (s_k = 1/||V_k||: columns
 // are stored unnormalised and scaled on the fly).  Reductions are deterministic: per-CTA partials,
 // then the last CTA to finish (integer ticket) sums them in a fixed order; no floating-point atomics.
 #include "device_common.cuh"
@@ -18,424 +18,7 @@
 
 namespace te {
 
-constexpr size_t kK1Smem = sizeof(double2) * (kSpmvChunk + kSpmvRows) + sizeof(int64_t) * (kSpmvRows + 1);
-
-template <bool CPLX, int NCW>
-__global__ void __launch_bounds__(kThreads, 2) k_spmv_proj(KDev d, int j) {
-  static_assert(kThreads == kSpmvRows, "one thread per tile row");
-  using VT = typename ValT<CPLX>::T;
-  extern __shared__ __align__(128) unsigned char smem[];
-  double2* prod = reinterpret_cast<double2*>(smem);
-  double2* ps = prod + kSpmvChunk;
-  int64_t* rps = reinterpret_cast<int64_t*>(ps + kSpmvRows);
-  __shared__ double sj_s;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) sj_s = step_gate(d, j, blockIdx.x == 0);
-  __syncthreads();
-  const double sj = sj_s;
-  if (sj == 0.0) return;
-
-  const VT* __restrict__ val = static_cast<const VT*>(d.val);
-  const int32_t* __restrict__ col = d.col;
-  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
-  const double2* __restrict__ halo = d.halo;
-  const int64_t n = d.n;
-  const int ncols = j + 1;
-  double2 acc[NCW];
-#pragma unroll
-  for (int q = 0; q < NCW; ++q) acc[q] = make_double2(0.0, 0.0);
-
-  const int64_t ntiles = (n + kSpmvRows - 1) / kSpmvRows;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = tile * kSpmvRows;
-    const int rows = (int)min((int64_t)kSpmvRows, n - r0);
-    for (int i = tid; i <= rows; i += kThreads) rps[i] = __ldg(d.rowptr + r0 + i);
-    __syncthreads();
-    const int64_t b = rps[0], e = rps[rows];
-    int64_t mylo = 0, myhi = 0;
-    if (tid < rows) { mylo = rps[tid]; myhi = rps[tid + 1]; }
-    double2 sum = make_double2(0.0, 0.0);
-    for (int64_t cb = b; cb < e; cb += kSpmvChunk) {
-      const int cnt = (int)min((int64_t)kSpmvChunk, e - cb);
-      // gather-multiply over the chunk's entries: coalesced col/val streams, 4 gathers in flight
-      for (int k0 = tid; k0 < cnt; k0 += 4 * kThreads) {
-        int cc[4];
-        VT vv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = k0 + u * kThreads;
-          if (k < cnt) {
-            cc[u] = __ldg(col + cb + k);
-            vv[u] = __ldg(val + cb + k);
-          }
-        }
-        double2 xx[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = k0 + u * kThreads;
-          if (k < cnt) xx[u] = (cc[u] < n) ? __ldg(x + cc[u]) : __ldg(halo + (cc[u] - n));
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = k0 + u * kThreads;
-          if (k < cnt) prod[k] = ValT<CPLX>::mul(vv[u], xx[u]);
-        }
-      }
-      __syncthreads();
-      const int64_t lo = max(mylo, cb), hi = min(myhi, cb + cnt);
-      for (int64_t q = lo; q < hi; ++q) sum = cadd(sum, prod[q - cb]);  // row order, left to right
-      __syncthreads();
-    }
-    const double2 p = make_double2(sum.x * sj, sum.y * sj);
-    if (tid < rows) d.W[r0 + tid] = p;
-    ps[tid] = p;
-    __syncthreads();
-    // sweep-1 projections on the fresh tile: warp w owns columns w, w+8, ...
-#pragma unroll
-    for (int q = 0; q < NCW; ++q) {
-      const int k = warp + kWarps * q;
-      if (k < ncols) {
-        const double2* Vk = d.V + (int64_t)k * d.ldv + r0;
-        if (rows == kSpmvRows) {
-          double2 v[kSpmvRows / 32];
-#pragma unroll
-          for (int s = 0; s < kSpmvRows / 32; ++s) v[s] = ld_stream(Vk + lane + 32 * s);
-#pragma unroll
-          for (int s = 0; s < kSpmvRows / 32; ++s) acc[q] = cfma_conj(v[s], ps[lane + 32 * s], acc[q]);
-        } else {
-          for (int i = lane; i < rows; i += 32) acc[q] = cfma_conj(ld_stream(Vk + i), ps[i], acc[q]);
-        }
-      }
-    }
-    __syncthreads();
-  }
-  finish_columns<NCW>(d, acc, ncols, 0, d.g1);
-}
-
-// --------------------------------------------------------------------------------------
-// K2: sweep-1 update + sweep-2 projections, V tile staged once (cp.async.bulk + mbarrier)
-// --------------------------------------------------------------------------------------
-constexpr int kStages = 4;
-constexpr int kStageBudget = 48 * 1024;   // bytes of V+W per stage
-
-size_t k2_smem_bytes(int ncols, int* tile_rows) {
-  int tr = 1024;
-  while (tr > 32 && (size_t)tr * (ncols + 1) * 16 > (size_t)kStageBudget) tr >>= 1;
-  if (tile_rows) *tile_rows = tr;
-  return (size_t)kStages * tr * (ncols + 1) * 16 + sizeof(double2) * kThreads + 128;
-}
-
-template <int NCW>
-__global__ void __launch_bounds__(kThreads, 1) k_update_proj(KDev d, int j, int TR) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bars[kStages];
-  __shared__ double2 coef[kMaxCols];
-  __shared__ int go_s;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ncols = j + 1;
-  if (tid == 0) go_s = (d.flag[0] == 0);
-  if (tid < ncols) {
-    const double sk = d.s[tid];
-    const double2 g = d.g1[tid];
-    coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);   // e1_k = s_k c1_k, c1_k = s_k g1_k
-  }
-  __syncthreads();
-  if (!go_s) return;
-
-  const int64_t n = d.n;
-  const int64_t ntiles = (n + TR - 1) / TR;
-  const size_t stage_elems = (size_t)TR * (ncols + 1);
-  double2* stage0 = reinterpret_cast<double2*>(smem);
-  double2* red = stage0 + kStages * stage_elems;   // kThreads double2 for the grouped update
-  const uint64_t pol = policy_evict_first();
-
-  auto issue = [&](int64_t tile, int st) {
-    const int64_t r0 = tile * TR;
-    const int rows = (int)min((int64_t)TR, n - r0);
-    const unsigned bytes = (unsigned)rows * 16u;
-    double2* Vs = stage0 + st * stage_elems;
-    mbar_expect_tx(&bars[st], bytes * (unsigned)(ncols + 1));
-    for (int k = 0; k < ncols; ++k) bulk_g2s(Vs + (size_t)k * TR, d.V + (int64_t)k * d.ldv + r0, bytes, &bars[st], pol);
-    bulk_g2s(Vs + (size_t)ncols * TR, d.W + r0, bytes, &bars[st], pol);
-  };
-
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      const int64_t tile = blockIdx.x + (int64_t)s * gridDim.x;
-      if (tile < ntiles) issue(tile, s);
-    }
-  }
-  double2 acc[NCW];
-#pragma unroll
-  for (int q = 0; q < NCW; ++q) acc[q] = make_double2(0.0, 0.0);
-
-  const int G = TR >= kThreads ? 1 : kThreads / TR;  // threads sharing one row in the update
-  for (int64_t it = 0;; ++it) {
-    const int64_t tile = blockIdx.x + it * gridDim.x;
-    if (tile >= ntiles) break;
-    const int st = (int)(it % kStages);
-    mbar_wait(&bars[st], (unsigned)((it / kStages) & 1));
-    double2* Vs = stage0 + st * stage_elems;
-    double2* Ws = Vs + (size_t)ncols * TR;
-    const int64_t r0 = tile * TR;
-    const int rows = (int)min((int64_t)TR, n - r0);
-    // ---- phase U: p' = p - V e1 (rows of the tile), written to HBM and back into the stage
-    if (G == 1) {
-      for (int i = tid; i < rows; i += kThreads) {
-        double2 a = make_double2(0.0, 0.0);
-        for (int k = 0; k < ncols; ++k) a = cfma(Vs[(size_t)k * TR + i], coef[k], a);
-        const double2 p = make_double2(Ws[i].x - a.x, Ws[i].y - a.y);
-        Ws[i] = p;
-        d.W[r0 + i] = p;
-      }
-    } else {
-      const int g = tid / TR, i = tid - g * TR;
-      double2 a = make_double2(0.0, 0.0);
-      if (i < rows)
-        for (int k = g; k < ncols; k += G) a = cfma(Vs[(size_t)k * TR + i], coef[k], a);
-      red[tid] = a;
-      __syncthreads();
-      if (g == 0 && i < rows) {
-        double2 t = red[i];
-        for (int gg = 1; gg < G; ++gg) t = cadd(t, red[gg * TR + i]);
-        const double2 p = make_double2(Ws[i].x - t.x, Ws[i].y - t.y);
-        Ws[i] = p;
-        d.W[r0 + i] = p;
-      }
-    }
-    __syncthreads();
-    // ---- phase D: g2_k += conj(V_ik) p'_i from the same staged tile
-#pragma unroll
-    for (int q = 0; q < NCW; ++q) {
-      const int k = warp + kWarps * q;
-      if (k < ncols) {
-        const double2* Vk = Vs + (size_t)k * TR;
-        for (int i = lane; i < rows; i += 32) acc[q] = cfma_conj(Vk[i], Ws[i], acc[q]);
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      // generic-proxy writes to this stage (p') must be ordered before the async-proxy refill
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const int64_t nt = blockIdx.x + (it + kStages) * gridDim.x;
-      if (nt < ntiles) issue(nt, st);
-    }
-  }
-  finish_columns<NCW>(d, acc, ncols, 1, d.g2);
-}
-
-// --------------------------------------------------------------------------------------
-// Register-streaming variants (default): a group of TPR lanes owns one row; lane q of the group
-// holds the row's V entries of columns k = q + TPR*c (c < kCPT) in registers, so each V element
-// is read from HBM exactly once per kernel and reused from registers by both the update and the
-// projection phase.  No shared-memory staging and no block-wide barriers inside the row loop.
-// --------------------------------------------------------------------------------------
-constexpr int kCPT = 8;  // columns per lane
-
-// Cross-lane/cross-warp column sums of acc (lanes with equal q = lane % TPR share columns), in
-// a fixed order, then the same last-CTA reduction as finish_columns.
-template <int TPR>
-__device__ __forceinline__ void finish_grouped(const KDev& d, double2 (&acc)[kCPT], int ncols, int ctr,
-                                               double2* out) {
-  __shared__ double2 red[kWarps][kMaxCols];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = lane % TPR;
-#pragma unroll
-  for (int c = 0; c < kCPT; ++c) {
-#pragma unroll
-    for (int off = TPR; off < 32; off <<= 1) {
-      acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, off);
-      acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, off);
-    }
-    const int k = q + TPR * c;
-    if (lane < TPR && k < ncols) red[warp][k] = acc[c];
-  }
-  __syncthreads();
-  if (tid < ncols) {
-    double2 s = red[0][tid];
-    for (int w = 1; w < kWarps; ++w) s = cadd(s, red[w][tid]);
-    d.part[(size_t)blockIdx.x * kMaxCols + tid] = s;
-  }
-  __threadfence();
-  __syncthreads();
-  __shared__ int last;
-  if (tid == 0) last = (atomicAdd(&d.counter[ctr], 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  __shared__ double2 seg[4][kMaxCols];
-  const int c = tid & (kMaxCols - 1), sgi = tid >> 6;
-  const int G = gridDim.x;
-  const int per = (G + 3) / 4;
-  double2 s = make_double2(0.0, 0.0);
-  if (c < ncols) {
-    const int b0 = sgi * per, b1 = min(G, b0 + per);
-    for (int b = b0; b < b1; ++b) s = cadd(s, ld_cg(d.part + (size_t)b * kMaxCols + c));
-  }
-  seg[sgi][c] = s;
-  __syncthreads();
-  if (tid < ncols) {
-    double2 t = seg[0][tid];
-    t = cadd(t, seg[1][tid]);
-    t = cadd(t, seg[2][tid]);
-    t = cadd(t, seg[3][tid]);
-    out[tid] = t;
-  }
-  if (tid == 0) d.counter[ctr] = 0u;
-}
-
-
-// K1 (register variant): CSR-vector SpMV with TPR lanes per row + in-register projections.
-// Rows of the block iteration pf ahead are pulled into L2 with bulk prefetches (V column
-// segments, rowptr, col and val ranges) so the register loads of the current iteration hit L2.
-template <bool CPLX, int TPR>
-__global__ void __launch_bounds__(kThreads, 2) k_spmv_proj_r(KDev d, int j, int pf) {
-  using VT = typename ValT<CPLX>::T;
-  __shared__ double sj_s;
-  const int tid = threadIdx.x, q = tid % TPR, grp = tid / TPR, warp = tid >> 5, lane = tid & 31;
-  constexpr int RPB = kThreads / TPR;
-  if (tid == 0) sj_s = step_gate(d, j, blockIdx.x == 0);
-  __syncthreads();
-  const double sj = sj_s;
-  if (sj == 0.0) return;
-  const VT* __restrict__ val = static_cast<const VT*>(d.val);
-  const int32_t* __restrict__ col = d.col;
-  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
-  const double2* __restrict__ halo = d.halo;
-  const int64_t n = d.n, ldv = d.ldv;
-  const int ncols = j + 1;
-  const int64_t stride = (int64_t)gridDim.x * RPB;
-  // warp 0 prefetches V column segments; warp 1 lane 0 the CSR ranges (rowptr values of the
-  // block iteration pf ahead are loaded one iteration earlier to keep the issue non-blocking)
-  auto pf_v = [&](int64_t rbp) {
-    if (rbp >= n) return;
-    const unsigned bytes = (unsigned)min((int64_t)RPB, n - rbp) * 16u;
-    for (int k = lane; k < ncols; k += 32) prefetch_l2(d.V + rbp + (int64_t)k * ldv, bytes);
-  };
-  auto pf_csr = [&](int64_t rbp, int64_t lo, int64_t hi) {
-    if (rbp >= n) return;
-    const int64_t rows = min((int64_t)RPB, n - rbp);
-    prefetch_range(d.rowptr, (size_t)rbp * 8, (size_t)(rbp + rows + 1) * 8);
-    prefetch_range(col, (size_t)lo * 4, (size_t)hi * 4);
-    prefetch_range(val, (size_t)lo * sizeof(VT), (size_t)hi * sizeof(VT));
-  };
-  int64_t nlo = 0, nhi = 0;  // rowptr bounds of block iteration (it + pf), loaded at it - 1
-  if (pf > 0) {
-    for (int i = 0; i < pf; ++i) {
-      const int64_t rbp = (int64_t)blockIdx.x * RPB + i * stride;
-      if (warp == 0) pf_v(rbp);
-      if (warp == 1 && lane == 0 && rbp < n) {
-        const int64_t lo = __ldg(d.rowptr + rbp), hi = __ldg(d.rowptr + min(rbp + RPB, n));
-        pf_csr(rbp, lo, hi);
-      }
-    }
-    const int64_t rbp = (int64_t)blockIdx.x * RPB + pf * stride;
-    if (warp == 1 && lane == 0 && rbp < n) {
-      nlo = __ldg(d.rowptr + rbp);
-      nhi = __ldg(d.rowptr + min(rbp + RPB, n));
-    }
-  }
-  double2 acc[kCPT];
-#pragma unroll
-  for (int c = 0; c < kCPT; ++c) acc[c] = make_double2(0.0, 0.0);
-  for (int64_t rb = (int64_t)blockIdx.x * RPB; rb < n; rb += stride) {
-    if (pf > 0) {
-      const int64_t rbp = rb + pf * stride;
-      if (warp == 0) pf_v(rbp);
-      if (warp == 1 && lane == 0 && rbp < n) {
-        pf_csr(rbp, nlo, nhi);
-        const int64_t rbn = rbp + stride;
-        if (rbn < n) {
-          nlo = __ldg(d.rowptr + rbn);
-          nhi = __ldg(d.rowptr + min(rbn + RPB, n));
-        }
-      }
-    }
-    const int64_t r = rb + grp;
-    const bool act = r < n;
-    double2 v[kCPT];
-#pragma unroll
-    for (int c = 0; c < kCPT; ++c) {
-      const int k = q + TPR * c;
-      v[c] = (act && k < ncols) ? ld_stream(d.V + r + (int64_t)k * ldv) : make_double2(0.0, 0.0);
-    }
-    double2 sum = make_double2(0.0, 0.0);
-    if (act) {
-      const int64_t lo = __ldg(d.rowptr + r), hi = __ldg(d.rowptr + r + 1);
-      for (int64_t e = lo + q; e < hi; e += TPR) {
-        const int c = __ldg(col + e);
-        const VT w = __ldg(val + e);
-        const double2 xv = (c < n) ? __ldg(x + c) : __ldg(halo + (c - n));
-        sum = cadd(sum, ValT<CPLX>::mul(w, xv));
-      }
-    }
-    sum = group_sum<TPR>(sum);
-    const double2 p = make_double2(sum.x * sj, sum.y * sj);
-    if (act && q == 0) d.W[r] = p;
-#pragma unroll
-    for (int c = 0; c < kCPT; ++c) acc[c] = cfma_conj(v[c], p, acc[c]);
-  }
-  finish_grouped<TPR>(d, acc, ncols, 0, d.g1);
-}
-
-// K2 (register variant): p' = p - V e1 and g2 = V^H p' with the row's V entries in registers
-template <int TPR>
-__global__ void __launch_bounds__(kThreads, 2) k_update_proj_r(KDev d, int j, int pf) {
-  __shared__ double2 coef[kMaxCols];
-  __shared__ int go_s;
-  const int tid = threadIdx.x, q = tid % TPR, grp = tid / TPR, warp = tid >> 5, lane = tid & 31;
-  constexpr int RPB = kThreads / TPR;
-  const int ncols = j + 1;
-  if (tid == 0) go_s = (d.flag[0] == 0);
-  if (tid < ncols) {
-    const double sk = d.s[tid];
-    const double2 g = d.g1[tid];
-    coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);
-  }
-  __syncthreads();
-  if (!go_s) return;
-  const int64_t n = d.n, ldv = d.ldv;
-  const int64_t stride = (int64_t)gridDim.x * RPB;
-  auto pf_rows = [&](int64_t rbp) {
-    if (rbp >= n) return;
-    const unsigned bytes = (unsigned)min((int64_t)RPB, n - rbp) * 16u;
-    for (int k = lane; k <= ncols; k += 32)
-      prefetch_l2(k < ncols ? (const void*)(d.V + rbp + (int64_t)k * ldv) : (const void*)(d.W + rbp), bytes);
-  };
-  if (warp == 0)
-    for (int i = 0; i < pf; ++i) pf_rows((int64_t)blockIdx.x * RPB + i * stride);
-  double2 acc[kCPT];
-#pragma unroll
-  for (int c = 0; c < kCPT; ++c) acc[c] = make_double2(0.0, 0.0);
-  for (int64_t rb = (int64_t)blockIdx.x * RPB; rb < n; rb += stride) {
-    if (pf > 0 && warp == 0) pf_rows(rb + pf * stride);
-    const int64_t r = rb + grp;
-    const bool act = r < n;
-    double2 v[kCPT];
-#pragma unroll
-    for (int c = 0; c < kCPT; ++c) {
-      const int k = q + TPR * c;
-      v[c] = (act && k < ncols) ? ld_stream(d.V + r + (int64_t)k * ldv) : make_double2(0.0, 0.0);
-    }
-    const double2 w = act ? __ldcs(d.W + r) : make_double2(0.0, 0.0);
-    double2 a = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int c = 0; c < kCPT; ++c) {
-      const int k = q + TPR * c;
-      if (k < ncols) a = cfma(v[c], coef[k], a);
-    }
-    a = group_sum<TPR>(a);
-    const double2 p = make_double2(w.x - a.x, w.y - a.y);
-    if (act && q == 0) d.W[r] = p;
-#pragma unroll
-    for (int c = 0; c < kCPT; ++c) acc[c] = cfma_conj(v[c], p, acc[c]);
-  }
-  finish_grouped<TPR>(d, acc, ncols, 1, d.g2);
-}
+constexpr int kCPT = 8;  // columns per lane of the register/shuffle projection kernel (k_proj_s)
 
 // --------------------------------------------------------------------------------------
 // TMA-tiled projection kernel (default path), warp-specialised:
@@ -1174,18 +757,6 @@ __global__ void k_csr_check(int64_t n, int64_t ncl, const int64_t* __restrict__ 
 // --------------------------------------------------------------------------------------
 // launchers
 // --------------------------------------------------------------------------------------
-#define TE_DISPATCH_NCW(ncw, ...)                 \
-  switch (ncw) {                                 \
-    case 1: { constexpr int NCW = 1; __VA_ARGS__; } break; \
-    case 2: { constexpr int NCW = 2; __VA_ARGS__; } break; \
-    case 3: { constexpr int NCW = 3; __VA_ARGS__; } break; \
-    case 4: { constexpr int NCW = 4; __VA_ARGS__; } break; \
-    case 5: { constexpr int NCW = 5; __VA_ARGS__; } break; \
-    case 6: { constexpr int NCW = 6; __VA_ARGS__; } break; \
-    case 7: { constexpr int NCW = 7; __VA_ARGS__; } break; \
-    default: { constexpr int NCW = 8; __VA_ARGS__; } break; \
-  }
-
 int kernel_attributes(int which, int* regs, int* max_threads, int* static_smem, int* max_dyn_smem) {
   const void* f = nullptr;
   switch (which) {
@@ -1193,8 +764,6 @@ int kernel_attributes(int which, int* regs, int* max_threads, int* static_smem, 
     case 1: f = (const void*)k_proj_tma<0>; break;
     case 2: f = (const void*)k_proj_tma<1>; break;
     case 3: f = (const void*)k_update_norm; break;
-    case 4: f = (const void*)k_spmv_proj_r<false, 4>; break;
-    case 5: f = (const void*)k_update_proj_r<8>; break;
     default: return -1;
   }
   cudaFuncAttributes a;
@@ -1227,12 +796,6 @@ cudaError_t configure_kernels() {
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   AttrState st{optin, cudaSuccess};
   auto set = [&](const void* f, size_t want) { set_attr(f, want, &st); };
-#define TE_SET(NCW)                                                        \
-  set((const void*)k_spmv_proj<false, NCW>, kK1Smem);                      \
-  set((const void*)k_spmv_proj<true, NCW>, kK1Smem);                       \
-  set((const void*)k_update_proj<NCW>, k2_smem_bytes(kMaxCols, nullptr) + 64 * 1024);
-  TE_SET(1) TE_SET(2) TE_SET(3) TE_SET(4) TE_SET(5) TE_SET(6) TE_SET(7) TE_SET(8)
-#undef TE_SET
   set((const void*)k_proj_tma<0>, kProjSmemBudget + 1024);
   set((const void*)k_proj_tma<3>, kProjSmemBudget + 1024);
   set((const void*)k_proj_tma<0, 8>, kProjSmemBudget + 1024);
@@ -1298,55 +861,13 @@ void launch_gram_update(const KDev& d, int j, bool write, const Launch& L) {
   TE_PROJ_TMA(3, j + 1, L.tmaps[j], d, j, S, R, C, write ? 1 : 0);
 }
 
-void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L) {
-  if (L.variant == 2) {
-    launch_spmv(d, cplx, j, L);
-    launch_proj_dots(d, j, L);
-    return;
-  }
-  if (L.variant == 0) {
-
-    const int tpr = tpr_for(j + 1, 4);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * L.num_sms, (d.n * tpr + kThreads - 1) / kThreads));
-    TE_DISPATCH_TPR(tpr, {
-      if (cplx)
-        k_spmv_proj_r<true, TPR><<<grid, kThreads, 0, L.stream>>>(d, j, L.prefetch);
-      else
-        k_spmv_proj_r<false, TPR><<<grid, kThreads, 0, L.stream>>>(d, j, L.prefetch);
-    });
-    return;
-  }
-  const int ncw = (j + 1 + kWarps - 1) / kWarps;
-  TE_DISPATCH_NCW(ncw, {
-    if (cplx)
-      k_spmv_proj<true, NCW><<<L.grid_k1, kThreads, kK1Smem, L.stream>>>(d, j);
-    else
-      k_spmv_proj<false, NCW><<<L.grid_k1, kThreads, kK1Smem, L.stream>>>(d, j);
-  });
-}
-
 void launch_update_proj(const KDev& d, int j, const Launch& L) {
-  if (L.variant == 2 && (L.proj_tma == 0 || (L.proj_tma == 2 && j + 1 <= kShuffleMaxCols))) {
+  if (L.proj_tma == 0 || (L.proj_tma == 2 && j + 1 <= kShuffleMaxCols)) {
     launch_proj_s(d, j, 1, L);
     return;
   }
-  if (L.variant == 2) {
-    const int S = proj_slots(j + 1), R = proj_rsub(j + 1), C = proj_consumers(j + 1);
-    TE_PROJ_TMA(1, j + 1, L.tmaps[j], d, j, S, R, C, 0);
-    return;
-  }
-  if (L.variant == 0) {
-    const int tpr = tpr_for(j + 1, 1);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * L.num_sms, (d.n * tpr + kThreads - 1) / kThreads));
-    TE_DISPATCH_TPR(tpr, { k_update_proj_r<TPR><<<grid, kThreads, 0, L.stream>>>(d, j, L.prefetch); });
-    return;
-  }
-  int tr = 0;
-  const size_t smem = k2_smem_bytes(j + 1, &tr);
-  const int64_t ntiles = (d.n + tr - 1) / tr;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(L.grid_k2, ntiles));
-  const int ncw = (j + 1 + kWarps - 1) / kWarps;
-  TE_DISPATCH_NCW(ncw, { k_update_proj<NCW><<<grid, kThreads, smem, L.stream>>>(d, j, tr); });
+  const int S = proj_slots(j + 1), R = proj_rsub(j + 1), C = proj_consumers(j + 1);
+  TE_PROJ_TMA(1, j + 1, L.tmaps[j], d, j, S, R, C, 0);
 }
 
 void launch_update_norm(const KDev& d, int j, bool write, const Launch& L) {

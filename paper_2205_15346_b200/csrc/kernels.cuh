@@ -16,19 +16,10 @@ namespace te {
 constexpr int kThreads = 256;        // block size of every hot-path kernel
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxCols = 64;         // TE_M_MAX
-constexpr int kSpmvRows = 256;       // K1 row tile
-constexpr int kSpmvChunk = 4096;     // K1 products staged in shared memory per chunk
-constexpr int kSpmvTileNnz = 4096;   // entries per nnz-balanced SpMV tile (cap), real values
-constexpr int kSpmvTileNnzC = 2048;  // complex values (two pipelined blocks per SM)
-constexpr int kSpmvMaxTileRows = 256;  // rows per pipelined-SpMV tile cap (kThreads / TPR)
 // warp-specialised ring SpMV tile capacities (entries) for its 4-stage and 3-stage layouts
 constexpr int kRingNnz4 = 4096, kRingNnzC4 = 2048;
 constexpr int kRingNnz3 = 5632, kRingNnzC3 = 2816;
 constexpr int kSellSigma = 4096;       // SELL-32-sigma sorting window (rows)
-constexpr int kAgCap = 1024;            // entries per async-gather SpMV tile (variant 5)
-constexpr int kAgMaxRows = 128;         // rows per async-gather tile cap (<= kThreads / TPR)
-constexpr int kSpmvTmaNnzCap = 512;     // entries per TMA SpMV tile (== kSpmvTmaNnz)
-constexpr int kSpmvTmaRowCap = 128;     // rows per TMA SpMV tile
 
 struct KDev {
   int64_t n;            // local rows
@@ -38,8 +29,6 @@ struct KDev {
   const int64_t* rowptr;
   const int32_t* col;
   const void* val;
-  const int64_t* tile_row;  // [ntiles+1] first row of each nnz-balanced SpMV tile
-  int64_t ntiles;
   const double2* const* peer_base;  // [nranks] V base of every rank in this address space (halo mode 1)
   const int64_t* peer_ldv;          // [nranks] their column strides
   const int32_t* halo_owner;        // [n_halo] owning rank of each halo entry
@@ -52,10 +41,6 @@ struct KDev {
   int64_t nslices;
   const int64_t* tile_ring;  // [4*ntiles_ring] {first row, end row, first entry, end entry} (variant 7)
   int64_t ntiles_ring;
-  const int64_t* tile_ag;    // [4*ntiles_ag] {first row, end row, first entry, end entry} (variant 5)
-  int64_t ntiles_ag;
-  const int64_t* tile_desc;  // [2*(ntiles_desc+1)] {first row, first entry} of the TMA SpMV tiles
-  int64_t ntiles_desc;
   const double2* halo;  // x entries for columns >= n (distributed); nullptr otherwise
   double* s;            // [m_cap+1] column scales
   double* alpha;        // [m_cap]
@@ -76,26 +61,19 @@ struct KDev {
 struct Launch {
   cudaStream_t stream;
   int num_sms;
-  int grid_k1, grid_k2, grid_k3;
-  const CUtensorMap* tmaps;  // [kMaxCols] 2-D maps of V, box = 64 doubles x (k+1) columns
-  int spmv_tpr;  // lanes per row of the standalone CSR-vector SpMV
-  int spmv_pipe_tpr;  // lanes per row of the pipelined SpMV (tile row cap = kThreads / this)
-  int spmv_pf;        // pipelined SpMV: L2 prefetch of tile t+2G (0 off, 1 on)
+  int grid_k3;               // streaming kernels (update_norm, combine, norm): up to 8 blocks per SM
+  const CUtensorMap* tmaps;  // [kMaxCols] 2-D maps of V, box = 64R doubles x (k+1) columns
   int spmv_force_halo;  // test hook: run the multi-rank (halo-aware) SpMV instantiation on one rank
-  int spmv_nf_wide;
-  int halo_peer;      // SpMV reads halo columns from peer memory (no staged exchange)
-  int spmv_ag_tpr;
-  int spmv_ring_tpr;  // lanes per row of the warp-specialised ring SpMV
-  int ring_stages;    // its ring depth: 4 (short real rows) or 3 (larger tiles)    // lanes per row of the async-gather SpMV (1..32)   // pipelined SpMV gathers in flight per lane: 0 -> 12 real / 8 complex, 1 -> 16 / 12
-  int proj_tma;   // 2: hybrid by column count (default), 1: TMA-tiled only, 0: register/shuffle only
-  int spmv_tiled; // 2: TMA-fed SpMV (default), 1: nnz-balanced tiled SpMV, 0: CSR-vector
-  int prefetch; // L2 bulk-prefetch distance in block iterations (0: off)
-  int variant;  // 2: SpMV + TMA-tiled projections (default); 0: register-streaming K1/K2;
-                //    1: shared-memory / bulk-copy staged K1/K2
+  int spmv_nf_wide;     // ring SpMV gathers in flight per lane: 0 -> 12 real / 8 complex, 1 -> 16 / 12
+  int halo_peer;        // SpMV reads halo columns from peer memory (no staged exchange)
+  int spmv_ring_tpr;    // lanes per row of the warp-specialised ring SpMV
+  int ring_stages;      // its ring depth: 4 (short real rows) or 3 (larger tiles)
+  int proj_tma;         // 2: hybrid by column count (default), 1: TMA-tiled only, 0: register/shuffle only
+  int spmv_tiled;       // 7: warp-specialised ring (default), 6: SELL-32-sigma
+  int prefetch;         // update_norm: L2 bulk-prefetch distance in block iterations (0: off)
 };
 
-// hot path (one Krylov step j = 3 launches; see kernels.cu)
-void launch_spmv_proj(const KDev& d, bool cplx, int j, const Launch& L);   // K1 (variants 0/1; variant 2 = K1a+K1b)
+// hot path (one Krylov step j = 4 launches; see kernels.cu)
 void launch_sell_build(bool cplx, int64_t npos, const int64_t* rowptr, const int32_t* col, const void* val,
                        const int32_t* perm, const int64_t* sptr, const int32_t* slen, int32_t* scol, void* sval,
                        cudaStream_t st);
@@ -128,7 +106,6 @@ void launch_csr_check(int64_t n, int64_t ncol_limit, const int64_t* rowptr, cons
 // distributed halo pack: out[t] = V_j[idx[t]]
 void launch_pack(const double2* x, const int32_t* idx, int64_t cnt, double2* out, cudaStream_t st);
 
-size_t k2_smem_bytes(int ncols, int* tile_rows);
 int proj_slots(int ncols);
 int proj_rsub(int ncols);
 int proj_consumers(int ncols);

@@ -114,16 +114,9 @@ struct te_handle {
   int variant = 2;
   int ortho = 0;  // 0 CGS2 (default), 1 paper-literal 3-term Lanczos (f1)
   int integrator = 0;  // 0 adaptive tanh-sinh (default), 1 Gauss-Legendre
-  int spmv_tpr = 4;
-  int spmv_pipe_tpr = 1;
-  int spmv_pf = 0;
   int spmv_nf_wide = 0;
   int spmv_force_halo = 0;
   int spmv_tiled = 7;
-  int64_t* d_tile_row = nullptr;
-  int64_t ntiles = 0;
-  int64_t* d_tile_desc = nullptr;
-  int64_t* d_tile_ag = nullptr;
   int64_t* d_tile_ring = nullptr;
   int64_t ntiles_ring = 0;
   int spmv_ring_tpr = 1;
@@ -135,9 +128,6 @@ struct te_handle {
   int32_t* d_slen = nullptr;
   int32_t* d_sperm = nullptr;
   int64_t nslices = 0;
-  int64_t ntiles_ag = 0;
-  int spmv_ag_tpr = 1;
-  int64_t ntiles_desc = 0;
   std::vector<CUtensorMap> tmaps;
   int prefetch = 0;
   cudaEvent_t ev0[kEvPool], ev1[kEvPool];
@@ -201,10 +191,6 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.peer_ldv = h->d_peer_ldv;
   d.halo_owner = h->d_halo_owner;
   d.halo_lidx = h->d_halo_lidx;
-  d.tile_row = h->d_tile_row;
-  d.ntiles = h->ntiles;
-  d.tile_desc = h->d_tile_desc;
-  d.tile_ag = h->d_tile_ag;
   d.tile_ring = h->d_tile_ring;
   d.ntiles_ring = h->ntiles_ring;
   d.scol = h->d_scol;
@@ -213,8 +199,6 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.slen = h->d_slen;
   d.sperm = h->d_sperm;
   d.nslices = h->nslices;
-  d.ntiles_ag = h->ntiles_ag;
-  d.ntiles_desc = h->ntiles_desc;
   d.alpha = h->d_small + kOffAlpha;
   d.beta = h->d_small + kOffBeta;
   d.flag = reinterpret_cast<int*>(h->d_small + kOffFlag);
@@ -232,11 +216,9 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   return d;
 }
 
-// halo mode 1 is used by the pipelined SpMV of the projection-kernel sets (and f1/f2); the other
-// SpMV variants keep the staged exchange
+// halo mode 1 is used by the ring SpMV; the SELL variant keeps the staged exchange
 bool peer_active(const te_handle* h) {
-  return h->dist && h->dist->nranks > 1 && h->halo_mode == 1 && (h->spmv_tiled == 4 || h->spmv_tiled == 7) &&
-         (h->variant >= 2 || h->ortho != 0);
+  return h->dist && h->dist->nranks > 1 && h->halo_mode == 1 && h->spmv_tiled == 7;
 }
 
 Launch make_launch(te_handle* h) {
@@ -244,19 +226,12 @@ Launch make_launch(te_handle* h) {
   L.stream = h->stream;
   L.num_sms = h->num_sms;
   const int64_t t256 = (h->n + 255) / 256;
-  L.grid_k1 = (int)std::max<int64_t>(1, std::min<int64_t>(2 * h->num_sms, t256));
-  L.grid_k2 = h->num_sms;
   L.grid_k3 = (int)std::max<int64_t>(1, std::min<int64_t>(8 * h->num_sms, t256));
-  L.variant = h->variant >= 2 ? 2 : h->variant;  // 2 hybrid, 3 TMA-only, 4 shuffle-only
   L.proj_tma = h->variant == 2 ? 2 : (h->variant == 3 ? 1 : (h->variant == 4 ? 0 : 0));
   L.tmaps = h->tmaps.data();
-  L.spmv_tpr = h->spmv_tpr;
-  L.spmv_pipe_tpr = h->spmv_pipe_tpr;
-  L.spmv_pf = h->spmv_pf;
   L.spmv_nf_wide = h->spmv_nf_wide;
   L.spmv_force_halo = h->spmv_force_halo;
   L.halo_peer = peer_active(h) ? 1 : 0;
-  L.spmv_ag_tpr = h->spmv_ag_tpr;
   L.spmv_ring_tpr = h->spmv_ring_tpr;
   L.ring_stages = h->ring_stages;
   L.spmv_tiled = h->spmv_tiled;
@@ -541,18 +516,12 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
       if ((rc = allreduce_sum(h, d.nrm2 + j, 1))) return rc;
       continue;
     }
-    if (h->variant >= 2) {
-      prof_begin(h);
-      te::launch_spmv(d, h->cplx, j, L); LCHECK("spmv");
-      prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
-      prof_begin(h);
-      te::launch_proj_dots(d, j, L); LCHECK("proj_dots");
-      prof_end(h, 5, 16.0 * n * ncols + 16.0 * n);
-    } else {
-      prof_begin(h);
-      te::launch_spmv_proj(d, h->cplx, j, L); LCHECK("spmv_proj");
-      prof_end(h, 0, bh + 16.0 * n + 16.0 * n * ncols + 16.0 * n);
-    }
+    prof_begin(h);
+    te::launch_spmv(d, h->cplx, j, L); LCHECK("spmv");
+    prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
+    prof_begin(h);
+    te::launch_proj_dots(d, j, L); LCHECK("proj_dots");
+    prof_end(h, 5, 16.0 * n * ncols + 16.0 * n);
     if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g1), 2 * (size_t)(j + 1)))) return rc;
     prof_begin(h);
     te::launch_update_proj(d, j, L); LCHECK("update_proj");
@@ -895,57 +864,15 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
       const int v = atoi(e);
       if (v == 1 || v == 2 || v == 4 || v == 8) t = v;
     }
-    h->spmv_pipe_tpr = t;
+    h->spmv_ring_tpr = t;
     h->spmv_nf_wide = !cplx && avg <= 16.0 * t;
-    if (const char* e = getenv("TE_SPMV_PF")) h->spmv_pf = atoi(e) != 0;
     if (const char* e = getenv("TE_SPMV_NF_WIDE")) h->spmv_nf_wide = atoi(e) != 0;
     if (const char* e = getenv("TE_SPMV_FORCE_HALO")) h->spmv_force_halo = atoi(e) != 0;
-  }
-  const int64_t tile_rows_cap = te::kSpmvMaxTileRows / h->spmv_pipe_tpr;
-  {  // nnz-balanced SpMV tiles: close a tile before it would exceed kSpmvTileNnz entries or
-     // 256/tpr rows (a single longer row gets a tile of its own; the kernels chunk it)
-    std::vector<int64_t> tr;
-    tr.reserve((size_t)(h->nnz / te::kSpmvTileNnz + n / te::kSpmvMaxTileRows + 2));
-    int64_t start = 0;
-    tr.push_back(0);
-    for (int64_t r = 0; r < n; ++r) {
-      const bool over_rows = (r + 1 - start) > tile_rows_cap;
-      const bool over_nnz = (rowptr[r + 1] - rowptr[start]) > (cplx ? te::kSpmvTileNnzC : te::kSpmvTileNnz) && r > start;
-      if (over_rows || over_nnz) {
-        tr.push_back(r);
-        start = r;
-      }
-    }
-    tr.push_back(n);
-    h->ntiles = (int64_t)tr.size() - 1;
-    if (cudaMalloc(&h->d_tile_row, sizeof(int64_t) * tr.size()) != cudaSuccess) return fail(TE_ERR_OOM, "tiles");
-    cudaMemcpyAsync(h->d_tile_row, tr.data(), sizeof(int64_t) * tr.size(), cudaMemcpyHostToDevice, h->stream);
-    // TMA SpMV tiles: <= kSpmvTmaNnzCap entries and <= kSpmvTmaRowCap rows; descriptors
-    // {first row, first entry} (a longer single row becomes a tile of its own)
-    std::vector<int64_t> td;
-    int64_t st = 0;
-    td.push_back(0);
-    td.push_back(0);
-    for (int64_t r = 0; r < n; ++r) {
-      const bool over_rows = (r + 1 - st) > te::kSpmvTmaRowCap;
-      const bool over_nnz = (rowptr[r + 1] - rowptr[st]) > te::kSpmvTmaNnzCap && r > st;
-      if (over_rows || over_nnz) {
-        td.push_back(r);
-        td.push_back(rowptr[r]);
-        st = r;
-      }
-    }
-    td.push_back(n);
-    td.push_back(rowptr[n]);
-    h->ntiles_desc = (int64_t)td.size() / 2 - 1;
-    if (cudaMalloc(&h->d_tile_desc, sizeof(int64_t) * td.size()) != cudaSuccess) return fail(TE_ERR_OOM, "tiles");
-    cudaMemcpyAsync(h->d_tile_desc, td.data(), sizeof(int64_t) * td.size(), cudaMemcpyHostToDevice, h->stream);
-    cudaStreamSynchronize(h->stream);
   }
   {  // warp-specialised ring SpMV (variant 7, default) tiles: <= kSpmvTileNnz(C) entries and
      // <= 480/tpr rows, {first row, end row, first entry, end entry}; lanes per row by the same rule
      // as the pipelined SpMV (measured best on configs 2-6: 1 / 2 / 8 / 2 / 4)
-    int tr = h->spmv_pipe_tpr;
+    int tr = h->spmv_ring_tpr;
     if (const char* e = getenv("TE_SPMV_RING_TPR")) {
       const int v = atoi(e);
       if (v == 1 || v == 2 || v == 4 || v == 8) tr = v;
@@ -978,36 +905,6 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
       cudaStreamSynchronize(h->stream);
     }
   }
-  {  // async-gather SpMV (variant 5) tiles: <= kAgCap entries and <= kThreads/tpr rows, stored as
-     // {first row, end row, first entry, end entry}; lanes per row = the largest power of two
-     // <= mean row length / 4 (1..32), so a full tile keeps every row group busy
-    const double avg = n > 0 ? (double)h->nnz / (double)n : 0.0;
-    int ta = 1;
-    while (ta < 32 && 2.0 * ta * 4.0 <= avg) ta <<= 1;
-    if (const char* e = getenv("TE_SPMV_AG_TPR")) {
-      const int v = atoi(e);
-      if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) ta = v;
-    }
-    h->spmv_ag_tpr = ta;
-    const int64_t rcap = std::min<int64_t>(te::kAgMaxRows, te::kThreads / ta);
-    std::vector<int64_t> tg;
-    int64_t st = 0;
-    for (int64_t r = 0; r < n; ++r) {
-      const bool over_rows = (r + 1 - st) > rcap;
-      const bool over_nnz = (rowptr[r + 1] - rowptr[st]) > te::kAgCap && r > st;
-      if (over_rows || over_nnz) {
-        tg.insert(tg.end(), {st, r, rowptr[st], rowptr[r]});
-        st = r;
-      }
-    }
-    if (n > 0) tg.insert(tg.end(), {st, n, rowptr[st], rowptr[n]});
-    h->ntiles_ag = (int64_t)tg.size() / 4;
-    if (!tg.empty()) {
-      if (cudaMalloc(&h->d_tile_ag, sizeof(int64_t) * tg.size()) != cudaSuccess) return fail(TE_ERR_OOM, "tiles");
-      cudaMemcpyAsync(h->d_tile_ag, tg.data(), sizeof(int64_t) * tg.size(), cudaMemcpyHostToDevice, h->stream);
-      cudaStreamSynchronize(h->stream);
-    }
-  }
   // validation + ||H||_1 on the device
   int* d_err = reinterpret_cast<int*>(h->d_counter + 4);
   unsigned long long* d_norm = reinterpret_cast<unsigned long long*>(h->d_small + kOffScalar);
@@ -1032,12 +929,6 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
   double nrm;
   std::memcpy(&nrm, &nb, sizeof nrm);
   h->norm1 = nrm;
-  {  // lanes per row of the standalone SpMV ~ average row length / 3 (power of two, 2..32)
-    const double avg = (double)h->nnz / (double)n;
-    int t = 2;
-    while (t < 32 && 3.0 * t < avg) t <<= 1;
-    h->spmv_tpr = t;
-  }
   h->launches += 1;
   return h;
 }
@@ -1090,9 +981,6 @@ void te_destroy(te_handle* h) {
   cudaFree(h->d_peer_base);
   cudaFree(h->d_peer_ldv);
   for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
-  cudaFree(h->d_tile_row);
-  cudaFree(h->d_tile_desc);
-  cudaFree(h->d_tile_ag);
   cudaFree(h->d_tile_ring);
   cudaFree(h->d_scol);
   cudaFree(h->d_sval);
@@ -1298,8 +1186,8 @@ int te_set_option(te_handle* h, int option, double value) {
       h->use_graph = value != 0.0;
       return TE_OK;
     case TE_OPT_KERNELS:
-      if (value < 0.0 || value > 4.0 || value != (double)(int)value)
-        return set_err(TE_ERR_ARG, "TE_OPT_KERNELS must be 0..4");
+      if (value != 2.0 && value != 3.0 && value != 4.0)
+        return set_err(TE_ERR_ARG, "TE_OPT_KERNELS must be 2 (hybrid), 3 (TMA ring) or 4 (shuffle)");
       h->variant = (int)value;
       return TE_OK;
     case TE_OPT_ORTHO:
@@ -1316,8 +1204,8 @@ int te_set_option(te_handle* h, int option, double value) {
       h->integrator = (int)value;
       return TE_OK;
     case TE_OPT_SPMV:
-      if (value < 0.0 || value > 7.0 || value != (double)(int)value)
-        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 0..7");
+      if (value != 6.0 && value != 7.0)
+        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 7 (ring) or 6 (SELL-32-sigma)");
       if (value == 6.0) {
         const int rc = build_sell(h);
         if (rc != TE_OK) return rc;
