@@ -137,14 +137,14 @@ int te_krylov_basis(te_handle* h, const te_c128* v1, int m, double tol_rate, dou
 enum {
   TE_OPT_PROFILE = 1,        /* 1: record CUDA events around every kernel launch (te_get_profile) */
   TE_OPT_GRAPH = 2,          /* 1 (default): replay each restart's launches as a CUDA graph      */
-  TE_OPT_KERNELS = 3,        /* kernel set (same arithmetic, kept for measured comparison):
-                                2 (default): nnz-balanced SpMV + projections chosen by column count
-                                  (register-streaming/shuffle kernel for <= 4 (dots) / <= 8 (update) columns, TMA-tiled above);
-                                3: SpMV + TMA-tiled (2-D tensor boxes) warp-specialised projections;
-                                4: SpMV + register-streaming/shuffle projections;
-                                0: register-streaming fused K1/K2; 1: shared-memory staged K1 and
-                                  bulk-copy staged K2                                                */
-  TE_OPT_PREFETCH = 4,       /* L2 bulk-prefetch distance (block iterations, 0..16; default 0)     */
+  TE_OPT_KERNELS = 3,        /* projection kernels (same arithmetic, kept for measured comparison):
+                                2 (default): chosen by column count (register-streaming/shuffle
+                                  kernel for <= 4 (dots) / <= 5 (update) columns, TMA-tiled above);
+                                3: TMA-tiled (2-D tensor boxes) warp-specialised projections only;
+                                4: register-streaming/shuffle projections only.  Other values:
+                                TE_ERR_ARG (round 1's fused sets 0/1 were removed)                  */
+  TE_OPT_PREFETCH = 4,       /* update_norm's L2 bulk-prefetch distance (block iterations, 0..16;
+                                default 0)                                                          */
   TE_OPT_ORTHO = 6,          /* orthogonalisation: 0 (default) CGS2 against the full basis (reading
                                 C1, BASELINE north star); 1 the paper's 3-term Lanczos recurrence as
                                 printed (Eq. 8; Alg. 1), B_H + 144n bytes/step;
@@ -157,31 +157,33 @@ enum {
                                 exchange before each SpMV; 1 the SpMV reads halo columns straight
                                 from the owning rank's V column (peer memory: CUDA IPC over NVLink,
                                 or the same address space) — SURVEY f4, the exchange fused into
-                                the SpMV.  Used with TE_OPT_SPMV 7 (default) or 4.            */
-  TE_OPT_SPMV = 5            /* SpMV kernel of kernel sets 2-4 (same arithmetic, measured choice):
-                                7 (default) warp-specialised ring: one producer warp bulk-copies
-                                (TMA engine) rowptr/col/val of nnz-balanced tiles into a 4-stage
-                                shared-memory ring, 15 consumer warps (TPR lanes per row, 12-16
+                                the SpMV.  Used with TE_OPT_SPMV 7 or 8.                       */
+  TE_OPT_SPMV = 5            /* SpMV kernel (same arithmetic, measured choice):
+                                8 staged-x ring: the ring below, and each tile's x windows (column
+                                ranges planned on the device at create: >= 2 distinct columns at
+                                >= 1/4 density) bulk-copied into shared memory too; entries are
+                                addressed by 16-bit slots (0xFFFF: gathered from global memory).
+                                The default when the plan stages >= 95 % of the entries
+                                (structured H: spin chains, bosons, the paper's §5 model);
+                                7 warp-specialised ring: one producer warp bulk-copies (TMA
+                                engine) rowptr/col/val of nnz-balanced tiles into a 3-4 stage
+                                shared-memory ring, 15 consumer warps (TPR lanes per row, 8-16
                                 register gathers in flight per lane) release stages per warp —
-                                no block barrier per tile;
-                                4 the same tiles double-buffered per block of 8 warps with a block
-                                barrier per tile;
+                                no block barrier per tile.  The default otherwise;
                                 6 SELL-32-sigma: rows sorted by length in 4096-row windows, 32-row
                                 slices stored column-major, one lane per row, software-pipelined
                                 loads (a padded copy of H is built on the device when selected;
-                                TE_ERR_ARG if padding would exceed the entry count);
-                                5 async gather: 1024-entry tiles, 3-stage bulk-copy ring, x gathers
-                                as cp.async copies into shared memory overlapping the previous
-                                tile's products;
-                                3 as 4 without the pipeline; 1 nnz-balanced tiles, entry-parallel products;
-                                2 TMA-fed (bulk copies of rowptr/col/val into a shared-memory ring,
-                                warp-specialised); 0 CSR-vector                                       */
+                                TE_ERR_ARG if padding would exceed the entry count).
+                                Other values: TE_ERR_ARG (round 1's slower variants were removed) */
 };
 int te_set_option(te_handle* h, int option, double value);
+/* Current value of an option (TE_OPT_SPMV reports the kernel the handle runs, e.g. the default
+ * chosen at create); TE_ERR_ARG for a null handle/pointer or an unknown option. */
+int te_get_option(const te_handle* h, int option, double* value);
 
 /* Per-kernel-class profile accumulated while TE_OPT_PROFILE is on (reset by te_set_option):
- * kernel: 0 spmv (K1a; fused spmv_proj K1 in variants 0/1), 1 update_proj (K2), 2 update_norm (K3),
- * 3 combine V.omega (K4), 4 halo pack (distributed), 5 proj_dots (K1b, variant 2), 6 host step
+ * kernel: 0 spmv (K1a), 1 update_proj (K2), 2 update_norm (K3),
+ * 3 combine V.omega (K4), 4 halo pack (distributed), 5 proj_dots (K1b), 6 host step
  * search (eigensolve + quadrature + omega; wall-clock ms, alg_bytes 0).  launches, total device milliseconds (CUDA events on the
  * launching stream) and algorithmic bytes. */
 typedef struct { int64_t launches; double total_ms; double alg_bytes; } te_kernel_profile;
@@ -193,9 +195,8 @@ int64_t te_launch_count(const te_handle* h);
 /* ||H||_1 of the handle's matrix (global for distributed handles). */
 double te_one_norm(const te_handle* h);
 
-/* Diagnostics: compiled attributes of a hot-path kernel (which: 0 spmv (the default ring kernel,
- * real values, one lane per row), 1 proj_dots, 2 update_proj (TMA), 3 update_norm, 4 spmv_proj
- * (register), 5 update_proj (register)). */
+/* Diagnostics: compiled attributes of a hot-path kernel (which: 0 spmv (the ring kernel, real
+ * values, one lane per row), 1 proj_dots, 2 update_proj (TMA), 3 update_norm). */
 int te_kernel_attributes(int which, int* regs, int* max_threads, int* static_smem, int* max_dyn_smem);
 
 /* Thread-local status / message of the last failing call (TE_OK / "" if none). */

@@ -97,7 +97,7 @@ __device__ __forceinline__ double step_gate(const KDev& d, int j, bool writer) {
     if (writer && d.ortho == 2) d.G[0] = make_double2(1.0, 0.0);
     return 1.0;
   }
-  const double b = sqrt(d.nrm2[j - 1]);
+  const double b = sqrt(d.defer ? d.gsync[0].x : d.nrm2[j - 1]);
   if (!isfinite(b)) {
     if (writer) { d.beta[j - 1] = b; d.flag[1] = j; d.flag[0] = 2; }
     return 0.0;
@@ -121,6 +121,24 @@ __device__ __forceinline__ double step_gate(const KDev& d, int j, bool writer) {
     }
   }
   return sj;
+}
+
+// The step-j gate decision as a pure function (every thread of a deferred update kernel evaluates it
+// from the same loads, in parallel with its coefficient loads; block 0 / thread 0 also runs
+// step_gate for the side effects, reaching the same decision)
+__device__ __forceinline__ double gate_value(const KDev& d, int j, int flag0, double nrm_prev) {
+  if (flag0 != 0) return 0.0;
+  if (j == 0) return 1.0;
+  const double b = sqrt(nrm_prev);
+  if (!isfinite(b) || b < d.tol_rate) return 0.0;
+  return 1.0 / b;
+}
+
+// Gate of the SpMV of step j: in defer mode (CGS2, f2) only the breakdown flag of earlier steps
+// (the SpMV writes H V_j unscaled; the update kernel applies s_j), else the full step gate.
+__device__ __forceinline__ double spmv_gate(const KDev& d, int j, bool writer) {
+  if (d.defer) return d.flag[0] != 0 ? 0.0 : 1.0;
+  return step_gate(d, j, writer);
 }
 
 // Per-CTA column partials -> global; the last CTA sums them in fixed block order.
@@ -218,6 +236,13 @@ struct ValT<true> {
   static __device__ __forceinline__ double2 ldcs(const double2* p) { return __ldcs(p); }
 };
 
+
+// halo entry hi of step j from the owning rank's V column (uncached: written by another GPU)
+__device__ __forceinline__ double2 peer_x(const KDev& d, int j, int hi) {
+  const int q = __ldg(d.halo_owner + hi);
+  const double2* base = d.peer_base[q];
+  return __ldcv(base + (int64_t)j * __ldg(d.peer_ldv + q) + __ldg(d.halo_lidx + hi));
+}
 
 template <int TPR>
 __device__ __forceinline__ double2 group_sum(double2 v) {

@@ -161,27 +161,54 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
   const int ncols = j + 1;
   __shared__ double2 c1s[kMaxCols];
   __shared__ double nrm_s[kConsumers];
-  if (tid == 0) go_s = (d.flag[0] == 0);
-  if (MODE == 1 && tid < ncols) {
-    const double sk = d.s[tid];
-    const double2 g = d.g1[tid];
-    coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);   // e1_k = s_k c1_k
+  __shared__ double sj_s;
+  // MODE 1 / 3 run the deferred gate of step j (device_common.cuh step_gate: s_j from the reduced
+  // ||p''_{j-1}||^2, breakdown test; block 0 records beta_{j-1}, s_j and, for f2, Gram row j):
+  // W holds H V_j unscaled, g1 its raw dots, so p' = s_j (W - V e1') with e1'_k = s_k^2 g1_k
+  const double sj = (MODE == 1 || MODE == 3) ? gate_value(d, j, d.flag[0], d.gsync[0].x) : (d.flag[0] == 0 ? 1.0 : 0.0);
+  if (tid == 0) {
+    if ((MODE == 1 || MODE == 3) && blockIdx.x == 0) step_gate(d, j, true);
+    sj_s = sj;
+    go_s = sj != 0.0;
   }
-  if (MODE == 3) {  // f2: c1 = s g1, c2 = c1 - G c1, coefficient on raw V_k: s_k (c1_k + c2_k)
+  if (MODE == 1 && tid < ncols) {
+    const double sk = tid == j ? sj : d.s[tid];
+    const double2 g = d.g1[tid];
+    coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);   // e1'_k = s_k^2 g1_k
+  }
+  if (MODE == 3) {  // f2: c1' = s g1, c2' = c1' - G c1', coefficient on raw V_k: s_k (c1'_k + c2'_k)
     if (tid < ncols) {
-      const double sk = d.s[tid];
+      const double sk = tid == j ? sj : d.s[tid];
       const double2 g = d.g1[tid];
       c1s[tid] = make_double2(sk * g.x, sk * g.y);
     }
     __syncthreads();
-    if (tid < ncols) {
+    if (tid < ncols && go_s) {
+      // Gram entries: rows/columns < j from earlier gates (global), row/column j formed here from
+      // the reduced dots of the previous update pass (the same values block 0's gate stores)
       double2 gc = make_double2(0.0, 0.0);
-      for (int l = 0; l < ncols; ++l) gc = cfma(d.G[tid * kMaxCols + l], c1s[l], gc);
+      for (int l = 0; l < ncols; ++l) {
+        double2 G;
+        if (l == tid) {
+          G = make_double2(1.0, 0.0);
+        } else if (tid < j && l < j) {
+          G = d.G[tid * kMaxCols + l];
+        } else if (l == j) {
+          const double sk = d.s[tid] * sj;
+          const double2 g = d.g2[tid];
+          G = make_double2(sk * g.x, sk * g.y);
+        } else {
+          const double sk = d.s[l] * sj;
+          const double2 g = d.g2[l];
+          G = make_double2(sk * g.x, -sk * g.y);
+        }
+        gc = cfma(G, c1s[l], gc);
+      }
       const double2 c1 = c1s[tid];
       const double2 c = make_double2(c1.x + (c1.x - gc.x), c1.y + (c1.y - gc.y));
-      const double sk = d.s[tid];
+      const double sk = tid == j ? sj : d.s[tid];
       coef[tid] = make_double2(sk * c.x, sk * c.y);
-      if (tid == j && blockIdx.x == 0 && d.flag[0] == 0) d.alpha[j] = c.x;  // Re(c1_j + c2_j)
+      if (tid == j && blockIdx.x == 0) d.alpha[j] = sj * c.x;  // Re(c1_j + c2_j) = s_j Re(c1'_j + c2'_j)
     }
   }
   // 1024-B alignment through an integer cast: the consumers then read the tiles with generic
@@ -272,7 +299,7 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
             if (k + 5 < ncols) a5 = cfma(Vs[(k + 5) * TR + row], coef[k + 5], a5);
             if (k + 6 < ncols) a6 = cfma(Vs[(k + 6) * TR + row], coef[k + 6], a6);
             const double2 a = cadd(cadd(cadd(a0, a1), cadd(a2, a3)), cadd(cadd(a4, a5), cadd(a6, a7)));
-            p = make_double2(p.x - a.x, p.y - a.y);
+            p = make_double2(sj * (p.x - a.x), sj * (p.y - a.y));
             if (row >= rows) p = make_double2(0.0, 0.0);
             else if (MODE == 1) d.W[r0 + row] = p;
             else {
@@ -369,6 +396,8 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
     for (int b = 0; b < G; ++b) t += __ldcg(d.partn + b);
     d.nrm2[j] = t;
   }
+  // ||p''_{j-1}||^2 rides with g1 in the step's first reduction (defer mode)
+  if (MODE == 0 && tid == 0) d.gsync[0] = make_double2(j > 0 ? d.nrm2[j - 1] : 0.0, 0.0);
   if (tid == 0) d.counter[ctr] = 0u;
 }
 
@@ -386,13 +415,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_proj_s(KDev d, int j) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = tid % TPR, grp = tid / TPR;
   constexpr int RPB = kThreads / TPR;
   const int ncols = j + 1;
-  if (tid == 0) go_s = (d.flag[0] == 0);
+  // MODE 1: the deferred step gate (as in k_proj_tma)
+  const double sj = MODE == 1 ? gate_value(d, j, d.flag[0], d.gsync[0].x) : (d.flag[0] == 0 ? 1.0 : 0.0);
+  if (tid == 0) {
+    if (MODE == 1 && blockIdx.x == 0) step_gate(d, j, true);
+    go_s = sj != 0.0;
+  }
+  for (int i = tid; i < kWarps * kMaxCols; i += kThreads) (&red[0][0])[i] = make_double2(0.0, 0.0);
   if (MODE == 1 && tid < ncols) {
-    const double sk = d.s[tid];
+    const double sk = tid == j ? sj : d.s[tid];
     const double2 g = d.g1[tid];
     coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);
   }
-  for (int i = tid; i < kWarps * kMaxCols; i += kThreads) (&red[0][0])[i] = make_double2(0.0, 0.0);
   __syncthreads();
   if (!go_s) return;
   const int64_t n = d.n, ldv = d.ldv;
@@ -415,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_proj_s(KDev d, int j) {
         if (k < ncols) a = cfma(v[c], coef[k], a);
       }
       a = group_sum<TPR>(a);
-      p = make_double2(p.x - a.x, p.y - a.y);
+      p = make_double2(sj * (p.x - a.x), sj * (p.y - a.y));
       if (act && q == 0) d.W[r] = p;
     }
 #pragma unroll
@@ -466,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_proj_s(KDev d, int j) {
     t = cadd(t, seg[3][tid]);
     out[tid] = t;
   }
+  if (MODE == 0 && tid == 0) d.gsync[0] = make_double2(j > 0 ? d.nrm2[j - 1] : 0.0, 0.0);
   if (tid == 0) d.counter[ctr] = 0u;
 }
 
@@ -479,9 +514,9 @@ __global__ void __launch_bounds__(kThreads) k_update_norm(KDev d, int j, int wri
   const int ncols = j + 1;
   if (tid == 0) {
     go_s = (d.flag[0] == 0);
-    if (go_s && blockIdx.x == 0) {  // alpha_j = Re(c1_j + c2_j) (reading C2)
+    if (go_s && blockIdx.x == 0) {  // alpha_j = Re(c1_j + c2_j) (reading C2); g1 = raw dots of H V_j
       const double sj = d.s[j];
-      d.alpha[j] = sj * (d.g1[j].x + d.g2[j].x);
+      d.alpha[j] = sj * (sj * d.g1[j].x + d.g2[j].x);
     }
   }
   if (tid < ncols) {

@@ -41,6 +41,14 @@ struct KDev {
   int64_t nslices;
   const int64_t* tile_ring;  // [4*ntiles_ring] {first row, end row, first entry, end entry} (variant 7)
   int64_t ntiles_ring;
+  // staged-x ring SpMV (variant 8): its own tiles, per-tile x ranges staged into shared memory by
+  // bulk copies, and per-entry 16-bit shared-memory slots (0xFFFF: gathered from global memory)
+  const int64_t* tile_xs;    // [4*ntiles_xs] {first row, end row, first entry, end entry}
+  int64_t ntiles_xs;
+  const int4* xs_meta;       // [ntiles_xs] {ranges, staged slots, global entries, 0}
+  const int2* xs_rng;        // [ntiles_xs * xs_rmax] {first column, length}; slots follow in order
+  const uint16_t* lcol;      // [nnz + 8] slot of each entry in its tile's staged x
+  int xs_ecap, xs_xcap, xs_rmax;  // entries per tile, staged x slots per tile, ranges per tile
   const double2* halo;  // x entries for columns >= n (distributed); nullptr otherwise
   double* s;            // [m_cap+1] column scales
   double* alpha;        // [m_cap]
@@ -56,6 +64,11 @@ struct KDev {
   int m;                // Krylov dimension of the current restart
   int ortho;            // 0 CGS2, 1 Lanczos (f1), 2 CGS2 with Gram-matrix second sweep (f2)
   double2* G;           // [kMaxCols x kMaxCols] Gram matrix <v_k, v_l> of the normalised basis (f2)
+  int defer;            // 1 (CGS2, f2): the SpMV writes H V_j unscaled and the step-j gate (s_j, breakdown)
+                        // runs in the update kernel after the step's first reduction, which also
+                        // carries ||p''_{j-1}||^2 (one allreduce fewer per step on several ranks);
+                        // 0 (f1 Lanczos): the SpMV applies the gate itself
+  double2* gsync;       // [1] .x = ||p''_{j-1}||^2 as reduced together with g1 (defer mode)
 };
 
 struct Launch {
@@ -68,8 +81,10 @@ struct Launch {
   int halo_peer;        // SpMV reads halo columns from peer memory (no staged exchange)
   int spmv_ring_tpr;    // lanes per row of the warp-specialised ring SpMV
   int ring_stages;      // its ring depth: 4 (short real rows) or 3 (larger tiles)
+  int spmv_xs_tpr;      // lanes per row of the staged-x ring SpMV
+  int xs_stages;        // its ring depth (2 or 3)
   int proj_tma;         // 2: hybrid by column count (default), 1: TMA-tiled only, 0: register/shuffle only
-  int spmv_tiled;       // 7: warp-specialised ring (default), 6: SELL-32-sigma
+  int spmv_tiled;       // 8: staged-x ring, 7: warp-specialised ring, 6: SELL-32-sigma
   int prefetch;         // update_norm: L2 bulk-prefetch distance in block iterations (0: off)
 };
 
@@ -87,6 +102,17 @@ void set_attr(const void* f, size_t want, void* ctx);
 void configure_spmv_kernels(void (*set_attr)(const void*, size_t, void*), void* ctx);
 const void* spmv_attr_kernel();  // the SpMV kernel reported by kernel_attributes(0)
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L);        // K1a: SpMV only
+// staged-x ring SpMV (spmv_xs.cu): plan (create time) and launch
+constexpr int kXsConsumers = 15;
+constexpr int kXsRmax = 64;      // x ranges per tile
+constexpr int kXsGap = 8;        // bridge gaps of < 8 unused x entries (128 B) inside a range
+constexpr size_t kXsBudget = 220 * 1024;  // shared memory of the 2-3 stage ring
+size_t spmv_xs_smem(bool cplx, int tpr, int ecap, int xcap, int stages);
+int xs_xcap_for(bool cplx, int tpr, int ecap, size_t budget, int stages);
+void launch_xs_plan(const int64_t* tiles, int64_t ntiles, const int32_t* col, int64_t ncol_stage, int xcap, int rmax,
+                    int gap, int4* meta, int2* rng, uint16_t* lcol, cudaStream_t st);
+void configure_xs_kernels(void (*set_attr)(const void*, size_t, void*), void* ctx, size_t budget);
+void launch_spmv_xs(const KDev& d, bool cplx, int j, const Launch& L);
 void launch_proj_dots(const KDev& d, int j, const Launch& L);              // K1b: g1 = V^H p (TMA)
 void launch_update_proj(const KDev& d, int j, const Launch& L);            // K2
 void launch_gram_update(const KDev& d, int j, bool write, const Launch& L); // f2: p'' = p - V(c1+c2) -> V_{j+1}, V^H p'', ||p''||^2

@@ -4,6 +4,7 @@
 //   7 k_spmv_ring  (default) warp-specialised: producer warp + 15 consumer warps, 3-4 stage
 //                  bulk-copy ring of nnz-balanced tiles, per-warp stage release
 //   6 k_spmv_sell  SELL-32-sigma copy of H, software-pipelined coalesced loads
+//   8 k_spmv_xs    (spmv_xs.cu) the ring with each tile's x windows staged by bulk copies
 // The variants measured slower in round 1 (CSR-vector, row tiles, TMA slots, block-pipelined,
 // async gather; DESIGN.md §6 keeps their numbers) were removed from the library.
 // All variants sum each row's products in a fixed order (deterministic); parity-tested against
@@ -17,12 +18,6 @@
 
 namespace te {
 
-// halo entry hi of step j from the owning rank's V column (uncached: written by another GPU)
-__device__ __forceinline__ double2 peer_x(const KDev& d, int j, int hi) {
-  const int q = __ldg(d.halo_owner + hi);
-  const double2* base = d.peer_base[q];
-  return __ldcv(base + (int64_t)j * __ldg(d.peer_ldv + q) + __ldg(d.halo_lidx + hi));
-}
 
 // SpMV variant 7 (warp-specialised ring): one producer warp issues the bulk copies of tiles into
 // a kRingStages-deep shared-memory ring (full/empty mbarriers); 15 consumer warps process every tile
@@ -60,7 +55,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_spmv_ring(KDev d, int j) {
   __shared__ double sj_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    sj_s = step_gate(d, j, blockIdx.x == 0);
+    sj_s = spmv_gate(d, j, blockIdx.x == 0);
     for (int k = 0; k < kRingStages; ++k) {
       mbar_init(&full[k], 1);
       mbar_init(&empty[k], kRingConsumers);
@@ -75,9 +70,20 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_spmv_ring(KDev d, int j) {
     if (lane != 0) return;
     const uint64_t pol = policy_evict_first();
     constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
+    // tile descriptors loaded one tile ahead, before the wait for a free stage
+    auto ld_desc = [&](int64_t t, longlong2& a, longlong2& b) {
+      if (t < d.ntiles_ring) {
+        a = __ldg(reinterpret_cast<const longlong2*>(d.tile_ring + 4 * t));
+        b = __ldg(reinterpret_cast<const longlong2*>(d.tile_ring + 4 * t) + 1);
+      }
+    };
+    longlong2 ca = make_longlong2(0, 0), cb = ca;
+    ld_desc(blockIdx.x, ca, cb);
     for (int64_t it = 0;; ++it) {
       const int64_t t = blockIdx.x + it * G;
       const int st = (int)(it % kRingStages);
+      longlong2 na = make_longlong2(0, 0), nb = na;
+      ld_desc(t + G, na, nb);
       if (it >= kRingStages) mbar_wait(&empty[st], (unsigned)(((it / kRingStages) - 1) & 1));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (t >= d.ntiles_ring) {  // tell the consumers there is nothing more
@@ -85,8 +91,9 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_spmv_ring(KDev d, int j) {
         mbar_expect_tx(&full[st], 0);
         break;
       }
-      const longlong2 a = __ldg(reinterpret_cast<const longlong2*>(d.tile_ring + 4 * t));
-      const longlong2 b = __ldg(reinterpret_cast<const longlong2*>(d.tile_ring + 4 * t) + 1);
+      const longlong2 a = ca, b = cb;
+      ca = na;
+      cb = nb;
       desc[st][0] = a.x; desc[st][1] = a.y; desc[st][2] = b.x; desc[st][3] = b.y;
       const int64_t cnt = b.y - b.x;
       const int64_t r0 = a.x & ~1LL, r1 = (a.y + 2) & ~1LL;
@@ -219,7 +226,7 @@ template <bool CPLX, bool HALO, int U>
 __global__ void __launch_bounds__(kThreads, 2) k_spmv_sell(KDev d, int j) {
   using VT = typename ValT<CPLX>::T;
   __shared__ double sj_s;
-  if (threadIdx.x == 0) sj_s = step_gate(d, j, blockIdx.x == 0);
+  if (threadIdx.x == 0) sj_s = spmv_gate(d, j, blockIdx.x == 0);
   __syncthreads();
   const double sj = sj_s;
   if (sj == 0.0) return;
@@ -292,6 +299,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_sell(KDev d, int j) {
 }
 
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
+  if (L.spmv_tiled == 8 && d.ntiles_xs > 0) {
+    launch_spmv_xs(d, cplx, j, L);
+    return;
+  }
   if (L.spmv_tiled == 6 && d.nslices > 0) {
     const bool hal = d.halo || L.spmv_force_halo;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)8 * L.num_sms, (d.nslices + kWarps - 1) / kWarps));
@@ -343,6 +354,7 @@ void configure_spmv_kernels(void (*set_attr)(const void*, size_t, void*), void* 
   TE_SETRING(1, 2) TE_SETRING(2, 2) TE_SETRING(4, 2) TE_SETRING(8, 2)
 #undef TE_SETRING
 #undef TE_SETRING_S
+  configure_xs_kernels(set_attr, ctx, kXsBudget);
 }
 
 // the default SpMV as launched for a real matrix with one lane per row (config 2)

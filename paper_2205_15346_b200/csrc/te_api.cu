@@ -101,7 +101,7 @@ struct te_handle {
   double2* d_V = nullptr;
   double2* d_W = nullptr;
   double* d_small = nullptr;  // alpha[64] beta[64] | flag (2 ints) | s[65] nrm2[64] scalar
-  double2* d_g = nullptr;     // g1[64] g2[64] coef[64]
+  double2* d_g = nullptr;     // [0] reduction slot (||p''_{j-1}||^2) | g1[64] | g2[64] | coef[64]
   double2* d_G = nullptr;     // Gram matrix 64 x 64 (f2)
   double2* d_part = nullptr;
   double* d_partn = nullptr;
@@ -121,6 +121,16 @@ struct te_handle {
   int64_t ntiles_ring = 0;
   int spmv_ring_tpr = 1;
   int ring_stages = 4;
+  // staged-x ring SpMV (variant 8): tiles + plan, built at create (kept when it is the default)
+  // or on first selection
+  int64_t* d_tile_xs = nullptr;
+  int64_t ntiles_xs = 0;
+  int4* d_xs_meta = nullptr;
+  int2* d_xs_rng = nullptr;
+  uint16_t* d_lcol = nullptr;
+  int spmv_xs_tpr = 1, xs_ecap = 0, xs_xcap = 0, xs_stages = 2;
+  double xs_global_frac = 1.0;  // entries the plan left to global gathers / nnz
+  int64_t ncol_limit = 0;
   // SELL-32-sigma copy of H (SpMV variant 6), built on first selection
   int32_t* d_scol = nullptr;
   void* d_sval = nullptr;
@@ -171,11 +181,17 @@ struct te_handle {
   int64_t n_send = 0;
 };
 
+extern "C" {
+static int build_sell(te_handle* h);
+}
+
 namespace {
 
 // device layout of d_small (doubles)
 constexpr int kOffAlpha = 0, kOffBeta = 64, kOffFlag = 128, kOffS = 130, kOffNrm = 196, kOffScalar = 260,
               kSmallLen = 264;
+// layout of d_g (double2): the reduction slot, g1, g2, the V.omega coefficients
+constexpr int kOffG1 = 1, kOffG2 = 65, kOffCoef = 129, kGLen = 193;
 
 KDev make_kdev(te_handle* h, double tol_rate, int m) {
   KDev d{};
@@ -193,6 +209,14 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.halo_lidx = h->d_halo_lidx;
   d.tile_ring = h->d_tile_ring;
   d.ntiles_ring = h->ntiles_ring;
+  d.tile_xs = h->d_tile_xs;
+  d.ntiles_xs = h->ntiles_xs;
+  d.xs_meta = h->d_xs_meta;
+  d.xs_rng = h->d_xs_rng;
+  d.lcol = h->d_lcol;
+  d.xs_ecap = h->xs_ecap;
+  d.xs_xcap = h->xs_xcap;
+  d.xs_rmax = te::kXsRmax;
   d.scol = h->d_scol;
   d.sval = h->d_sval;
   d.sptr = h->d_sptr;
@@ -204,8 +228,10 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.flag = reinterpret_cast<int*>(h->d_small + kOffFlag);
   d.s = h->d_small + kOffS;
   d.nrm2 = h->d_small + kOffNrm;
-  d.g1 = h->d_g;
-  d.g2 = h->d_g + 64;
+  d.gsync = h->d_g;
+  d.g1 = h->d_g + kOffG1;
+  d.g2 = h->d_g + kOffG2;
+  d.defer = h->ortho != 1;
   d.part = h->d_part;
   d.partn = h->d_partn;
   d.counter = h->d_counter;
@@ -216,9 +242,9 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   return d;
 }
 
-// halo mode 1 is used by the ring SpMV; the SELL variant keeps the staged exchange
+// halo mode 1 is used by the ring SpMVs (7, 8); the SELL variant keeps the staged exchange
 bool peer_active(const te_handle* h) {
-  return h->dist && h->dist->nranks > 1 && h->halo_mode == 1 && h->spmv_tiled == 7;
+  return h->dist && h->dist->nranks > 1 && h->halo_mode == 1 && (h->spmv_tiled == 7 || h->spmv_tiled == 8);
 }
 
 Launch make_launch(te_handle* h) {
@@ -233,6 +259,8 @@ Launch make_launch(te_handle* h) {
   L.spmv_force_halo = h->spmv_force_halo;
   L.halo_peer = peer_active(h) ? 1 : 0;
   L.spmv_ring_tpr = h->spmv_ring_tpr;
+  L.spmv_xs_tpr = h->spmv_xs_tpr;
+  L.xs_stages = h->xs_stages;
   L.ring_stages = h->ring_stages;
   L.spmv_tiled = h->spmv_tiled;
   L.prefetch = h->prefetch;
@@ -288,7 +316,8 @@ int ensure_workspace(te_handle* h, int m) {
   if (h->d_small == nullptr) {
     CK(cudaMalloc(&h->d_small, sizeof(double) * kSmallLen));
     CK(cudaMemsetAsync(h->d_small, 0, sizeof(double) * kSmallLen, s));
-    CK(cudaMalloc(&h->d_g, sizeof(double2) * 3 * 64));
+    CK(cudaMalloc(&h->d_g, sizeof(double2) * kGLen));
+    CK(cudaMemsetAsync(h->d_g, 0, sizeof(double2) * kGLen, s));
     CK(cudaMalloc(&h->d_G, sizeof(double2) * te::kMaxCols * te::kMaxCols));
     CK(cudaMemsetAsync(h->d_G, 0, sizeof(double2) * te::kMaxCols * te::kMaxCols, s));
     h->max_grid = 8 * h->num_sms;
@@ -500,38 +529,39 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
       if ((rc = allreduce_sum(h, d.nrm2 + j, 1))) return rc;
       continue;
     }
-    if (h->ortho == 2) {  // f2: CGS2 with the Gram-matrix second sweep, two V passes per step
-      prof_begin(h);
-      te::launch_spmv(d, h->cplx, j, L); LCHECK("spmv");
-      prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
-      prof_begin(h);
-      te::launch_proj_dots(d, j, L); LCHECK("proj_dots");
-      prof_end(h, 5, 16.0 * n * ncols + 16.0 * n);
-      if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g1), 2 * (size_t)(j + 1)))) return rc;
-      const bool wr = j + 1 < m;
-      prof_begin(h);
-      te::launch_gram_update(d, j, wr, L); LCHECK("gram_update");
-      prof_end(h, 1, 16.0 * n * ncols + 16.0 * n + (wr ? 16.0 * n : 0.0));
-      if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g2), 2 * (size_t)(j + 1)))) return rc;
-      if ((rc = allreduce_sum(h, d.nrm2 + j, 1))) return rc;
-      continue;
-    }
+    // CGS2 and f2 (defer mode): the SpMV writes H V_j unscaled; the update kernel applies s_j after
+    // the step's first reduction, which carries ||p''_{j-1}||^2 next to g1 (and, for f2, the
+    // previous update pass's Gram dots g2): 2 allreduces per step for CGS2, 1 for f2 (plus one
+    // barrier per step in peer-load halo mode, where a rank's SpMV reads its peers' V_j)
     prof_begin(h);
     te::launch_spmv(d, h->cplx, j, L); LCHECK("spmv");
     prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
     prof_begin(h);
     te::launch_proj_dots(d, j, L); LCHECK("proj_dots");
     prof_end(h, 5, 16.0 * n * ncols + 16.0 * n);
-    if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g1), 2 * (size_t)(j + 1)))) return rc;
-    prof_begin(h);
-    te::launch_update_proj(d, j, L); LCHECK("update_proj");
-    prof_end(h, 1, 16.0 * n * ncols + 32.0 * n);
-    if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g2), 2 * (size_t)(j + 1)))) return rc;
-    const bool write = j + 1 < m;
-    prof_begin(h);
-    te::launch_update_norm(d, j, write, L); LCHECK("update_norm");
-    prof_end(h, 2, 16.0 * n * ncols + 16.0 * n + (write ? 16.0 * n : 0.0));
-    if ((rc = allreduce_sum(h, d.nrm2 + j, 1))) return rc;
+    const bool wr = j + 1 < m;
+    if (h->ortho == 2) {  // f2: CGS2 with the Gram-matrix second sweep, two V passes per step
+      if ((rc = allreduce_sum(h, reinterpret_cast<double*>(h->d_g), 2 * (size_t)(kOffG2 + j)))) return rc;
+      prof_begin(h);
+      te::launch_gram_update(d, j, wr, L); LCHECK("gram_update");
+      prof_end(h, 1, 16.0 * n * ncols + 16.0 * n + (wr ? 16.0 * n : 0.0));
+    } else {
+      if ((rc = allreduce_sum(h, reinterpret_cast<double*>(h->d_g), 2 * (size_t)(kOffG1 + j + 1)))) return rc;
+      prof_begin(h);
+      te::launch_update_proj(d, j, L); LCHECK("update_proj");
+      prof_end(h, 1, 16.0 * n * ncols + 32.0 * n);
+      if ((rc = allreduce_sum(h, reinterpret_cast<double*>(d.g2), 2 * (size_t)(j + 1)))) return rc;
+      prof_begin(h);
+      te::launch_update_norm(d, j, wr, L); LCHECK("update_norm");
+      prof_end(h, 2, 16.0 * n * ncols + 16.0 * n + (wr ? 16.0 * n : 0.0));
+    }
+    if (peer_active(h) && wr) {  // V_{j+1} complete on every rank before any rank's next SpMV reads it
+      if ((rc = allreduce_sum(h, h->d_small + kOffScalar, 1))) return rc;
+    }
+  }
+  if (h->ortho != 1) {  // the last step's ||p''_{m-1}||^2 (h_{m+1,m}) is reduced once per restart
+    const int rc = allreduce_sum(h, h->d_small + kOffNrm + (m - 1), 1);
+    if (rc) return rc;
   }
   te::launch_finalize(d, m - 1, L); LCHECK("finalize");
   ++h->launches;
@@ -724,10 +754,10 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
         const double s = q == 0 ? 1.0 : 1.0 / beta[q - 1];
         h->h_coef[q] = make_double2(om[q].real() * s, om[q].imag() * s);
       }
-      CK(cudaMemcpyAsync(h->d_g + 128, h->h_coef, sizeof(double2) * m_eff, cudaMemcpyHostToDevice, h->stream));
+      CK(cudaMemcpyAsync(h->d_g + kOffCoef, h->h_coef, sizeof(double2) * m_eff, cudaMemcpyHostToDevice, h->stream));
       KDev d = make_kdev(h, tol_rate, m);
       Launch L = make_launch(h);
-      te::launch_combine(d, h->d_g + 128, m_eff, h->d_W, L);
+      te::launch_combine(d, h->d_g + kOffCoef, m_eff, h->d_W, L);
       ++h->launches;
       CK(cudaMemcpyAsync(smp->out + (size_t)si * h->n, h->d_W, vbytes, cudaMemcpyDeviceToHost, h->stream));
       CK(cudaStreamSynchronize(h->stream));  // h_coef is reused below
@@ -744,7 +774,7 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
       h->prof[6].launches += 1;
       h->prof[6].total_ms += ms;
     }
-    CK(cudaMemcpyAsync(h->d_g + 128, h->h_coef, sizeof(double2) * m_eff, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_g + kOffCoef, h->h_coef, sizeof(double2) * m_eff, cudaMemcpyHostToDevice, h->stream));
     {
       KDev d = make_kdev(h, tol_rate, m);
       Launch L = make_launch(h);
@@ -752,7 +782,7 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
         prof_begin(h);  // creates the event pool on first use
         cudaEventRecord(h->evk0, h->stream);
       }
-      te::launch_combine(d, h->d_g + 128, m_eff, h->d_V, L);
+      te::launch_combine(d, h->d_g + kOffCoef, m_eff, h->d_V, L);
       ++h->launches;
       if (peer_active(h)) {  // peers read the new V_0 directly in the next SpMV: barrier
         const int rc = allreduce_sum(h, h->d_small + kOffScalar, 1);
@@ -791,6 +821,77 @@ int check_evolve_args(te_handle* h, double t, double tol, int m_max) {
   if (!(t >= 0.0) || !std::isfinite(t)) return set_err(TE_ERR_ARG, "t must be finite and >= 0");
   if (!(tol > 0.0) || !std::isfinite(tol)) return set_err(TE_ERR_ARG, "tol must be > 0");
   if (m_max < 1 || m_max > TE_M_MAX) return set_err(TE_ERR_ARG, "m_max must be in [1, %d]", TE_M_MAX);
+  return TE_OK;
+}
+
+// ---------------------------------------------------------------- staged-x SpMV plan
+void free_xs(te_handle* h) {
+  cudaFree(h->d_tile_xs);
+  cudaFree(h->d_xs_meta);
+  cudaFree(h->d_xs_rng);
+  cudaFree(h->d_lcol);
+  h->d_tile_xs = nullptr;
+  h->d_xs_meta = nullptr;
+  h->d_xs_rng = nullptr;
+  h->d_lcol = nullptr;
+  h->ntiles_xs = 0;
+}
+
+// Tiles of <= 32*15/TPR rows and <= xs_ecap entries (TPR: <= 8 entries per lane of a mean-length
+// row), then the device plan (spmv_xs.cu): per tile the x ranges to stage and each entry's slot.
+// rowptr: host copy of the (local) row pointers.
+int plan_xs(te_handle* h, const int64_t* rowptr) {
+  free_xs(h);
+  const int64_t n = h->n;
+  const double avg = n > 0 ? (double)h->nnz / (double)n : 0.0;
+  int tx = 1;  // measured (config 2): one lane per row beats 2 / 4 (larger tiles, longer x ranges)
+  while (tx < 8 && 16.0 * tx < avg) tx <<= 1;
+  if (const char* e = getenv("TE_SPMV_XS_TPR")) {
+    const int v = atoi(e);
+    if (v == 1 || v == 2 || v == 4 || v == 8) tx = v;
+  }
+  h->spmv_xs_tpr = tx;
+  h->xs_ecap = h->cplx ? 2048 : 4096;
+  if (const char* e = getenv("TE_SPMV_XS_ECAP")) h->xs_ecap = std::max(64, std::min(8192, atoi(e)));
+  h->xs_stages = 2;
+  if (const char* e = getenv("TE_SPMV_XS_STAGES")) h->xs_stages = atoi(e) == 3 ? 3 : 2;
+  h->xs_xcap = te::xs_xcap_for(h->cplx, tx, h->xs_ecap, te::kXsBudget, h->xs_stages);
+  const int64_t rcap = 32 * te::kXsConsumers / tx;
+  std::vector<int64_t> tg;
+  int64_t st = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    const bool over_rows = (r + 1 - st) > rcap;
+    const bool over_nnz = (rowptr[r + 1] - rowptr[st]) > h->xs_ecap && r > st;
+    if (over_rows || over_nnz) {
+      tg.insert(tg.end(), {st, r, rowptr[st], rowptr[r]});
+      st = r;
+    }
+  }
+  if (n > 0) tg.insert(tg.end(), {st, n, rowptr[st], rowptr[n]});
+  const int64_t nt = (int64_t)tg.size() / 4;
+  if (nt == 0) return TE_OK;
+  if (cudaMalloc(&h->d_tile_xs, sizeof(int64_t) * tg.size()) != cudaSuccess ||
+      cudaMalloc(&h->d_xs_meta, sizeof(int4) * nt) != cudaSuccess ||
+      cudaMalloc(&h->d_xs_rng, sizeof(int2) * nt * te::kXsRmax) != cudaSuccess ||
+      cudaMalloc(&h->d_lcol, sizeof(uint16_t) * (h->nnz + 16)) != cudaSuccess) {
+    cudaGetLastError();
+    free_xs(h);
+    return set_err(TE_ERR_OOM, "staged-x SpMV plan: out of device memory");
+  }
+  cudaStream_t s = h->stream ? h->stream : h->own_stream;
+  CK(cudaMemcpyAsync(h->d_tile_xs, tg.data(), sizeof(int64_t) * tg.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(h->d_lcol, 0xFF, sizeof(uint16_t) * (h->nnz + 16), s));
+  CK(cudaMemsetAsync(h->d_xs_rng, 0, sizeof(int2) * nt * te::kXsRmax, s));
+  te::launch_xs_plan(h->d_tile_xs, nt, h->d_col, h->n, h->xs_xcap, te::kXsRmax, te::kXsGap, h->d_xs_meta, h->d_xs_rng,
+                     h->d_lcol, s);
+  CK(cudaGetLastError());
+  std::vector<int4> meta((size_t)nt);
+  CK(cudaMemcpyAsync(meta.data(), h->d_xs_meta, sizeof(int4) * nt, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  int64_t ng = 0;
+  for (const int4& m : meta) ng += m.z;
+  h->ntiles_xs = nt;
+  h->xs_global_frac = h->nnz > 0 ? (double)ng / (double)h->nnz : 0.0;
   return TE_OK;
 }
 
@@ -929,6 +1030,19 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
   double nrm;
   std::memcpy(&nrm, &nb, sizeof nrm);
   h->norm1 = nrm;
+  h->ncol_limit = ncol_limit;
+  {  // staged-x SpMV: the default when its plan stages >= 95 % of the entries (structured H);
+     // otherwise its buffers are released (re-planned if selected later).  TE_SPMV_DEFAULT overrides.
+    if (plan_xs(h, rowptr) != TE_OK) return fail(TE_ERR_OOM, "staged-x plan");
+    int def = h->ntiles_xs > 0 && h->xs_global_frac <= 0.05 ? 8 : 7;
+    if (const char* e = getenv("TE_SPMV_DEFAULT")) {
+      const int v = atoi(e);
+      if (v == 6 || v == 7 || v == 8) def = v;
+    }
+    if (def != 8) free_xs(h);
+    h->spmv_tiled = def == 6 ? 7 : def;
+    if (def == 6 && build_sell(h) == TE_OK) h->spmv_tiled = 6;
+  }
   h->launches += 1;
   return h;
 }
@@ -982,6 +1096,10 @@ void te_destroy(te_handle* h) {
   cudaFree(h->d_peer_ldv);
   for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
   cudaFree(h->d_tile_ring);
+  cudaFree(h->d_tile_xs);
+  cudaFree(h->d_xs_meta);
+  cudaFree(h->d_xs_rng);
+  cudaFree(h->d_lcol);
   cudaFree(h->d_scol);
   cudaFree(h->d_sval);
   cudaFree(h->d_sptr);
@@ -1204,10 +1322,17 @@ int te_set_option(te_handle* h, int option, double value) {
       h->integrator = (int)value;
       return TE_OK;
     case TE_OPT_SPMV:
-      if (value != 6.0 && value != 7.0)
-        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 7 (ring) or 6 (SELL-32-sigma)");
+      if (value != 6.0 && value != 7.0 && value != 8.0)
+        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 8 (staged-x ring), 7 (ring) or 6 (SELL-32-sigma)");
       if (value == 6.0) {
         const int rc = build_sell(h);
+        if (rc != TE_OK) return rc;
+      }
+      if (value == 8.0 && h->ntiles_xs == 0) {
+        std::vector<int64_t> rp((size_t)h->n + 1);
+        if (cudaMemcpy(rp.data(), h->d_rowptr, sizeof(int64_t) * (h->n + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+          return set_err(TE_ERR_CUDA, "staged-x plan: rowptr copy");
+        const int rc = plan_xs(h, rp.data());
         if (rc != TE_OK) return rc;
       }
       h->spmv_tiled = (int)value;
@@ -1218,6 +1343,22 @@ int te_set_option(te_handle* h, int option, double value) {
       return TE_OK;
     default:
       return set_err(TE_ERR_ARG, "unknown option %d", option);
+  }
+}
+
+int te_get_option(const te_handle* h, int option, double* value) {
+  clear_err();
+  if (!h || !value) return set_err(TE_ERR_ARG, "null argument");
+  switch (option) {
+    case TE_OPT_PROFILE: *value = h->profile ? 1.0 : 0.0; return TE_OK;
+    case TE_OPT_GRAPH: *value = h->use_graph ? 1.0 : 0.0; return TE_OK;
+    case TE_OPT_KERNELS: *value = h->variant; return TE_OK;
+    case TE_OPT_PREFETCH: *value = h->prefetch; return TE_OK;
+    case TE_OPT_SPMV: *value = h->spmv_tiled; return TE_OK;
+    case TE_OPT_ORTHO: *value = h->ortho; return TE_OK;
+    case TE_OPT_INTEGRATOR: *value = h->integrator; return TE_OK;
+    case TE_OPT_HALO: *value = h->halo_mode; return TE_OK;
+    default: return set_err(TE_ERR_ARG, "unknown option %d", option);
   }
 }
 

@@ -87,6 +87,8 @@ def load():
     L.te_destroy.argtypes = [V]
     L.te_set_option.restype = C.c_int
     L.te_set_option.argtypes = [V, C.c_int, D]
+    L.te_get_option.restype = C.c_int
+    L.te_get_option.argtypes = [V, C.c_int, P(D)]
     L.te_get_profile.restype = C.c_int
     L.te_get_profile.argtypes = [V, C.c_int, P(KernelProfile)]
     L.te_launch_count.restype = I64
@@ -282,6 +284,13 @@ def te_krylov_basis(h: Handle, v1, m, tol_rate, want_V=True):
 def te_set_option(h: Handle, option: int, value: float):
     L = load()
     _check(L, L.te_set_option(h.ptr, int(option), float(value)))
+
+
+def te_get_option(h: Handle, option: int) -> float:
+    L = load()
+    v = C.c_double(0.0)
+    _check(L, L.te_get_option(h.ptr, int(option), C.byref(v)))
+    return v.value
 
 
 def te_get_profile(h: Handle):

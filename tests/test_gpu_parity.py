@@ -35,8 +35,8 @@ def small_cases():
 CASES = small_cases()
 
 
-KERNEL_SETS = [(2, 7), (2, 6), (3, 7), (4, 7)]
-KERNEL_IDS = ["hybrid-spmvring", "hybrid-spmvsell", "tma", "shuffle"]
+KERNEL_SETS = [(2, 8), (2, 7), (2, 6), (3, 7), (4, 7)]
+KERNEL_IDS = ["hybrid-spmvxs", "hybrid-spmvring", "hybrid-spmvsell", "tma", "shuffle"]
 
 
 @pytest.mark.parametrize("kset", KERNEL_SETS, ids=KERNEL_IDS)
@@ -107,6 +107,57 @@ def test_spmv_ring_variants(gpu_lib, name, c, tpr, halo, stages, monkeypatch):
     assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-12 * scale
     assert np.linalg.norm(g["V"] - o["V"]) <= 1e-10
     h.close()
+
+
+XS_CASES = RING_CASES + [("xxz_L14", configs.build(2, L=14)), ("bh_L7_N7", configs.build(3, L=7, N=7)),
+                         ("banded_n8192", configs.build(4, n=8192))]
+
+
+@pytest.mark.parametrize("ecap", [0, 256])
+@pytest.mark.parametrize("tpr", [1, 2, 4, 8])
+@pytest.mark.parametrize("halo", [0, 1])
+@pytest.mark.parametrize("name,c", XS_CASES, ids=[x[0] for x in XS_CASES])
+def test_spmv_xs_variants(gpu_lib, name, c, tpr, halo, ecap, monkeypatch):
+    """Staged-x ring SpMV (TE_OPT_SPMV = 8) for every lanes-per-row choice, plain and halo-aware,
+    with the default tile size and with 256-entry tiles (many tiles per CTA: the 2-stage ring wraps,
+    ranges cut by the slot budget), on matrices whose x windows are fully staged (spin chains,
+    bosons), partly staged (banded + uniform) and hardly at all (uniform random columns, long
+    rows: the global-gather path), vs the oracle's Arnoldi basis."""
+    te = gpu_lib
+    if c is None:
+        c = _long_row_case()
+    monkeypatch.setenv("TE_SPMV_XS_TPR", str(tpr))
+    monkeypatch.setenv("TE_SPMV_FORCE_HALO", str(halo))
+    if ecap:
+        monkeypatch.setenv("TE_SPMV_XS_ECAP", str(ecap))
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    te.te_set_option(h, te.TE_OPT_SPMV, 8)
+    assert te.te_get_option(h, te.TE_OPT_SPMV) == 8
+    g = te.te_krylov_basis(h, c["v0"], 12, c["tol"] / c["t"], want_V=True)
+    o = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), c["v0"], 12, c["tol"] / c["t"])
+    scale = max(1.0, np.abs(o["alpha"]).max(), np.abs(o["beta"]).max())
+    assert g["m_eff"] == o["m_eff"]
+    assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-12 * scale
+    assert np.abs(g["beta"] - o["beta"]).max() <= 1e-12 * scale
+    assert np.linalg.norm(g["V"] - o["V"]) <= 1e-10
+    h.close()
+
+
+def test_spmv_default_choice(gpu_lib):
+    """The staged-x SpMV is chosen at create when its plan stages >= 95 % of the entries (spin chain,
+    bosons), the plain ring otherwise (uniform random columns); TE_OPT_SPMV switches either way."""
+    te = gpu_lib
+    # (a random matrix must be large enough that a tile's uniform columns are isolated in x)
+    for c, want in ((configs.build(5, L=12), 8), (configs.build(3, L=7, N=7), 8), (configs.build(1, n=1 << 18), 7)):
+        h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+        assert te.te_get_option(h, te.TE_OPT_SPMV) == want
+        other = 7 if want == 8 else 8
+        v1, _ = te.te_evolve(h, c["v0"], 0.5, 1e-9, 16)
+        te.te_set_option(h, te.TE_OPT_SPMV, other)
+        assert te.te_get_option(h, te.TE_OPT_SPMV) == other
+        v2, _ = te.te_evolve(h, c["v0"], 0.5, 1e-9, 16)
+        assert np.linalg.norm(v1 - v2) <= 1e-12
+        h.close()
 
 
 @pytest.mark.parametrize("halo", [0, 1])
@@ -491,12 +542,14 @@ def test_full_size_config5_xxz_nnn_L26(gpu_lib):
     assert np.abs(w1 - w0).max() <= 2 * st["err_bound"] + 1e-9
 
 
-def _forced_wrap_parity(te, c, sched, m, ring_min_wraps=4):
+def _forced_wrap_parity(te, c, sched, m, ring_min_wraps=4, spmv=None):
     """Forced-schedule evolution vs the oracle element by element (<= 1e-10, north star) at a
     size where every CTA of the ring SpMV takes many tiles (the ring wraps, the mbarrier phase
     flips many times).  The SpMV instantiation (value type, lanes per row, ring depth) depends only
     on the value type and the mean row length, so it is the one the full-size config launches."""
     h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    if spmv is not None:
+        te.te_set_option(h, te.TE_OPT_SPMV, spmv)
     v, st = te.te_evolve_schedule(h, c["v0"], sched, c["tol"], m)
     h.close()
     ref = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], float(sum(sched)), c["tol"], m, schedule=sched)
@@ -509,20 +562,22 @@ def _forced_wrap_parity(te, c, sched, m, ring_min_wraps=4):
     return err
 
 
-def test_forced_parity_complex_ring_wraps_config4_n2e20(gpu_lib):
+@pytest.mark.parametrize("spmv", [7, 8])
+def test_forced_parity_complex_ring_wraps_config4_n2e20(gpu_lib, spmv):
     """Complex H through the ring SpMV at a wrapping size: config 4's model at n = 2^20 (32
     complex entries per row, the k_spmv_ring<complex, TPR 4, 3 stages> instantiation of the full
     2^24 config), m = 8, two forced restarts, element by element against the oracle."""
     c = configs.build(4, n=1 << 20)
-    _forced_wrap_parity(gpu_lib, c, [0.05, 0.05], 8)
+    _forced_wrap_parity(gpu_lib, c, [0.05, 0.05], 8, spmv=spmv)
 
 
-def test_forced_parity_config5_instantiation_L22(gpu_lib):
+@pytest.mark.parametrize("spmv", [7, 8])
+def test_forced_parity_config5_instantiation_L22(gpu_lib, spmv):
     """Config 5's model at L = 22 (n = 4,194,304, 23 entries per row on average: the TPR 2 /
     3-stage real ring instantiation of the full L = 26 config), m = 10, one forced restart,
     element by element against the oracle."""
     c = configs.build(5, L=22)
-    _forced_wrap_parity(gpu_lib, c, [0.1], 10)
+    _forced_wrap_parity(gpu_lib, c, [0.1], 10, spmv=spmv)
 
 
 def test_distributed_api_single_rank(gpu_lib):
