@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -14,10 +15,16 @@
 te_handle* te_internal_create_local(int64_t n_loc, int64_t n_global, int64_t row_begin, const int64_t* rowptr,
                                     const int32_t* col_local, const void* val, bool cplx, te_dist* dist,
                                     int64_t ncol_limit);
+struct HaloCsr {  // the entries of the local rows whose columns live on other ranks
+  std::vector<int32_t> rows;     // local rows with at least one such entry
+  std::vector<int64_t> rowptr;   // [rows.size() + 1]
+  std::vector<int32_t> col;      // halo index (position in the received halo vector)
+  std::vector<unsigned char> val;  // double or double2 per entry
+};
 int te_internal_setup_halo(te_handle* h, int64_t n_halo, const std::vector<int64_t>& recv_counts,
                            const std::vector<int64_t>& send_counts, const std::vector<int32_t>& send_idx,
                            double norm1_global, const std::vector<int64_t>& halo_global,
-                           const std::vector<int64_t>& row_starts);
+                           const std::vector<int64_t>& row_starts, const HaloCsr& hc);
 int te_internal_set_error(int code, const char* msg);
 cudaStream_t te_internal_stream(te_handle* h);
 double te_internal_local_norm1(te_handle* h);
@@ -100,6 +107,11 @@ extern "C" te_handle* te_create_csr_dist(te_dist* d, int64_t n_global, int64_t r
   std::vector<int32_t> col_local(std::max<int64_t>(1, nnz));
   std::vector<int32_t> send_idx;
   int64_t n_halo = 0, n_send = 0;
+  std::vector<int64_t> lrp;
+  std::vector<int32_t> lcol;
+  std::vector<unsigned char> lval;
+  HaloCsr hc;
+  double norm_rows = 0.0;
   te_handle* h = nullptr;
   int64_t* dbuf = nullptr;
   cudaStream_t st = nullptr;
@@ -206,18 +218,63 @@ extern "C" te_handle* te_create_csr_dist(te_dist* d, int64_t n_global, int64_t r
     cudaFree(dneed);
     cudaFree(dgive);
   }
-  // 5. local handle with local column indices (Hermiticity needs the global matrix: not checked)
-  h = te_internal_create_local(n_loc, n_global, row_begin, rowptr_local, col_local.data(), val, val_is_complex != 0,
-                               d, n_loc + n_halo);
+  // 5. split every row into its local-column entries (the handle's CSR: the SpMV runs on them
+  //    while the halo is in flight) and its halo entries (a small CSR over the rows that have
+  //    any, added by k_spmv_halo once the halo arrived); ||H||_1 from the full rows.  Local
+  //    handle with local column indices (Hermiticity needs the global matrix: not checked)
+  {
+    const size_t vb = val_is_complex ? 16 : 8;
+    const unsigned char* vin = static_cast<const unsigned char*>(val);
+    lrp.assign((size_t)n_loc + 1, 0);
+    lcol.reserve((size_t)std::max<int64_t>(1, nnz));
+    lval.reserve((size_t)std::max<int64_t>(1, nnz) * vb);
+    hc.rowptr.push_back(0);
+    for (int64_t r = 0; r < n_loc; ++r) {
+      double rs = 0.0;
+      bool any = false;
+      for (int64_t q = rowptr_local[r]; q < rowptr_local[r + 1]; ++q) {
+        const int32_t c = col_local[(size_t)q];
+        const unsigned char* v = vin + (size_t)q * vb;
+        double a = 0.0;
+        if (val_is_complex) {
+          double re, im;
+          std::memcpy(&re, v, 8);
+          std::memcpy(&im, v + 8, 8);
+          a = std::hypot(re, im);
+        } else {
+          double re;
+          std::memcpy(&re, v, 8);
+          a = std::fabs(re);
+        }
+        rs += a;
+        if (c < n_loc) {
+          lcol.push_back(c);
+          lval.insert(lval.end(), v, v + vb);
+        } else {
+          hc.col.push_back(c - (int32_t)n_loc);
+          hc.val.insert(hc.val.end(), v, v + vb);
+          any = true;
+        }
+      }
+      lrp[(size_t)r + 1] = (int64_t)lcol.size();
+      if (any) {
+        hc.rows.push_back((int32_t)r);
+        hc.rowptr.push_back((int64_t)hc.col.size());
+      }
+      norm_rows = std::max(norm_rows, rs);
+    }
+  }
+  h = te_internal_create_local(n_loc, n_global, row_begin, lrp.data(), lcol.data(), lval.data(), val_is_complex != 0,
+                               d, n_loc);
   if (!h && P == 1) goto fail;
   {
     // 6. halo buffers and peer tables first (their allocations can fail too), then
     //    ||H||_1 = max over all rows of the row abs sums (allreduce max), together with a
     //    "local setup failed" flag, so that a failure on one rank fails every rank
     bool local_ok = h != nullptr;
-    const double norm_loc = h ? te_internal_local_norm1(h) : 0.0;
+    const double norm_loc = norm_rows;
     if (local_ok &&
-        te_internal_setup_halo(h, n_halo, recv_counts, send_counts, send_idx, norm_loc, halo, row_starts) != TE_OK)
+        te_internal_setup_halo(h, n_halo, recv_counts, send_counts, send_idx, norm_loc, halo, row_starts, hc) != TE_OK)
       local_ok = false;
     double nv[2] = {norm_loc, local_ok ? 0.0 : 1.0};
     if (P > 1) {

@@ -49,7 +49,15 @@ struct KDev {
   const int2* xs_rng;        // [ntiles_xs * xs_rmax] {first column, length}; slots follow in order
   const uint16_t* lcol;      // [nnz + 8] slot of each entry in its tile's staged x
   int xs_ecap, xs_xcap, xs_rmax;  // entries per tile, staged x slots per tile, ranges per tile
-  const double2* halo;  // x entries for columns >= n (distributed); nullptr otherwise
+  int xs_xpol;               // L2 policy of the staged x copies: 0 normal, 1 evict_last
+  const double2* halo;  // received halo entries (distributed, NCCL exchange); nullptr otherwise
+  // distributed handles: the entries of local rows whose columns live on other ranks, kept apart
+  // from the local CSR (rowptr/col/val above hold local columns only) and added by k_spmv_halo
+  const int32_t* hrow;     // [nh] local rows with halo entries
+  const int64_t* hrowptr;  // [nh + 1]
+  const int32_t* hcol;     // halo index of each entry
+  const void* hval;
+  int64_t nh;
   double* s;            // [m_cap+1] column scales
   double* alpha;        // [m_cap]
   double* beta;         // [m_cap]
@@ -78,7 +86,9 @@ struct Launch {
   const CUtensorMap* tmaps;  // [kMaxCols] 2-D maps of V, box = 64R doubles x (k+1) columns
   int spmv_force_halo;  // test hook: run the multi-rank (halo-aware) SpMV instantiation on one rank
   int spmv_nf_wide;     // ring SpMV gathers in flight per lane: 0 -> 12 real / 8 complex, 1 -> 16 / 12
-  int halo_peer;        // SpMV reads halo columns from peer memory (no staged exchange)
+  int halo_peer;        // halo entries read from peer memory (no staged exchange)
+  int grid_spmv;        // CTAs of the (persistent) SpMV: num_sms, or fewer so that the NCCL halo
+                        // exchange running concurrently on the side stream finds free SMs
   int spmv_ring_tpr;    // lanes per row of the warp-specialised ring SpMV
   int ring_stages;      // its ring depth: 4 (short real rows) or 3 (larger tiles)
   int spmv_xs_tpr;      // lanes per row of the staged-x ring SpMV
@@ -102,6 +112,7 @@ void set_attr(const void* f, size_t want, void* ctx);
 void configure_spmv_kernels(void (*set_attr)(const void*, size_t, void*), void* ctx);
 const void* spmv_attr_kernel();  // the SpMV kernel reported by kernel_attributes(0)
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L);        // K1a: SpMV only
+void launch_spmv_halo(const KDev& d, bool cplx, int j, const Launch& L);   // K1a': + halo entries (distributed)
 // staged-x ring SpMV (spmv_xs.cu): plan (create time) and launch
 constexpr int kXsConsumers = 15;
 constexpr int kXsRmax = 64;      // x ranges per tile

@@ -22,6 +22,10 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // optional: asynchronous error polling (a failed peer ends te_evolve instead of hanging it)
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  bool is_fake = false;  // the test stand-in (tests/support/fake_nccl.cu): no graph capture
 };
 
 inline NcclApi& nccl() {
@@ -60,6 +64,9 @@ inline NcclApi& nccl() {
     TE_SYM(GroupEnd, "ncclGroupEnd")
     TE_SYM(GetErrorString, "ncclGetErrorString")
 #undef TE_SYM
+    a.CommGetAsyncError = reinterpret_cast<decltype(a.CommGetAsyncError)>(dlsym(lib, "ncclCommGetAsyncError"));
+    a.CommAbort = reinterpret_cast<decltype(a.CommAbort)>(dlsym(lib, "ncclCommAbort"));
+    a.is_fake = dlsym(lib, "fake_nccl_calls") != nullptr;
     a.ok = true;
     return a;
   }();

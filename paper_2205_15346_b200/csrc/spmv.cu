@@ -298,13 +298,52 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmv_sell(KDev d, int j) {
   }
 }
 
+// Halo part of a distributed SpMV: W[r] += s_j sum_k H_{r,c_k} x_halo[c_k] over the entries of row
+// r whose columns live on other ranks (x_halo: the received halo vector, or the owning rank's V
+// column through peer memory).  Runs after the local-column SpMV of the same step, so each row's
+// sum is (its local entries in CSR order) + (its halo entries in CSR order): deterministic.
+template <bool CPLX, bool PEER>
+__global__ void __launch_bounds__(kThreads) k_spmv_halo(KDev d, int j) {
+  using VT = typename ValT<CPLX>::T;
+  __shared__ double sj_s;
+  if (threadIdx.x == 0) sj_s = d.flag[0] != 0 ? 0.0 : (d.defer || j == 0 ? 1.0 : d.s[j]);
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+  const VT* __restrict__ hv = static_cast<const VT*>(d.hval);
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < d.nh; i += (int64_t)gridDim.x * kThreads) {
+    const int64_t a = __ldg(d.hrowptr + i), b = __ldg(d.hrowptr + i + 1);
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t k = a; k < b; ++k) {
+      const int c = __ldg(d.hcol + k);
+      const double2 xv = PEER ? peer_x(d, j, c) : __ldg(d.halo + c);
+      acc = cadd(acc, ValT<CPLX>::mul(__ldg(hv + k), xv));
+    }
+    const int r = __ldg(d.hrow + i);
+    const double2 w = d.W[r];
+    d.W[r] = make_double2(w.x + sj * acc.x, w.y + sj * acc.y);
+  }
+}
+
+void launch_spmv_halo(const KDev& d, bool cplx, int j, const Launch& L) {
+  if (d.nh <= 0) return;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)8 * L.num_sms, (d.nh + kThreads - 1) / kThreads));
+  if (cplx) {
+    if (L.halo_peer) k_spmv_halo<true, true><<<grid, kThreads, 0, L.stream>>>(d, j);
+    else k_spmv_halo<true, false><<<grid, kThreads, 0, L.stream>>>(d, j);
+  } else {
+    if (L.halo_peer) k_spmv_halo<false, true><<<grid, kThreads, 0, L.stream>>>(d, j);
+    else k_spmv_halo<false, false><<<grid, kThreads, 0, L.stream>>>(d, j);
+  }
+}
+
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
   if (L.spmv_tiled == 8 && d.ntiles_xs > 0) {
     launch_spmv_xs(d, cplx, j, L);
     return;
   }
   if (L.spmv_tiled == 6 && d.nslices > 0) {
-    const bool hal = d.halo || L.spmv_force_halo;
+    const bool hal = L.spmv_force_halo;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)8 * L.num_sms, (d.nslices + kWarps - 1) / kWarps));
     if (cplx) {
       if (hal) k_spmv_sell<true, true, 4><<<grid, kThreads, 0, L.stream>>>(d, j);
@@ -315,7 +354,7 @@ void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
     }
     return;
   }
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(L.num_sms, d.ntiles_ring));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(L.grid_spmv, d.ntiles_ring));
 #define TE_RING_S(T, H, S)                                                                                      \
   if (cplx) {                                                                                                   \
     if (L.spmv_nf_wide) k_spmv_ring<true, T, H, 12, S><<<grid, kRingThreads, spmv_ring_smem<true, S>(), L.stream>>>(d, j);   \
@@ -328,7 +367,7 @@ void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
   if (L.ring_stages == 3) { TE_RING_S(T, H, 3) } else { TE_RING_S(T, H, 4) }
 #define TE_RING(T)                                                                                 \
   case T:                                                                                          \
-    if (L.halo_peer) { TE_RING_H(T, 2) } else if (d.halo || L.spmv_force_halo) { TE_RING_H(T, 1) } \
+    if (L.spmv_force_halo) { TE_RING_H(T, 1) }                                                    \
     else { TE_RING_H(T, 0) }                                                                       \
     break;
   switch (L.spmv_ring_tpr) {
@@ -351,7 +390,6 @@ void configure_spmv_kernels(void (*set_attr)(const void*, size_t, void*), void* 
 #define TE_SETRING(T, H) TE_SETRING_S(T, H, 3) TE_SETRING_S(T, H, 4)
   TE_SETRING(1, 0) TE_SETRING(2, 0) TE_SETRING(4, 0) TE_SETRING(8, 0)
   TE_SETRING(1, 1) TE_SETRING(2, 1) TE_SETRING(4, 1) TE_SETRING(8, 1)
-  TE_SETRING(1, 2) TE_SETRING(2, 2) TE_SETRING(4, 2) TE_SETRING(8, 2)
 #undef TE_SETRING
 #undef TE_SETRING_S
   configure_xs_kernels(set_attr, ctx, kXsBudget);

@@ -30,6 +30,11 @@ constexpr int kXsThreads = (kXsConsumers + 1) * 32;
 
 __host__ __device__ constexpr size_t rnd16(size_t b) { return (b + 15) & ~(size_t)15; }
 
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void bulk_g2s_nohint(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
@@ -191,6 +196,7 @@ __global__ void __launch_bounds__(kXsThreads, 1) k_spmv_xs(KDev d, int j) {
   const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
   if (warp == C) {  // ------------------------------------------------------------ producer warp
     const uint64_t pol = policy_evict_first();  // H: streamed once
+    const uint64_t polx = policy_evict_last();
     constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
     const int2* rngs = reinterpret_cast<const int2*>(d.xs_rng);
     // descriptor, meta and x ranges of tile t: loaded one tile ahead (before the wait for a free
@@ -261,8 +267,13 @@ __global__ void __launch_bounds__(kXsThreads, 1) k_spmv_xs(KDev d, int j) {
         }
         const int tot0 = __shfl_sync(0xffffffffu, s0, 31);
         const int b0 = s0 - r0.y, b1 = tot0 + s1 - r1.y;
-        if (r0.y > 0) bulk_g2s_nohint(base + oX + (size_t)b0 * 16, x + r0.x, (unsigned)r0.y * 16u, &full[st]);
-        if (r1.y > 0) bulk_g2s_nohint(base + oX + (size_t)b1 * 16, x + r1.x, (unsigned)r1.y * 16u, &full[st]);
+        if (d.xs_xpol) {  // x kept in L2 ahead of the streamed H (evict_first)
+          if (r0.y > 0) bulk_g2s(base + oX + (size_t)b0 * 16, x + r0.x, (unsigned)r0.y * 16u, &full[st], polx);
+          if (r1.y > 0) bulk_g2s(base + oX + (size_t)b1 * 16, x + r1.x, (unsigned)r1.y * 16u, &full[st], polx);
+        } else {
+          if (r0.y > 0) bulk_g2s_nohint(base + oX + (size_t)b0 * 16, x + r0.x, (unsigned)r0.y * 16u, &full[st]);
+          if (r1.y > 0) bulk_g2s_nohint(base + oX + (size_t)b1 * 16, x + r1.x, (unsigned)r1.y * 16u, &full[st]);
+        }
       }
       cur = nxt;
     }
@@ -349,7 +360,7 @@ size_t spmv_xs_smem(bool cplx, int tpr, int ecap, int xcap, int stages) {
 }
 
 void launch_spmv_xs(const KDev& d, bool cplx, int j, const Launch& L) {
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(L.num_sms, d.ntiles_xs));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(L.grid_spmv, d.ntiles_xs));
   const size_t smem = spmv_xs_smem(cplx, L.spmv_xs_tpr, d.xs_ecap, d.xs_xcap, L.xs_stages);
 #define TE_XS_S(T, H, S)                                                                  \
   if (cplx) k_spmv_xs<true, T, H, 8, S><<<grid, kXsThreads, smem, L.stream>>>(d, j);      \
@@ -358,7 +369,7 @@ void launch_spmv_xs(const KDev& d, bool cplx, int j, const Launch& L) {
   if (L.xs_stages == 3) { TE_XS_S(T, H, 3) } else { TE_XS_S(T, H, 2) }
 #define TE_XS(T)                                                                                 \
   case T:                                                                                        \
-    if (L.halo_peer) { TE_XS_H(T, 2) } else if (d.halo || L.spmv_force_halo) { TE_XS_H(T, 1) } \
+    if (L.spmv_force_halo) { TE_XS_H(T, 1) }                                                    \
     else { TE_XS_H(T, 0) }                                                                       \
     break;
   switch (L.spmv_xs_tpr) {
@@ -380,7 +391,6 @@ void configure_xs_kernels(void (*set_attr)(const void*, size_t, void*), void* ct
   set((const void*)k_spmv_xs<true, T, H, 8, 3>, budget);
   TE_SETXS(1, 0) TE_SETXS(2, 0) TE_SETXS(4, 0) TE_SETXS(8, 0)
   TE_SETXS(1, 1) TE_SETXS(2, 1) TE_SETXS(4, 1) TE_SETXS(8, 1)
-  TE_SETXS(1, 2) TE_SETXS(2, 2) TE_SETXS(4, 2) TE_SETXS(8, 2)
 #undef TE_SETXS
 }
 

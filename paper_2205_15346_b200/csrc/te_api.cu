@@ -128,7 +128,7 @@ struct te_handle {
   int4* d_xs_meta = nullptr;
   int2* d_xs_rng = nullptr;
   uint16_t* d_lcol = nullptr;
-  int spmv_xs_tpr = 1, xs_ecap = 0, xs_xcap = 0, xs_stages = 2;
+  int spmv_xs_tpr = 1, xs_ecap = 0, xs_xcap = 0, xs_stages = 2, xs_xpol = 0;
   double xs_global_frac = 1.0;  // entries the plan left to global gathers / nnz
   int64_t ncol_limit = 0;
   // SELL-32-sigma copy of H (SpMV variant 6), built on first selection
@@ -167,6 +167,15 @@ struct te_handle {
   te_dist* dist = nullptr;
   int64_t n_halo = 0;
   double2* d_halo = nullptr;
+  // halo entries of the local rows (k_spmv_halo) and the side stream of the halo exchange
+  int32_t* d_hrow = nullptr;
+  int64_t* d_hrowptr = nullptr;
+  int32_t* d_hcol = nullptr;
+  void* d_hval = nullptr;
+  int64_t nh = 0, nh_entries = 0;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int comm_sms = 8;  // SMs the SpMV leaves free for the concurrent NCCL exchange (TE_COMM_SMS)
   double2* d_sendbuf = nullptr;
   int32_t* d_send_idx = nullptr;
   // halo mode 1 (TE_OPT_HALO): halo columns read from peer memory inside the SpMV
@@ -203,6 +212,11 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.col = h->d_col;
   d.val = h->d_val;
   d.halo = h->d_halo;
+  d.hrow = h->d_hrow;
+  d.hrowptr = h->d_hrowptr;
+  d.hcol = h->d_hcol;
+  d.hval = h->d_hval;
+  d.nh = h->nh;
   d.peer_base = h->d_peer_base;
   d.peer_ldv = h->d_peer_ldv;
   d.halo_owner = h->d_halo_owner;
@@ -217,6 +231,7 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.xs_ecap = h->xs_ecap;
   d.xs_xcap = h->xs_xcap;
   d.xs_rmax = te::kXsRmax;
+  d.xs_xpol = h->xs_xpol;
   d.scol = h->d_scol;
   d.sval = h->d_sval;
   d.sptr = h->d_sptr;
@@ -242,9 +257,11 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   return d;
 }
 
-// halo mode 1 is used by the ring SpMVs (7, 8); the SELL variant keeps the staged exchange
-bool peer_active(const te_handle* h) {
-  return h->dist && h->dist->nranks > 1 && h->halo_mode == 1 && (h->spmv_tiled == 7 || h->spmv_tiled == 8);
+// halo mode 1: k_spmv_halo reads the halo entries from the owning ranks' V columns (any SpMV variant)
+bool peer_active(const te_handle* h) { return h->dist && h->dist->nranks > 1 && h->halo_mode == 1; }
+// the NCCL halo exchange runs on the side stream concurrently with the local-column SpMV
+bool exchange_active(const te_handle* h) {
+  return h->dist && h->dist->nranks > 1 && !peer_active(h) && (h->n_send > 0 || h->n_halo > 0);
 }
 
 Launch make_launch(te_handle* h) {
@@ -258,6 +275,7 @@ Launch make_launch(te_handle* h) {
   L.spmv_nf_wide = h->spmv_nf_wide;
   L.spmv_force_halo = h->spmv_force_halo;
   L.halo_peer = peer_active(h) ? 1 : 0;
+  L.grid_spmv = exchange_active(h) ? std::max(1, h->num_sms - h->comm_sms) : h->num_sms;
   L.spmv_ring_tpr = h->spmv_ring_tpr;
   L.spmv_xs_tpr = h->spmv_xs_tpr;
   L.xs_stages = h->xs_stages;
@@ -401,13 +419,18 @@ int allreduce_sum(te_handle* h, double* buf, size_t count) {
   return TE_OK;
 }
 
+// Fork: the side stream waits for everything issued so far on the main stream (V_j complete), packs
+// V_j[send_idx] and runs the grouped send/recv into the halo buffer while the main stream runs
+// the local-column SpMV; halo_join makes the main stream wait before k_spmv_halo.  Both are
+// plain event edges, so a captured restart graph contains them (and the NCCL calls) as well.
 int halo_exchange(te_handle* h, int j) {
-  if (!h->dist || h->dist->nranks == 1 || peer_active(h)) return TE_OK;
+  if (!exchange_active(h)) return TE_OK;
   const double2* x = h->d_V + (int64_t)j * h->ldv;
+  CK(cudaEventRecord(h->ev_fork, h->stream));
+  CK(cudaStreamWaitEvent(h->comm_stream, h->ev_fork, 0));
   if (h->n_send > 0) {
-    prof_begin(h);
-    te::launch_pack(x, h->d_send_idx, h->n_send, h->d_sendbuf, h->stream);
-    prof_end(h, 4, 16.0 * 2 * (double)h->n_send + 4.0 * (double)h->n_send);
+    te::launch_pack(x, h->d_send_idx, h->n_send, h->d_sendbuf, h->comm_stream);
+    ++h->launches;
   }
   auto& N = te::nccl();
   CKN(N.GroupStart());
@@ -415,13 +438,19 @@ int halo_exchange(te_handle* h, int j) {
   for (int q = 0; q < h->dist->nranks; ++q) {
     if (q == h->dist->rank) continue;
     if (h->send_counts[q] > 0)
-      CKN(N.Send(h->d_sendbuf + so, 2 * (size_t)h->send_counts[q], ncclDouble, q, h->dist->comm, h->stream));
+      CKN(N.Send(h->d_sendbuf + so, 2 * (size_t)h->send_counts[q], ncclDouble, q, h->dist->comm, h->comm_stream));
     if (h->recv_counts[q] > 0)
-      CKN(N.Recv(h->d_halo + ro, 2 * (size_t)h->recv_counts[q], ncclDouble, q, h->dist->comm, h->stream));
+      CKN(N.Recv(h->d_halo + ro, 2 * (size_t)h->recv_counts[q], ncclDouble, q, h->dist->comm, h->comm_stream));
     so += h->send_counts[q];
     ro += h->recv_counts[q];
   }
   CKN(N.GroupEnd());
+  CK(cudaEventRecord(h->ev_join, h->comm_stream));
+  return TE_OK;
+}
+int halo_join(te_handle* h) {
+  if (!exchange_active(h)) return TE_OK;
+  CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
   return TE_OK;
 }
 
@@ -498,14 +527,10 @@ int setup_peers(te_handle* h) {
 
 int issue_arnoldi(te_handle* h, int m, double tol_rate) {
   int lj = -1;
-  if (peer_active(h) && h->peer_for_V != h->d_V) {
-    const int rc = setup_peers(h);
-    if (rc) return rc;
-  }
   KDev d = make_kdev(h, tol_rate, m);
   Launch L = make_launch(h);
   const double n = (double)h->n;
-  const double bh = (double)h->nnz * ((h->cplx ? 16.0 : 8.0) + 4.0) + 8.0 * (n + 1.0);
+  const double bh = (double)(h->nnz + h->nh_entries) * ((h->cplx ? 16.0 : 8.0) + 4.0) + 8.0 * (n + 1.0);
   te::launch_restart_init(d, L); LCHECK("restart_init");
   ++h->launches;
   for (int j = 0; j < m; ++j) {
@@ -516,6 +541,8 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
     if (h->ortho == 1) {  // paper-literal Lanczos (Eq. 8 as printed)
       prof_begin(h);
       te::launch_spmv(d, h->cplx, j, L); LCHECK("spmv");
+      if ((rc = halo_join(h))) return rc;
+      te::launch_spmv_halo(d, h->cplx, j, L); LCHECK("spmv_halo");
       prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
       const double nv = j > 0 ? 2.0 : 1.0;
       prof_begin(h);
@@ -535,6 +562,8 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
     // barrier per step in peer-load halo mode, where a rank's SpMV reads its peers' V_j)
     prof_begin(h);
     te::launch_spmv(d, h->cplx, j, L); LCHECK("spmv");
+    if ((rc = halo_join(h))) return rc;
+    te::launch_spmv_halo(d, h->cplx, j, L); LCHECK("spmv_halo");
     prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
     prof_begin(h);
     te::launch_proj_dots(d, j, L); LCHECK("proj_dots");
@@ -573,13 +602,42 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
 // One restart's Arnoldi decomposition.  With graphs on (default, single rank) the launch sequence
 // is captured once per (m, tol_rate, kernel set, basis allocation, profiling) and replayed; the
 // profiling events are captured as event-record nodes and read back after each replay.
+// Wait for the restart on the host.  With several ranks the wait polls the communicator's
+// asynchronous error state, so a failed or vanished peer ends te_evolve with TE_ERR_NCCL (the
+// communicator is aborted) instead of blocking forever in a collective.
+int wait_restart(te_handle* h) {
+  if (!h->dist || h->dist->nranks == 1 || !te::nccl().CommGetAsyncError) {
+    CK(cudaStreamSynchronize(h->stream));
+    return TE_OK;
+  }
+  for (int spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(h->stream);
+    if (q == cudaSuccess) return TE_OK;
+    if (q != cudaErrorNotReady) CK(q);
+    ncclResult_t ar = ncclSuccess;
+    if (te::nccl().CommGetAsyncError(h->dist->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+      if (te::nccl().CommAbort) te::nccl().CommAbort(h->dist->comm);
+      h->dist->comm = nullptr;
+      return set_err(TE_ERR_NCCL, "NCCL communicator failed during the restart: %s", te::nccl().GetErrorString(ar));
+    }
+    if (spin > 64) usleep(20);
+  }
+}
+
 int run_arnoldi(te_handle* h, int m, double tol_rate) {
-  // profiling uses per-launch CUDA events, which graphs do not time: direct launches then
-  const bool graph = h->use_graph && !h->profile && (!h->dist || h->dist->nranks == 1);
+  if (h->dist && h->dist->nranks > 1 && !h->dist->comm) return set_err(TE_ERR_NCCL, "communicator was aborted");
+  if (peer_active(h) && h->peer_for_V != h->d_V) {  // collective; never inside a graph capture
+    const int rc = setup_peers(h);
+    if (rc) return rc;
+  }
+  // profiling uses per-launch CUDA events, which graphs do not time: direct launches then.  With
+  // several ranks the restart graph holds the NCCL calls too (NCCL supports stream capture); the
+  // test stand-in for NCCL (tests/support/fake_nccl.cu) does not, so it runs direct launches
+  const bool graph = h->use_graph && !h->profile && (!h->dist || h->dist->nranks == 1 || !te::nccl().is_fake);
   if (!graph) {
     int rc = issue_arnoldi(h, m, tol_rate);
     if (rc) return rc;
-    CK(cudaStreamSynchronize(h->stream));
+    if ((rc = wait_restart(h))) return rc;
     if (h->profile) prof_collect(h);
     return TE_OK;
   }
@@ -634,7 +692,10 @@ int run_arnoldi(te_handle* h, int m, double tol_rate) {
   }
   CK(cudaGraphLaunch(h->gexec, h->stream));
   h->launches += h->g_launches;
-  CK(cudaStreamSynchronize(h->stream));
+  {
+    const int rc = wait_restart(h);
+    if (rc) return rc;
+  }
   if (h->profile) {
     for (int i = 0; i < h->g_nev; ++i) {
       h->ev_cls[i] = h->g_ev_cls[i];
@@ -854,6 +915,7 @@ int plan_xs(te_handle* h, const int64_t* rowptr) {
   h->xs_ecap = h->cplx ? 2048 : 4096;
   if (const char* e = getenv("TE_SPMV_XS_ECAP")) h->xs_ecap = std::max(64, std::min(8192, atoi(e)));
   h->xs_stages = 2;
+  if (const char* e = getenv("TE_SPMV_XS_XPOL")) h->xs_xpol = atoi(e) != 0;
   if (const char* e = getenv("TE_SPMV_XS_STAGES")) h->xs_stages = atoi(e) == 3 ? 3 : 2;
   h->xs_xcap = te::xs_xcap_for(h->cplx, tx, h->xs_ecap, te::kXsBudget, h->xs_stages);
   const int64_t rcap = 32 * te::kXsConsumers / tx;
@@ -1090,6 +1152,13 @@ void te_destroy(te_handle* h) {
   cudaFree(h->d_partn);
   cudaFree(h->d_counter);
   cudaFree(h->d_halo);
+  cudaFree(h->d_hrow);
+  cudaFree(h->d_hrowptr);
+  cudaFree(h->d_hcol);
+  cudaFree(h->d_hval);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
   cudaFree(h->d_halo_owner);
   cudaFree(h->d_halo_lidx);
   cudaFree(h->d_peer_base);
@@ -1429,11 +1498,37 @@ ncclComm_t te_internal_comm(te_dist* d) { return d->comm; }
 int te_internal_nranks(te_dist* d) { return d->nranks; }
 int te_internal_rank(te_dist* d) { return d->rank; }
 
+struct HaloCsr {
+  std::vector<int32_t> rows;
+  std::vector<int64_t> rowptr;
+  std::vector<int32_t> col;
+  std::vector<unsigned char> val;
+};
 int te_internal_setup_halo(te_handle* h, int64_t n_halo, const std::vector<int64_t>& recv_counts,
                            const std::vector<int64_t>& send_counts, const std::vector<int32_t>& send_idx,
                            double norm1_global, const std::vector<int64_t>& halo_global,
-                           const std::vector<int64_t>& row_starts) {
+                           const std::vector<int64_t>& row_starts, const HaloCsr& hc) {
   h->n_halo = n_halo;
+  h->nh = (int64_t)hc.rows.size();
+  h->nh_entries = (int64_t)hc.col.size();
+  if (h->nh > 0) {
+    CK(cudaMalloc(&h->d_hrow, sizeof(int32_t) * h->nh));
+    CK(cudaMalloc(&h->d_hrowptr, sizeof(int64_t) * (h->nh + 1)));
+    CK(cudaMalloc(&h->d_hcol, sizeof(int32_t) * std::max<int64_t>(1, h->nh_entries)));
+    CK(cudaMalloc(&h->d_hval, std::max<size_t>(16, hc.val.size())));
+    CK(cudaMemcpy(h->d_hrow, hc.rows.data(), sizeof(int32_t) * h->nh, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_hrowptr, hc.rowptr.data(), sizeof(int64_t) * (h->nh + 1), cudaMemcpyHostToDevice));
+    if (h->nh_entries > 0) {
+      CK(cudaMemcpy(h->d_hcol, hc.col.data(), sizeof(int32_t) * h->nh_entries, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->d_hval, hc.val.data(), hc.val.size(), cudaMemcpyHostToDevice));
+    }
+  }
+  if (h->dist && h->dist->nranks > 1) {
+    CK(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    if (const char* e = getenv("TE_COMM_SMS")) h->comm_sms = std::max(0, std::min(h->num_sms - 1, atoi(e)));
+  }
   if (n_halo > 0) {  // owner rank and owner-local row of every halo entry (halo mode 1)
     std::vector<int32_t> own((size_t)n_halo), lidx((size_t)n_halo);
     int64_t k = 0;
