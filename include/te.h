@@ -195,6 +195,19 @@ int64_t te_launch_count(const te_handle* h);
 /* ||H||_1 of the handle's matrix (global for distributed handles). */
 double te_one_norm(const te_handle* h);
 
+/* Host-side small problem of one restart, exported for testing without a GPU (the same code
+ * te_evolve runs on the host, host_math.cpp):
+ * te_small_eig: T = tridiag(beta[0..m-2], alpha, beta[0..m-2]) = U diag(lam) U^T by implicit
+ *   symmetric QR; lam[m] unsorted, U[m*m] row-major (column k = eigenvector k).
+ * te_step_search: Alg. 1 step 2 (reading O-6 of DESIGN.md) on that T with
+ *   h = h_{m+1,m}: the step tau and its error integral err = int_0^tau f (Eq. 16) with
+ *   err <= tol_rate tau; integrator 0 tanh-sinh (with the O-5a floor), 1 Gauss-Legendre.
+ *   TE_ERR_STEP_COLLAPSE below 1e-13 t_total. */
+int te_small_eig(int m, const double* alpha, const double* beta, double* lam, double* U);
+int te_step_search(int m, const double* alpha, const double* beta, double h, int breakdown, int first,
+                   double tau_prev, double rem, double tol_rate, double t_total, int integrator, double* tau,
+                   double* err, int* quad_ok);
+
 /* Diagnostics: compiled attributes of a hot-path kernel (which: 0 spmv (the ring kernel, real
  * values, one lane per row), 1 proj_dots, 2 update_proj (TMA), 3 update_norm). */
 int te_kernel_attributes(int which, int* regs, int* max_threads, int* static_smem, int* max_dyn_smem);

@@ -6,68 +6,62 @@
 namespace te {
 
 // ------------------------------------------------------------------------------------------
-// implicit QL with Wilkinson-type shifts on a symmetric tridiagonal matrix, accumulating the
-// rotations into U (columns = eigenvectors).  Textbook algorithm (Golub & Van Loan §8.3,
-// "tql2"/"tqli" family), restated in 0-based form.
+// Eigen-decomposition of the real symmetric tridiagonal T = tridiag(beta, alpha, beta) (P:331:
+// "diagonalise once per restart") by implicit symmetric QR steps with the Wilkinson shift and
+// bulge chasing (Golub & Van Loan, Matrix Computations, §8.3: Algorithms 8.3.2-8.3.3), written
+// out here: every step applies Givens rotations G in planes (k, k+1), T <- G T G^T, and
+// accumulates Z <- Z G^T, so that T = Z diag(lam) Z^T at the end (columns of Z = eigenvectors).
+// Deflation: an off-diagonal |b_i| <= 2^-53 (|a_i| + |a_{i+1}|) is set to 0.
 // ------------------------------------------------------------------------------------------
 bool tridiag_eig(int m, const double* alpha, const double* beta, SmallEig& out) {
   out.m = m;
-  std::vector<double> d(alpha, alpha + m), e(m, 0.0);
-  for (int i = 0; i + 1 < m; ++i) e[i] = beta[i];
-  std::vector<double>& z = out.U;
-  z.assign((size_t)m * m, 0.0);
-  for (int i = 0; i < m; ++i) z[(size_t)i * m + i] = 1.0;
-  for (int l = 0; l < m; ++l) {
-    int iter = 0;
-    int mm;
-    do {
-      for (mm = l; mm < m - 1; ++mm) {
-        const double dd = std::fabs(d[mm]) + std::fabs(d[mm + 1]);
-        if (std::fabs(e[mm]) + dd == dd) break;
+  std::vector<double> a(alpha, alpha + m), b(m > 1 ? m - 1 : 1, 0.0);
+  for (int i = 0; i + 1 < m; ++i) b[i] = beta[i];
+  std::vector<double>& Z = out.U;  // row-major m x m
+  Z.assign((size_t)m * m, 0.0);
+  for (int i = 0; i < m; ++i) Z[(size_t)i * m + i] = 1.0;
+  const double tiny = std::ldexp(1.0, -53);
+  auto negligible = [&](int i) { return std::fabs(b[i]) <= tiny * (std::fabs(a[i]) + std::fabs(a[i + 1])); };
+  int hi = m - 1, steps = 0;
+  while (hi > 0) {
+    if (negligible(hi - 1)) {  // trailing eigenvalue converged
+      b[hi - 1] = 0.0;
+      --hi;
+      continue;
+    }
+    int lo = hi - 1;  // the unreduced block [lo, hi]
+    while (lo > 0 && !negligible(lo - 1)) --lo;
+    if (lo > 0) b[lo - 1] = 0.0;
+    if (++steps > 60 * m) return false;
+    // Wilkinson shift from the trailing 2 x 2 block of [lo, hi]
+    const double dl = 0.5 * (a[hi - 1] - a[hi]);
+    const double bh = b[hi - 1];
+    const double mu = a[hi] - bh * bh / (dl + (dl >= 0.0 ? 1.0 : -1.0) * std::hypot(dl, bh));
+    double x = a[lo] - mu, z = b[lo];
+    for (int k = lo; k < hi; ++k) {
+      const double r = std::hypot(x, z);
+      const double c = r == 0.0 ? 1.0 : x / r, s = r == 0.0 ? 0.0 : z / r;
+      if (k > lo) b[k - 1] = r;  // the bulge at (k+1, k-1) is rotated away
+      const double app = a[k], aqq = a[k + 1], apq = b[k];
+      a[k] = c * c * app + 2.0 * c * s * apq + s * s * aqq;
+      a[k + 1] = s * s * app - 2.0 * c * s * apq + c * c * aqq;
+      b[k] = c * s * (aqq - app) + (c * c - s * s) * apq;
+      if (k + 1 < hi) {  // new bulge at (k+2, k)
+        z = s * b[k + 1];
+        b[k + 1] *= c;
+        x = b[k];
       }
-      if (mm != l) {
-        if (iter++ == 100) return false;
-        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-        double r = std::hypot(g, 1.0);
-        g = d[mm] - d[l] + e[l] / (g + std::copysign(r, g));
-        double s = 1.0, c = 1.0, p = 0.0;
-        int i;
-        bool deflated = false;
-        for (i = mm - 1; i >= l; --i) {
-          double f = s * e[i];
-          const double b = c * e[i];
-          r = std::hypot(f, g);
-          e[i + 1] = r;
-          if (r == 0.0) {
-            d[i + 1] -= p;
-            e[mm] = 0.0;
-            deflated = true;
-            break;
-          }
-          s = f / r;
-          c = g / r;
-          g = d[i + 1] - p;
-          r = (d[i] - g) * s + 2.0 * c * b;
-          p = s * r;
-          d[i + 1] = g + p;
-          g = c * r - b;
-          for (int k = 0; k < m; ++k) {
-            double* zk = &z[(size_t)k * m];
-            f = zk[i + 1];
-            zk[i + 1] = s * zk[i] + c * f;
-            zk[i] = c * zk[i] - s * f;
-          }
-        }
-        if (deflated) continue;
-        d[l] -= p;
-        e[l] = g;
-        e[mm] = 0.0;
+      for (int i = 0; i < m; ++i) {
+        double* zr = &Z[(size_t)i * m];
+        const double zp = zr[k], zq = zr[k + 1];
+        zr[k] = c * zp + s * zq;
+        zr[k + 1] = c * zq - s * zp;
       }
-    } while (mm != l);
+    }
   }
-  out.lam = d;
+  out.lam = a;
   out.c.resize(m);
-  for (int k = 0; k < m; ++k) out.c[k] = z[(size_t)(m - 1) * m + k] * z[k];
+  for (int k = 0; k < m; ++k) out.c[k] = Z[(size_t)(m - 1) * m + k] * Z[k];
   return true;
 }
 

@@ -17,7 +17,8 @@ struct SmallEig {
   double h = 0.0;           // h_{m+1,m}
 };
 
-// T = tridiag(beta[0..m-2], alpha[0..m-1], beta[0..m-2]); returns false if QL fails to converge.
+// T = tridiag(beta[0..m-2], alpha[0..m-1], beta[0..m-2]); returns false if the implicit QR
+// iteration fails to converge.
 bool tridiag_eig(int m, const double* alpha, const double* beta, SmallEig& out);
 
 // f(tau) = h |sum_k c_k e^{-i lam_k tau}|

@@ -22,6 +22,16 @@
 
 #include <chrono>
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a profiler is attached
+
+namespace {
+// NVTX range for the lifetime of a scope (te_evolve, each restart's Krylov decomposition, the
+// host step search, V.omega): nsys/ncu timelines show the algorithm's phases
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+}  // namespace
 
 using te::KDev;
 using te::Launch;
@@ -130,6 +140,10 @@ struct te_handle {
   uint16_t* d_lcol = nullptr;
   int spmv_xs_tpr = 1, xs_ecap = 0, xs_xcap = 0, xs_stages = 2, xs_xpol = 0;
   double xs_global_frac = 1.0;  // entries the plan left to global gathers / nnz
+  uint8_t* d_xs_code = nullptr;  // value dictionary (<= 255 distinct off-diagonal values)
+  void* d_xs_diag = nullptr;
+  void* d_xs_dict = nullptr;
+  int xs_ndict = 0;
   int64_t ncol_limit = 0;
   // SELL-32-sigma copy of H (SpMV variant 6), built on first selection
   int32_t* d_scol = nullptr;
@@ -232,6 +246,10 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.xs_xcap = h->xs_xcap;
   d.xs_rmax = te::kXsRmax;
   d.xs_xpol = h->xs_xpol;
+  d.xs_code = h->d_xs_code;
+  d.xs_diag = h->d_xs_diag;
+  d.xs_dict = h->d_xs_dict;
+  d.xs_ndict = h->xs_ndict;
   d.scol = h->d_scol;
   d.sval = h->d_sval;
   d.sptr = h->d_sptr;
@@ -530,7 +548,13 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
   KDev d = make_kdev(h, tol_rate, m);
   Launch L = make_launch(h);
   const double n = (double)h->n;
-  const double bh = (double)(h->nnz + h->nh_entries) * ((h->cplx ? 16.0 : 8.0) + 4.0) + 8.0 * (n + 1.0);
+  const double vbytes = h->cplx ? 16.0 : 8.0;
+  // H bytes of the streamed format: CSR (value + int32 column), staged-x (value + 16-bit slot),
+  // staged-x with the value dictionary (8-bit code + 16-bit slot, plus one diagonal value per row)
+  double bh = (double)(h->nnz + h->nh_entries) * (vbytes + 4.0) + 8.0 * (n + 1.0);
+  if (h->spmv_tiled == 8 && h->ntiles_xs > 0)
+    bh = h->d_xs_code ? (double)h->nnz * 3.0 + n * vbytes + 8.0 * (n + 1.0) : (double)h->nnz * (vbytes + 2.0) + 8.0 * (n + 1.0);
+  if (h->spmv_tiled == 8 && h->ntiles_xs > 0) bh += (double)h->nh_entries * (vbytes + 4.0);
   te::launch_restart_init(d, L); LCHECK("restart_init");
   ++h->launches;
   for (int j = 0; j < m; ++j) {
@@ -625,6 +649,7 @@ int wait_restart(te_handle* h) {
 }
 
 int run_arnoldi(te_handle* h, int m, double tol_rate) {
+  Nvtx range("te: Krylov decomposition (Alg. 1 step 1)");
   if (h->dist && h->dist->nranks > 1 && !h->dist->comm) return set_err(TE_ERR_NCCL, "communicator was aborted");
   if (peer_active(h) && h->peer_for_V != h->d_V) {  // collective; never inside a graph capture
     const int rc = setup_peers(h);
@@ -727,6 +752,7 @@ struct Sampling {
 
 int evolve_core(te_handle* h, double t, double tol, int m_max, const double* forced, int64_t nforced,
                 te_stats* st, const Sampling* smp = nullptr) {
+  Nvtx range("te_evolve");
   te_stats S{};
   S.one_norm = h->norm1;
   S.roundoff_step = (double)h->n_global * h->norm1 * std::ldexp(1.0, -52);  // Eq. 17
@@ -780,6 +806,7 @@ int evolve_core(te_handle* h, double t, double tol, int m_max, const double* for
     bool brk = false;
     if ((rc = read_flag(h, m, &m_eff, &brk))) { fill(); return rc; }
     const auto host_t0 = std::chrono::steady_clock::now();
+    Nvtx range_host("te: eigensolve + error integral + step search (Alg. 1 step 2)");
     const double* alpha = h->h_small + kOffAlpha;
     const double* beta = h->h_small + kOffBeta;
     te::SmallEig E;
@@ -887,6 +914,13 @@ int check_evolve_args(te_handle* h, double t, double tol, int m_max) {
 
 // ---------------------------------------------------------------- staged-x SpMV plan
 void free_xs(te_handle* h) {
+  cudaFree(h->d_xs_code);
+  cudaFree(h->d_xs_diag);
+  cudaFree(h->d_xs_dict);
+  h->d_xs_code = nullptr;
+  h->d_xs_diag = nullptr;
+  h->d_xs_dict = nullptr;
+  h->xs_ndict = 0;
   cudaFree(h->d_tile_xs);
   cudaFree(h->d_xs_meta);
   cudaFree(h->d_xs_rng);
@@ -901,8 +935,77 @@ void free_xs(te_handle* h) {
 // Tiles of <= 32*15/TPR rows and <= xs_ecap entries (TPR: <= 8 entries per lane of a mean-length
 // row), then the device plan (spmv_xs.cu): per tile the x ranges to stage and each entry's slot.
 // rowptr: host copy of the (local) row pointers.
+// Value dictionary on the device: distinct off-diagonal values (bit patterns) into a 1024-slot hash
+// table; if there are at most 255, sorted by bit pattern they become codes 0..254 (255: diagonal).
+int build_dict(te_handle* h) {
+  if (const char* e = getenv("TE_SPMV_XS_DICT"))
+    if (atoi(e) == 0) return TE_OK;
+  cudaStream_t s = h->stream ? h->stream : h->own_stream;
+  constexpr int cap = 1024;
+  const size_t tb = te::dict_slot_bytes() * cap;
+  void* table = nullptr;
+  unsigned* count = nullptr;
+  CK(cudaMalloc(&table, tb + 16));
+  count = reinterpret_cast<unsigned*>(static_cast<char*>(table) + tb);
+  CK(cudaMemsetAsync(table, 0, tb + 16, s));
+  te::launch_dict_insert(h->n, h->d_rowptr, h->d_col, h->d_val, h->cplx, table, cap, count, s);
+  std::vector<unsigned char> ht(tb + 16);
+  CK(cudaMemcpyAsync(ht.data(), table, tb + 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFree(table);
+  unsigned cnt = 0;
+  std::memcpy(&cnt, ht.data() + tb, sizeof cnt);
+  if (cnt > 255) return TE_OK;
+  struct Slot { unsigned state, pad; double re, im; };
+  std::vector<std::pair<std::pair<uint64_t, uint64_t>, double2>> keys;
+  for (int i = 0; i < cap; ++i) {
+    Slot sl;
+    std::memcpy(&sl, ht.data() + (size_t)i * sizeof(Slot), sizeof sl);
+    if (sl.state != 2u) continue;
+    uint64_t a, b;
+    std::memcpy(&a, &sl.re, 8);
+    std::memcpy(&b, &sl.im, 8);
+    keys.push_back({{a, b}, make_double2(sl.re, sl.im)});
+  }
+  std::sort(keys.begin(), keys.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+  const int nd = (int)keys.size();
+  std::vector<double2> kd((size_t)std::max(1, nd));
+  std::vector<double> vr((size_t)std::max(1, nd));
+  for (int i = 0; i < nd; ++i) {
+    kd[(size_t)i] = keys[(size_t)i].second;
+    vr[(size_t)i] = keys[(size_t)i].second.x;
+  }
+  const size_t vb = h->cplx ? 16 : 8;
+  double2* dkeys = nullptr;
+  CK(cudaMalloc(&dkeys, sizeof(double2) * kd.size()));
+  if (cudaMalloc(&h->d_xs_code, (size_t)h->nnz + 32) != cudaSuccess || cudaMalloc(&h->d_xs_diag, vb * (h->n + 2)) != cudaSuccess ||
+      cudaMalloc(&h->d_xs_dict, vb * 256) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(dkeys);
+    cudaFree(h->d_xs_code); cudaFree(h->d_xs_diag); cudaFree(h->d_xs_dict);
+    h->d_xs_code = nullptr; h->d_xs_diag = nullptr; h->d_xs_dict = nullptr;
+    return TE_OK;  // no room for the codes: stream the values as they are
+  }
+  CK(cudaMemcpyAsync(dkeys, kd.data(), sizeof(double2) * kd.size(), cudaMemcpyHostToDevice, s));
+  if (h->cplx) CK(cudaMemcpyAsync(h->d_xs_dict, kd.data(), sizeof(double2) * nd, cudaMemcpyHostToDevice, s));
+  else CK(cudaMemcpyAsync(h->d_xs_dict, vr.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(h->d_xs_code, 0, (size_t)h->nnz + 32, s));
+  CK(cudaMemsetAsync(h->d_xs_diag, 0, vb * (h->n + 2), s));
+  te::launch_dict_codes(h->n, h->d_rowptr, h->d_col, h->d_val, h->cplx, dkeys, nd, h->d_xs_code, h->d_xs_diag, s);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  cudaFree(dkeys);
+  h->xs_ndict = nd;
+  return TE_OK;
+}
+
 int plan_xs(te_handle* h, const int64_t* rowptr) {
   free_xs(h);
+  {
+    const int rc = build_dict(h);
+    if (rc) return rc;
+  }
+  const bool dict = h->d_xs_code != nullptr;
   const int64_t n = h->n;
   const double avg = n > 0 ? (double)h->nnz / (double)n : 0.0;
   int tx = 1;  // measured (config 2): one lane per row beats 2 / 4 (larger tiles, longer x ranges)
@@ -912,12 +1015,12 @@ int plan_xs(te_handle* h, const int64_t* rowptr) {
     if (v == 1 || v == 2 || v == 4 || v == 8) tx = v;
   }
   h->spmv_xs_tpr = tx;
-  h->xs_ecap = h->cplx ? 2048 : 4096;
+  h->xs_ecap = dict ? 8192 : (h->cplx ? 2048 : 4096);
   if (const char* e = getenv("TE_SPMV_XS_ECAP")) h->xs_ecap = std::max(64, std::min(8192, atoi(e)));
   h->xs_stages = 2;
   if (const char* e = getenv("TE_SPMV_XS_XPOL")) h->xs_xpol = atoi(e) != 0;
   if (const char* e = getenv("TE_SPMV_XS_STAGES")) h->xs_stages = atoi(e) == 3 ? 3 : 2;
-  h->xs_xcap = te::xs_xcap_for(h->cplx, tx, h->xs_ecap, te::kXsBudget, h->xs_stages);
+  h->xs_xcap = te::xs_xcap_for(h->cplx, tx, h->xs_ecap, te::kXsBudget, h->xs_stages, dict);
   const int64_t rcap = 32 * te::kXsConsumers / tx;
   std::vector<int64_t> tg;
   int64_t st = 0;
@@ -1438,6 +1541,32 @@ int te_get_profile(const te_handle* h, int kernel, te_kernel_profile* out) {
 }
 
 int64_t te_launch_count(const te_handle* h) { return h ? h->launches : -1; }
+
+int te_small_eig(int m, const double* alpha, const double* beta, double* lam, double* U) {
+  clear_err();
+  if (m < 1 || m > TE_M_MAX || !alpha || (m > 1 && !beta) || !lam || !U) return set_err(TE_ERR_ARG, "bad arguments");
+  te::SmallEig E;
+  if (!te::tridiag_eig(m, alpha, beta, E)) return set_err(TE_ERR_NUMERICAL, "tridiagonal eigensolver did not converge");
+  for (int k = 0; k < m; ++k) lam[k] = E.lam[(size_t)k];
+  for (size_t i = 0; i < (size_t)m * m; ++i) U[i] = E.U[i];
+  return TE_OK;
+}
+
+int te_step_search(int m, const double* alpha, const double* beta, double h, int breakdown, int first,
+                   double tau_prev, double rem, double tol_rate, double t_total, int integrator, double* tau,
+                   double* err, int* quad_ok) {
+  clear_err();
+  if (m < 1 || m > TE_M_MAX || !alpha || (m > 1 && !beta) || !tau || !err) return set_err(TE_ERR_ARG, "bad arguments");
+  te::SmallEig E;
+  if (!te::tridiag_eig(m, alpha, beta, E)) return set_err(TE_ERR_NUMERICAL, "tridiagonal eigensolver did not converge");
+  E.h = h;
+  const te::StepResult r = te::find_step(E, breakdown != 0, first != 0, tau_prev, rem, tol_rate, t_total, integrator);
+  if (r.collapse) return set_err(TE_ERR_STEP_COLLAPSE, "step size collapsed below 1e-13 t");
+  *tau = r.tau;
+  *err = r.err;
+  if (quad_ok) *quad_ok = r.quad_ok ? 1 : 0;
+  return TE_OK;
+}
 double te_one_norm(const te_handle* h) { return h ? h->norm1 : -1.0; }
 
 // ------------------------------------------------------------------------------------------

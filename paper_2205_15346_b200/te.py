@@ -87,6 +87,10 @@ def load():
     L.te_destroy.argtypes = [V]
     L.te_set_option.restype = C.c_int
     L.te_set_option.argtypes = [V, C.c_int, D]
+    L.te_small_eig.restype = C.c_int
+    L.te_small_eig.argtypes = [C.c_int, V, V, V, V]
+    L.te_step_search.restype = C.c_int
+    L.te_step_search.argtypes = [C.c_int, V, V, D, C.c_int, C.c_int, D, D, D, D, C.c_int, P(D), P(D), P(C.c_int)]
     L.te_get_option.restype = C.c_int
     L.te_get_option.argtypes = [V, C.c_int, P(D)]
     L.te_get_profile.restype = C.c_int
@@ -284,6 +288,33 @@ def te_krylov_basis(h: Handle, v1, m, tol_rate, want_V=True):
 def te_set_option(h: Handle, option: int, value: float):
     L = load()
     _check(L, L.te_set_option(h.ptr, int(option), float(value)))
+
+
+def te_small_eig(alpha, beta):
+    """Host eigensolver of the library (no GPU needed): returns (lam, U), U[:, k] eigenvectors."""
+    L = load()
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    m = a.shape[0]
+    b = np.zeros(max(1, m), dtype=np.float64)
+    b[: max(0, m - 1)] = np.asarray(beta, dtype=np.float64)[: max(0, m - 1)]
+    lam = np.zeros(m)
+    U = np.zeros((m, m))
+    _check(L, L.te_small_eig(m, _ptr(a), _ptr(b), _ptr(lam), _ptr(U)))
+    return lam, U
+
+
+def te_step_search(alpha, beta, h, breakdown, first, tau_prev, rem, tol_rate, t_total, integrator=0):
+    """Host step search of the library (no GPU needed): returns (tau, err, quad_ok)."""
+    L = load()
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    m = a.shape[0]
+    b = np.zeros(max(1, m), dtype=np.float64)
+    b[: max(0, m - 1)] = np.asarray(beta, dtype=np.float64)[: max(0, m - 1)]
+    tau, err, ok = C.c_double(0), C.c_double(0), C.c_int(0)
+    _check(L, L.te_step_search(m, _ptr(a), _ptr(b), float(h), int(bool(breakdown)), int(bool(first)), float(tau_prev),
+                               float(rem), float(tol_rate), float(t_total), int(integrator), C.byref(tau),
+                               C.byref(err), C.byref(ok)))
+    return tau.value, err.value, bool(ok.value)
 
 
 def te_get_option(h: Handle, option: int) -> float:

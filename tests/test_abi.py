@@ -119,3 +119,51 @@ def test_binding_rejects_bad_buffers_before_the_c_call(lib):
         te.te_create_csr(2, np.array([0, 1]), np.array([1, 0]), np.array([1.0, 1.0]))      # rowptr too short
     with pytest.raises(ValueError):
         te.te_create_csr(2, np.array([0, 1, 3]), np.array([1, 0]), np.array([1.0, 1.0]))   # col shorter than nnz
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 8, 40, 64])
+def test_host_eigensolver_against_numpy(lib, m):
+    """The library's host tridiagonal eigensolver (te_small_eig, implicit symmetric QR)
+    against numpy.linalg.eigh: eigenvalues, T U = U diag(lam), U orthogonal; also a matrix with
+    negligible couplings (deflation), a zero matrix and repeated eigenvalues."""
+    g = np.random.default_rng(m)
+    cases = [(g.standard_normal(m), np.abs(g.standard_normal(max(0, m - 1))) + 0.1)]
+    if m > 2:
+        b = np.abs(g.standard_normal(m - 1)) + 0.1
+        b[m // 2] = 1e-300
+        cases += [(g.standard_normal(m), b), (np.zeros(m), np.zeros(m - 1)), (np.ones(m), np.zeros(m - 1) + 1e-17)]
+    for a, b in cases:
+        T = np.diag(a) + np.diag(b, 1) + np.diag(b, -1) if m > 1 else np.diag(a)
+        lam, U = te.te_small_eig(a, b)
+        assert np.allclose(np.sort(lam), np.linalg.eigvalsh(T), atol=1e-13 * max(1, np.abs(T).max()), rtol=0)
+        assert np.abs(T @ U - U * lam).max() <= 1e-13 * max(1, np.abs(T).max()) * m
+        assert np.abs(U.T @ U - np.eye(m)).max() <= 1e-13 * m
+
+
+@pytest.mark.parametrize("first", [True, False])
+@pytest.mark.parametrize("integrator", [0, 1])
+def test_host_step_search_matches_oracle(lib, first, integrator):
+    """The library's host step search (te_step_search: Eq. 16 integral + Alg. 1 step 2) against the
+    oracle's find_step on the same T: the same step (both follow reading O-6 with the same
+    decisions) and error integrals within the quadrature tolerance 1e-3 max(e, tol_rate tau)."""
+    from oracle import krylov as K
+    for seed in range(6):
+        g = np.random.default_rng(100 + seed)
+        m = 8 + seed
+        a = g.standard_normal(m)
+        b = np.abs(g.standard_normal(m)) + 0.3
+        h = b[m - 1] * 1e-3
+        tol_rate, t = 1e-6, 3.0
+        lam, U = K.small_eig(a, b[: m - 1])
+        f = lambda x: K.integrand(lam, U, h, x)  # noqa: E731
+        integ = (lambda lo, hi: K.tanh_sinh(f, lo, hi, floor=tol_rate * (hi - lo))[0]) if integrator == 0 else \
+            (lambda lo, hi: K.gauss_legendre(f, lo, hi)[0])
+        to, eo = K.find_step(integ, False, first, 0.4, t, tol_rate, t)
+        tg, eg, ok = te.te_step_search(a, b[: m - 1], h, False, first, 0.4, t, tol_rate, t, integrator)
+        assert ok
+        assert abs(tg - to) <= 1e-12 * t
+        assert abs(eg - eo) <= 1e-3 * max(eo, tol_rate * to) + 1e-18
+        assert eg <= tol_rate * tg * (1 + 1e-12)
+    # breakdown: the remaining time in one step
+    tg, eg, _ = te.te_step_search(a, b[: m - 1], 0.0, True, first, 0.4, t, tol_rate, t, integrator)
+    assert tg == t and eg == 0.0

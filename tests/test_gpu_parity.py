@@ -109,23 +109,37 @@ def test_spmv_ring_variants(gpu_lib, name, c, tpr, halo, stages, monkeypatch):
     h.close()
 
 
+def _complex_dict_case():
+    """XXZ+NNN at L=10 with complex couplings: off-diagonal entries times e^{+-i phi} (Hermitian),
+    so the value dictionary holds complex values."""
+    c = dict(configs.build(5, L=10))
+    rows = np.repeat(np.arange(c["n"]), np.diff(c["rowptr"]))
+    ph = np.where(c["col"] > rows, np.exp(0.7j), np.exp(-0.7j))
+    c["val"] = np.where(c["col"] == rows, c["val"] + 0j, c["val"] * ph)
+    return c
+
+
 XS_CASES = RING_CASES + [("xxz_L14", configs.build(2, L=14)), ("bh_L7_N7", configs.build(3, L=7, N=7)),
-                         ("banded_n8192", configs.build(4, n=8192))]
+                         ("banded_n8192", configs.build(4, n=8192)), ("xxznnn_L10_cplx", _complex_dict_case())]
 
 
+@pytest.mark.parametrize("dict_", [1, 0], ids=["dict", "nodict"])
 @pytest.mark.parametrize("ecap", [0, 256])
 @pytest.mark.parametrize("tpr", [1, 2, 4, 8])
 @pytest.mark.parametrize("halo", [0, 1])
 @pytest.mark.parametrize("name,c", XS_CASES, ids=[x[0] for x in XS_CASES])
-def test_spmv_xs_variants(gpu_lib, name, c, tpr, halo, ecap, monkeypatch):
+def test_spmv_xs_variants(gpu_lib, name, c, tpr, halo, ecap, dict_, monkeypatch):
     """Staged-x ring SpMV (TE_OPT_SPMV = 8) for every lanes-per-row choice, plain and halo-aware,
     with the default tile size and with 256-entry tiles (many tiles per CTA: the 2-stage ring wraps,
     ranges cut by the slot budget), on matrices whose x windows are fully staged (spin chains,
     bosons), partly staged (banded + uniform) and hardly at all (uniform random columns, long
-    rows: the global-gather path), vs the oracle's Arnoldi basis."""
+    rows: the global-gather path), with and without the value dictionary (8-bit codes; real and
+    complex values; matrices with more than 255 distinct values keep their values), vs the
+    oracle's Arnoldi basis."""
     te = gpu_lib
     if c is None:
         c = _long_row_case()
+    monkeypatch.setenv("TE_SPMV_XS_DICT", str(dict_))
     monkeypatch.setenv("TE_SPMV_XS_TPR", str(tpr))
     monkeypatch.setenv("TE_SPMV_FORCE_HALO", str(halo))
     if ecap:
