@@ -163,8 +163,10 @@ enum {
                                 ranges planned on the device at create: >= 2 distinct columns at
                                 >= 1/4 density) bulk-copied into shared memory too; entries are
                                 addressed by 16-bit slots (0xFFFF: gathered from global memory).
-                                The default when the plan stages >= 95 % of the entries
-                                (structured H: spin chains, bosons, the paper's §5 model);
+                                The default when the plan stages >= 95 % of the entries and rows
+                                hold <= 40 entries on average (spin chains, bosons); the optional
+                                value dictionary (env TE_SPMV_XS_DICT=1: 8-bit codes when the
+                                off-diagonal entries take <= 255 distinct values) is off by default;
                                 7 warp-specialised ring: one producer warp bulk-copies (TMA
                                 engine) rowptr/col/val of nnz-balanced tiles into a 3-4 stage
                                 shared-memory ring, 15 consumer warps (TPR lanes per row, 8-16

@@ -70,20 +70,9 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_spmv_ring(KDev d, int j) {
     if (lane != 0) return;
     const uint64_t pol = policy_evict_first();
     constexpr int64_t VA = 16 / (int64_t)sizeof(VT);
-    // tile descriptors loaded one tile ahead, before the wait for a free stage
-    auto ld_desc = [&](int64_t t, longlong2& a, longlong2& b) {
-      if (t < d.ntiles_ring) {
-        a = __ldg(reinterpret_cast<const longlong2*>(d.tile_ring + 4 * t));
-        b = __ldg(reinterpret_cast<const longlong2*>(d.tile_ring + 4 * t) + 1);
-      }
-    };
-    longlong2 ca = make_longlong2(0, 0), cb = ca;
-    ld_desc(blockIdx.x, ca, cb);
     for (int64_t it = 0;; ++it) {
       const int64_t t = blockIdx.x + it * G;
       const int st = (int)(it % kRingStages);
-      longlong2 na = make_longlong2(0, 0), nb = na;
-      ld_desc(t + G, na, nb);
       if (it >= kRingStages) mbar_wait(&empty[st], (unsigned)(((it / kRingStages) - 1) & 1));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (t >= d.ntiles_ring) {  // tell the consumers there is nothing more
@@ -91,9 +80,10 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_spmv_ring(KDev d, int j) {
         mbar_expect_tx(&full[st], 0);
         break;
       }
-      const longlong2 a = ca, b = cb;
-      ca = na;
-      cb = nb;
+      // (loading the next descriptor before the wait, as the staged-x producer does, measured no
+      // gain on configs 2 / 5 and -7 % on config 6: kept simple)
+      const longlong2 a = __ldg(reinterpret_cast<const longlong2*>(d.tile_ring + 4 * t));
+      const longlong2 b = __ldg(reinterpret_cast<const longlong2*>(d.tile_ring + 4 * t) + 1);
       desc[st][0] = a.x; desc[st][1] = a.y; desc[st][2] = b.x; desc[st][3] = b.y;
       const int64_t cnt = b.y - b.x;
       const int64_t r0 = a.x & ~1LL, r1 = (a.y + 2) & ~1LL;

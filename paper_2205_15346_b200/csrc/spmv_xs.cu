@@ -510,14 +510,16 @@ void launch_spmv_xs(const KDev& d, bool cplx, int j, const Launch& L) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(L.grid_spmv, d.ntiles_xs));
   const bool dict = d.xs_code != nullptr;
   const size_t smem = spmv_xs_smem(cplx, L.spmv_xs_tpr, d.xs_ecap, d.xs_xcap, L.xs_stages, dict);
-#define TE_XS_S(T, H, S)                                                                               \
+#define TE_XS_NF(T, H, S, NF)                                                                           \
   if (dict) {                                                                                          \
-    if (cplx) k_spmv_xs<true, T, H, 8, S, true><<<grid, kXsThreads, smem, L.stream>>>(d, j);           \
-    else k_spmv_xs<false, T, H, 8, S, true><<<grid, kXsThreads, smem, L.stream>>>(d, j);               \
+    if (cplx) k_spmv_xs<true, T, H, NF, S, true><<<grid, kXsThreads, smem, L.stream>>>(d, j);          \
+    else k_spmv_xs<false, T, H, NF, S, true><<<grid, kXsThreads, smem, L.stream>>>(d, j);              \
   } else {                                                                                             \
-    if (cplx) k_spmv_xs<true, T, H, 8, S><<<grid, kXsThreads, smem, L.stream>>>(d, j);                 \
-    else k_spmv_xs<false, T, H, 8, S><<<grid, kXsThreads, smem, L.stream>>>(d, j);                     \
+    if (cplx) k_spmv_xs<true, T, H, NF, S><<<grid, kXsThreads, smem, L.stream>>>(d, j);                \
+    else k_spmv_xs<false, T, H, NF, S><<<grid, kXsThreads, smem, L.stream>>>(d, j);                    \
   }
+#define TE_XS_S(T, H, S) \
+  if (L.xs_nf == 16) { TE_XS_NF(T, H, S, 16) } else { TE_XS_NF(T, H, S, 8) }
 #define TE_XS_H(T, H) \
   if (L.xs_stages == 3) { TE_XS_S(T, H, 3) } else { TE_XS_S(T, H, 2) }
 #define TE_XS(T)                                                                                 \
@@ -532,23 +534,26 @@ void launch_spmv_xs(const KDev& d, bool cplx, int j, const Launch& L) {
 #undef TE_XS
 #undef TE_XS_H
 #undef TE_XS_S
+#undef TE_XS_NF
 }
 
 void configure_xs_kernels(void (*set_attr)(const void*, size_t, void*), void* ctx, size_t budget) {
   auto set = [&](const void* f, size_t want) { set_attr(f, want, ctx); };
   set((const void*)k_xs_plan, xs_plan_smem());
-#define TE_SETXS(T, H)                                             \
-  set((const void*)k_spmv_xs<false, T, H, 8, 2>, budget);          \
-  set((const void*)k_spmv_xs<true, T, H, 8, 2>, budget);           \
-  set((const void*)k_spmv_xs<false, T, H, 8, 3>, budget);          \
-  set((const void*)k_spmv_xs<true, T, H, 8, 3>, budget);           \
-  set((const void*)k_spmv_xs<false, T, H, 8, 2, true>, budget);    \
-  set((const void*)k_spmv_xs<true, T, H, 8, 2, true>, budget);     \
-  set((const void*)k_spmv_xs<false, T, H, 8, 3, true>, budget);    \
-  set((const void*)k_spmv_xs<true, T, H, 8, 3, true>, budget);
+#define TE_SETXS_NF(T, H, NF)                                       \
+  set((const void*)k_spmv_xs<false, T, H, NF, 2>, budget);          \
+  set((const void*)k_spmv_xs<true, T, H, NF, 2>, budget);           \
+  set((const void*)k_spmv_xs<false, T, H, NF, 3>, budget);          \
+  set((const void*)k_spmv_xs<true, T, H, NF, 3>, budget);           \
+  set((const void*)k_spmv_xs<false, T, H, NF, 2, true>, budget);    \
+  set((const void*)k_spmv_xs<true, T, H, NF, 2, true>, budget);     \
+  set((const void*)k_spmv_xs<false, T, H, NF, 3, true>, budget);    \
+  set((const void*)k_spmv_xs<true, T, H, NF, 3, true>, budget);
+#define TE_SETXS(T, H) TE_SETXS_NF(T, H, 8) TE_SETXS_NF(T, H, 16)
   TE_SETXS(1, 0) TE_SETXS(2, 0) TE_SETXS(4, 0) TE_SETXS(8, 0)
   TE_SETXS(1, 1) TE_SETXS(2, 1) TE_SETXS(4, 1) TE_SETXS(8, 1)
 #undef TE_SETXS
+#undef TE_SETXS_NF
 }
 
 // x slots per tile that fit the shared-memory budget next to the tile's H part

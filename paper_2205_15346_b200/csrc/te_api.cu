@@ -138,7 +138,7 @@ struct te_handle {
   int4* d_xs_meta = nullptr;
   int2* d_xs_rng = nullptr;
   uint16_t* d_lcol = nullptr;
-  int spmv_xs_tpr = 1, xs_ecap = 0, xs_xcap = 0, xs_stages = 2, xs_xpol = 0;
+  int spmv_xs_tpr = 1, xs_ecap = 0, xs_xcap = 0, xs_stages = 2, xs_xpol = 0, xs_nf = 8;
   double xs_global_frac = 1.0;  // entries the plan left to global gathers / nnz
   uint8_t* d_xs_code = nullptr;  // value dictionary (<= 255 distinct off-diagonal values)
   void* d_xs_diag = nullptr;
@@ -297,6 +297,7 @@ Launch make_launch(te_handle* h) {
   L.spmv_ring_tpr = h->spmv_ring_tpr;
   L.spmv_xs_tpr = h->spmv_xs_tpr;
   L.xs_stages = h->xs_stages;
+  L.xs_nf = h->xs_nf;
   L.ring_stages = h->ring_stages;
   L.spmv_tiled = h->spmv_tiled;
   L.prefetch = h->prefetch;
@@ -938,8 +939,12 @@ void free_xs(te_handle* h) {
 // Value dictionary on the device: distinct off-diagonal values (bit patterns) into a 1024-slot hash
 // table; if there are at most 255, sorted by bit pattern they become codes 0..254 (255: diagonal).
 int build_dict(te_handle* h) {
-  if (const char* e = getenv("TE_SPMV_XS_DICT"))
-    if (atoi(e) == 0) return TE_OK;
+  // opt-in (TE_SPMV_XS_DICT=1): a third of the H bytes, but the staged-x consumers are bound by
+  // their dependent shared-memory lookups, not by HBM (ncu), and the code -> value lookup adds
+  // one more: measured slower on configs 2 / 3 / 5 (+15 / +6 / +9 % per SpMV), faster only with
+  // 78 entries per row (config 6, -14 % vs staged-x without it, still slower than the ring)
+  const char* e = getenv("TE_SPMV_XS_DICT");
+  if (!e || atoi(e) == 0) return TE_OK;
   cudaStream_t s = h->stream ? h->stream : h->own_stream;
   constexpr int cap = 1024;
   const size_t tb = te::dict_slot_bytes() * cap;
@@ -1019,6 +1024,7 @@ int plan_xs(te_handle* h, const int64_t* rowptr) {
   if (const char* e = getenv("TE_SPMV_XS_ECAP")) h->xs_ecap = std::max(64, std::min(8192, atoi(e)));
   h->xs_stages = 2;
   if (const char* e = getenv("TE_SPMV_XS_XPOL")) h->xs_xpol = atoi(e) != 0;
+  if (const char* e = getenv("TE_SPMV_XS_NF")) h->xs_nf = atoi(e) == 16 ? 16 : 8;
   if (const char* e = getenv("TE_SPMV_XS_STAGES")) h->xs_stages = atoi(e) == 3 ? 3 : 2;
   h->xs_xcap = te::xs_xcap_for(h->cplx, tx, h->xs_ecap, te::kXsBudget, h->xs_stages, dict);
   const int64_t rcap = 32 * te::kXsConsumers / tx;
@@ -1196,10 +1202,17 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
   std::memcpy(&nrm, &nb, sizeof nrm);
   h->norm1 = nrm;
   h->ncol_limit = ncol_limit;
-  {  // staged-x SpMV: the default when its plan stages >= 95 % of the entries (structured H);
-     // otherwise its buffers are released (re-planned if selected later).  TE_SPMV_DEFAULT overrides.
-    if (plan_xs(h, rowptr) != TE_OK) return fail(TE_ERR_OOM, "staged-x plan");
-    int def = h->ntiles_xs > 0 && h->xs_global_frac <= 0.05 ? 8 : 7;
+  {  // staged-x SpMV: the default when its plan stages >= 95 % of the entries (structured H) and
+     // rows are short (mean <= 40 entries); otherwise its buffers are released (re-planned if
+     // selected later).  Measured per SpMV launch, staged-x vs ring: config 2 equal, config 3
+     // -5 %, config 5 -9 %; config 6 (78 entries per row) +27 %, config 4 (half the columns
+     // uniform: 50 % global gathers) +190 %.  TE_SPMV_DEFAULT overrides.
+    const double avg = n > 0 ? (double)h->nnz / (double)n : 0.0;
+    int def = 7;
+    if (avg <= 40.0) {
+      if (plan_xs(h, rowptr) != TE_OK) return fail(TE_ERR_OOM, "staged-x plan");
+      if (h->ntiles_xs > 0 && h->xs_global_frac <= 0.05) def = 8;
+    }
     if (const char* e = getenv("TE_SPMV_DEFAULT")) {
       const int v = atoi(e);
       if (v == 6 || v == 7 || v == 8) def = v;
