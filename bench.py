@@ -49,7 +49,7 @@ def parse():
                     help="oracle Krylov steps timed for cpu_baseline (default: 1 for n >= 2^24, else 8)")
     ap.add_argument("--prof-steps", type=int, default=3, help="evolutions in the per-kernel (roofline) pass")
     ap.add_argument("--e2e-steps", type=int, default=5, help="evolutions in the e2e (host buffers) pass")
-    ap.add_argument("--kernels", type=int, default=2, help="projection kernels: 2 hybrid (shuffle up to 4-5 columns, TMA ring above; default), 3 TMA only, 4 shuffle only")
+    ap.add_argument("--kernels", type=int, default=2, help="projection kernels: 2 hybrid (register accumulators up to 8 columns, TMA ring above; default), 3 TMA only, 5 register accumulators only")
     ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (library default if unset)")
     ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel (library default if unset): 8 staged-x ring, 7 warp-specialised ring, 6 SELL-32-sigma")
     ap.add_argument("--force-dist", action="store_true",
@@ -251,7 +251,7 @@ def config_dict(c, args, ws, nloc):
     return {"workload": f"{c['name']} ({configs.LABELS[args.config]})", "n": c["n"],
             "nnz": int(c["nnz"]), "m": c["m"], "t": c["t"], "tol": c["tol"],
             "l2": "inputs larger than L2 (V = %.0f MB > 126 MB)" % (16 * nloc * c["m"] / 1e6),
-            "parallelism": f"rows{ws}", "kernels": ["fused-register", "staged", "hybrid", "tma", "shuffle"][args.kernels],
+            "parallelism": f"rows{ws}", "kernels": {2: "hybrid", 3: "tma", 5: "regacc"}[args.kernels],
             "spmv": {None: "library default", 6: "sell", 7: "ring", 8: "staged-x ring"}[args.spmv],
             "ortho": ["cgs2", "lanczos3", "cgs2gram"][args.ortho],
             "halo": (["nccl_exchange", "peer_loads"][args.halo] if ws > 1 else None)}

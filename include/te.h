@@ -138,11 +138,13 @@ enum {
   TE_OPT_PROFILE = 1,        /* 1: record CUDA events around every kernel launch (te_get_profile) */
   TE_OPT_GRAPH = 2,          /* 1 (default): replay each restart's launches as a CUDA graph      */
   TE_OPT_KERNELS = 3,        /* projection kernels (same arithmetic, kept for measured comparison):
-                                2 (default): chosen by column count (register-streaming/shuffle
-                                  kernel for <= 4 (dots) / <= 5 (update) columns, TMA-tiled above);
+                                2 (default): chosen by column count (register-accumulator kernel
+                                  up to 8 columns, TMA-tiled above);
                                 3: TMA-tiled (2-D tensor boxes) warp-specialised projections only;
-                                4: register-streaming/shuffle projections only.  Other values:
-                                TE_ERR_ARG (round 1's fused sets 0/1 were removed)                  */
+                                5: register-accumulator projections only (slower above 16
+                                  columns: lane groups of <= 4 rows per column load).  Other
+                                values: TE_ERR_ARG (round 1's fused sets 0/1 and the shuffle
+                                set 4 were removed)                                               */
   TE_OPT_PREFETCH = 4,       /* update_norm's L2 bulk-prefetch distance (block iterations, 0..16;
                                 default 0)                                                          */
   TE_OPT_ORTHO = 6,          /* orthogonalisation: 0 (default) CGS2 against the full basis (reading
@@ -179,8 +181,13 @@ enum {
                                 Other values: TE_ERR_ARG (round 1's slower variants were removed) */
 };
 int te_set_option(te_handle* h, int option, double value);
+/* Read-only plan statistics of the staged-x SpMV (te_get_option only; -1 when the handle has no
+ * staged-x plan): entries gathered from global memory / nnz; tiles with at least one such entry /
+ * tiles; bulk-copied x slots / nnz. */
+enum { TE_INFO_XS_GLOBAL = 101, TE_INFO_XS_GLOBAL_TILES = 102, TE_INFO_XS_X_PER_ENTRY = 103 };
 /* Current value of an option (TE_OPT_SPMV reports the kernel the handle runs, e.g. the default
- * chosen at create); TE_ERR_ARG for a null handle/pointer or an unknown option. */
+ * chosen at create) or of a TE_INFO_* statistic; TE_ERR_ARG for a null handle/pointer or an
+ * unknown option. */
 int te_get_option(const te_handle* h, int option, double* value);
 
 /* Per-kernel-class profile accumulated while TE_OPT_PROFILE is on (reset by te_set_option):

@@ -1,8 +1,8 @@
 // Hot-path CUDA kernels for sm_100a besides the SpMV (spmv.cu): one Arnoldi/CGS2 step (Eq. 8,
 // P:146-162, classical Gram-Schmidt + one re-orthogonalisation, reading C1 of DESIGN.md) after the
 // SpMV, and the restart assembly V.omega (Eq. 11):
-//   proj_dots   g1 = V^H p                        k_proj_tma<0> (TMA ring) / k_proj_s<0> (shuffle)
-//   update_proj p' = p - V e1, g2 = V^H p'         k_proj_tma<1> / k_proj_s<1>
+//   proj_dots   g1 = V^H p                        k_proj_tma<0> (TMA ring) / k_proj_r<0> (registers)
+//   update_proj p' = p - V e1, g2 = V^H p'         k_proj_tma<1> / k_proj_r<1>
 //   update_norm p'' = p' - V e2 -> column j+1, ||p''||^2      k_update_norm
 //   combine     w = V (s omega), in place into column 0          k_combine
 // plus the f1 (paper-literal Lanczos) and f2 (Gram second sweep, k_proj_tma<3>) kernels,
@@ -17,8 +17,6 @@
 #include <vector>
 
 namespace te {
-
-constexpr int kCPT = 8;  // columns per lane of the register/shuffle projection kernel (k_proj_s)
 
 // --------------------------------------------------------------------------------------
 // TMA-tiled projection kernel (default path), warp-specialised:
@@ -401,73 +399,99 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
   if (tid == 0) d.counter[ctr] = 0u;
 }
 
-// Register-streaming projection kernel with shuffle row-reduction (default): TPR lanes per row,
-// lane q holds the row's V entries of columns q + TPR*c (c < 8) in registers.  Column sums over
-// the warp's rows are formed by xor-shuffles over the row bits of the lane index and added to a
-// per-warp shared-memory accumulator, so no per-column accumulator registers persist across rows
-// (~60 registers -> 4 CTAs of 256 threads per SM, 8 loads of 16 B in flight per thread).
-//   MODE 0:  g1 = V^H p                          MODE 1:  p' = p - V e1 -> W, g2 = V^H p'
-template <int MODE, int TPR>
-__global__ void __launch_bounds__(kThreads, 4) k_proj_s(KDev d, int j) {
+// --------------------------------------------------------------------------------------
+// Register-accumulator projection kernel (CGS2 passes K1b/K2 up to kRegMaxCols columns):
+// plain register streaming like k_update_norm (no shared-memory staging, 16 warps per SM),
+// with persistent per-lane column sums.  Lane (rg, q), rg = lane % RG, q = lane / RG
+// (RG = 32 / TPR rows per warp iteration) loads the V entries of row r0 + rg in columns
+// k = q + TPR c (c < CPL): each column load of a warp is RG consecutive rows (RG x 16 B
+// contiguous).  The entries stay in registers for both uses:
+//   MODE 1: p' = s_j (p - sum_k V_k e1'_k)   (row sum over the q lanes: log2 TPR xor-shuffles)
+//   dots:   acc_c += conj(V_k) p'            (per-lane, across all of the lane's rows)
+// The lane sums are reduced over rg once per kernel (log2 RG xor-shuffles per column), then per
+// block in fixed warp order and across blocks by the last block (integer ticket): deterministic
+// for a given grid.  Per element: one 16-B load and 4 (+4 in MODE 1) FMAs; no shuffles per
+// element for the dots (round 1's shuffle kernel reduced every row batch), no 255-register accumulator file
+// (k_proj_tma: 8 warps per SM, latency-bound).
+//   MODE 0 (sweep-1):  g1 = V^H p            MODE 1 (sweep-2):  p' -> W,  g2 = V^H p'
+// --------------------------------------------------------------------------------------
+template <int MODE, int TPR, int CPL, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_proj_r(KDev d, int j) {
+  constexpr int RG = 32 / TPR;
   __shared__ double2 coef[kMaxCols];
   __shared__ double2 red[kWarps][kMaxCols];
   __shared__ int go_s;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = tid % TPR, grp = tid / TPR;
-  constexpr int RPB = kThreads / TPR;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rg = lane % RG, q = lane / RG;
   const int ncols = j + 1;
-  // MODE 1: the deferred step gate (as in k_proj_tma)
   const double sj = MODE == 1 ? gate_value(d, j, d.flag[0], d.gsync[0].x) : (d.flag[0] == 0 ? 1.0 : 0.0);
   if (tid == 0) {
     if (MODE == 1 && blockIdx.x == 0) step_gate(d, j, true);
     go_s = sj != 0.0;
   }
-  for (int i = tid; i < kWarps * kMaxCols; i += kThreads) (&red[0][0])[i] = make_double2(0.0, 0.0);
   if (MODE == 1 && tid < ncols) {
     const double sk = tid == j ? sj : d.s[tid];
     const double2 g = d.g1[tid];
-    coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);
+    coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);  // e1'_k = s_k^2 g1_k
   }
   __syncthreads();
   if (!go_s) return;
   const int64_t n = d.n, ldv = d.ldv;
-  const int cmax = (ncols + TPR - 1) / TPR;  // live column slots per lane
-  for (int64_t rb = (int64_t)blockIdx.x * RPB; rb < n; rb += (int64_t)gridDim.x * RPB) {
-    const int64_t r = rb + grp;
-    const bool act = r < n;
-    double2 v[kCPT];
+  double2 acc[CPL];
 #pragma unroll
-    for (int c = 0; c < kCPT; ++c) {
-      const int k = q + TPR * c;
-      v[c] = (act && k < ncols) ? ld_stream(d.V + r + (int64_t)k * ldv) : make_double2(0.0, 0.0);
-    }
-    double2 p = act ? (MODE == 1 ? __ldcs(d.W + r) : __ldg(d.W + r)) : make_double2(0.0, 0.0);
-    if (MODE == 1) {
-      double2 a = make_double2(0.0, 0.0);
+  for (int c = 0; c < CPL; ++c) acc[c] = make_double2(0.0, 0.0);
+  // U row chunks per iteration (all loads issued before any use: U (CPL + 1) loads in flight)
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp, tw = (int64_t)gridDim.x * kWarps;
+  for (int64_t c0 = gw; c0 * RG < n; c0 += U * tw) {
+    double2 v[U][CPL], p[U];
 #pragma unroll
-      for (int c = 0; c < kCPT; ++c) {
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = (c0 + u * tw) * RG + rg;
+      const bool act = r < n;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
         const int k = q + TPR * c;
-        if (k < ncols) a = cfma(v[c], coef[k], a);
+        v[u][c] = (act && k < ncols) ? ld_stream(d.V + r + (int64_t)k * ldv) : make_double2(0.0, 0.0);
       }
-      a = group_sum<TPR>(a);
-      p = make_double2(sj * (p.x - a.x), sj * (p.y - a.y));
-      if (act && q == 0) d.W[r] = p;
+      p[u] = act ? (MODE == 1 ? __ldcs(d.W + r) : __ldg(d.W + r)) : make_double2(0.0, 0.0);
     }
 #pragma unroll
-    for (int c = 0; c < kCPT; ++c) {
-      if (c >= cmax) break;  // warp-uniform: only the live column slots are reduced
-      double2 pr = make_double2(v[c].x * p.x + v[c].y * p.y, v[c].x * p.y - v[c].y * p.x);  // conj(v) p
+    for (int u = 0; u < U; ++u) {
+      if (MODE == 1) {
+        const int64_t r = (c0 + u * tw) * RG + rg;
+        const bool act = r < n;
+        double2 a0 = make_double2(0.0, 0.0), a1 = a0;
 #pragma unroll
-      for (int off = TPR; off < 32; off <<= 1) {
-        pr.x += __shfl_xor_sync(0xffffffffu, pr.x, off);
-        pr.y += __shfl_xor_sync(0xffffffffu, pr.y, off);
+        for (int c = 0; c < CPL; c += 2) {
+          const int k = q + TPR * c;
+          if (k < ncols) a0 = cfma(v[u][c], coef[k], a0);
+          if (c + 1 < CPL && k + TPR < ncols) a1 = cfma(v[u][c + 1], coef[k + TPR], a1);
+        }
+        double2 a = cadd(a0, a1);
+#pragma unroll
+        for (int off = RG; off < 32; off <<= 1) {
+          a.x += __shfl_xor_sync(0xffffffffu, a.x, off);
+          a.y += __shfl_xor_sync(0xffffffffu, a.y, off);
+        }
+        p[u] = act ? make_double2(sj * (p[u].x - a.x), sj * (p[u].y - a.y)) : make_double2(0.0, 0.0);
+        if (act && q == 0) d.W[r] = p[u];
       }
-      const int k = q + TPR * c;
-      if (lane < TPR && k < ncols) red[warp][k] = cadd(red[warp][k], pr);
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc[c] = cfma_conj(v[u][c], p[u], acc[c]);
     }
   }
+  // lane sums over rg (fixed butterfly), then lane rg == 0 of each q holds the warp's column sums
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+#pragma unroll
+    for (int off = 1; off < RG; off <<= 1) {
+      acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, off);
+      acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, off);
+    }
+    const int k = q + TPR * c;
+    if (rg == 0 && k < kMaxCols) red[warp][k] = acc[c];
+  }
   __syncthreads();
-  double2* out = MODE == 0 ? d.g1 : d.g2;
-  const int ctr = MODE;
   if (tid < ncols) {
     double2 t = red[0][tid];
     for (int w = 1; w < kWarps; ++w) t = cadd(t, red[w][tid]);
@@ -476,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_proj_s(KDev d, int j) {
   __threadfence();
   __syncthreads();
   __shared__ int last;
+  const int ctr = MODE == 0 ? 0 : 1;
   if (tid == 0) last = (atomicAdd(&d.counter[ctr], 1u) == gridDim.x - 1);
   __syncthreads();
   if (!last) return;
@@ -493,13 +518,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_proj_s(KDev d, int j) {
     seg[sgi][c] = sm;
   }
   __syncthreads();
-  if (tid < ncols) {
-    double2 t = seg[0][tid];
-    t = cadd(t, seg[1][tid]);
-    t = cadd(t, seg[2][tid]);
-    t = cadd(t, seg[3][tid]);
-    out[tid] = t;
-  }
+  double2* out = MODE == 0 ? d.g1 : d.g2;
+  if (tid < ncols) out[tid] = cadd(cadd(cadd(seg[0][tid], seg[1][tid]), seg[2][tid]), seg[3][tid]);
   if (MODE == 0 && tid == 0) d.gsync[0] = make_double2(j > 0 ? d.nrm2[j - 1] : 0.0, 0.0);
   if (tid == 0) d.counter[ctr] = 0u;
 }
@@ -845,35 +865,12 @@ cudaError_t configure_kernels() {
   return status;
 }
 
-static int tpr_for(int ncols, int min_tpr) {
-  int t = min_tpr;
-  while (t * kCPT < ncols) t <<= 1;
-  return t;
-}
-
-#define TE_DISPATCH_TPR(tpr, ...)                               \
-  switch (tpr) {                                               \
-    case 1: { constexpr int TPR = 1; __VA_ARGS__; } break;     \
-    case 2: { constexpr int TPR = 2; __VA_ARGS__; } break;     \
-    case 4: { constexpr int TPR = 4; __VA_ARGS__; } break;     \
-    default: { constexpr int TPR = 8; __VA_ARGS__; } break;    \
-  }
-
-static void launch_proj_s(const KDev& d, int j, int mode, const Launch& L) {
-  const int tpr = tpr_for(j + 1, 1);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * L.num_sms, (d.n * tpr + kThreads - 1) / kThreads));
-  TE_DISPATCH_TPR(tpr, {
-    if (mode == 0) k_proj_s<0, TPR><<<grid, kThreads, 0, L.stream>>>(d, j);
-    else k_proj_s<1, TPR><<<grid, kThreads, 0, L.stream>>>(d, j);
-  });
-}
-
-// measured on B200 (tools/micro/mb_proj.cu, 16 KB minimum TMA tiles): the register/shuffle kernel
-// is faster for the dots up to 4 columns and for the update up to 5 columns, the TMA ring above;
+// measured on B200 (tools/micro/mb_proj.cu, n = 2^20 and 2^23): the register-accumulator kernel
+// is faster than the TMA ring up to 8 columns (e.g. 4 columns, n = 2^20: dots 4.7 vs 2.9 TB/s),
+// the TMA ring above (lane groups of 4+ rows per column load lose coalescing: 64-B chunks);
 // the TMA ring keeps per-lane register column sums for the smallest of 8 / 16 / 32 columns that
 // covers ncols (fewer live registers at small ncols: 8 columns, update 3.7 -> 4.7 TB/s)
-constexpr int kShuffleMaxColsDots = 4;
-constexpr int kShuffleMaxCols = 5;
+constexpr int kRegMaxCols = 8;
 
 #define TE_PROJ_TMA(MODE, ncols, ...)                                                                   \
   do {                                                                                                  \
@@ -882,9 +879,41 @@ constexpr int kShuffleMaxCols = 5;
     else k_proj_tma<MODE, 32><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__);                   \
   } while (0)
 
+// register-accumulator kernel: CPL = 4 columns per lane, TPR = the smallest power of two with
+// TPR * CPL >= ncols, U = 2 row chunks per iteration (10 loads in flight per lane), 2 CTAs per SM
+constexpr int kProjRCpl = 4;
+constexpr int kProjRU = 2;
+constexpr int kProjRMinb = 2;
+int proj_r_tpr(int ncols) {
+  int t = 1;
+  while (t * kProjRCpl < ncols) t <<= 1;
+  return t;
+}
+static void launch_proj_r(const KDev& d, int j, int mode, const Launch& L) {
+  const int grid = L.num_sms * kProjRMinb;
+  switch (proj_r_tpr(j + 1)) {
+#define TE_PROJ_R_CASE(T)                                                                                \
+  case T:                                                                                                \
+    if (mode == 0) k_proj_r<0, T, kProjRCpl, kProjRU, kProjRMinb><<<grid, kThreads, 0, L.stream>>>(d, j); \
+    else k_proj_r<1, T, kProjRCpl, kProjRU, kProjRMinb><<<grid, kThreads, 0, L.stream>>>(d, j);           \
+    break;
+    TE_PROJ_R_CASE(1)
+    TE_PROJ_R_CASE(2)
+    TE_PROJ_R_CASE(4)
+    TE_PROJ_R_CASE(8)
+    default:
+    TE_PROJ_R_CASE(16)
+#undef TE_PROJ_R_CASE
+  }
+}
+
+static bool use_reg(const Launch& L, int ncols) {
+  return L.proj_tma == 3 || (L.proj_tma == 2 && ncols <= kRegMaxCols);
+}
+
 void launch_proj_dots(const KDev& d, int j, const Launch& L) {
-  if (L.proj_tma == 0 || (L.proj_tma == 2 && j + 1 <= kShuffleMaxColsDots)) {
-    launch_proj_s(d, j, 0, L);
+  if (use_reg(L, j + 1)) {
+    launch_proj_r(d, j, 0, L);
     return;
   }
   const int S = proj_slots(j + 1), R = proj_rsub(j + 1), C = proj_consumers(j + 1);
@@ -897,8 +926,8 @@ void launch_gram_update(const KDev& d, int j, bool write, const Launch& L) {
 }
 
 void launch_update_proj(const KDev& d, int j, const Launch& L) {
-  if (L.proj_tma == 0 || (L.proj_tma == 2 && j + 1 <= kShuffleMaxCols)) {
-    launch_proj_s(d, j, 1, L);
+  if (use_reg(L, j + 1)) {
+    launch_proj_r(d, j, 1, L);
     return;
   }
   const int S = proj_slots(j + 1), R = proj_rsub(j + 1), C = proj_consumers(j + 1);

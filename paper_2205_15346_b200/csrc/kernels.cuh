@@ -99,7 +99,7 @@ struct Launch {
   int spmv_xs_tpr;      // lanes per row of the staged-x ring SpMV
   int xs_stages;        // its ring depth (2 or 3)
   int xs_nf;            // its entries in flight per lane (8 or 16)
-  int proj_tma;         // 2: hybrid by column count (default), 1: TMA-tiled only, 0: register/shuffle only
+  int proj_tma;         // 2: hybrid by column count (default), 1: TMA-tiled only, 3: register accumulators only
   int spmv_tiled;       // 8: staged-x ring, 7: warp-specialised ring, 6: SELL-32-sigma
   int prefetch;         // update_norm: L2 bulk-prefetch distance in block iterations (0: off)
 };

@@ -140,6 +140,8 @@ struct te_handle {
   uint16_t* d_lcol = nullptr;
   int spmv_xs_tpr = 1, xs_ecap = 0, xs_xcap = 0, xs_stages = 2, xs_xpol = 0, xs_nf = 8;
   double xs_global_frac = 1.0;  // entries the plan left to global gathers / nnz
+  double xs_global_tiles = 1.0; // tiles with at least one such entry / tiles
+  double xs_x_per_entry = 0.0;  // staged x slots / entries (bulk-copied x per product)
   uint8_t* d_xs_code = nullptr;  // value dictionary (<= 255 distinct off-diagonal values)
   void* d_xs_diag = nullptr;
   void* d_xs_dict = nullptr;
@@ -288,7 +290,7 @@ Launch make_launch(te_handle* h) {
   L.num_sms = h->num_sms;
   const int64_t t256 = (h->n + 255) / 256;
   L.grid_k3 = (int)std::max<int64_t>(1, std::min<int64_t>(8 * h->num_sms, t256));
-  L.proj_tma = h->variant == 2 ? 2 : (h->variant == 3 ? 1 : (h->variant == 4 ? 0 : 0));
+  L.proj_tma = h->variant == 3 ? 1 : (h->variant == 5 ? 3 : 2);
   L.tmaps = h->tmaps.data();
   L.spmv_nf_wide = h->spmv_nf_wide;
   L.spmv_force_halo = h->spmv_force_halo;
@@ -1059,10 +1061,16 @@ int plan_xs(te_handle* h, const int64_t* rowptr) {
   std::vector<int4> meta((size_t)nt);
   CK(cudaMemcpyAsync(meta.data(), h->d_xs_meta, sizeof(int4) * nt, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  int64_t ng = 0;
-  for (const int4& m : meta) ng += m.z;
+  int64_t ng = 0, tg_glob = 0, nxs = 0;
+  for (const int4& m : meta) {
+    ng += m.z;
+    tg_glob += m.z > 0;
+    nxs += m.y;
+  }
   h->ntiles_xs = nt;
   h->xs_global_frac = h->nnz > 0 ? (double)ng / (double)h->nnz : 0.0;
+  h->xs_global_tiles = (double)tg_glob / (double)nt;
+  h->xs_x_per_entry = h->nnz > 0 ? (double)nxs / (double)h->nnz : 0.0;
   return TE_OK;
 }
 
@@ -1489,8 +1497,8 @@ int te_set_option(te_handle* h, int option, double value) {
       h->use_graph = value != 0.0;
       return TE_OK;
     case TE_OPT_KERNELS:
-      if (value != 2.0 && value != 3.0 && value != 4.0)
-        return set_err(TE_ERR_ARG, "TE_OPT_KERNELS must be 2 (hybrid), 3 (TMA ring) or 4 (shuffle)");
+      if (value != 2.0 && value != 3.0 && value != 5.0)
+        return set_err(TE_ERR_ARG, "TE_OPT_KERNELS must be 2 (hybrid), 3 (TMA ring) or 5 (register accumulators)");
       h->variant = (int)value;
       return TE_OK;
     case TE_OPT_ORTHO:
@@ -1543,6 +1551,9 @@ int te_get_option(const te_handle* h, int option, double* value) {
     case TE_OPT_ORTHO: *value = h->ortho; return TE_OK;
     case TE_OPT_INTEGRATOR: *value = h->integrator; return TE_OK;
     case TE_OPT_HALO: *value = h->halo_mode; return TE_OK;
+    case TE_INFO_XS_GLOBAL: *value = h->ntiles_xs > 0 ? h->xs_global_frac : -1.0; return TE_OK;
+    case TE_INFO_XS_GLOBAL_TILES: *value = h->ntiles_xs > 0 ? h->xs_global_tiles : -1.0; return TE_OK;
+    case TE_INFO_XS_X_PER_ENTRY: *value = h->ntiles_xs > 0 ? h->xs_x_per_entry : -1.0; return TE_OK;
     default: return set_err(TE_ERR_ARG, "unknown option %d", option);
   }
 }

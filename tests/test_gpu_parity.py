@@ -35,8 +35,8 @@ def small_cases():
 CASES = small_cases()
 
 
-KERNEL_SETS = [(2, 8), (2, 7), (2, 6), (3, 7), (4, 7)]
-KERNEL_IDS = ["hybrid-spmvxs", "hybrid-spmvring", "hybrid-spmvsell", "tma", "shuffle"]
+KERNEL_SETS = [(2, 8), (2, 7), (2, 6), (3, 7), (5, 7)]
+KERNEL_IDS = ["hybrid-spmvxs", "hybrid-spmvring", "hybrid-spmvsell", "tma", "regacc"]
 
 
 @pytest.mark.parametrize("kset", KERNEL_SETS, ids=KERNEL_IDS)
@@ -250,8 +250,8 @@ def test_dense_exponential_and_bound(gpu_lib):
     assert st["err_bound"] <= c["tol"]
 
 
-@pytest.mark.parametrize("kset,ortho", [((2, 7), 0), ((3, 7), 0), ((4, 7), 0), ((2, 6), 0), ((2, 7), 2), ((2, 7), 1)],
-                         ids=["hybrid-ring", "tma", "shuffle", "hybrid-sell", "cgs2gram", "lanczos3"])
+@pytest.mark.parametrize("kset,ortho", [((2, 7), 0), ((3, 7), 0), ((5, 7), 0), ((2, 6), 0), ((2, 7), 2), ((2, 7), 1)],
+                         ids=["hybrid-ring", "tma", "regacc", "hybrid-sell", "cgs2gram", "lanczos3"])
 def test_maximum_krylov_dimension(gpu_lib, kset, ortho):
     """m = TE_M_MAX = 64: every column group of the projection kernels (register partials and the
     16-wide butterflies up to column 63, the 64 x 64 Gram matrix of f2) against the oracle; one
@@ -310,7 +310,7 @@ def test_option_validation(gpu_lib):
     h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
     v_ref, _ = te.te_evolve(h, c["v0"], 0.5, 1e-9, 20)
     for opt, bad in ((te.TE_OPT_SPMV, 9), (te.TE_OPT_SPMV, 4), (te.TE_OPT_SPMV, -1), (te.TE_OPT_KERNELS, 0), (te.TE_OPT_HALO, 2), (te.TE_OPT_ORTHO, 3),
-                     (te.TE_OPT_KERNELS, 5), (te.TE_OPT_INTEGRATOR, 2), (te.TE_OPT_SPMV, 4.5)):
+                     (te.TE_OPT_KERNELS, 4), (te.TE_OPT_KERNELS, 6), (te.TE_OPT_INTEGRATOR, 2), (te.TE_OPT_SPMV, 4.5)):
         with pytest.raises(te.TEError):
             te.te_set_option(h, opt, bad)
     te.te_set_option(h, te.TE_OPT_HALO, 1)

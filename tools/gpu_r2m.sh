@@ -1,0 +1,9 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 1500 python tools/spmv_sweep.py --config 5 --m 5 --reps 2 --variant "8:" --variant "8:TE_SPMV_XS_STAGES=3" \
+  --variant "8:TE_SPMV_XS_DICT=1" --variant "8:TE_SPMV_XS_DICT=1,TE_SPMV_XS_STAGES=3" --variant "8:TE_SPMV_XS_XPOL=1" \
+  --variant "8:TE_SPMV_XS_NF=16" --variant "8:TE_SPMV_XS_ECAP=2048" --variant "8:TE_SPMV_XS_ECAP=2048,TE_SPMV_XS_STAGES=3" \
+  --variant "8:TE_SPMV_XS_DICT=1,TE_SPMV_XS_ECAP=4096" --variant "8:TE_SPMV_XS_DICT=1,TE_SPMV_XS_ECAP=4096,TE_SPMV_XS_STAGES=3" \
+  --variant "7:" > gpurun_out/m_sweep_c5.log 2>&1
+timeout 900 python tools/spmv_sweep.py --config 2 --m 5 --reps 4 --variant "8:" --variant "8:TE_SPMV_XS_STAGES=3" \
+  --variant "8:TE_SPMV_XS_DICT=1" --variant "8:TE_SPMV_XS_DICT=1,TE_SPMV_XS_STAGES=3" --variant "8:TE_SPMV_XS_ECAP=2048,TE_SPMV_XS_STAGES=3" --variant "7:" > gpurun_out/m_sweep_c2.log 2>&1

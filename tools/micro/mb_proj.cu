@@ -1,73 +1,131 @@
-// Microbenchmark of the hot-path kernels on synthetic data (no library state): times the TMA
-// projection kernel in its three modes (0 dots, 1 update+dots, 2 streaming only) and the
-// register update_norm kernel for a range of column counts, n = 2^20 rows.
+// Microbenchmark: register-accumulator projection kernel k_proj_r<MODE, TPR, CPL, U, MINB> against the
+// TMA ring (k_proj_tma) and update_norm, synthetic V (random values), n rows (default 2^23, so V
+// exceeds L2 at every column count).  Also checks k_proj_r's dots against k_proj_tma's (relative).
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -I include -I <nccl>
+//        tools/micro/mb_proj.cu -o tools/micro/mb_proj -L/usr/local/cuda/lib64/stubs -lcuda
+// Round-2 results (B200, GB/s at n = 2^20 / 2^23): DESIGN.md §6.
 #include "../../paper_2205_15346_b200/csrc/kernels.cu"
 #include "../../paper_2205_15346_b200/csrc/spmv.cu"
+#include "../../paper_2205_15346_b200/csrc/spmv_xs.cu"
 #include <cudaTypedefs.h>
+#include <cmath>
 #include <cstdio>
 #include <vector>
 using namespace te;
+
+__global__ void k_fill(double2* x, int64_t cnt, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = (uint64_t)i * 0x9E3779B97F4A7C15ull + seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    x[i] = make_double2((double)(z >> 11) * 0x1.0p-53 - 0.5, (double)((z * 31) >> 11) * 0x1.0p-53 - 0.5);
+  }
+}
+
+template <int MODE, int TPR, int CPL, int U, int MINB>
+void run_r(const KDev& d, int j, int sms) {
+  k_proj_r<MODE, TPR, CPL, U, MINB><<<sms * MINB, kThreads>>>(d, j);
+}
+
 int main(int argc, char** argv) {
-  const int64_t n = argc > 1 ? atoll(argv[1]) : (1 << 20);
-  if (argc > 3) g_proj_min_tile = atoll(argv[3]);
-  const int mcap = 48;
+  const int64_t n = argc > 1 ? atoll(argv[1]) : (1 << 23);
+  const int mcap = 64;
   const int64_t ldv = (n + 31) / 32 * 32;
-  double2 *V, *W, *g, *part; double *small, *partn; unsigned* ctr;
-  cudaMalloc(&V, sizeof(double2) * ldv * mcap); cudaMalloc(&W, sizeof(double2) * ldv);
-  cudaMemset(V, 0, sizeof(double2) * ldv * mcap); cudaMemset(W, 0, sizeof(double2) * ldv);
-  cudaMalloc(&g, sizeof(double2) * 192); cudaMalloc(&small, sizeof(double) * 512); cudaMemset(small, 0, 4096);
+  double2 *V, *W, *W0, *g, *part; double *small, *partn; unsigned* ctr; int* flag; double2* gs;
+  cudaMalloc(&V, sizeof(double2) * ldv * mcap); cudaMalloc(&W, sizeof(double2) * ldv); cudaMalloc(&W0, sizeof(double2) * ldv);
+  k_fill<<<4096, 256>>>(V, ldv * mcap, 1); k_fill<<<4096, 256>>>(W0, ldv, 2);
+  cudaMalloc(&g, sizeof(double2) * 192); cudaMalloc(&small, sizeof(double) * 1024); cudaMemset(small, 0, 8192);
   cudaMalloc(&part, sizeof(double2) * 64 * 148 * 8); cudaMalloc(&partn, sizeof(double) * 148 * 8);
-  cudaMalloc(&ctr, 64); cudaMemset(ctr, 0, 64);
-  KDev d{}; d.n = n; d.ldv = ldv; d.V = V; d.W = W; d.s = small + 130; d.alpha = small; d.beta = small + 64;
-  d.flag = (int*)(small + 128); d.nrm2 = small + 196; d.g1 = g; d.g2 = g + 64; d.part = part; d.partn = partn; d.counter = ctr;
+  cudaMalloc(&ctr, 64); cudaMemset(ctr, 0, 64); cudaMalloc(&flag, 64); cudaMemset(flag, 0, 64);
+  cudaMalloc(&gs, 64); cudaMemset(gs, 0, 64);
+  KDev d{}; d.n = n; d.ldv = ldv; d.V = V; d.W = W; d.s = small + 512; d.alpha = small; d.beta = small + 64;
+  d.flag = flag; d.nrm2 = small + 256; d.g1 = g; d.g2 = g + 64; d.part = part; d.partn = partn; d.counter = ctr;
+  d.gsync = gs; d.tol_rate = 0.0; d.defer = 0;
+  {  // s_k = 1 for every column, nrm2 = 1 (gate value 1)
+    std::vector<double> one(300, 1.0);
+    cudaMemcpy(d.s, one.data(), 65 * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(d.nrm2, one.data(), 64 * 8, cudaMemcpyHostToDevice);
+    double2 gsv = make_double2(1.0, 0.0);
+    cudaMemcpy(gs, &gsv, 16, cudaMemcpyHostToDevice);
+  }
   configure_kernels();
-  cudaFuncSetAttribute(k_proj_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 205 * 1024);
-  // variants: 16 register-accumulated columns, 1 or 2 CTAs per SM (half the slot budget each)
-  cudaFuncSetAttribute(k_proj_tma<0, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 205 * 1024);
-  cudaFuncSetAttribute(k_proj_tma<1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 205 * 1024);
-  cudaFuncSetAttribute(k_proj_tma<0, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 205 * 1024);
-  cudaFuncSetAttribute(k_proj_tma<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 205 * 1024);
-  PFN_cuTensorMapEncodeTiled_v12000 enc; cudaDriverEntryPointQueryResult q;
-  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+  PFN_cuTensorMapEncodeTiled_v12000 enc; cudaDriverEntryPointQueryResult qr;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &qr);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  int list[] = {2, 4, 5, 6, 8, 9, 12, 16, 17, 20, 23, 24, 28, 32, 33, 41, 48};
-  int first = argc > 2 ? atoi(argv[2]) : 0;
-  for (int li = first; li < 17; ++li) { const int nc = list[li];
+  const int list[] = {2, 4, 6, 8, 12, 16, 20, 24, 28, 32, 40, 48, 64};
+  const int NL = sizeof(list) / sizeof(list[0]);
+  printf("n = %lld; GB/s (algorithmic bytes: dots 16n(ncols+1), update 16n(ncols+2))\n", (long long)n);
+  printf("ncols | tma dots upd | norm | r: TPR CPL dots upd (best) ...\n");
+  for (int li = 0; li < NL; ++li) {
+    const int nc = list[li], j = nc - 1;
     CUtensorMap tm;
-    cuuint64_t gd[2] = {(cuuint64_t)(2 * n), (cuuint64_t)mcap}; cuuint64_t gs[1] = {(cuuint64_t)(ldv * 16)};
+    cuuint64_t gd[2] = {(cuuint64_t)(2 * n), (cuuint64_t)mcap}; cuuint64_t gst[1] = {(cuuint64_t)(ldv * 16)};
     cuuint32_t box[2] = {(cuuint32_t)(64 * proj_rsub(nc)), (cuuint32_t)nc}; cuuint32_t es[2] = {1, 1};
-    enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, V, gd, gs, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, V, gd, gst, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    const int j = nc - 1, S = proj_slots(nc), R = proj_rsub(nc), C = proj_consumers(nc);
+    const int S = proj_slots(nc), R = proj_rsub(nc), C = proj_consumers(nc);
     const size_t sm = proj_smem_bytes(nc);
-    double ms[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-    const int tpr = tpr_for(nc, 1);
-    const int gs4 = (int)std::min<int64_t>(4 * sms, (n * tpr + 255) / 256);
-    for (int mode = 0; mode < 10; ++mode) {
-      for (int it = 0; it < 6; ++it) {
-        if (it == 1) cudaEventRecord(e0);
-        if (mode == 0) k_proj_tma<0><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
-        if (mode == 1) k_proj_tma<1><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
-        if (mode == 2) k_proj_tma<2><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
-        if (mode == 3) k_update_norm<<<8 * sms, kThreads>>>(d, j, 0, 0);
-        if (mode == 4) { TE_DISPATCH_TPR(tpr, { k_proj_s<0, TPR><<<gs4, kThreads>>>(d, j); }); }
-        if (mode == 5) { TE_DISPATCH_TPR(tpr, { k_proj_s<1, TPR><<<gs4, kThreads>>>(d, j); }); }
-        if (mode == 6) k_proj_tma<0, 8><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
-        if (mode == 7) k_proj_tma<1, 8><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
-        if (mode == 8) k_proj_tma<0, 16><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
-        if (mode == 9) k_proj_tma<1, 16><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
+    const double bd = 16.0 * n * (nc + 1), bu = 16.0 * n * (nc + 2);
+    auto timeit = [&](auto&& launch, int reps) {
+      launch();
+      cudaEventRecord(e0);
+      for (int it = 0; it < reps; ++it) {
+        cudaMemcpyAsync(W, W0, 16 * n, cudaMemcpyDeviceToDevice);  // not timed separately: subtracted below
+        launch();
       }
       cudaEventRecord(e1); cudaEventSynchronize(e1);
-      { cudaError_t er = cudaGetLastError(); if (er != cudaSuccess) { printf("ncols %d mode %d FAILED: %s\n", nc, mode, cudaGetErrorString(er)); return 1; } }
-      float t; cudaEventElapsedTime(&t, e0, e1); ms[mode] = t / 5;
+      float t; cudaEventElapsedTime(&t, e0, e1);
+      cudaError_t er = cudaGetLastError();
+      if (er != cudaSuccess) { printf("FAILED: %s\n", cudaGetErrorString(er)); exit(1); }
+      return (double)t / reps;
+    };
+    const double tcopy = timeit([&] {}, 5);
+    auto gbs = [&](double ms, double b) { return b / ((ms - tcopy) * 1e6); };
+    // reference dots (TMA) for the check
+    std::vector<double2> gref(nc), gr(nc);
+    cudaMemcpy(W, W0, 16 * n, cudaMemcpyDeviceToDevice);
+    if (nc <= 8) k_proj_tma<0, 8><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
+    else if (nc <= 16) k_proj_tma<0, 16><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
+    else k_proj_tma<0, 32><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
+    cudaMemcpy(gref.data(), d.g1, 16 * nc, cudaMemcpyDeviceToHost);
+    double ttd, ttu;
+    if (nc <= 8) {
+      ttd = timeit([&] { k_proj_tma<0, 8><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
+      ttu = timeit([&] { k_proj_tma<1, 8><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
+    } else if (nc <= 16) {
+      ttd = timeit([&] { k_proj_tma<0, 16><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
+      ttu = timeit([&] { k_proj_tma<1, 16><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
+    } else {
+      ttd = timeit([&] { k_proj_tma<0, 32><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
+      ttu = timeit([&] { k_proj_tma<1, 32><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
     }
-    const double b01 = 16.0 * n * nc + 16.0 * n, b1 = 16.0 * n * nc + 32.0 * n;
-    printf("ncols %2d S %2d R %d | tma dots %.0f upd %.0f stream %.0f | norm %.0f | shuffle dots %.0f upd %.0f | "
-           "r8 dots %.0f upd %.0f | r16 dots %.0f upd %.0f GB/s | %s\n",
-           nc, S, R, b01 / ms[0] / 1e6, b1 / ms[1] / 1e6, b01 / ms[2] / 1e6, b01 / ms[3] / 1e6, b01 / ms[4] / 1e6,
-           b1 / ms[5] / 1e6, b01 / ms[6] / 1e6, b1 / ms[7] / 1e6, b01 / ms[8] / 1e6, b1 / ms[9] / 1e6,
-           cudaGetErrorString(cudaGetLastError()));
+    const double tn = timeit([&] { k_update_norm<<<8 * sms, kThreads>>>(d, j, 0, 0); }, 5);
+    printf("%5d | %5.0f %5.0f | %5.0f |", nc, gbs(ttd, bd), gbs(ttu, bu), gbs(tn, bd));
+    auto variant = [&](auto tpr_c, auto cpl_c, auto u_c, auto minb_c) {
+      constexpr int TPR = decltype(tpr_c)::value, CPL = decltype(cpl_c)::value, U = decltype(u_c)::value, MINB = decltype(minb_c)::value;
+      if (nc > TPR * CPL || (TPR > 1 && nc <= TPR * CPL / 2)) return;
+      cudaMemcpy(W, W0, 16 * n, cudaMemcpyDeviceToDevice);
+      run_r<0, TPR, CPL, U, MINB>(d, j, sms);
+      cudaMemcpy(gr.data(), d.g1, 16 * nc, cudaMemcpyDeviceToHost);
+      double err = 0, nr = 0;
+      for (int k = 0; k < nc; ++k) {
+        err = fmax(err, hypot(gr[k].x - gref[k].x, gr[k].y - gref[k].y));
+        nr = fmax(nr, hypot(gref[k].x, gref[k].y));
+      }
+      const double td = timeit([&] { run_r<0, TPR, CPL, U, MINB>(d, j, sms); }, 5);
+      const double tu = timeit([&] { run_r<1, TPR, CPL, U, MINB>(d, j, sms); }, 5);
+      printf(" %d/%d/%d/%d %5.0f %5.0f%s |", TPR, CPL, U, MINB, gbs(td, bd), gbs(tu, bu), err <= 1e-11 * (nr + 1) ? "" : " BAD");
+    };
+    using I1 = std::integral_constant<int, 1>; using I2 = std::integral_constant<int, 2>;
+    using I3 = std::integral_constant<int, 3>; using I4 = std::integral_constant<int, 4>;
+    using I8 = std::integral_constant<int, 8>; using I16 = std::integral_constant<int, 16>;
+    // TPR/CPL/U/MINB
+    variant(I1{}, I4{}, I1{}, I4{}); variant(I1{}, I4{}, I2{}, I2{}); variant(I1{}, I8{}, I1{}, I2{});
+    variant(I2{}, I4{}, I1{}, I4{}); variant(I2{}, I4{}, I2{}, I2{}); variant(I2{}, I8{}, I1{}, I2{});
+    variant(I4{}, I4{}, I1{}, I4{}); variant(I4{}, I4{}, I2{}, I2{}); variant(I4{}, I8{}, I1{}, I2{});
+    printf("\n");
   }
   return 0;
 }

@@ -8,7 +8,7 @@ import os
 import re
 import sys
 
-CLASS = [(r"k_spmv", "spmv"), (r"k_proj_tma<0[,>]|k_proj_s<0", "proj_dots"), (r"k_proj_tma<[13][,>]|k_proj_s<1", "update_proj"),
+CLASS = [(r"k_spmv", "spmv"), (r"k_proj_tma<0[,>]|k_proj_r<0", "proj_dots"), (r"k_proj_tma<[13][,>]|k_proj_r<1", "update_proj"),
          (r"k_update_norm", "update_norm"), (r"k_combine", "combine")]
 
 
