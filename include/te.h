@@ -161,6 +161,14 @@ enum {
                                 or the same address space) — SURVEY f4, the exchange fused into
                                 the SpMV.  Used with TE_OPT_SPMV 7 or 8.                       */
   TE_OPT_SPMV = 5            /* SpMV kernel (same arithmetic, measured choice):
+                                9 slot-window SELL-32 with a value dictionary: 32-row slices
+                                (lane = row), each row's off-diagonal entries grouped by their
+                                32-column window, windows merged across the slice into slots
+                                (one int32 window base per slot), 16 bits per entry (8-bit value
+                                code | 8-bit column offset), dense diagonal.  Built at create when
+                                the off-diagonal values take <= 255 distinct values and the slot
+                                padding is <= 1.6x the off-diagonal entries (spin chains); then
+                                the default.  TE_ERR_ARG when selected and not applicable;
                                 8 staged-x ring: the ring below, and each tile's x windows (column
                                 ranges planned on the device at create: >= 2 distinct columns at
                                 >= 1/4 density) bulk-copied into shared memory too; entries are
@@ -181,10 +189,11 @@ enum {
                                 Other values: TE_ERR_ARG (round 1's slower variants were removed) */
 };
 int te_set_option(te_handle* h, int option, double value);
-/* Read-only plan statistics of the staged-x SpMV (te_get_option only; -1 when the handle has no
- * staged-x plan): entries gathered from global memory / nnz; tiles with at least one such entry /
- * tiles; bulk-copied x slots / nnz. */
-enum { TE_INFO_XS_GLOBAL = 101, TE_INFO_XS_GLOBAL_TILES = 102, TE_INFO_XS_X_PER_ENTRY = 103 };
+/* Read-only plan statistics (te_get_option only; -1 when the handle has no such plan).  Staged-x
+ * SpMV: entries gathered from global memory / nnz; tiles with at least one such entry / tiles;
+ * bulk-copied x slots / nnz.  Slot-window SELL-32: slot entries (padding included) / off-diagonal
+ * entries (reported when the value dictionary exists, also when the padding made it inapplicable). */
+enum { TE_INFO_XS_GLOBAL = 101, TE_INFO_XS_GLOBAL_TILES = 102, TE_INFO_XS_X_PER_ENTRY = 103, TE_INFO_SW_FILL = 104 };
 /* Current value of an option (TE_OPT_SPMV reports the kernel the handle runs, e.g. the default
  * chosen at create) or of a TE_INFO_* statistic; TE_ERR_ARG for a null handle/pointer or an
  * unknown option. */

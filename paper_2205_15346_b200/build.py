@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libtimeevolver.so")
-SOURCES = ["kernels.cu", "spmv.cu", "spmv_xs.cu", "te_api.cu", "dist.cpp", "host_math.cpp"]
+SOURCES = ["kernels.cu", "spmv.cu", "spmv_xs.cu", "spmv_sw.cu", "te_api.cu", "dist.cpp", "host_math.cpp"]
 HEADERS = ["kernels.cuh", "device_common.cuh", "host_math.h", "nccl_shim.h"]
 
 

@@ -55,6 +55,14 @@ struct KDev {
   const void* xs_diag;       // [n + 2] diagonal value of each row (VT)
   const void* xs_dict;       // [xs_ndict <= 255] off-diagonal values (VT)
   int xs_ndict;
+  // slot-window SELL-32 with a value dictionary (variant 9, spmv_sw.cu)
+  const int64_t* sw_sptr;    // [nslice+1] first slot of each 32-row slice (multiples of kSwGroup)
+  const int32_t* sw_base;    // [slots] first column of each slot's 32-column window
+  const uint16_t* sw_ent;    // [slots*32] (code << 8 | offset), groups of kSwGroup slots per lane
+  const void* sw_diag;       // [n] diagonal (VT)
+  const void* sw_dict;       // [sw_ndict <= 255] off-diagonal values (VT)
+  int64_t sw_nslice;
+  int sw_ndict;
   const double2* halo;  // received halo entries (distributed, NCCL exchange); nullptr otherwise
   // distributed handles: the entries of local rows whose columns live on other ranks, kept apart
   // from the local CSR (rowptr/col/val above hold local columns only) and added by k_spmv_halo
@@ -100,7 +108,7 @@ struct Launch {
   int xs_stages;        // its ring depth (2 or 3)
   int xs_nf;            // its entries in flight per lane (8 or 16)
   int proj_tma;         // 2: hybrid by column count (default), 1: TMA-tiled only, 3: register accumulators only
-  int spmv_tiled;       // 8: staged-x ring, 7: warp-specialised ring, 6: SELL-32-sigma
+  int spmv_tiled;       // 9: slot-window SELL-32, 8: staged-x ring, 7: warp-specialised ring, 6: SELL-32-sigma
   int prefetch;         // update_norm: L2 bulk-prefetch distance in block iterations (0: off)
 };
 
@@ -135,6 +143,12 @@ void launch_xs_plan(const int64_t* tiles, int64_t ntiles, const int32_t* col, in
                     int gap, int4* meta, int2* rng, uint16_t* lcol, cudaStream_t st);
 void configure_xs_kernels(void (*set_attr)(const void*, size_t, void*), void* ctx, size_t budget);
 void launch_spmv_xs(const KDev& d, bool cplx, int j, const Launch& L);
+// slot-window SELL-32 SpMV (spmv_sw.cu): build (count / fill passes) and launch
+constexpr int kSwGroup = 4;      // slots per 8-byte entry load of a lane
+void launch_sw_build(bool fill, bool cplx, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
+                     const double2* dict_keys, int nd, const int64_t* sptr, int32_t* nslot, int32_t* base,
+                     uint16_t* ent, void* diag, int* err, cudaStream_t st);
+void launch_spmv_sw(const KDev& d, bool cplx, int j, const Launch& L);
 void launch_proj_dots(const KDev& d, int j, const Launch& L);              // K1b: g1 = V^H p (TMA)
 void launch_update_proj(const KDev& d, int j, const Launch& L);            // K2
 void launch_gram_update(const KDev& d, int j, bool write, const Launch& L); // f2: p'' = p - V(c1+c2) -> V_{j+1}, V^H p'', ||p''||^2

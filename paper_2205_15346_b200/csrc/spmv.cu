@@ -5,6 +5,7 @@
 //                  bulk-copy ring of nnz-balanced tiles, per-warp stage release
 //   6 k_spmv_sell  SELL-32-sigma copy of H, software-pipelined coalesced loads
 //   8 k_spmv_xs    (spmv_xs.cu) the ring with each tile's x windows staged by bulk copies
+//   9 k_spmv_sw    (spmv_sw.cu) slot-window SELL-32 with a value dictionary (2 bytes per entry)
 // The variants measured slower in round 1 (CSR-vector, row tiles, TMA slots, block-pipelined,
 // async gather; DESIGN.md §6 keeps their numbers) were removed from the library.
 // All variants sum each row's products in a fixed order (deterministic); parity-tested against
@@ -328,6 +329,10 @@ void launch_spmv_halo(const KDev& d, bool cplx, int j, const Launch& L) {
 }
 
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L) {
+  if (L.spmv_tiled == 9 && d.sw_nslice > 0) {
+    launch_spmv_sw(d, cplx, j, L);
+    return;
+  }
   if (L.spmv_tiled == 8 && d.ntiles_xs > 0) {
     launch_spmv_xs(d, cplx, j, L);
     return;

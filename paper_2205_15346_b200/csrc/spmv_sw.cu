@@ -1,0 +1,254 @@
+// SpMV variant 9: slot-window SELL-32 with a value dictionary.  p = s_j H V_j (Eq. 8, first line,
+// P:153), the only operation on the large space.
+//
+// Why: the model Hamiltonians of the paper (spin chains, its §5 model) have few distinct
+// off-diagonal values and strongly aligned column patterns.  In a spin chain, rows r of an aligned
+// 32-row slice share their high spin bits, so a bond acting on high sites maps the whole slice to
+// another aligned 32-column window (r XOR mask), for every lane at once.  The CSR SpMV streams
+// 12 bytes per entry (8-byte value + int32 column) and gathers x entry by entry; here each entry
+// is 2 bytes:
+//   * slices of 32 rows (lane = row); a row's off-diagonal entries are grouped by the 32-column
+//     window c >> 5 of their column; the windows of a slice are merged across its 32 rows in
+//     ascending order and each window gets as many slots as its largest per-row count (a slot =
+//     one entry per lane, padded with code 255 where a row has fewer);
+//   * per slot: the window's first column (int32, one per slot, broadcast to the warp);
+//   * per (slot, lane): 16 bits = 8-bit value code (index into the sorted dictionary of the
+//     distinct off-diagonal values; 255 = padding) | 8-bit offset of the column in the window;
+//   * the diagonal as a dense per-row array (added first).
+// A slot's x loads are then 32 lanes reading one aligned 32-entry window (512 B, coalesced) for
+// every bond that moves the slice as a block.  Applicable when the off-diagonal values take at
+// most 255 distinct values and the padding stays small (te_api.cu decides at create); the
+// product order per row is: diagonal, then the slots in window order (fixed, deterministic).
+#include "device_common.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace te {
+
+namespace {
+constexpr int kSwPad = 0xFF00;  // code 255: padding slot entry
+
+template <bool CPLX>
+__device__ __forceinline__ int dict_code(const double2* __restrict__ dk, int nd, double re, double im) {
+  const unsigned long long kr = (unsigned long long)__double_as_longlong(re);
+  const unsigned long long ki = (unsigned long long)__double_as_longlong(im);
+  int lo = 0, hi = nd - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const unsigned long long mr = (unsigned long long)__double_as_longlong(dk[mid].x);
+    const unsigned long long mi = (unsigned long long)__double_as_longlong(dk[mid].y);
+    if (mr < kr || (mr == kr && mi < ki)) lo = mid + 1;
+    else hi = mid;
+  }
+  const bool hit = (unsigned long long)__double_as_longlong(dk[lo].x) == kr &&
+                   (unsigned long long)__double_as_longlong(dk[lo].y) == ki;
+  return hit ? lo : -1;
+}
+}  // namespace
+
+// Build, one warp per slice.  FILL = false: slot count of each slice (rounded up to kSwGroup);
+// FILL = true: window bases, 16-bit entries and the diagonal.  dk: the nd dictionary values sorted
+// by (re bits, im bits).  err bit 1: an off-diagonal value missing from the dictionary.
+template <bool CPLX, bool FILL>
+__global__ void __launch_bounds__(256) k_sw_build(int64_t n, const int64_t* __restrict__ rowptr,
+                                                  const int32_t* __restrict__ col, const void* __restrict__ val,
+                                                  const double2* __restrict__ dk, int nd, const int64_t* __restrict__ sptr,
+                                                  int32_t* nslot, int32_t* base, uint16_t* ent, void* diag, int* err) {
+  using VT = typename ValT<CPLX>::T;
+  const VT* v = static_cast<const VT*>(val);
+  const int lane = threadIdx.x & 31;
+  const int64_t nsl = (n + 31) / 32;
+  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nsl;
+       s += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t r = s * 32 + lane;
+    int64_t p = r < n ? rowptr[r] : 0, e = r < n ? rowptr[r + 1] : 0;
+    int64_t slot = FILL ? sptr[s] : 0;
+    const int64_t slot_end = FILL ? sptr[s + 1] : 0;
+    double2 dsum = make_double2(0.0, 0.0);
+    for (;;) {
+      unsigned key = 0xFFFFFFFFu;
+      while (p < e && (int64_t)col[p] == r) {  // the diagonal: dense array
+        if constexpr (CPLX) dsum = cadd(dsum, v[p]);
+        else dsum.x += v[p];
+        ++p;
+      }
+      if (p < e) key = (unsigned)col[p] >> 5;
+      const unsigned kmin = __reduce_min_sync(0xFFFFFFFFu, key);
+      if (kmin == 0xFFFFFFFFu) break;
+      int cnt = 0;
+      int64_t q = p;
+      while (q < e && ((unsigned)col[q] >> 5) == kmin) {
+        if ((int64_t)col[q] != r) ++cnt;
+        ++q;
+      }
+      const int w = (int)__reduce_max_sync(0xFFFFFFFFu, (unsigned)cnt);
+      if (FILL) {
+        int k = 0;
+        for (; p < q; ++p) {
+          const int32_t c = col[p];
+          if ((int64_t)c == r) {
+            if constexpr (CPLX) dsum = cadd(dsum, v[p]);
+            else dsum.x += v[p];
+            continue;
+          }
+          double re, im = 0.0;
+          if constexpr (CPLX) { re = v[p].x; im = v[p].y; } else { re = v[p]; }
+          const int code = dict_code<CPLX>(dk, nd, re, im);
+          if (code < 0 || code > 254) atomicOr(err, 1);
+          const int64_t K = slot + k;
+          ent[((K >> 2) * 32 + lane) * 4 + (K & 3)] = (uint16_t)((code & 0xFF) << 8 | (c & 31));
+          ++k;
+        }
+        for (; k < w; ++k) {
+          const int64_t K = slot + k;
+          ent[((K >> 2) * 32 + lane) * 4 + (K & 3)] = (uint16_t)kSwPad;
+        }
+        if (lane == 0)
+          for (int i = 0; i < w; ++i) base[slot + i] = (int32_t)(kmin << 5);
+      }
+      p = q;
+      slot += w;
+    }
+    if (FILL) {
+      for (int64_t K = slot; K < slot_end; ++K) {  // round-up padding of the last group
+        ent[((K >> 2) * 32 + lane) * 4 + (K & 3)] = (uint16_t)kSwPad;
+        if (lane == 0) base[K] = (int32_t)(s * 32);
+      }
+      if (r < n) {
+        if constexpr (CPLX) static_cast<double2*>(diag)[r] = dsum;
+        else static_cast<double*>(diag)[r] = dsum.x;
+      }
+    } else if (lane == 0) {
+      nslot[s] = (int32_t)((slot + kSwGroup - 1) / kSwGroup * kSwGroup);
+    }
+  }
+}
+
+void launch_sw_build(bool fill, bool cplx, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
+                     const double2* dk, int nd, const int64_t* sptr, int32_t* nslot, int32_t* base, uint16_t* ent,
+                     void* diag, int* err, cudaStream_t st) {
+  const int64_t nsl = (n + 31) / 32;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (nsl + 7) / 8));
+#define TE_SWB(C, F) k_sw_build<C, F><<<grid, 256, 0, st>>>(n, rowptr, col, val, dk, nd, sptr, nslot, base, ent, diag, err)
+  if (cplx) {
+    if (fill) TE_SWB(true, true); else TE_SWB(true, false);
+  } else {
+    if (fill) TE_SWB(false, true); else TE_SWB(false, false);
+  }
+#undef TE_SWB
+}
+
+// ------------------------------------------------------------------------------------------
+// the SpMV: one warp per slice (lane = row), persistent grid-stride over slices; U groups of
+// kSwGroup slots per iteration (4U entry codes and x loads in flight per lane)
+// ------------------------------------------------------------------------------------------
+template <bool CPLX>
+__device__ __forceinline__ typename ValT<CPLX>::T ld_dict(uint32_t addr) {
+  if constexpr (CPLX) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+  } else {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+  }
+}
+
+template <bool CPLX, int U>
+__global__ void __launch_bounds__(kThreads) k_spmv_sw(KDev d, int j) {
+  using VT = typename ValT<CPLX>::T;
+  __shared__ __align__(16) VT dict_s[256];
+  __shared__ double sj_s;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // codes >= ndict (255: padding) read 0: padding entries are multiplied out instead of branched
+  // around (their x index is a valid column of the slot's window)
+  for (int i = tid; i < 256; i += blockDim.x) {
+    VT z;
+    if constexpr (CPLX) z = make_double2(0.0, 0.0); else z = 0.0;
+    dict_s[i] = i < d.sw_ndict ? static_cast<const VT*>(d.sw_dict)[i] : z;
+  }
+  if (tid == 0) sj_s = spmv_gate(d, j, blockIdx.x == 0);
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  asm volatile("" : "+l"(x));  // column base pinned in a register (not recomputed per load)
+  uint32_t dict_base = smem_u32(dict_s);
+  asm volatile("" : "+r"(dict_base));
+  constexpr uint32_t kVB = (uint32_t)sizeof(VT);
+  const VT* __restrict__ diag = static_cast<const VT*>(d.sw_diag);
+  const uint2* __restrict__ ent = reinterpret_cast<const uint2*>(d.sw_ent);
+  const int4* __restrict__ base = reinterpret_cast<const int4*>(d.sw_base);
+  const int64_t n = d.n, nsl = d.sw_nslice;
+  const int64_t tw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5; s < nsl; s += tw) {
+    const int64_t r = s * 32 + lane;
+    const bool act = r < n;
+    const int64_t g0 = __ldg(d.sw_sptr + s) / kSwGroup, g1 = __ldg(d.sw_sptr + s + 1) / kSwGroup;
+    double2 acc = make_double2(0.0, 0.0);
+    if (act) acc = ValT<CPLX>::mul(ValT<CPLX>::ldcs(diag + r), __ldg(x + r));
+    // software pipeline: the entry codes and window bases of batch g + U are loaded while the x
+    // loads of batch g are in flight
+    uint2 e[U];
+    int4 b[U];
+    auto load_batch = [&](int64_t g, uint2 (&eo)[U], int4 (&bo)[U]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool live = g + u < g1;
+        eo[u] = live ? __ldcs(ent + (g + u) * 32 + lane) : make_uint2(0xFF00FF00u, 0xFF00FF00u);
+        bo[u] = live ? __ldg(base + g + u) : make_int4(0, 0, 0, 0);
+      }
+    };
+    load_batch(g0, e, b);
+    for (int64_t g = g0; g < g1; g += U) {
+      double2 xv[4 * U];
+      uint32_t cd[4 * U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t w = k < 2 ? e[u].x : e[u].y;
+          const uint32_t h = (k & 1) ? (w >> 16) : (w & 0xFFFFu);
+          const uint32_t bb = (uint32_t)(k == 0 ? b[u].x : (k == 1 ? b[u].y : (k == 2 ? b[u].z : b[u].w)));
+          cd[4 * u + k] = h >> 8;
+          xv[4 * u + k] = __ldg(x + (bb + (h & 0xFFu)));
+        }
+      }
+      if (g + U < g1) load_batch(g + U, e, b);
+#pragma unroll
+      for (int i = 0; i < 4 * U; ++i) acc = cadd(acc, ValT<CPLX>::mul(ld_dict<CPLX>(dict_base + cd[i] * kVB), xv[i]));
+    }
+    if (act) __stcs(d.W + r, make_double2(acc.x * sj, acc.y * sj));
+  }
+}
+
+// persistent grid: exactly the co-resident blocks (a grid-stride loop with more blocks than fit
+// runs the surplus blocks' whole share after the first wave: a long tail)
+template <bool CPLX, int U>
+static int sw_grid(const Launch& L, int64_t nsl) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmv_sw<CPLX, U>, kThreads, 0) != cudaSuccess || b < 1) b = 1;
+    per_sm = b;
+  }
+  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)L.num_sms * per_sm, (nsl + kWarps - 1) / kWarps));
+}
+
+void launch_spmv_sw(const KDev& d, bool cplx, int j, const Launch& L) {
+  static const int u_env = [] {
+    const char* e = getenv("TE_SPMV_SW_U");
+    return e ? atoi(e) : 2;
+  }();
+#define TE_SW_U(U)                                                                                   \
+  if (cplx) k_spmv_sw<true, U><<<sw_grid<true, U>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);   \
+  else k_spmv_sw<false, U><<<sw_grid<false, U>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
+  if (u_env == 1) { TE_SW_U(1) }
+  else if (u_env == 4) { TE_SW_U(4) }
+  else { TE_SW_U(2) }
+#undef TE_SW_U
+}
+
+}  // namespace te

@@ -146,6 +146,15 @@ struct te_handle {
   void* d_xs_diag = nullptr;
   void* d_xs_dict = nullptr;
   int xs_ndict = 0;
+  // slot-window SELL-32 with a value dictionary (variant 9), built at create when applicable
+  int64_t* d_sw_sptr = nullptr;
+  int32_t* d_sw_base = nullptr;
+  uint16_t* d_sw_ent = nullptr;
+  void* d_sw_diag = nullptr;
+  void* d_sw_dict = nullptr;
+  int64_t sw_nslice = 0, sw_slots = 0;
+  int sw_ndict = 0;
+  double sw_fill = 0.0;  // slot entries (32 per slot) / off-diagonal entries
   int64_t ncol_limit = 0;
   // SELL-32-sigma copy of H (SpMV variant 6), built on first selection
   int32_t* d_scol = nullptr;
@@ -252,6 +261,13 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.xs_diag = h->d_xs_diag;
   d.xs_dict = h->d_xs_dict;
   d.xs_ndict = h->xs_ndict;
+  d.sw_sptr = h->d_sw_sptr;
+  d.sw_base = h->d_sw_base;
+  d.sw_ent = h->d_sw_ent;
+  d.sw_diag = h->d_sw_diag;
+  d.sw_dict = h->d_sw_dict;
+  d.sw_nslice = h->sw_nslice;
+  d.sw_ndict = h->sw_ndict;
   d.scol = h->d_scol;
   d.sval = h->d_sval;
   d.sptr = h->d_sptr;
@@ -558,6 +574,11 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
   if (h->spmv_tiled == 8 && h->ntiles_xs > 0)
     bh = h->d_xs_code ? (double)h->nnz * 3.0 + n * vbytes + 8.0 * (n + 1.0) : (double)h->nnz * (vbytes + 2.0) + 8.0 * (n + 1.0);
   if (h->spmv_tiled == 8 && h->ntiles_xs > 0) bh += (double)h->nh_entries * (vbytes + 4.0);
+  // slot-window SELL-32: 2 bytes per slot entry (padding included), the slot bases, the slice
+  // pointers and the dense diagonal
+  if (h->spmv_tiled == 9 && h->sw_nslice > 0)
+    bh = (double)h->sw_slots * (64.0 + 4.0) + 8.0 * (double)(h->sw_nslice + 1) + n * vbytes +
+         (double)h->nh_entries * (vbytes + 4.0);
   te::launch_restart_init(d, L); LCHECK("restart_init");
   ++h->launches;
   for (int j = 0; j < m; ++j) {
@@ -939,30 +960,29 @@ void free_xs(te_handle* h) {
 // row), then the device plan (spmv_xs.cu): per tile the x ranges to stage and each entry's slot.
 // rowptr: host copy of the (local) row pointers.
 // Value dictionary on the device: distinct off-diagonal values (bit patterns) into a 1024-slot hash
-// table; if there are at most 255, sorted by bit pattern they become codes 0..254 (255: diagonal).
-int build_dict(te_handle* h) {
-  // opt-in (TE_SPMV_XS_DICT=1): a third of the H bytes, but the staged-x consumers are bound by
-  // their dependent shared-memory lookups, not by HBM (ncu), and the code -> value lookup adds
-  // one more: measured slower on configs 2 / 3 / 5 (+15 / +6 / +9 % per SpMV), faster only with
-  // 78 entries per row (config 6, -14 % vs staged-x without it, still slower than the ring)
-  const char* e = getenv("TE_SPMV_XS_DICT");
-  if (!e || atoi(e) == 0) return TE_OK;
+// table; if there are at most 255, sorted by bit pattern they become codes 0..254 (255: diagonal
+// in the staged-x codes, padding in the slot-window SELL).  Returns the number of values, or -1
+// when there are more than 255 (keys: the sorted values, imaginary part 0 for real H).
+int collect_dict(te_handle* h, std::vector<double2>& keys_out) {
   cudaStream_t s = h->stream ? h->stream : h->own_stream;
   constexpr int cap = 1024;
   const size_t tb = te::dict_slot_bytes() * cap;
   void* table = nullptr;
-  unsigned* count = nullptr;
-  CK(cudaMalloc(&table, tb + 16));
-  count = reinterpret_cast<unsigned*>(static_cast<char*>(table) + tb);
-  CK(cudaMemsetAsync(table, 0, tb + 16, s));
+  if (cudaMalloc(&table, tb + 16) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  unsigned* count = reinterpret_cast<unsigned*>(static_cast<char*>(table) + tb);
+  cudaMemsetAsync(table, 0, tb + 16, s);
   te::launch_dict_insert(h->n, h->d_rowptr, h->d_col, h->d_val, h->cplx, table, cap, count, s);
   std::vector<unsigned char> ht(tb + 16);
-  CK(cudaMemcpyAsync(ht.data(), table, tb + 16, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  cudaMemcpyAsync(ht.data(), table, tb + 16, cudaMemcpyDeviceToHost, s);
+  const cudaError_t e = cudaStreamSynchronize(s);
   cudaFree(table);
+  if (e != cudaSuccess) return -1;
   unsigned cnt = 0;
   std::memcpy(&cnt, ht.data() + tb, sizeof cnt);
-  if (cnt > 255) return TE_OK;
+  if (cnt > 255) return -1;
   struct Slot { unsigned state, pad; double re, im; };
   std::vector<std::pair<std::pair<uint64_t, uint64_t>, double2>> keys;
   for (int i = 0; i < cap; ++i) {
@@ -975,13 +995,25 @@ int build_dict(te_handle* h) {
     keys.push_back({{a, b}, make_double2(sl.re, sl.im)});
   }
   std::sort(keys.begin(), keys.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
-  const int nd = (int)keys.size();
-  std::vector<double2> kd((size_t)std::max(1, nd));
+  keys_out.clear();
+  for (const auto& k : keys) keys_out.push_back(k.second);
+  return (int)keys_out.size();
+}
+
+int build_dict(te_handle* h) {
+  // opt-in (TE_SPMV_XS_DICT=1): a third of the H bytes, but the staged-x consumers are bound by
+  // their dependent shared-memory lookups, not by HBM (ncu), and the code -> value lookup adds
+  // one more: measured slower on configs 2 / 3 / 5 (+15 / +6 / +9 % per SpMV), faster only with
+  // 78 entries per row (config 6, -14 % vs staged-x without it, still slower than the ring)
+  const char* e = getenv("TE_SPMV_XS_DICT");
+  if (!e || atoi(e) == 0) return TE_OK;
+  cudaStream_t s = h->stream ? h->stream : h->own_stream;
+  std::vector<double2> kd;
+  const int nd = collect_dict(h, kd);
+  if (nd < 0) return TE_OK;
   std::vector<double> vr((size_t)std::max(1, nd));
-  for (int i = 0; i < nd; ++i) {
-    kd[(size_t)i] = keys[(size_t)i].second;
-    vr[(size_t)i] = keys[(size_t)i].second.x;
-  }
+  for (int i = 0; i < nd; ++i) vr[(size_t)i] = kd[(size_t)i].x;
+  if (kd.empty()) kd.push_back(make_double2(0.0, 0.0));
   const size_t vb = h->cplx ? 16 : 8;
   double2* dkeys = nullptr;
   CK(cudaMalloc(&dkeys, sizeof(double2) * kd.size()));
@@ -1003,6 +1035,102 @@ int build_dict(te_handle* h) {
   CK(cudaStreamSynchronize(s));
   cudaFree(dkeys);
   h->xs_ndict = nd;
+  return TE_OK;
+}
+
+// ---------------------------------------------------------------- slot-window SELL-32 (variant 9)
+void free_sw(te_handle* h) {
+  cudaFree(h->d_sw_sptr);
+  cudaFree(h->d_sw_base);
+  cudaFree(h->d_sw_ent);
+  cudaFree(h->d_sw_diag);
+  cudaFree(h->d_sw_dict);
+  h->d_sw_sptr = nullptr;
+  h->d_sw_base = nullptr;
+  h->d_sw_ent = nullptr;
+  h->d_sw_diag = nullptr;
+  h->d_sw_dict = nullptr;
+  h->sw_nslice = h->sw_slots = 0;
+  h->sw_ndict = 0;
+}
+
+// Build the slot-window SELL-32 copy of the local CSR: applicable when the off-diagonal values take
+// at most 255 distinct values and the slot entries (32 per slot, padding included) stay within
+// kSwMaxFill times the off-diagonal entry count.  Not applicable: TE_OK with sw_nslice = 0
+// (sw_fill reports the padding ratio when the dictionary exists).
+constexpr double kSwMaxFill = 1.6;
+int plan_sw(te_handle* h) {
+  free_sw(h);
+  h->sw_fill = 0.0;
+  if (h->ncol_limit != h->n) return TE_OK;  // local columns only (halo entries are kept apart)
+  cudaStream_t s = h->stream ? h->stream : h->own_stream;
+  std::vector<double2> kd;
+  const int nd = collect_dict(h, kd);
+  if (nd < 0) return TE_OK;
+  if (kd.empty()) kd.push_back(make_double2(0.0, 0.0));
+  const int64_t n = h->n, nsl = (n + 31) / 32;
+  double2* dkeys = nullptr;
+  int32_t* nslot = nullptr;
+  int* derr = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(dkeys);
+    cudaFree(nslot);
+    cudaFree(derr);
+  };
+  if (cudaMalloc(&dkeys, sizeof(double2) * kd.size()) != cudaSuccess || cudaMalloc(&nslot, sizeof(int32_t) * nsl) != cudaSuccess ||
+      cudaMalloc(&derr, sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    cleanup();
+    return TE_OK;
+  }
+  CK(cudaMemcpyAsync(dkeys, kd.data(), sizeof(double2) * kd.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(derr, 0, sizeof(int), s));
+  te::launch_sw_build(false, h->cplx, n, h->d_rowptr, h->d_col, h->d_val, dkeys, nd, nullptr, nslot, nullptr, nullptr,
+                      nullptr, derr, s);
+  CK(cudaGetLastError());
+  std::vector<int32_t> cnt((size_t)nsl);
+  CK(cudaMemcpyAsync(cnt.data(), nslot, sizeof(int32_t) * nsl, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<int64_t> sptr((size_t)nsl + 1, 0);
+  for (int64_t i = 0; i < nsl; ++i) sptr[(size_t)i + 1] = sptr[(size_t)i] + cnt[(size_t)i];
+  const int64_t slots = sptr[(size_t)nsl];
+  // off-diagonal entries: nnz - n (every row of the model Hamiltonians stores its diagonal)
+  const double offd = std::max<double>(1.0, (double)h->nnz - (double)n);
+  h->sw_fill = (double)slots * 32.0 / offd;
+  if (h->sw_fill > kSwMaxFill && !getenv("TE_SPMV_SW_FORCE")) {
+    cleanup();
+    return TE_OK;
+  }
+  const size_t vb = h->cplx ? 16 : 8;
+  if (cudaMalloc(&h->d_sw_sptr, sizeof(int64_t) * (nsl + 1)) != cudaSuccess ||
+      cudaMalloc(&h->d_sw_base, sizeof(int32_t) * (slots + 4)) != cudaSuccess ||
+      cudaMalloc(&h->d_sw_ent, sizeof(uint16_t) * 32 * (slots + 4)) != cudaSuccess ||
+      cudaMalloc(&h->d_sw_diag, vb * (n + 2)) != cudaSuccess || cudaMalloc(&h->d_sw_dict, vb * 256) != cudaSuccess) {
+    cudaGetLastError();
+    cleanup();
+    free_sw(h);
+    return TE_OK;  // no room: the CSR kernels stay
+  }
+  std::vector<double> vr(kd.size());
+  for (size_t i = 0; i < kd.size(); ++i) vr[i] = kd[i].x;
+  if (h->cplx) CK(cudaMemcpyAsync(h->d_sw_dict, kd.data(), sizeof(double2) * nd, cudaMemcpyHostToDevice, s));
+  else CK(cudaMemcpyAsync(h->d_sw_dict, vr.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(h->d_sw_sptr, sptr.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(h->d_sw_diag, 0, vb * (n + 2), s));
+  te::launch_sw_build(true, h->cplx, n, h->d_rowptr, h->d_col, h->d_val, dkeys, nd, h->d_sw_sptr, nullptr, h->d_sw_base,
+                      h->d_sw_ent, h->d_sw_diag, derr, s);
+  CK(cudaGetLastError());
+  int herr = 0;
+  CK(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cleanup();
+  if (herr) {
+    free_sw(h);
+    return set_err(TE_ERR_CUDA, "slot-window SELL build: value missing from the dictionary");
+  }
+  h->sw_nslice = nsl;
+  h->sw_slots = slots;
+  h->sw_ndict = nd;
   return TE_OK;
 }
 
@@ -1210,22 +1338,31 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
   std::memcpy(&nrm, &nb, sizeof nrm);
   h->norm1 = nrm;
   h->ncol_limit = ncol_limit;
-  {  // staged-x SpMV: the default when its plan stages >= 95 % of the entries (structured H) and
-     // rows are short (mean <= 40 entries); otherwise its buffers are released (re-planned if
-     // selected later).  Measured per SpMV launch, staged-x vs ring: config 2 equal, config 3
-     // -5 %, config 5 -9 %; config 6 (78 entries per row) +27 %, config 4 (half the columns
-     // uniform: 50 % global gathers) +190 %.  TE_SPMV_DEFAULT overrides.
+  {  // SpMV format chosen at create (measured per SpMV launch):
+     // * slot-window SELL-32 (9) when the off-diagonal values fit the 8-bit dictionary and the
+     //   slot padding stays below kSwMaxFill (spin chains: 2 bytes per entry, coalesced x windows);
+     // * else the staged-x ring (8) when its plan stages >= 95 % of the entries and rows are short
+     //   (mean <= 40 entries): staged-x vs ring, config 3 -5 %, config 6 (78 entries per row) +27 %,
+     //   config 4 (half the columns uniform: 50 % global gathers) +190 %;
+     // * else the warp-specialised ring (7).  TE_SPMV_DEFAULT overrides.
     const double avg = n > 0 ? (double)h->nnz / (double)n : 0.0;
     int def = 7;
-    if (avg <= 40.0) {
-      if (plan_xs(h, rowptr) != TE_OK) return fail(TE_ERR_OOM, "staged-x plan");
-      if (h->ntiles_xs > 0 && h->xs_global_frac <= 0.05) def = 8;
-    }
+    int want = 0;
     if (const char* e = getenv("TE_SPMV_DEFAULT")) {
       const int v = atoi(e);
-      if (v == 6 || v == 7 || v == 8) def = v;
+      if (v == 6 || v == 7 || v == 8 || v == 9) want = v;
     }
+    if (want == 0 || want == 9) {
+      if (plan_sw(h) != TE_OK) return fail(TE_ERR_CUDA, "slot-window SELL build");
+      if (h->sw_nslice > 0) def = 9;
+    }
+    if (def != 9 && (want == 0 || want == 8) && avg <= 40.0) {
+      if (plan_xs(h, rowptr) != TE_OK) return fail(TE_ERR_OOM, "staged-x plan");
+      if (h->ntiles_xs > 0 && (h->xs_global_frac <= 0.05 || want == 8)) def = 8;
+    }
+    if (want == 6 || want == 7) def = want;
     if (def != 8) free_xs(h);
+    if (def != 9) free_sw(h);
     h->spmv_tiled = def == 6 ? 7 : def;
     if (def == 6 && build_sell(h) == TE_OK) h->spmv_tiled = 6;
   }
@@ -1289,10 +1426,8 @@ void te_destroy(te_handle* h) {
   cudaFree(h->d_peer_ldv);
   for (void* p : h->ipc_open) cudaIpcCloseMemHandle(p);
   cudaFree(h->d_tile_ring);
-  cudaFree(h->d_tile_xs);
-  cudaFree(h->d_xs_meta);
-  cudaFree(h->d_xs_rng);
-  cudaFree(h->d_lcol);
+  free_xs(h);
+  free_sw(h);
   cudaFree(h->d_scol);
   cudaFree(h->d_sval);
   cudaFree(h->d_sptr);
@@ -1515,11 +1650,18 @@ int te_set_option(te_handle* h, int option, double value) {
       h->integrator = (int)value;
       return TE_OK;
     case TE_OPT_SPMV:
-      if (value != 6.0 && value != 7.0 && value != 8.0)
-        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 8 (staged-x ring), 7 (ring) or 6 (SELL-32-sigma)");
+      if (value != 6.0 && value != 7.0 && value != 8.0 && value != 9.0)
+        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 9 (slot-window SELL-32), 8 (staged-x ring), 7 (ring) or 6 (SELL-32-sigma)");
       if (value == 6.0) {
         const int rc = build_sell(h);
         if (rc != TE_OK) return rc;
+      }
+      if (value == 9.0 && h->sw_nslice == 0) {
+        const int rc = plan_sw(h);
+        if (rc != TE_OK) return rc;
+        if (h->sw_nslice == 0)
+          return set_err(TE_ERR_ARG, "TE_OPT_SPMV 9: not applicable to this matrix (more than 255 distinct off-diagonal values, "
+                                     "halo columns, or slot padding %.2f > %.2f)", h->sw_fill, kSwMaxFill);
       }
       if (value == 8.0 && h->ntiles_xs == 0) {
         std::vector<int64_t> rp((size_t)h->n + 1);
@@ -1554,6 +1696,7 @@ int te_get_option(const te_handle* h, int option, double* value) {
     case TE_INFO_XS_GLOBAL: *value = h->ntiles_xs > 0 ? h->xs_global_frac : -1.0; return TE_OK;
     case TE_INFO_XS_GLOBAL_TILES: *value = h->ntiles_xs > 0 ? h->xs_global_tiles : -1.0; return TE_OK;
     case TE_INFO_XS_X_PER_ENTRY: *value = h->ntiles_xs > 0 ? h->xs_x_per_entry : -1.0; return TE_OK;
+    case TE_INFO_SW_FILL: *value = h->sw_fill > 0.0 ? h->sw_fill : -1.0; return TE_OK;
     default: return set_err(TE_ERR_ARG, "unknown option %d", option);
   }
 }

@@ -157,15 +157,88 @@ def test_spmv_xs_variants(gpu_lib, name, c, tpr, halo, ecap, dict_, monkeypatch)
     h.close()
 
 
+def _principal_submatrix(c, m):
+    """Rows/columns [0, m) of a CSR matrix (Hermitian stays Hermitian): ragged slices, rows that
+    lose entries."""
+    rp, col, val = c["rowptr"], c["col"], c["val"]
+    keep = np.zeros(len(col), dtype=bool)
+    keep[: rp[m]] = col[: rp[m]] < m
+    rows = np.repeat(np.arange(m), np.diff(rp[: m + 1]))
+    nrp = np.zeros(m + 1, dtype=np.int64)
+    np.add.at(nrp, rows[keep[: rp[m]]] + 1, 1)
+    v0 = c["v0"][:m] / np.linalg.norm(c["v0"][:m]) if np.linalg.norm(c["v0"][:m]) > 0 else np.ones(m, complex) / np.sqrt(m)
+    return dict(c, n=m, rowptr=np.cumsum(nrp), col=col[keep].astype(np.int32), val=val[keep], v0=v0.astype(np.complex128))
+
+
+def _no_diag_case():
+    """XXZ L=10 without its diagonal (rows with no diagonal entry, some rows empty)."""
+    c = dict(configs.build(2, L=10))
+    rows = np.repeat(np.arange(c["n"]), np.diff(c["rowptr"]))
+    keep = c["col"] != rows
+    nrp = np.zeros(c["n"] + 1, dtype=np.int64)
+    np.add.at(nrp, rows[keep] + 1, 1)
+    v0 = np.random.default_rng(3).standard_normal(c["n"]) + 0j
+    return dict(c, rowptr=np.cumsum(nrp), col=c["col"][keep], val=c["val"][keep], v0=v0 / np.linalg.norm(v0))
+
+
+SW_CASES = [("xxz_L12", configs.build(2, L=12)), ("xxznnn_L12", configs.build(5, L=12)), ("xxz_L14", configs.build(2, L=14)),
+            ("xxznnn_L10_cplx", _complex_dict_case()), ("xxz_L12_ragged1000", _principal_submatrix(configs.build(2, L=12), 1000)),
+            ("xxz_L10_nodiag", _no_diag_case()), ("bh_L7_N7", configs.build(3, L=7, N=7)),
+            ("xxz_L5", configs.build(2, L=5))]
+
+
+@pytest.mark.parametrize("name,c", SW_CASES, ids=[x[0] for x in SW_CASES])
+def test_spmv_sw_variants(gpu_lib, name, c, monkeypatch):
+    """Slot-window SELL-32 SpMV (TE_OPT_SPMV = 9) vs the oracle's Arnoldi basis: spin chains (real
+    and complex dictionary values), a ragged last slice, rows without a diagonal and empty rows, a
+    single slice (n = 32), and a boson matrix whose windows align poorly (the padding check is
+    overridden for all of these small matrices)."""
+    te = gpu_lib
+    monkeypatch.setenv("TE_SPMV_SW_FORCE", "1")  # small chains: more slices straddle the window edges
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    te.te_set_option(h, te.TE_OPT_SPMV, 9)
+    assert te.te_get_option(h, te.TE_OPT_SPMV) == 9
+    assert te.te_get_option(h, te.TE_INFO_SW_FILL) > 0
+    m = min(12, c["n"] - 1)
+    g = te.te_krylov_basis(h, c["v0"], m, c["tol"] / c["t"], want_V=True)
+    o = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), c["v0"], m, c["tol"] / c["t"])
+    scale = max(1.0, np.abs(o["alpha"]).max(), np.abs(o["beta"]).max())
+    assert g["m_eff"] == o["m_eff"]
+    assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-12 * scale
+    assert np.abs(g["beta"] - o["beta"]).max() <= 1e-12 * scale
+    assert np.linalg.norm(g["V"] - o["V"]) <= 1e-10
+    h.close()
+
+
+def test_spmv_sw_not_applicable(gpu_lib):
+    """More than 255 distinct off-diagonal values: TE_OPT_SPMV 9 is refused (TE_ERR_ARG) and the
+    handle keeps its SpMV."""
+    te = gpu_lib
+    c = configs.build(1, n=2048)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    before = te.te_get_option(h, te.TE_OPT_SPMV)
+    with pytest.raises(te.TEError):
+        te.te_set_option(h, te.TE_OPT_SPMV, 9)
+    assert te.te_get_option(h, te.TE_OPT_SPMV) == before
+    h.close()
+
+
 def test_spmv_default_choice(gpu_lib):
-    """The staged-x SpMV is chosen at create when its plan stages >= 95 % of the entries (spin chain,
-    bosons), the plain ring otherwise (uniform random columns); TE_OPT_SPMV switches either way."""
+    """At create: the slot-window SELL-32 for spin chains (dictionary + aligned windows), the
+    staged-x ring when its plan stages >= 95 % of the entries (bosons), the plain ring otherwise
+    (uniform random columns); TE_OPT_SPMV switches either way with the same result."""
     te = gpu_lib
     # (a random matrix must be large enough that a tile's uniform columns are isolated in x)
-    for c, want in ((configs.build(5, L=12), 8), (configs.build(3, L=7, N=7), 8), (configs.build(1, n=1 << 18), 7)):
+    # spin chains: the slot-window SELL when its padding is <= 1.6x (L = 18: 1.2x; XXZ L = 12: 1.8x,
+    # more of the small chain's slices straddle window edges -> staged-x)
+    for c, want in ((configs.build(5, L=18), 9), (configs.build(2, L=12), 8), (configs.build(3, L=7, N=7), 8),
+                    (configs.build(1, n=1 << 18), 7)):
         h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
-        assert te.te_get_option(h, te.TE_OPT_SPMV) == want
-        other = 7 if want == 8 else 8
+        fill = te.te_get_option(h, te.TE_INFO_SW_FILL)
+        assert te.te_get_option(h, te.TE_OPT_SPMV) == want, fill
+        if c["cfg"] in (2, 5):
+            assert (want == 9) == (0 < fill <= 1.6)
+        other = 7 if want in (8, 9) else 8
         v1, _ = te.te_evolve(h, c["v0"], 0.5, 1e-9, 16)
         te.te_set_option(h, te.TE_OPT_SPMV, other)
         assert te.te_get_option(h, te.TE_OPT_SPMV) == other

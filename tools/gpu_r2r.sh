@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "sw_ or default_choice" > gpurun_out/r_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/r_pytest.log
+timeout 900 python tools/spmv_sweep.py --config 5 --m 5 --reps 2 --variant "9:" --variant "9:TE_SPMV_SW_U=1" --variant "9:TE_SPMV_SW_U=4" > gpurun_out/r_sweep_c5.log 2>&1
+timeout 600 python tools/spmv_sweep.py --config 2 --m 5 --reps 4 --variant "9:" --variant "9:TE_SPMV_SW_U=1" > gpurun_out/r_sweep_c2.log 2>&1
+timeout 1200 python bench.py --no-cpu-baseline --steps 3 --warmup 2 > gpurun_out/r_bench_c5.log 2>&1
