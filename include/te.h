@@ -161,6 +161,14 @@ enum {
                                 or the same address space) — SURVEY f4, the exchange fused into
                                 the SpMV.  Used with TE_OPT_SPMV 7 or 8.                       */
   TE_OPT_SPMV = 5            /* SpMV kernel (same arithmetic, measured choice):
+                                10 column-blocked ring: a copy of the CSR split into equal column
+                                blocks of <= 48 MB of x (env TE_SPMV_COLBLK_MB), the ring (7) run
+                                once per block (lanes per row from the block's mean row length),
+                                passes after the first accumulating into W; each pass gathers
+                                from one L2-resident block.  Built at create and the
+                                default when the ring is chosen and x exceeds 160 MB (single
+                                rank; TE_SPMV_COLBLK=0 disables); TE_ERR_ARG when selected and
+                                x fits one block;
                                 9 slot-window SELL-32 with a value dictionary: 32-row slices
                                 (lane = row), each row's off-diagonal entries grouped by their
                                 32-column window, windows merged across the slice into slots

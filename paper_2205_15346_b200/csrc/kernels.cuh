@@ -63,6 +63,7 @@ struct KDev {
   const void* sw_dict;       // [sw_ndict <= 255] off-diagonal values (VT)
   int64_t sw_nslice;
   int sw_ndict;
+  int accw;             // SpMV writes W += s_j (H V_j) instead of W = (column-blocked passes > 0)
   const double2* halo;  // received halo entries (distributed, NCCL exchange); nullptr otherwise
   // distributed handles: the entries of local rows whose columns live on other ranks, kept apart
   // from the local CSR (rowptr/col/val above hold local columns only) and added by k_spmv_halo
@@ -108,7 +109,7 @@ struct Launch {
   int xs_stages;        // its ring depth (2 or 3)
   int xs_nf;            // its entries in flight per lane (8 or 16)
   int proj_tma;         // 2: hybrid by column count (default), 1: TMA-tiled only, 3: register accumulators only
-  int spmv_tiled;       // 9: slot-window SELL-32, 8: staged-x ring, 7: warp-specialised ring, 6: SELL-32-sigma
+  int spmv_tiled;       // 10: column-blocked ring, 9: slot-window SELL-32, 8: staged-x ring, 7: ring, 6: SELL-32-sigma
   int prefetch;         // update_norm: L2 bulk-prefetch distance in block iterations (0: off)
 };
 
@@ -126,6 +127,12 @@ void set_attr(const void* f, size_t want, void* ctx);
 void configure_spmv_kernels(void (*set_attr)(const void*, size_t, void*), void* ctx);
 const void* spmv_attr_kernel();  // the SpMV kernel reported by kernel_attributes(0)
 void launch_spmv(const KDev& d, bool cplx, int j, const Launch& L);        // K1a: SpMV only
+// column-blocked CSR (variant 10): entries of each B-column block stored as their own CSR (the
+// entries of a row keep their order inside each block); count / fill passes on the device
+void launch_colblk_count(int64_t n, const int64_t* rowptr, const int32_t* col, int64_t B, int nb, int32_t* cnt,
+                         cudaStream_t st);
+void launch_colblk_fill(int64_t n, const int64_t* rowptr, const int32_t* col, const void* val, bool cplx, int64_t B,
+                        int b, const int64_t* rowptr_b, int32_t* col_b, void* val_b, cudaStream_t st);
 void launch_spmv_halo(const KDev& d, bool cplx, int j, const Launch& L);   // K1a': + halo entries (distributed)
 // staged-x ring SpMV (spmv_xs.cu): plan (create time) and launch
 constexpr int kXsConsumers = 15;

@@ -6,6 +6,8 @@
 //   6 k_spmv_sell  SELL-32-sigma copy of H, software-pipelined coalesced loads
 //   8 k_spmv_xs    (spmv_xs.cu) the ring with each tile's x windows staged by bulk copies
 //   9 k_spmv_sw    (spmv_sw.cu) slot-window SELL-32 with a value dictionary (2 bytes per entry)
+//  10 the ring over a column-blocked copy of H: one pass per column block of x (x block
+//     L2-resident while the pass gathers from it), passes > 0 accumulate into W
 // The variants measured slower in round 1 (CSR-vector, row tiles, TMA slots, block-pipelined,
 // async gather; DESIGN.md §6 keeps their numbers) were removed from the library.
 // All variants sum each row's products in a fixed order (deterministic); parity-tested against
@@ -44,6 +46,13 @@ struct RingLayout {
 };
 template <bool CPLX, int STG>
 size_t spmv_ring_smem() { return RingLayout<CPLX, STG>::kBytes; }
+
+// row result: W = s_j acc, or W += s_j acc in the passes > 0 of the column-blocked SpMV
+__device__ __forceinline__ void ring_out(const KDev& d, int64_t r, double2 acc, double sj) {
+  double2 v = make_double2(acc.x * sj, acc.y * sj);
+  if (d.accw) v = cadd(__ldcs(d.W + r), v);
+  __stcs(d.W + r, v);
+}
 
 template <bool CPLX, int TPR, int HM, int NF, int STG>
 __global__ void __launch_bounds__(kRingThreads, 1) k_spmv_ring(KDev d, int j) {
@@ -148,13 +157,13 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_spmv_ring(KDev d, int j) {
           if (q0 + w * TPR < hi) acc = cadd(acc, ValT<CPLX>::mul(vv[q0 + w * TPR], xx[w]));
       }
       if (TPR > 1) acc = group_sum<TPR>(acc);
-      if (act && q == 0) __stcs(d.W + ra + i, make_double2(acc.x * sj, acc.y * sj));
+      if (act && q == 0) ring_out(d, ra + i, acc, sj);
     } else if (warp == (int)(t % kRingConsumers)) {  // one long row: one warp, from global memory
       const VT* __restrict__ val = static_cast<const VT*>(d.val);
       double2 acc = make_double2(0.0, 0.0);
       for (int64_t k = b + lane; k < e; k += 32) acc = cadd(acc, ValT<CPLX>::mul(__ldg(val + k), gx(__ldg(d.col + k))));
       acc = warp_sum(acc);
-      if (lane == 0) __stcs(d.W + ra, make_double2(acc.x * sj, acc.y * sj));
+      if (lane == 0) ring_out(d, ra, acc, sj);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
@@ -391,6 +400,58 @@ void configure_spmv_kernels(void (*set_attr)(const void*, size_t, void*), void* 
 }
 
 // the default SpMV as launched for a real matrix with one lane per row (config 2)
+// ------------------------------------------------------------------------------------------
+// column-blocked CSR build (variant 10): block b holds the entries with columns in
+// [b B, (b+1) B); within a row they are a contiguous run of the sorted CSR row
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ int64_t row_lower_bound(const int32_t* __restrict__ col, int64_t lo, int64_t hi, int64_t c) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)col[mid] < c) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+__global__ void k_colblk_count(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, int64_t B,
+                               int nb, int32_t* cnt) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = rowptr[r], e = rowptr[r + 1];
+    int64_t lo = a;
+    for (int b = 0; b < nb; ++b) {
+      const int64_t hi = b + 1 < nb ? row_lower_bound(col, lo, e, (int64_t)(b + 1) * B) : e;
+      cnt[(int64_t)b * n + r] = (int32_t)(hi - lo);
+      lo = hi;
+    }
+  }
+}
+template <bool CPLX>
+__global__ void k_colblk_fill(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                              const void* __restrict__ val, int64_t B, int b, const int64_t* __restrict__ rowptr_b,
+                              int32_t* col_b, void* val_b) {
+  using VT = typename ValT<CPLX>::T;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = rowptr[r], e = rowptr[r + 1];
+    const int64_t lo = b > 0 ? row_lower_bound(col, a, e, (int64_t)b * B) : a;
+    const int64_t hi = row_lower_bound(col, lo, e, (int64_t)(b + 1) * B);
+    int64_t o = rowptr_b[r];
+    for (int64_t k = lo; k < hi; ++k, ++o) {
+      col_b[o] = col[k];
+      static_cast<VT*>(val_b)[o] = static_cast<const VT*>(val)[k];
+    }
+  }
+}
+void launch_colblk_count(int64_t n, const int64_t* rowptr, const int32_t* col, int64_t B, int nb, int32_t* cnt,
+                         cudaStream_t st) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (n + 255) / 256));
+  k_colblk_count<<<grid, 256, 0, st>>>(n, rowptr, col, B, nb, cnt);
+}
+void launch_colblk_fill(int64_t n, const int64_t* rowptr, const int32_t* col, const void* val, bool cplx, int64_t B,
+                        int b, const int64_t* rowptr_b, int32_t* col_b, void* val_b, cudaStream_t st) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (n + 255) / 256));
+  if (cplx) k_colblk_fill<true><<<grid, 256, 0, st>>>(n, rowptr, col, val, B, b, rowptr_b, col_b, val_b);
+  else k_colblk_fill<false><<<grid, 256, 0, st>>>(n, rowptr, col, val, B, b, rowptr_b, col_b, val_b);
+}
+
 const void* spmv_attr_kernel() { return (const void*)k_spmv_ring<false, 1, 0, 16, 4>; }
 
 }  // namespace te

@@ -155,6 +155,18 @@ struct te_handle {
   int64_t sw_nslice = 0, sw_slots = 0;
   int sw_ndict = 0;
   double sw_fill = 0.0;  // slot entries (32 per slot) / off-diagonal entries
+  // column-blocked copy of H for the ring (variant 10): one CSR + ring tile table per cb_cols
+  // columns of x, built at create for large x (single rank)
+  struct ColBlk {
+    int64_t* rowptr = nullptr;
+    int32_t* col = nullptr;
+    void* val = nullptr;
+    int64_t* tiles = nullptr;
+    int64_t ntiles = 0;
+    int tpr = 1;
+  };
+  std::vector<ColBlk> cb;
+  int64_t cb_cols = 0;
   int64_t ncol_limit = 0;
   // SELL-32-sigma copy of H (SpMV variant 6), built on first selection
   int32_t* d_scol = nullptr;
@@ -562,6 +574,129 @@ int setup_peers(te_handle* h) {
                                           (int)lj, cudaGetErrorString(e_));                 \
   } while (0)
 
+void free_colblk(te_handle* h);
+// column-blocked ring: x larger than kColBlkMinX is split into nb equal column blocks of at most
+// colblk_bytes() of x each (TE_SPMV_COLBLK_MB, default 48 MB: measured on config 4 (n = 2^24,
+// 268 MB of x) 96 / 64 / 48 / 32 / 24 MB blocks: 4.56 / 4.41 / 3.66 / 4.01 / 4.73 ms per SpMV vs
+// 5.81 ms for the ring over the whole CSR), rounded to 32 columns
+constexpr double kColBlkMinX = 160.0 * 1024 * 1024;
+double colblk_bytes() {
+  const char* e = getenv("TE_SPMV_COLBLK_MB");
+  const double v = e ? atof(e) : 48.0;
+  return std::max(1e-3, v) * 1024.0 * 1024.0;
+}
+int64_t colblk_cols(int64_t n) {
+  const int64_t nb = std::max<int64_t>(1, (int64_t)std::ceil(16.0 * (double)n / colblk_bytes()));
+  return std::max<int64_t>(32, ((n + nb - 1) / nb + 31) / 32 * 32);
+}
+
+// nnz-balanced tiles of the warp-specialised ring: <= 480/tpr rows and <= the stage capacity in
+// entries, {first row, end row, first entry, end entry}
+std::vector<int64_t> ring_tiles(int64_t n, const int64_t* rowptr, bool cplx, int stages, int tpr) {
+  const int64_t rcap = 480 / tpr;
+  const int64_t ncap = stages == 3 ? (cplx ? te::kRingNnzC3 : te::kRingNnz3) : (cplx ? te::kRingNnzC4 : te::kRingNnz4);
+  std::vector<int64_t> tg;
+  int64_t st = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    const bool over_rows = (r + 1 - st) > rcap;
+    const bool over_nnz = (rowptr[r + 1] - rowptr[st]) > ncap && r > st;
+    if (over_rows || over_nnz) {
+      tg.insert(tg.end(), {st, r, rowptr[st], rowptr[r]});
+      st = r;
+    }
+  }
+  if (n > 0) tg.insert(tg.end(), {st, n, rowptr[st], rowptr[n]});
+  return tg;
+}
+
+// Column-blocked copy of the (single-rank) CSR: block b = columns [b B, (b+1) B); each block is a
+// CSR over all rows with its own ring tile table and lanes per row (from its mean row length).
+// Counts on the device, prefix sums on the host, fill on the device.  Leaves h->cb empty when
+// there is no room.
+int build_colblk(te_handle* h, int64_t B) {
+  free_colblk(h);
+  const int64_t n = h->n;
+  const int nb = (int)((n + B - 1) / B);
+  if (nb < 2 || h->ncol_limit != n) return TE_OK;
+  cudaStream_t s = h->stream ? h->stream : h->own_stream;
+  int32_t* dcnt = nullptr;
+  if (cudaMalloc(&dcnt, sizeof(int32_t) * (size_t)n * nb) != cudaSuccess) {
+    cudaGetLastError();
+    return TE_OK;
+  }
+  te::launch_colblk_count(n, h->d_rowptr, h->d_col, B, nb, dcnt, s);
+  std::vector<int32_t> cnt((size_t)n * nb);
+  CK(cudaMemcpyAsync(cnt.data(), dcnt, sizeof(int32_t) * (size_t)n * nb, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFree(dcnt);
+  const size_t vb = h->cplx ? 16 : 8;
+  std::vector<int64_t> rp((size_t)n + 1);
+  h->cb.resize((size_t)nb);
+  for (int b = 0; b < nb; ++b) {
+    rp[0] = 0;
+    for (int64_t r = 0; r < n; ++r) rp[(size_t)r + 1] = rp[(size_t)r] + cnt[(size_t)b * n + r];
+    const int64_t nz = rp[(size_t)n];
+    auto& Bk = h->cb[(size_t)b];
+    // lanes per row of this block's pass: the handle's rule (<= 20 real / 8 complex entries per lane)
+    const double avg = (double)nz / (double)n;
+    int tpr = 1;
+    while (tpr < 8 && avg > (h->cplx ? 8.0 : 20.0) * tpr) tpr <<= 1;
+    Bk.tpr = tpr;
+    const std::vector<int64_t> tg = ring_tiles(n, rp.data(), h->cplx, h->ring_stages, tpr);
+    Bk.ntiles = (int64_t)tg.size() / 4;
+    // (+8 padding entries: the ring's 16-byte-aligned bulk copies may read past the last entry)
+    if (cudaMalloc(&Bk.rowptr, sizeof(int64_t) * (n + 2)) != cudaSuccess || cudaMalloc(&Bk.col, 4 * (size_t)(nz + 8)) != cudaSuccess ||
+        cudaMalloc(&Bk.val, vb * (size_t)(nz + 8)) != cudaSuccess || cudaMalloc(&Bk.tiles, sizeof(int64_t) * std::max<size_t>(4, tg.size())) != cudaSuccess) {
+      cudaGetLastError();
+      free_colblk(h);
+      return TE_OK;
+    }
+    CK(cudaMemcpyAsync(Bk.rowptr, rp.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(Bk.col, 0, 4 * (size_t)(nz + 8), s));
+    CK(cudaMemsetAsync(Bk.val, 0, vb * (size_t)(nz + 8), s));
+    if (!tg.empty()) CK(cudaMemcpyAsync(Bk.tiles, tg.data(), sizeof(int64_t) * tg.size(), cudaMemcpyHostToDevice, s));
+    te::launch_colblk_fill(n, h->d_rowptr, h->d_col, h->d_val, h->cplx, B, b, Bk.rowptr, Bk.col, Bk.val, s);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));  // rp / tg are reused for the next block
+  }
+  h->cb_cols = B;
+  return TE_OK;
+}
+
+void free_colblk(te_handle* h) {
+  for (auto& b : h->cb) {
+    cudaFree(b.rowptr);
+    cudaFree(b.col);
+    cudaFree(b.val);
+    cudaFree(b.tiles);
+  }
+  h->cb.clear();
+  h->cb_cols = 0;
+}
+
+// K1a: the SpMV of step j.  Column-blocked (variant 10): one ring pass per column block, passes > 0
+// accumulate into W (stream-ordered launches; row sums block by block, deterministic)
+void spmv_call(te_handle* h, const KDev& d, int j, const Launch& L) {
+  if (h->spmv_tiled != 10 || h->cb.empty()) {
+    te::launch_spmv(d, h->cplx, j, L);
+    return;
+  }
+  Launch Lr = L;
+  Lr.spmv_tiled = 7;
+  for (size_t b = 0; b < h->cb.size(); ++b) {
+    KDev db = d;
+    db.rowptr = h->cb[b].rowptr;
+    db.col = h->cb[b].col;
+    db.val = h->cb[b].val;
+    db.tile_ring = h->cb[b].tiles;
+    db.ntiles_ring = h->cb[b].ntiles;
+    db.accw = b > 0 ? 1 : 0;
+    Lr.spmv_ring_tpr = h->cb[b].tpr;
+    te::launch_spmv(db, h->cplx, j, Lr);
+  }
+  h->launches += (int64_t)h->cb.size() - 1;
+}
+
 int issue_arnoldi(te_handle* h, int m, double tol_rate) {
   int lj = -1;
   KDev d = make_kdev(h, tol_rate, m);
@@ -574,6 +709,8 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
   if (h->spmv_tiled == 8 && h->ntiles_xs > 0)
     bh = h->d_xs_code ? (double)h->nnz * 3.0 + n * vbytes + 8.0 * (n + 1.0) : (double)h->nnz * (vbytes + 2.0) + 8.0 * (n + 1.0);
   if (h->spmv_tiled == 8 && h->ntiles_xs > 0) bh += (double)h->nh_entries * (vbytes + 4.0);
+  // column-blocked ring: algorithmic bytes are those of the CSR it was cut from (the per-pass row
+  // pointers and the W re-reads of passes > 0 are overhead of the method, not counted)
   // slot-window SELL-32: 2 bytes per slot entry (padding included), the slot bases, the slice
   // pointers and the dense diagonal
   if (h->spmv_tiled == 9 && h->sw_nslice > 0)
@@ -588,7 +725,7 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
     const double ncols = j + 1;
     if (h->ortho == 1) {  // paper-literal Lanczos (Eq. 8 as printed)
       prof_begin(h);
-      te::launch_spmv(d, h->cplx, j, L); LCHECK("spmv");
+      spmv_call(h, d, j, L); LCHECK("spmv");
       if ((rc = halo_join(h))) return rc;
       te::launch_spmv_halo(d, h->cplx, j, L); LCHECK("spmv_halo");
       prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
@@ -609,7 +746,7 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
     // previous update pass's Gram dots g2): 2 allreduces per step for CGS2, 1 for f2 (plus one
     // barrier per step in peer-load halo mode, where a rank's SpMV reads its peers' V_j)
     prof_begin(h);
-    te::launch_spmv(d, h->cplx, j, L); LCHECK("spmv");
+    spmv_call(h, d, j, L); LCHECK("spmv");
     if ((rc = halo_join(h))) return rc;
     te::launch_spmv_halo(d, h->cplx, j, L); LCHECK("spmv_halo");
     prof_end(h, 0, bh + 16.0 * n + 16.0 * n);
@@ -1292,20 +1429,7 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     const double avg = n > 0 ? (double)h->nnz / (double)n : 0.0;
     h->ring_stages = (!cplx && avg <= 16.0) ? 4 : 3;
     if (const char* e = getenv("TE_SPMV_RING_STAGES")) h->ring_stages = atoi(e) == 3 ? 3 : 4;
-    const int64_t rcap = 480 / tr;
-    const int64_t ncap = h->ring_stages == 3 ? (cplx ? te::kRingNnzC3 : te::kRingNnz3)
-                                             : (cplx ? te::kRingNnzC4 : te::kRingNnz4);
-    std::vector<int64_t> tg;
-    int64_t st = 0;
-    for (int64_t r = 0; r < n; ++r) {
-      const bool over_rows = (r + 1 - st) > rcap;
-      const bool over_nnz = (rowptr[r + 1] - rowptr[st]) > ncap && r > st;
-      if (over_rows || over_nnz) {
-        tg.insert(tg.end(), {st, r, rowptr[st], rowptr[r]});
-        st = r;
-      }
-    }
-    if (n > 0) tg.insert(tg.end(), {st, n, rowptr[st], rowptr[n]});
+    const std::vector<int64_t> tg = ring_tiles(n, rowptr, cplx, h->ring_stages, h->spmv_ring_tpr);
     h->ntiles_ring = (int64_t)tg.size() / 4;
     if (!tg.empty()) {
       if (cudaMalloc(&h->d_tile_ring, sizeof(int64_t) * tg.size()) != cudaSuccess) return fail(TE_ERR_OOM, "tiles");
@@ -1365,6 +1489,13 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     if (def != 9) free_sw(h);
     h->spmv_tiled = def == 6 ? 7 : def;
     if (def == 6 && build_sell(h) == TE_OK) h->spmv_tiled = 6;
+    // * the ring over column blocks (10) when x outgrows L2 (16 n > kColBlkMinX) on a single rank:
+    //   each pass gathers from one L2-resident 2^22-column block of x instead of DRAM
+    const char* cbe = getenv("TE_SPMV_COLBLK");
+    if (h->spmv_tiled == 7 && want == 0 && 16.0 * (double)n > kColBlkMinX && !(cbe && atoi(cbe) == 0)) {
+      if (build_colblk(h, colblk_cols(n)) != TE_OK) return fail(TE_ERR_CUDA, "column-blocked copy");
+      if (!h->cb.empty()) h->spmv_tiled = 10;
+    }
   }
   h->launches += 1;
   return h;
@@ -1428,6 +1559,7 @@ void te_destroy(te_handle* h) {
   cudaFree(h->d_tile_ring);
   free_xs(h);
   free_sw(h);
+  free_colblk(h);
   cudaFree(h->d_scol);
   cudaFree(h->d_sval);
   cudaFree(h->d_sptr);
@@ -1650,8 +1782,15 @@ int te_set_option(te_handle* h, int option, double value) {
       h->integrator = (int)value;
       return TE_OK;
     case TE_OPT_SPMV:
-      if (value != 6.0 && value != 7.0 && value != 8.0 && value != 9.0)
-        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 9 (slot-window SELL-32), 8 (staged-x ring), 7 (ring) or 6 (SELL-32-sigma)");
+      if (value != 6.0 && value != 7.0 && value != 8.0 && value != 9.0 && value != 10.0)
+        return set_err(TE_ERR_ARG, "TE_OPT_SPMV must be 10 (column-blocked ring), 9 (slot-window SELL-32), 8 (staged-x ring), "
+                                   "7 (ring) or 6 (SELL-32-sigma)");
+      if (value == 10.0 && h->cb.empty()) {
+        const int rc = build_colblk(h, colblk_cols(h->n));
+        if (rc != TE_OK) return rc;
+        if (h->cb.empty())
+          return set_err(TE_ERR_ARG, "TE_OPT_SPMV 10: not applicable (x fits one column block, halo columns, or no memory)");
+      }
       if (value == 6.0) {
         const int rc = build_sell(h);
         if (rc != TE_OK) return rc;

@@ -210,6 +210,39 @@ def test_spmv_sw_variants(gpu_lib, name, c, monkeypatch):
     h.close()
 
 
+CB_CASES = [("cfg1_n4096", configs.build(1)), ("banded_n8192", configs.build(4, n=8192)),
+            ("bh_L6_N6_ragged", configs.build(3, L=6, N=6)), ("cfg1_n1000_ragged", configs.build(1, n=1000)),
+            ("xxz_L10_nodiag", _no_diag_case())]
+
+
+@pytest.mark.parametrize("kb", [1, 2])
+@pytest.mark.parametrize("name,c", CB_CASES, ids=[x[0] for x in CB_CASES])
+def test_spmv_colblk_variants(gpu_lib, name, c, kb, monkeypatch):
+    """Column-blocked ring SpMV (TE_OPT_SPMV = 10): one ring pass per column block of x (kb KB of x
+    per block: 4-128 blocks), passes > 0 accumulating into W, lanes per row chosen per block; rows
+    with no entry in a block, empty rows, a ragged last block; vs the oracle's Arnoldi basis and a
+    forced-schedule evolution."""
+    te = gpu_lib
+    monkeypatch.setenv("TE_SPMV_COLBLK_MB", str(kb / 1024.0))
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    te.te_set_option(h, te.TE_OPT_SPMV, 10)
+    assert te.te_get_option(h, te.TE_OPT_SPMV) == 10
+    g = te.te_krylov_basis(h, c["v0"], 12, c["tol"] / c["t"], want_V=True)
+    o = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), c["v0"], 12, c["tol"] / c["t"])
+    scale = max(1.0, np.abs(o["alpha"]).max(), np.abs(o["beta"]).max())
+    assert g["m_eff"] == o["m_eff"]
+    assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-12 * scale
+    assert np.abs(g["beta"] - o["beta"]).max() <= 1e-12 * scale
+    assert np.linalg.norm(g["V"] - o["V"]) <= 1e-10
+    # a forced-schedule evolution through the same kernel matches the oracle
+    t = min(c["t"], 1.0)
+    v, st = te.te_evolve(h, c["v0"], t, c["tol"], 12)
+    sched = te.te_get_schedule(h)
+    ref = K.evolve(c["rowptr"], c["col"], c["val"], c["v0"], t, c["tol"], 12, schedule=[x[0] for x in sched])
+    assert np.linalg.norm(v - ref["v"]) <= 1e-10
+    h.close()
+
+
 def test_spmv_sw_not_applicable(gpu_lib):
     """More than 255 distinct off-diagonal values: TE_OPT_SPMV 9 is refused (TE_ERR_ARG) and the
     handle keeps its SpMV."""
