@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5, help="evolutions in the e2e (host buffers) pass")
     ap.add_argument("--kernels", type=int, default=2, help="projection kernels: 2 hybrid (register accumulators up to 8 columns, TMA ring above; default), 3 TMA only, 5 register accumulators only")
     ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (library default if unset)")
-    ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel (library default if unset): 8 staged-x ring, 7 warp-specialised ring, 6 SELL-32-sigma")
+    ap.add_argument("--spmv", type=int, default=None, help="SpMV kernel (library default if unset): 10 column-blocked ring, 9 slot-window SELL-32, 8 staged-x ring, 7 warp-specialised ring, 6 SELL-32-sigma")
     ap.add_argument("--force-dist", action="store_true",
                     help="single rank through the distributed API (te_dist_init/te_create_csr_dist), for testing")
     ap.add_argument("--halo", type=int, default=0, help="N>1: 0 NCCL halo exchange (default), 1 SpMV reads peer memory (f4)")
@@ -252,7 +252,8 @@ def config_dict(c, args, ws, nloc):
             "nnz": int(c["nnz"]), "m": c["m"], "t": c["t"], "tol": c["tol"],
             "l2": "inputs larger than L2 (V = %.0f MB > 126 MB)" % (16 * nloc * c["m"] / 1e6),
             "parallelism": f"rows{ws}", "kernels": {2: "hybrid", 3: "tma", 5: "regacc"}[args.kernels],
-            "spmv": {None: "library default", 6: "sell", 7: "ring", 8: "staged-x ring"}[args.spmv],
+            "spmv": {None: "library default", 6: "sell", 7: "ring", 8: "staged-x ring", 9: "slot-window sell",
+                     10: "column-blocked ring"}[args.spmv],
             "ortho": ["cgs2", "lanczos3", "cgs2gram"][args.ortho],
             "halo": (["nccl_exchange", "peer_loads"][args.halo] if ws > 1 else None)}
 
@@ -453,7 +454,9 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic",
-        "config": config_dict(c, args, ws, nloc),
+        "config": {**config_dict(c, args, ws, nloc),
+                   "spmv_ran": {6: "sell", 7: "ring", 8: "staged-x ring", 9: "slot-window sell", 10: "column-blocked ring"}
+                   .get(int(te.te_get_option(h, te.TE_OPT_SPMV)), "?")},
         "krylov_steps_per_step": ksteps / args.steps,
         "restarts_per_step": stats[-1]["n_restarts"],
         "achieved_hbm_gbs": all_bytes / (all_ms * 1e-3) / 1e9 if all_ms > 0 else None,

@@ -156,8 +156,8 @@ __device__ __forceinline__ typename ValT<CPLX>::T ld_dict(uint32_t addr) {
   }
 }
 
-template <bool CPLX, int U>
-__global__ void __launch_bounds__(kThreads) k_spmv_sw(KDev d, int j) {
+template <bool CPLX, int U, int XM = 0, int MINB = 1>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmv_sw(KDev d, int j) {
   using VT = typename ValT<CPLX>::T;
   __shared__ __align__(16) VT dict_s[256];
   __shared__ double sj_s;
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv_sw(KDev d, int j) {
           const uint32_t h = (k & 1) ? (w >> 16) : (w & 0xFFFFu);
           const uint32_t bb = (uint32_t)(k == 0 ? b[u].x : (k == 1 ? b[u].y : (k == 2 ? b[u].z : b[u].w)));
           cd[4 * u + k] = h >> 8;
-          xv[4 * u + k] = __ldg(x + (bb + (h & 0xFFu)));
+          xv[4 * u + k] = XM ? ld_stream(x + (bb + (h & 0xFFu))) : __ldg(x + (bb + (h & 0xFFu)));
         }
       }
       if (g + U < g1) load_batch(g + U, e, b);
@@ -226,15 +226,16 @@ __global__ void __launch_bounds__(kThreads) k_spmv_sw(KDev d, int j) {
 
 // persistent grid: exactly the co-resident blocks (a grid-stride loop with more blocks than fit
 // runs the surplus blocks' whole share after the first wave: a long tail)
-template <bool CPLX, int U>
+template <bool CPLX, int U, int XM = 0, int MINB = 1>
 static int sw_grid(const Launch& L, int64_t nsl) {
   static int per_sm = 0;
   if (per_sm == 0) {
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmv_sw<CPLX, U>, kThreads, 0) != cudaSuccess || b < 1) b = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmv_sw<CPLX, U, XM, MINB>, kThreads, 0) != cudaSuccess || b < 1) b = 1;
     per_sm = b;
   }
-  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)L.num_sms * per_sm, (nsl + kWarps - 1) / kWarps));
+  // (grid_spmv < num_sms leaves SMs free for a concurrent NCCL halo exchange)
+  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)L.grid_spmv * per_sm, (nsl + kWarps - 1) / kWarps));
 }
 
 void launch_spmv_sw(const KDev& d, bool cplx, int j, const Launch& L) {
@@ -242,13 +243,19 @@ void launch_spmv_sw(const KDev& d, bool cplx, int j, const Launch& L) {
     const char* e = getenv("TE_SPMV_SW_U");
     return e ? atoi(e) : 2;
   }();
-#define TE_SW_U(U)                                                                                   \
-  if (cplx) k_spmv_sw<true, U><<<sw_grid<true, U>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);   \
-  else k_spmv_sw<false, U><<<sw_grid<false, U>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
+#define TE_SW_V(U, XM, MB)                                                                                                      \
+  if (cplx) k_spmv_sw<true, U, XM, MB><<<sw_grid<true, U, XM, MB>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);            \
+  else k_spmv_sw<false, U, XM, MB><<<sw_grid<false, U, XM, MB>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
+#define TE_SW_U(U) TE_SW_V(U, 0, 3)
   if (u_env == 1) { TE_SW_U(1) }
   else if (u_env == 4) { TE_SW_U(4) }
+  else if (u_env == 21) { TE_SW_V(2, 1, 1) }
+  else if (u_env == 16) { TE_SW_V(1, 0, 6) }
+  else if (u_env == 24) { TE_SW_V(2, 0, 4) }
+  else if (u_env == 161) { TE_SW_V(1, 1, 6) }
   else { TE_SW_U(2) }
 #undef TE_SW_U
+#undef TE_SW_V
 }
 
 }  // namespace te
