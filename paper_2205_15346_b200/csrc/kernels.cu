@@ -47,9 +47,21 @@ static size_t proj_slot_bytes(int ncols) {
 // Tile i -> slot i % S; slot s is owned by consumer warp s % C for its whole life, so each slot
 // is consumed by one warp in round order and no warp can poll a slot's full barrier one phase
 // early (mbarrier parity aliasing).
+// Slot s is owned by warp s % C, so unless C divides S some warps own one slot more and process
+// more tiles: 9 slots over 7 warps give two warps 2/9 of the tiles (64 % balance).  The slot count
+// is rounded down to a multiple of C when that keeps >= 3/4 of the slots (8, 9 -> 7; 11, 12 kept:
+// there the deeper ring wins).  Measured (tools/micro/mb_proj.cu, update pass, n = 2^23): 20
+// columns 5.4 -> 6.2 TB/s, 24: 5.0 -> 6.5, 40: 4.8 -> 5.7, 48: 4.8 -> 6.2; 8, 16, 32 columns (11-12
+// slots) lost 0.4-0.6 TB/s when rounded to 7, so they keep their slots.  g_proj_balance = 0: off.
+int g_proj_balance = 1;
 int proj_slots(int ncols) {
   int s = (int)(kProjSmemBudget / proj_slot_bytes(ncols));
-  return s > kMaxSlots ? kMaxSlots : (s < 1 ? 1 : s);
+  s = s > kMaxSlots ? kMaxSlots : (s < 1 ? 1 : s);
+  if (g_proj_balance && s > kConsumers) {
+    const int sb = s / kConsumers * kConsumers;
+    if (4 * sb >= 3 * s) s = sb;
+  }
+  return s;
 }
 int proj_consumers(int ncols) {
   const int s = proj_slots(ncols);

@@ -7,6 +7,7 @@
 #include "../../paper_2205_15346_b200/csrc/kernels.cu"
 #include "../../paper_2205_15346_b200/csrc/spmv.cu"
 #include "../../paper_2205_15346_b200/csrc/spmv_xs.cu"
+#include "../../paper_2205_15346_b200/csrc/spmv_sw.cu"
 #include <cudaTypedefs.h>
 #include <cmath>
 #include <cstdio>
@@ -30,6 +31,7 @@ void run_r(const KDev& d, int j, int sms) {
 
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : (1 << 23);
+  if (argc > 2) g_proj_balance = atoi(argv[2]);
   const int mcap = 64;
   const int64_t ldv = (n + 31) / 32 * 32;
   double2 *V, *W, *W0, *g, *part; double *small, *partn; unsigned* ctr; int* flag; double2* gs;

@@ -43,9 +43,17 @@ def main():
         a["ns"] += m.get("gpu__time_duration.sum", 0)
         a["kernels"].add(re.sub(r"\(.*", "", name).strip())
     out = {}
+    # one SpMV call may be several launches (the column-blocked ring: one pass per column block);
+    # per-call figures use the number of Krylov steps (one proj_dots launch each)
+    steps = agg["proj_dots"]["launches"] if "proj_dots" in agg else None
     for c, a in agg.items():
-        out[c] = {"launches_captured": a["launches"], "dram_bytes_per_launch": a["dram"] / a["launches"],
-                  "ncu_time_us_per_launch": a["ns"] / a["launches"] / 1e3, "kernels": sorted(a["kernels"])}
+        calls = a["launches"]
+        if c == "spmv" and steps and a["launches"] > steps and a["launches"] % steps == 0:
+            calls = steps
+        out[c] = {"launches_captured": calls, "dram_bytes_per_launch": a["dram"] / calls,
+                  "ncu_time_us_per_launch": a["ns"] / calls / 1e3, "kernels": sorted(a["kernels"])}
+        if calls != a["launches"]:
+            out[c]["kernel_launches_per_call"] = a["launches"] // calls
     tpath = os.path.join("profiles", "ncu_traffic.json")
     tab = json.load(open(tpath)) if os.path.exists(tpath) else {}
     tab[wl] = out
@@ -68,7 +76,7 @@ def main():
             f.write(f"| {k} | {v[0]} | {v[1] / 1e3:.1f} | {v[1] / S:.3f} |\n")
     with open(prefix + "_traffic.md", "w") as f:
         f.write(f"# DRAM traffic per launch by kernel class ({wl}), one full restart (ncu --metrics)\n\n")
-        f.write("| class | launches | DRAM MB/launch | ncu us/launch | DRAM GB/s (ncu) | kernels |\n|---|---|---|---|---|---|\n")
+        f.write("| class | calls | DRAM MB/call | ncu us/call | DRAM GB/s (ncu) | kernels |\n|---|---|---|---|---|---|\n")
         for c, o in out.items():
             f.write(f"| {c} | {o['launches_captured']} | {o['dram_bytes_per_launch'] / 1e6:.1f} | "
                     f"{o['ncu_time_us_per_launch']:.1f} | {o['dram_bytes_per_launch'] / o['ncu_time_us_per_launch'] / 1e3:.0f} | "

@@ -1,18 +1,22 @@
-"""Small evolutions through every shipped SpMV variant (staged-x with and without the value
-dictionary, ring, SELL), projection kernel set and orthogonalisation mode, for compute-sanitizer
-(memcheck / racecheck / synccheck; tools/sanitize.sh).  Sizes span several tiles per CTA: the
-staged-x and ring SpMVs run with small tiles (TE_SPMV_XS_ECAP=256) so their mbarrier rings wrap."""
+"""Small evolutions through every shipped SpMV format (slot-window SELL-32, column-blocked ring,
+staged-x with and without the value dictionary, ring, SELL-sigma), projection kernel set and
+orthogonalisation mode, for compute-sanitizer (memcheck / racecheck / synccheck;
+tools/sanitize.sh).  Sizes span several tiles per CTA: the staged-x SpMV runs with small tiles
+(TE_SPMV_XS_ECAP=256) so its mbarrier ring wraps; the column-blocked ring with 1 KB column blocks;
+the slot-window format with the padding check overridden (small chains)."""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("TE_SPMV_XS_ECAP", "256")
-import numpy as np  # noqa: E402
+os.environ.setdefault("TE_SPMV_COLBLK_MB", str(1.0 / 1024))
+os.environ.setdefault("TE_SPMV_SW_FORCE", "1")
 from paper_2205_15346_b200 import te  # noqa: E402
 from workloads import configs  # noqa: E402
 
 cases = [configs.build(2, L=12), configs.build(3, L=6, N=6), configs.build(1, n=1000), configs.build(5, L=11)]
-runs = [(2, 8, 0, "1"), (2, 8, 0, "0"), (2, 7, 0, "1"), (2, 6, 0, "1"), (3, 7, 0, "1"), (4, 7, 0, "1"),
-        (2, 8, 2, "1"), (2, 8, 1, "1")]
+# (kernel set, SpMV, ortho, staged-x dictionary)
+runs = [(2, 9, 0, "0"), (2, 10, 0, "0"), (2, 8, 0, "1"), (2, 8, 0, "0"), (2, 7, 0, "1"), (2, 6, 0, "1"),
+        (3, 7, 0, "1"), (5, 7, 0, "1"), (2, 8, 2, "1"), (2, 8, 1, "1")]
 for c in cases:
     for kset, spmv, ortho, dct in runs:
         os.environ["TE_SPMV_XS_DICT"] = dct
@@ -20,7 +24,7 @@ for c in cases:
         te.te_set_option(h, te.TE_OPT_KERNELS, kset)
         try:
             te.te_set_option(h, te.TE_OPT_SPMV, spmv)
-        except te.TEError:  # SELL refuses very uneven rows
+        except te.TEError:  # SELL refuses very uneven rows; the slot-window format needs a dictionary
             pass
         te.te_set_option(h, te.TE_OPT_ORTHO, ortho)
         v, st = te.te_evolve(h, c["v0"], 0.5, 1e-8, 24)
