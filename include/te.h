@@ -181,15 +181,14 @@ enum {
                                 ranges planned on the device at create: >= 2 distinct columns at
                                 >= 1/4 density) bulk-copied into shared memory too; entries are
                                 addressed by 16-bit slots (0xFFFF: gathered from global memory).
-                                The default when the plan stages >= 95 % of the entries and rows
-                                hold <= 40 entries on average (spin chains, bosons); the optional
-                                value dictionary (env TE_SPMV_XS_DICT=1: 8-bit codes when the
-                                off-diagonal entries take <= 255 distinct values) is off by default;
+                                The default when the plan stages >= 95 % of the entries, rows hold
+                                <= 40 entries on average and the slot-window format does not
+                                apply (bosons);
                                 7 warp-specialised ring: one producer warp bulk-copies (TMA
                                 engine) rowptr/col/val of nnz-balanced tiles into a 3-4 stage
                                 shared-memory ring, 15 consumer warps (TPR lanes per row, 8-16
                                 register gathers in flight per lane) release stages per warp —
-                                no block barrier per tile.  The default otherwise;
+                                no block barrier per tile.  The default otherwise (x <= 160 MB);
                                 6 SELL-32-sigma: rows sorted by length in 4096-row windows, 32-row
                                 slices stored column-major, one lane per row, software-pipelined
                                 loads (a padded copy of H is built on the device when selected;

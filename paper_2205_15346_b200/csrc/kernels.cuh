@@ -50,11 +50,6 @@ struct KDev {
   const uint16_t* lcol;      // [nnz + 8] slot of each entry in its tile's staged x
   int xs_ecap, xs_xcap, xs_rmax;  // entries per tile, staged x slots per tile, ranges per tile
   int xs_xpol;               // L2 policy of the staged x copies: 0 normal, 1 evict_last
-  // value dictionary (staged-x SpMV): 8-bit code per entry (255: the row's diagonal entry)
-  const uint8_t* xs_code;    // [nnz + 32] or nullptr (values streamed as they are)
-  const void* xs_diag;       // [n + 2] diagonal value of each row (VT)
-  const void* xs_dict;       // [xs_ndict <= 255] off-diagonal values (VT)
-  int xs_ndict;
   // slot-window SELL-32 with a value dictionary (variant 9, spmv_sw.cu)
   const int64_t* sw_sptr;    // [nslice+1] first slot of each 32-row slice (multiples of kSwGroup)
   const int32_t* sw_base;    // [slots] first column of each slot's 32-column window
@@ -139,12 +134,10 @@ constexpr int kXsConsumers = 15;
 constexpr int kXsRmax = 64;      // x ranges per tile
 constexpr int kXsGap = 8;        // bridge gaps of < 8 unused x entries (128 B) inside a range
 constexpr size_t kXsBudget = 220 * 1024;  // shared memory of the 2-3 stage ring
-size_t spmv_xs_smem(bool cplx, int tpr, int ecap, int xcap, int stages, bool dict);
-int xs_xcap_for(bool cplx, int tpr, int ecap, size_t budget, int stages, bool dict);
+size_t spmv_xs_smem(bool cplx, int tpr, int ecap, int xcap, int stages);
+int xs_xcap_for(bool cplx, int tpr, int ecap, size_t budget, int stages);
 void launch_dict_insert(int64_t n, const int64_t* rowptr, const int32_t* col, const void* val, bool cplx, void* table,
                         int cap, unsigned* count, cudaStream_t st);
-void launch_dict_codes(int64_t n, const int64_t* rowptr, const int32_t* col, const void* val, bool cplx,
-                       const double2* dict, int nd, uint8_t* code, void* diag, cudaStream_t st);
 size_t dict_slot_bytes();
 void launch_xs_plan(const int64_t* tiles, int64_t ntiles, const int32_t* col, int64_t ncol_stage, int xcap, int rmax,
                     int gap, int4* meta, int2* rng, uint16_t* lcol, cudaStream_t st);

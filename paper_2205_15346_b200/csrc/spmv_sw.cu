@@ -46,6 +46,65 @@ __device__ __forceinline__ int dict_code(const double2* __restrict__ dk, int nd,
 }
 }  // namespace
 
+// ------------------------------------------------------------------------------------------
+// value dictionary (create time): the distinct off-diagonal values of H, bit for bit (exact), into
+// an open-addressing hash table; at most 255 of them (the couplings of a model Hamiltonian: XXZ
+// 2-3, Bose-Hubbard <= 156) become the 8-bit codes of the slot-window format.
+// ------------------------------------------------------------------------------------------
+struct DictSlot {
+  unsigned state;  // 0 empty, 1 being written, 2 ready
+  unsigned pad;
+  double re, im;
+};
+
+__global__ void k_dict_insert(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                              const void* __restrict__ val, bool cplx, DictSlot* table, int cap, unsigned* count) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    if (*(volatile unsigned*)count > 255u) return;
+    for (int64_t k = rowptr[r]; k < rowptr[r + 1]; ++k) {
+      if (col[k] == (int32_t)r) continue;
+      double re, im = 0.0;
+      if (cplx) {
+        const double2 v = static_cast<const double2*>(val)[k];
+        re = v.x;
+        im = v.y;
+      } else {
+        re = static_cast<const double*>(val)[k];
+      }
+      const unsigned long long kr = (unsigned long long)__double_as_longlong(re);
+      const unsigned long long ki = (unsigned long long)__double_as_longlong(im);
+      unsigned long long hsh = kr * 0x9E3779B97F4A7C15ull ^ (ki + 0x632BE59BD9B4E019ull) * 0xBF58476D1CE4E5B9ull;
+      hsh ^= hsh >> 29;
+      for (int probe = 0; probe < cap; ++probe) {
+        DictSlot* sl = table + ((hsh + probe) & (unsigned long long)(cap - 1));
+        unsigned st = *(volatile unsigned*)&sl->state;
+        if (st == 0u) {
+          if (atomicCAS(&sl->state, 0u, 1u) == 0u) {
+            sl->re = re;
+            sl->im = im;
+            __threadfence();
+            atomicExch(&sl->state, 2u);
+            atomicAdd(count, 1u);
+            break;
+          }
+          st = 1u;
+        }
+        while (st == 1u) st = *(volatile unsigned*)&sl->state;
+        if ((unsigned long long)__double_as_longlong(*(volatile double*)&sl->re) == kr &&
+            (unsigned long long)__double_as_longlong(*(volatile double*)&sl->im) == ki)
+          break;
+      }
+    }
+  }
+}
+
+void launch_dict_insert(int64_t n, const int64_t* rowptr, const int32_t* col, const void* val, bool cplx, void* table,
+                        int cap, unsigned* count, cudaStream_t st) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + 255) / 256));
+  k_dict_insert<<<grid, 256, 0, st>>>(n, rowptr, col, val, cplx, static_cast<DictSlot*>(table), cap, count);
+}
+size_t dict_slot_bytes() { return sizeof(DictSlot); }
+
 // Build, one warp per slice.  FILL = false: slot count of each slice (rounded up to kSwGroup);
 // FILL = true: window bases, 16-bit entries and the diagonal.  dk: the nd dictionary values sorted
 // by (re bits, im bits).  err bit 1: an off-diagonal value missing from the dictionary.

@@ -154,144 +154,32 @@ void launch_xs_plan(const int64_t* tiles, int64_t ntiles, const int32_t* col, in
 }
 
 // ------------------------------------------------------------------------------------------
-// value dictionary (create time): when the off-diagonal entries take at most 255 distinct values
-// (the couplings of a model Hamiltonian: XXZ 2, Bose-Hubbard <= 156), the staged-x SpMV streams
-// an 8-bit code per entry instead of the 8/16-byte value; code 255 marks the diagonal entry,
-// whose value comes from a dense per-row array.  Values are compared bit for bit (exact).
-// ------------------------------------------------------------------------------------------
-struct DictSlot {
-  unsigned state;  // 0 empty, 1 being written, 2 ready
-  unsigned pad;
-  double re, im;
-};
-
-__global__ void k_dict_insert(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                              const void* __restrict__ val, bool cplx, DictSlot* table, int cap, unsigned* count) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-    if (*(volatile unsigned*)count > 255u) return;
-    for (int64_t k = rowptr[r]; k < rowptr[r + 1]; ++k) {
-      if (col[k] == (int32_t)r) continue;
-      double re, im = 0.0;
-      if (cplx) {
-        const double2 v = static_cast<const double2*>(val)[k];
-        re = v.x;
-        im = v.y;
-      } else {
-        re = static_cast<const double*>(val)[k];
-      }
-      const unsigned long long kr = (unsigned long long)__double_as_longlong(re);
-      const unsigned long long ki = (unsigned long long)__double_as_longlong(im);
-      unsigned long long hsh = kr * 0x9E3779B97F4A7C15ull ^ (ki + 0x632BE59BD9B4E019ull) * 0xBF58476D1CE4E5B9ull;
-      hsh ^= hsh >> 29;
-      for (int probe = 0; probe < cap; ++probe) {
-        DictSlot* sl = table + ((hsh + probe) & (unsigned long long)(cap - 1));
-        unsigned st = *(volatile unsigned*)&sl->state;
-        if (st == 0u) {
-          if (atomicCAS(&sl->state, 0u, 1u) == 0u) {
-            sl->re = re;
-            sl->im = im;
-            __threadfence();
-            atomicExch(&sl->state, 2u);
-            atomicAdd(count, 1u);
-            break;
-          }
-          st = 1u;
-        }
-        while (st == 1u) st = *(volatile unsigned*)&sl->state;
-        if ((unsigned long long)__double_as_longlong(*(volatile double*)&sl->re) == kr &&
-            (unsigned long long)__double_as_longlong(*(volatile double*)&sl->im) == ki)
-          break;
-      }
-    }
-  }
-}
-
-// codes of every entry (binary search of the bit patterns in the sorted dictionary) and the dense
-// diagonal; dict: nd values sorted by (re bits, im bits)
-__global__ void k_dict_codes(int64_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                             const void* __restrict__ val, bool cplx, const double2* __restrict__ dict, int nd,
-                             uint8_t* code, void* diag) {
-  __shared__ unsigned long long kre[256], kim[256];
-  for (int i = threadIdx.x; i < nd; i += blockDim.x) {
-    kre[i] = (unsigned long long)__double_as_longlong(dict[i].x);
-    kim[i] = (unsigned long long)__double_as_longlong(dict[i].y);
-  }
-  __syncthreads();
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-    for (int64_t k = rowptr[r]; k < rowptr[r + 1]; ++k) {
-      double re, im = 0.0;
-      if (cplx) {
-        const double2 v = static_cast<const double2*>(val)[k];
-        re = v.x;
-        im = v.y;
-      } else {
-        re = static_cast<const double*>(val)[k];
-      }
-      if (col[k] == (int32_t)r) {
-        code[k] = 255;
-        if (cplx) static_cast<double2*>(diag)[r] = make_double2(re, im);
-        else static_cast<double*>(diag)[r] = re;
-        continue;
-      }
-      const unsigned long long kr = (unsigned long long)__double_as_longlong(re);
-      const unsigned long long ki = (unsigned long long)__double_as_longlong(im);
-      int lo = 0, hi = nd - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (kre[mid] < kr || (kre[mid] == kr && kim[mid] < ki)) lo = mid + 1;
-        else hi = mid;
-      }
-      code[k] = (uint8_t)lo;
-    }
-  }
-}
-
-void launch_dict_insert(int64_t n, const int64_t* rowptr, const int32_t* col, const void* val, bool cplx, void* table,
-                        int cap, unsigned* count, cudaStream_t st) {
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + 255) / 256));
-  k_dict_insert<<<grid, 256, 0, st>>>(n, rowptr, col, val, cplx, static_cast<DictSlot*>(table), cap, count);
-}
-void launch_dict_codes(int64_t n, const int64_t* rowptr, const int32_t* col, const void* val, bool cplx,
-                       const double2* dict, int nd, uint8_t* code, void* diag, cudaStream_t st) {
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + 255) / 256));
-  k_dict_codes<<<grid, 256, 0, st>>>(n, rowptr, col, val, cplx, dict, nd, code, diag);
-}
-size_t dict_slot_bytes() { return sizeof(DictSlot); }
-
-// ------------------------------------------------------------------------------------------
 // the SpMV
 // ------------------------------------------------------------------------------------------
-// stage layout: [x slots | values (or 8-bit codes + per-row diagonal, DICT) | rowptr | 16-bit slots]
-template <bool CPLX, int TPR, bool DICT = false>
+// stage layout: [x slots | values | rowptr | 16-bit slots]
+template <bool CPLX, int TPR>
 struct XsLayout {
   using VT = typename ValT<CPLX>::T;
   static constexpr int kRcap = 32 * kXsConsumers / TPR;
   __host__ __device__ static size_t xb(int xcap) { return (size_t)xcap * 16; }
-  __host__ __device__ static size_t vb(int ecap) {
-    return DICT ? rnd16((size_t)ecap + 32) + rnd16((size_t)(kRcap + 4) * sizeof(VT))
-                : rnd16((size_t)(ecap + 2) * sizeof(VT));
-  }
-  __host__ __device__ static size_t db(int ecap) { return rnd16((size_t)ecap + 32); }  // DICT: diag offset in vb
+  __host__ __device__ static size_t vb(int ecap) { return rnd16((size_t)(ecap + 2) * sizeof(VT)); }
   __host__ __device__ static size_t rb() { return rnd16((size_t)(kRcap + 4) * 8); }
   __host__ __device__ static size_t lb(int ecap) { return rnd16((size_t)(ecap + 16) * 2); }
   __host__ __device__ static size_t stage(int ecap, int xcap) { return xb(xcap) + vb(ecap) + rb() + lb(ecap); }
 };
 
-template <bool CPLX, int TPR, int HM, int NF, int STG, bool DICT = false>
+template <bool CPLX, int TPR, int HM, int NF, int STG>
 __global__ void __launch_bounds__(kXsThreads, 1) k_spmv_xs(KDev d, int j) {
   using VT = typename ValT<CPLX>::T;
-  using LY = XsLayout<CPLX, TPR, DICT>;
+  using LY = XsLayout<CPLX, TPR>;
   constexpr int C = kXsConsumers;
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ __align__(8) uint64_t full[STG], empty[STG];
   __shared__ int64_t desc[STG][4];
   __shared__ int gcount[STG];
   __shared__ double sj_s;
-  __shared__ VT dict_s[DICT ? 255 : 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ecap = d.xs_ecap, xcap = d.xs_xcap;
-  if (DICT)
-    for (int i = tid; i < d.xs_ndict; i += blockDim.x) dict_s[i] = static_cast<const VT*>(d.xs_dict)[i];
   const size_t oX = 0, oV = LY::xb(xcap), oR = oV + LY::vb(ecap), oL = oR + LY::rb();
   const size_t stage_bytes = LY::stage(ecap, xcap);
   if (tid == 0) {
@@ -353,31 +241,19 @@ __global__ void __launch_bounds__(kXsThreads, 1) k_spmv_xs(KDev d, int j) {
       if (lane == 0) {
         desc[st][0] = a.x; desc[st][1] = a.y; desc[st][2] = b.x; desc[st][3] = b.y;
         gcount[st] = mt.z;
-        unsigned br = 0, bv = 0, bl = 0, bd = 0;
-        int64_t r0i = 0, v0 = 0, l0 = 0, d0 = 0;
+        unsigned br = 0, bv = 0, bl = 0;
+        int64_t r0i = 0, v0 = 0, l0 = 0;
         if (staged) {
           r0i = a.x & ~1LL;
           br = (unsigned)((((a.y + 2) & ~1LL) - r0i) * 8);
-          if (DICT) {  // 8-bit codes of the tile's entries and the diagonal of its rows
-            v0 = b.x & ~15LL;
-            bv = (unsigned)(((b.y + 15) & ~15LL) - v0);
-            d0 = a.x & ~(VA - 1);
-            bd = (unsigned)((((a.y + VA - 1) & ~(VA - 1)) - d0) * sizeof(VT));
-          } else {
-            v0 = b.x & ~(VA - 1);
-            bv = (unsigned)((((b.y + VA - 1) & ~(VA - 1)) - v0) * sizeof(VT));
-          }
+          v0 = b.x & ~(VA - 1);
+          bv = (unsigned)((((b.y + VA - 1) & ~(VA - 1)) - v0) * sizeof(VT));
           l0 = b.x & ~7LL;
           bl = (unsigned)((((b.y + 7) & ~7LL) - l0) * 2);
         }
-        mbar_expect_tx(&full[st], br + bv + bl + bd + (staged ? (unsigned)mt.y * 16u : 0u));
+        mbar_expect_tx(&full[st], br + bv + bl + (staged ? (unsigned)mt.y * 16u : 0u));
         if (br) bulk_g2s(base + oR, d.rowptr + r0i, br, &full[st], pol);
-        if (DICT) {
-          if (bv) bulk_g2s(base + oV, d.xs_code + v0, bv, &full[st], pol);
-          if (bd) bulk_g2s(base + oV + LY::db(ecap), static_cast<const VT*>(d.xs_diag) + d0, bd, &full[st], pol);
-        } else if (bv) {
-          bulk_g2s(base + oV, static_cast<const VT*>(d.val) + v0, bv, &full[st], pol);
-        }
+        if (bv) bulk_g2s(base + oV, static_cast<const VT*>(d.val) + v0, bv, &full[st], pol);
         if (bl) bulk_g2s(base + oL, d.lcol + l0, bl, &full[st], pol);
       }
       __syncwarp();
@@ -425,8 +301,6 @@ __global__ void __launch_bounds__(kXsThreads, 1) k_spmv_xs(KDev d, int j) {
       const unsigned char* base = sm + (size_t)st * stage_bytes;
       const double2* xs = reinterpret_cast<const double2*>(base + oX);
       const VT* vv = reinterpret_cast<const VT*>(base + oV) + (b & (VA - 1));
-      const uint8_t* cd = base + oV + (b & 15);                                            // DICT
-      const VT* dg = reinterpret_cast<const VT*>(base + oV + LY::db(ecap)) + (ra & (VA - 1));  // DICT
       const int64_t* rp = reinterpret_cast<const int64_t*>(base + oR) + (ra & 1);
       const uint16_t* lc = reinterpret_cast<const uint16_t*>(base + oL) + (b & 7);
       const int rows = (int)(rb - ra);
@@ -444,16 +318,7 @@ __global__ void __launch_bounds__(kXsThreads, 1) k_spmv_xs(KDev d, int j) {
           }
 #pragma unroll
           for (int w = 0; w < NF; ++w)
-            if (q0 + w * TPR < hi) {
-              VT v;
-              if (DICT) {
-                const unsigned c = cd[q0 + w * TPR];
-                v = c == 255u ? dg[i] : dict_s[c];
-              } else {
-                v = vv[q0 + w * TPR];
-              }
-              acc = cadd(acc, ValT<CPLX>::mul(v, xx[w]));
-            }
+            if (q0 + w * TPR < hi) acc = cadd(acc, ValT<CPLX>::mul(vv[q0 + w * TPR], xx[w]));
         }
       } else {
         for (int q0 = lo + q; q0 < hi; q0 += NF * TPR) {
@@ -468,16 +333,7 @@ __global__ void __launch_bounds__(kXsThreads, 1) k_spmv_xs(KDev d, int j) {
           }
 #pragma unroll
           for (int w = 0; w < NF; ++w)
-            if (q0 + w * TPR < hi) {
-              VT v;
-              if (DICT) {
-                const unsigned c = cd[q0 + w * TPR];
-                v = c == 255u ? dg[i] : dict_s[c];
-              } else {
-                v = vv[q0 + w * TPR];
-              }
-              acc = cadd(acc, ValT<CPLX>::mul(v, xx[w]));
-            }
+            if (q0 + w * TPR < hi) acc = cadd(acc, ValT<CPLX>::mul(vv[q0 + w * TPR], xx[w]));
         }
       }
       if (TPR > 1) acc = group_sum<TPR>(acc);
@@ -494,12 +350,11 @@ __global__ void __launch_bounds__(kXsThreads, 1) k_spmv_xs(KDev d, int j) {
   }
 }
 
-size_t spmv_xs_smem(bool cplx, int tpr, int ecap, int xcap, int stages, bool dict) {
+size_t spmv_xs_smem(bool cplx, int tpr, int ecap, int xcap, int stages) {
   switch (tpr) {
-#define TE_XS_SM(T)                                                                                          \
-  case T:                                                                                                    \
-    return stages * (dict ? (cplx ? XsLayout<true, T, true>::stage(ecap, xcap) : XsLayout<false, T, true>::stage(ecap, xcap)) \
-                          : (cplx ? XsLayout<true, T>::stage(ecap, xcap) : XsLayout<false, T>::stage(ecap, xcap)));
+#define TE_XS_SM(T) \
+  case T:           \
+    return stages * (cplx ? XsLayout<true, T>::stage(ecap, xcap) : XsLayout<false, T>::stage(ecap, xcap));
     TE_XS_SM(1) TE_XS_SM(2) TE_XS_SM(4)
     default: TE_XS_SM(8)
 #undef TE_XS_SM
@@ -508,16 +363,10 @@ size_t spmv_xs_smem(bool cplx, int tpr, int ecap, int xcap, int stages, bool dic
 
 void launch_spmv_xs(const KDev& d, bool cplx, int j, const Launch& L) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(L.grid_spmv, d.ntiles_xs));
-  const bool dict = d.xs_code != nullptr;
-  const size_t smem = spmv_xs_smem(cplx, L.spmv_xs_tpr, d.xs_ecap, d.xs_xcap, L.xs_stages, dict);
-#define TE_XS_NF(T, H, S, NF)                                                                           \
-  if (dict) {                                                                                          \
-    if (cplx) k_spmv_xs<true, T, H, NF, S, true><<<grid, kXsThreads, smem, L.stream>>>(d, j);          \
-    else k_spmv_xs<false, T, H, NF, S, true><<<grid, kXsThreads, smem, L.stream>>>(d, j);              \
-  } else {                                                                                             \
-    if (cplx) k_spmv_xs<true, T, H, NF, S><<<grid, kXsThreads, smem, L.stream>>>(d, j);                \
-    else k_spmv_xs<false, T, H, NF, S><<<grid, kXsThreads, smem, L.stream>>>(d, j);                    \
-  }
+  const size_t smem = spmv_xs_smem(cplx, L.spmv_xs_tpr, d.xs_ecap, d.xs_xcap, L.xs_stages);
+#define TE_XS_NF(T, H, S, NF)                                                                  \
+  if (cplx) k_spmv_xs<true, T, H, NF, S><<<grid, kXsThreads, smem, L.stream>>>(d, j);          \
+  else k_spmv_xs<false, T, H, NF, S><<<grid, kXsThreads, smem, L.stream>>>(d, j);
 #define TE_XS_S(T, H, S) \
   if (L.xs_nf == 16) { TE_XS_NF(T, H, S, 16) } else { TE_XS_NF(T, H, S, 8) }
 #define TE_XS_H(T, H) \
@@ -544,11 +393,7 @@ void configure_xs_kernels(void (*set_attr)(const void*, size_t, void*), void* ct
   set((const void*)k_spmv_xs<false, T, H, NF, 2>, budget);          \
   set((const void*)k_spmv_xs<true, T, H, NF, 2>, budget);           \
   set((const void*)k_spmv_xs<false, T, H, NF, 3>, budget);          \
-  set((const void*)k_spmv_xs<true, T, H, NF, 3>, budget);           \
-  set((const void*)k_spmv_xs<false, T, H, NF, 2, true>, budget);    \
-  set((const void*)k_spmv_xs<true, T, H, NF, 2, true>, budget);     \
-  set((const void*)k_spmv_xs<false, T, H, NF, 3, true>, budget);    \
-  set((const void*)k_spmv_xs<true, T, H, NF, 3, true>, budget);
+  set((const void*)k_spmv_xs<true, T, H, NF, 3>, budget);
 #define TE_SETXS(T, H) TE_SETXS_NF(T, H, 8) TE_SETXS_NF(T, H, 16)
   TE_SETXS(1, 0) TE_SETXS(2, 0) TE_SETXS(4, 0) TE_SETXS(8, 0)
   TE_SETXS(1, 1) TE_SETXS(2, 1) TE_SETXS(4, 1) TE_SETXS(8, 1)
@@ -557,11 +402,9 @@ void configure_xs_kernels(void (*set_attr)(const void*, size_t, void*), void* ct
 }
 
 // x slots per tile that fit the shared-memory budget next to the tile's H part
-int xs_xcap_for(bool cplx, int tpr, int ecap, size_t budget, int stages, bool dict) {
+int xs_xcap_for(bool cplx, int tpr, int ecap, size_t budget, int stages) {
   size_t h = 0;
-#define TE_XS_H0(T)                                                                                                \
-  h = dict ? (cplx ? XsLayout<true, T, true>::stage(ecap, 0) : XsLayout<false, T, true>::stage(ecap, 0))          \
-           : (cplx ? XsLayout<true, T>::stage(ecap, 0) : XsLayout<false, T>::stage(ecap, 0));
+#define TE_XS_H0(T) h = cplx ? XsLayout<true, T>::stage(ecap, 0) : XsLayout<false, T>::stage(ecap, 0);
   switch (tpr) {
     case 1: TE_XS_H0(1) break;
     case 2: TE_XS_H0(2) break;

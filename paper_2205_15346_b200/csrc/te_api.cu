@@ -142,10 +142,6 @@ struct te_handle {
   double xs_global_frac = 1.0;  // entries the plan left to global gathers / nnz
   double xs_global_tiles = 1.0; // tiles with at least one such entry / tiles
   double xs_x_per_entry = 0.0;  // staged x slots / entries (bulk-copied x per product)
-  uint8_t* d_xs_code = nullptr;  // value dictionary (<= 255 distinct off-diagonal values)
-  void* d_xs_diag = nullptr;
-  void* d_xs_dict = nullptr;
-  int xs_ndict = 0;
   // slot-window SELL-32 with a value dictionary (variant 9), built at create when applicable
   int64_t* d_sw_sptr = nullptr;
   int32_t* d_sw_base = nullptr;
@@ -269,10 +265,6 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.xs_xcap = h->xs_xcap;
   d.xs_rmax = te::kXsRmax;
   d.xs_xpol = h->xs_xpol;
-  d.xs_code = h->d_xs_code;
-  d.xs_diag = h->d_xs_diag;
-  d.xs_dict = h->d_xs_dict;
-  d.xs_ndict = h->xs_ndict;
   d.sw_sptr = h->d_sw_sptr;
   d.sw_base = h->d_sw_base;
   d.sw_ent = h->d_sw_ent;
@@ -707,7 +699,7 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
   // staged-x with the value dictionary (8-bit code + 16-bit slot, plus one diagonal value per row)
   double bh = (double)(h->nnz + h->nh_entries) * (vbytes + 4.0) + 8.0 * (n + 1.0);
   if (h->spmv_tiled == 8 && h->ntiles_xs > 0)
-    bh = h->d_xs_code ? (double)h->nnz * 3.0 + n * vbytes + 8.0 * (n + 1.0) : (double)h->nnz * (vbytes + 2.0) + 8.0 * (n + 1.0);
+    bh = (double)h->nnz * (vbytes + 2.0) + 8.0 * (n + 1.0);
   if (h->spmv_tiled == 8 && h->ntiles_xs > 0) bh += (double)h->nh_entries * (vbytes + 4.0);
   // column-blocked ring: algorithmic bytes are those of the CSR it was cut from (the per-pass row
   // pointers and the W re-reads of passes > 0 are overhead of the method, not counted)
@@ -1075,13 +1067,6 @@ int check_evolve_args(te_handle* h, double t, double tol, int m_max) {
 
 // ---------------------------------------------------------------- staged-x SpMV plan
 void free_xs(te_handle* h) {
-  cudaFree(h->d_xs_code);
-  cudaFree(h->d_xs_diag);
-  cudaFree(h->d_xs_dict);
-  h->d_xs_code = nullptr;
-  h->d_xs_diag = nullptr;
-  h->d_xs_dict = nullptr;
-  h->xs_ndict = 0;
   cudaFree(h->d_tile_xs);
   cudaFree(h->d_xs_meta);
   cudaFree(h->d_xs_rng);
@@ -1097,8 +1082,8 @@ void free_xs(te_handle* h) {
 // row), then the device plan (spmv_xs.cu): per tile the x ranges to stage and each entry's slot.
 // rowptr: host copy of the (local) row pointers.
 // Value dictionary on the device: distinct off-diagonal values (bit patterns) into a 1024-slot hash
-// table; if there are at most 255, sorted by bit pattern they become codes 0..254 (255: diagonal
-// in the staged-x codes, padding in the slot-window SELL).  Returns the number of values, or -1
+// table; if there are at most 255, sorted by bit pattern they become codes 0..254 (255: padding in
+// the slot-window SELL).  Returns the number of values, or -1
 // when there are more than 255 (keys: the sorted values, imaginary part 0 for real H).
 int collect_dict(te_handle* h, std::vector<double2>& keys_out) {
   cudaStream_t s = h->stream ? h->stream : h->own_stream;
@@ -1135,44 +1120,6 @@ int collect_dict(te_handle* h, std::vector<double2>& keys_out) {
   keys_out.clear();
   for (const auto& k : keys) keys_out.push_back(k.second);
   return (int)keys_out.size();
-}
-
-int build_dict(te_handle* h) {
-  // opt-in (TE_SPMV_XS_DICT=1): a third of the H bytes, but the staged-x consumers are bound by
-  // their dependent shared-memory lookups, not by HBM (ncu), and the code -> value lookup adds
-  // one more: measured slower on configs 2 / 3 / 5 (+15 / +6 / +9 % per SpMV), faster only with
-  // 78 entries per row (config 6, -14 % vs staged-x without it, still slower than the ring)
-  const char* e = getenv("TE_SPMV_XS_DICT");
-  if (!e || atoi(e) == 0) return TE_OK;
-  cudaStream_t s = h->stream ? h->stream : h->own_stream;
-  std::vector<double2> kd;
-  const int nd = collect_dict(h, kd);
-  if (nd < 0) return TE_OK;
-  std::vector<double> vr((size_t)std::max(1, nd));
-  for (int i = 0; i < nd; ++i) vr[(size_t)i] = kd[(size_t)i].x;
-  if (kd.empty()) kd.push_back(make_double2(0.0, 0.0));
-  const size_t vb = h->cplx ? 16 : 8;
-  double2* dkeys = nullptr;
-  CK(cudaMalloc(&dkeys, sizeof(double2) * kd.size()));
-  if (cudaMalloc(&h->d_xs_code, (size_t)h->nnz + 32) != cudaSuccess || cudaMalloc(&h->d_xs_diag, vb * (h->n + 2)) != cudaSuccess ||
-      cudaMalloc(&h->d_xs_dict, vb * 256) != cudaSuccess) {
-    cudaGetLastError();
-    cudaFree(dkeys);
-    cudaFree(h->d_xs_code); cudaFree(h->d_xs_diag); cudaFree(h->d_xs_dict);
-    h->d_xs_code = nullptr; h->d_xs_diag = nullptr; h->d_xs_dict = nullptr;
-    return TE_OK;  // no room for the codes: stream the values as they are
-  }
-  CK(cudaMemcpyAsync(dkeys, kd.data(), sizeof(double2) * kd.size(), cudaMemcpyHostToDevice, s));
-  if (h->cplx) CK(cudaMemcpyAsync(h->d_xs_dict, kd.data(), sizeof(double2) * nd, cudaMemcpyHostToDevice, s));
-  else CK(cudaMemcpyAsync(h->d_xs_dict, vr.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, s));
-  CK(cudaMemsetAsync(h->d_xs_code, 0, (size_t)h->nnz + 32, s));
-  CK(cudaMemsetAsync(h->d_xs_diag, 0, vb * (h->n + 2), s));
-  te::launch_dict_codes(h->n, h->d_rowptr, h->d_col, h->d_val, h->cplx, dkeys, nd, h->d_xs_code, h->d_xs_diag, s);
-  CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(s));
-  cudaFree(dkeys);
-  h->xs_ndict = nd;
-  return TE_OK;
 }
 
 // ---------------------------------------------------------------- slot-window SELL-32 (variant 9)
@@ -1273,11 +1220,7 @@ int plan_sw(te_handle* h) {
 
 int plan_xs(te_handle* h, const int64_t* rowptr) {
   free_xs(h);
-  {
-    const int rc = build_dict(h);
-    if (rc) return rc;
-  }
-  const bool dict = h->d_xs_code != nullptr;
+
   const int64_t n = h->n;
   const double avg = n > 0 ? (double)h->nnz / (double)n : 0.0;
   int tx = 1;  // measured (config 2): one lane per row beats 2 / 4 (larger tiles, longer x ranges)
@@ -1287,13 +1230,13 @@ int plan_xs(te_handle* h, const int64_t* rowptr) {
     if (v == 1 || v == 2 || v == 4 || v == 8) tx = v;
   }
   h->spmv_xs_tpr = tx;
-  h->xs_ecap = dict ? 8192 : (h->cplx ? 2048 : 4096);
+  h->xs_ecap = h->cplx ? 2048 : 4096;
   if (const char* e = getenv("TE_SPMV_XS_ECAP")) h->xs_ecap = std::max(64, std::min(8192, atoi(e)));
   h->xs_stages = 2;
   if (const char* e = getenv("TE_SPMV_XS_XPOL")) h->xs_xpol = atoi(e) != 0;
   if (const char* e = getenv("TE_SPMV_XS_NF")) h->xs_nf = atoi(e) == 16 ? 16 : 8;
   if (const char* e = getenv("TE_SPMV_XS_STAGES")) h->xs_stages = atoi(e) == 3 ? 3 : 2;
-  h->xs_xcap = te::xs_xcap_for(h->cplx, tx, h->xs_ecap, te::kXsBudget, h->xs_stages, dict);
+  h->xs_xcap = te::xs_xcap_for(h->cplx, tx, h->xs_ecap, te::kXsBudget, h->xs_stages);
   const int64_t rcap = 32 * te::kXsConsumers / tx;
   std::vector<int64_t> tg;
   int64_t st = 0;

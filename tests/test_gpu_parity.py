@@ -123,23 +123,19 @@ XS_CASES = RING_CASES + [("xxz_L14", configs.build(2, L=14)), ("bh_L7_N7", confi
                          ("banded_n8192", configs.build(4, n=8192)), ("xxznnn_L10_cplx", _complex_dict_case())]
 
 
-@pytest.mark.parametrize("dict_", [1, 0], ids=["dict", "nodict"])
 @pytest.mark.parametrize("ecap", [0, 256])
 @pytest.mark.parametrize("tpr", [1, 2, 4, 8])
 @pytest.mark.parametrize("halo", [0, 1])
 @pytest.mark.parametrize("name,c", XS_CASES, ids=[x[0] for x in XS_CASES])
-def test_spmv_xs_variants(gpu_lib, name, c, tpr, halo, ecap, dict_, monkeypatch):
+def test_spmv_xs_variants(gpu_lib, name, c, tpr, halo, ecap, monkeypatch):
     """Staged-x ring SpMV (TE_OPT_SPMV = 8) for every lanes-per-row choice, plain and halo-aware,
     with the default tile size and with 256-entry tiles (many tiles per CTA: the 2-stage ring wraps,
     ranges cut by the slot budget), on matrices whose x windows are fully staged (spin chains,
     bosons), partly staged (banded + uniform) and hardly at all (uniform random columns, long
-    rows: the global-gather path), with and without the value dictionary (8-bit codes; real and
-    complex values; matrices with more than 255 distinct values keep their values), vs the
-    oracle's Arnoldi basis."""
+    rows: the global-gather path), real and complex values, vs the oracle's Arnoldi basis."""
     te = gpu_lib
     if c is None:
         c = _long_row_case()
-    monkeypatch.setenv("TE_SPMV_XS_DICT", str(dict_))
     monkeypatch.setenv("TE_SPMV_XS_TPR", str(tpr))
     monkeypatch.setenv("TE_SPMV_FORCE_HALO", str(halo))
     if ecap:
@@ -682,20 +678,25 @@ def _forced_wrap_parity(te, c, sched, m, ring_min_wraps=4, spmv=None):
     return err
 
 
-@pytest.mark.parametrize("spmv", [7, 8])
-def test_forced_parity_complex_ring_wraps_config4_n2e20(gpu_lib, spmv):
+@pytest.mark.parametrize("spmv", [7, 8, 10])
+def test_forced_parity_complex_ring_wraps_config4_n2e20(gpu_lib, spmv, monkeypatch):
     """Complex H through the ring SpMV at a wrapping size: config 4's model at n = 2^20 (32
     complex entries per row, the k_spmv_ring<complex, TPR 4, 3 stages> instantiation of the full
-    2^24 config), m = 8, two forced restarts, element by element against the oracle."""
+    2^24 config), m = 8, two forced restarts, element by element against the oracle.  spmv 10: the
+    column-blocked ring as config 4 runs it (6 blocks of 2.7 MB here; 16 entries per row per pass
+    in the diagonal block, the rest uniform: TPR 1-2 per pass)."""
+    if spmv == 10:
+        monkeypatch.setenv("TE_SPMV_COLBLK_MB", "2.7")
     c = configs.build(4, n=1 << 20)
     _forced_wrap_parity(gpu_lib, c, [0.05, 0.05], 8, spmv=spmv)
 
 
-@pytest.mark.parametrize("spmv", [7, 8])
+@pytest.mark.parametrize("spmv", [7, 8, 9])
 def test_forced_parity_config5_instantiation_L22(gpu_lib, spmv):
     """Config 5's model at L = 22 (n = 4,194,304, 23 entries per row on average: the TPR 2 /
-    3-stage real ring instantiation of the full L = 26 config), m = 10, one forced restart,
-    element by element against the oracle."""
+    3-stage real ring instantiation of the full L = 26 config; spmv 9: the slot-window SELL-32 that
+    config 5 runs by default, with the same dictionary and window structure), m = 10, one forced
+    restart, element by element against the oracle."""
     c = configs.build(5, L=22)
     _forced_wrap_parity(gpu_lib, c, [0.1], 10, spmv=spmv)
 

@@ -1,5 +1,5 @@
 """Small evolutions through every shipped SpMV format (slot-window SELL-32, column-blocked ring,
-staged-x with and without the value dictionary, ring, SELL-sigma), projection kernel set and
+staged-x, ring, SELL-sigma), projection kernel set and
 orthogonalisation mode, for compute-sanitizer (memcheck / racecheck / synccheck;
 tools/sanitize.sh).  Sizes span several tiles per CTA: the staged-x SpMV runs with small tiles
 (TE_SPMV_XS_ECAP=256) so its mbarrier ring wraps; the column-blocked ring with 1 KB column blocks;
@@ -14,12 +14,10 @@ from paper_2205_15346_b200 import te  # noqa: E402
 from workloads import configs  # noqa: E402
 
 cases = [configs.build(2, L=12), configs.build(3, L=6, N=6), configs.build(1, n=1000), configs.build(5, L=11)]
-# (kernel set, SpMV, ortho, staged-x dictionary)
-runs = [(2, 9, 0, "0"), (2, 10, 0, "0"), (2, 8, 0, "1"), (2, 8, 0, "0"), (2, 7, 0, "1"), (2, 6, 0, "1"),
-        (3, 7, 0, "1"), (5, 7, 0, "1"), (2, 8, 2, "1"), (2, 8, 1, "1")]
+# (kernel set, SpMV, ortho)
+runs = [(2, 9, 0), (2, 10, 0), (2, 8, 0), (2, 7, 0), (2, 6, 0), (3, 7, 0), (5, 7, 0), (2, 8, 2), (2, 8, 1)]
 for c in cases:
-    for kset, spmv, ortho, dct in runs:
-        os.environ["TE_SPMV_XS_DICT"] = dct
+    for kset, spmv, ortho in runs:
         h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
         te.te_set_option(h, te.TE_OPT_KERNELS, kset)
         try:

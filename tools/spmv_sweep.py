@@ -4,8 +4,9 @@ run with per-launch CUDA events (TE_OPT_PROFILE) and the SpMV's time per launch 
 its algorithmic GB/s and the staged-x plan statistics.
 
   python tools/spmv_sweep.py --config 5 --m 6 --reps 2 \
-      --variant "8:" --variant "8:TE_SPMV_XS_DICT=1" --variant "7:"
-A variant is "<spmv>:<ENV=VAL,ENV=VAL,...>" (spmv: 8 staged-x, 7 ring, 6 SELL)."""
+      --variant "9:" --variant "8:" --variant "8:TE_SPMV_XS_STAGES=3" --variant "7:"
+A variant is "<spmv>:<ENV=VAL,ENV=VAL,...>" (spmv: 10 column-blocked ring, 9 slot-window SELL-32,
+8 staged-x, 7 ring, 6 SELL-sigma)."""
 from __future__ import annotations
 
 import argparse
