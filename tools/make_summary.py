@@ -1,90 +1,51 @@
-"""Collect bench.py JSON lines (gpurun_out/fin_*.log) into profiles/r01_bench_*.json and
-profiles/r01_summary.md.  Usage: python tools/make_summary.py [glob | --from-profiles]"""
+"""Rebuild profiles/<round>_summary.md from the committed bench lines profiles/<round>_bench_*.json.
+Usage: python tools/make_summary.py [round]   (default r02)"""
 import glob
 import json
 import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-pat = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "fin_*.log")
-
+RND = sys.argv[1] if len(sys.argv) > 1 else "r02"
 LABEL = {1: "1 random n=4096", 2: "2 XXZ L=20", 3: "3 Bose-Hubbard 12/12", 4: "4 random banded n=2^24",
          5: "5 XXZ+NNN L=26", 6: "6 paper §5 model d=1,565,904 (P:527)"}
 
 
-def line_of(path):
-    for l in reversed(open(path).read().splitlines()):
-        if l.startswith("{"):
-            return json.loads(l)
-    return None
-
-
-rows = {"cgs2": [], "lanczos3": [], "cgs2gram": []}
-ref = None
-if pat == "--from-profiles":  # rebuild the summary from the committed bench lines
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r01_bench_*.json"))):
+def main():
+    rows, ref = [], None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", f"{RND}_bench_*.json"))):
         d = json.load(open(f))
         if d.get("impl") == "reference":
             ref = d
             continue
         cfg = int(os.path.basename(f).split("config")[1].split("_")[0].split(".")[0])
-        rows[d["config"]["ortho"]].append((cfg, d))
-else:
-  for f in sorted(glob.glob(pat)):
-    d = line_of(f)
-    if d is None:
-        continue
-    if d.get("impl") == "reference":
-        ref = d
-        json.dump(d, open(os.path.join(ROOT, "profiles", "r01_bench_reference_xxz_L20.json"), "w"), indent=1)
-        continue
-    tag = os.path.basename(f)[4:-4]           # e.g. c2, c2_f2
-    cfg = int(tag.split("_")[0][1:])
-    ortho = d["config"]["ortho"]
-    name = f"r01_bench_config{cfg}" + ("" if ortho == "cgs2" else "_" + ortho) + ".json"
-    json.dump(d, open(os.path.join(ROOT, "profiles", name), "w"), indent=1)
-    rows[ortho].append((cfg, d))
+        rows.append((cfg, d))
+    rows.sort(key=lambda x: (x[0], x[1]["config"].get("ortho", "")))
+    out = [f"# Bench summary ({RND}, one B200, bench.py lines in profiles/{RND}_bench_*.json)", "",
+           "value = Krylov steps / device time (CUDA events, inputs resident, restart graphs); e2e = the same "
+           "through te_evolve with host buffers; roofline = the kernel class with the largest device time "
+           "(algorithmic bytes of §6 / its event time, peak = measured 6536 GB/s copy); traffic = its DRAM "
+           "bytes per call from ncu over one restart (profiles/ncu_traffic.json).", "",
+           "| config | ortho | SpMV | Krylov steps/s | e2e | roofline kernel | frac | traffic / alg | SpMV / dots / update / norm GB/s | SM MHz (reasons) | oracle steps/s |",
+           "|---|---|---|---|---|---|---|---|---|---|---|"]
+    for cfg, d in rows:
+        r, k = d["roofline"], d["kernels"]
+        tr = f"{r['traffic'] / r['alg_bytes_per_launch']:.2f}" if r.get("traffic") else "—"
+        g = lambda name: f"{k[name]['gbs']:.0f}" if name in k else "—"  # noqa: E731
+        cl = d.get("clocks") or {}
+        cpu = d.get("cpu_baseline", {}).get("value")
+        out.append(f"| {LABEL[cfg]} | {d['config'].get('ortho')} | {d['config'].get('spmv_ran', '?')} | {d['value']:.1f} | "
+                   f"{d['e2e']['value']:.1f} | {r['kernel']} | {r['frac']:.3f} | {tr} | "
+                   f"{g('spmv')} / {g('proj_dots')} / {g('update_proj')} / {g('update_norm')} | "
+                   f"{cl.get('sm_mhz')} ({', '.join(cl.get('reasons', [])) or '-'}) | "
+                   f"{'%.3g' % cpu if cpu else '—'} |")
+    if ref:
+        out += ["", f"Reference arm (`bench.py --impl reference`, the oracle as it stands, 1 thread): "
+                    f"{ref['value']:.4g} {ref['unit']} on {ref['config']['workload']}; sample: {ref['cpu_baseline']['sample']}."]
+    path = os.path.join(ROOT, "profiles", f"{RND}_summary.md")
+    open(path, "w").write("\n".join(out) + "\n")
+    print("\n".join(out))
 
 
-def gbs(d, k):
-    v = d["kernels"].get(k)
-    return "-" if not v or v["gbs"] is None else f"{v['gbs']:.0f}"
-
-
-out = ["# Round 1 measurements (B200, 1 GPU, default kernel set; bench.py, final kernels)", "",
-       "Value = Krylov steps/s of one full te_evolve per step (CUDA graphs, inputs resident); e2e = the",
-       "same through te_evolve with pinned host buffers. Per-kernel GB/s = algorithmic bytes / summed",
-       "CUDA-event time of that class in the profiled pass. Peak 6544 GB/s (MEASURED_PEAKS.json).", ""]
-hdr = ("| config | Krylov steps/s | e2e | ms/evolve | restarts | Krylov steps | bound | dominant kernel, frac | "
-       "GB/s spmv / dots / update / norm | SM MHz (reasons) | oracle steps/s (1 thread) |")
-sep = "|" + "---|" * 11
-for ortho, title in (("cgs2", "CGS2 (north star)"), ("cgs2gram", "f2: CGS2 with the Gram-matrix second sweep"),
-                     ("lanczos3", "f1: paper-literal 3-term Lanczos")):
-    if not rows[ortho]:
-        continue
-    out += [f"## {title}", "", hdr, sep]
-    for cfg, d in sorted(rows[ortho], key=lambda x: x[0]):
-        st = d["steps"]
-        r = d["roofline"]
-        cb = d.get("cpu_baseline")
-        ck = d.get("clocks", {})
-        out.append(f"| {LABEL[cfg]} | {d['value']:.1f} | {d['e2e']['value']:.1f} | {d['ms_per_step']:.1f} | "
-                   f"{d['config']['restarts_per_step']} | {d['config']['krylov_steps_per_step']:.0f} | "
-                   f"{d.get('err_bound', float('nan')):.2e} | "
-                   f"{r['kernel']} {r['frac']:.2f} | {gbs(d, 'spmv')} / {gbs(d, 'proj_dots')} / {gbs(d, 'update_proj')} / "
-                   f"{gbs(d, 'update_norm')} | {ck.get('sm_mhz')} ({','.join(ck.get('reasons', [])) or '-'}) | "
-                   f"{'%.3g' % cb['value'] if cb else '-'} |")
-    out.append("")
-for cfg, d in rows["cgs2"]:
-    if cfg == 6 and "paper_context" in d:
-        pc = d["paper_context"]
-        out += ["## Paper §5 benchmark (config 6)", "",
-                f"* one full evolution to t = 10 (err_max 1e-7, m = 40): {pc['ours_wall_s']:.3f} s on one B200 "
-                f"(the paper: {pc['paper_wall_s']:.0f} s, {pc['paper_hw']}; context, not a target)",
-                f"* analytic error bound {pc['err_bound']:.3g}; cumulative roundoff estimate {pc['roundoff_total']:.3g} "
-                "(the paper prints 3.2e-6 for the same run, P:531 — reading C15: the estimate is summed over restarts)", ""]
-if ref:
-    out += ["## Reference arm (oracle, 1 thread)", "", f"* {ref['config']['workload']}: {ref['value']:.3g} Krylov steps/s "
-            f"({ref['cpu_baseline']['sample']})", ""]
-open(os.path.join(ROOT, "profiles", "r01_summary.md"), "w").write("\n".join(out) + "\n")
-print("\n".join(out))
+if __name__ == "__main__":
+    main()
