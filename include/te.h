@@ -172,18 +172,20 @@ enum {
                                 9 slot-window SELL-32 with a value dictionary: 32-row slices
                                 (lane = row), each row's off-diagonal entries grouped by their
                                 32-column window, windows merged across the slice into slots
-                                (one int32 window base per slot), 16 bits per entry (8-bit value
-                                code | 8-bit column offset), dense diagonal.  Built at create when
+                                (one int32 window base per slot), 8 bits per entry (3-bit value
+                                code | 5-bit column offset) when the dictionary holds <= 7 values,
+                                else 16 bits (8-bit code | 8-bit offset), dense diagonal.  Built at create when
                                 the off-diagonal values take <= 255 distinct values and the slot
-                                padding is <= 1.6x the off-diagonal entries (spin chains); then
+                                entries are <= 2.0x (8-bit) / 1.6x (16-bit) the off-diagonal
+                                entries (spin chains); then
                                 the default.  TE_ERR_ARG when selected and not applicable;
                                 8 staged-x ring: the ring below, and each tile's x windows (column
                                 ranges planned on the device at create: >= 2 distinct columns at
                                 >= 1/4 density) bulk-copied into shared memory too; entries are
                                 addressed by 16-bit slots (0xFFFF: gathered from global memory).
                                 The default when the plan stages >= 95 % of the entries, rows hold
-                                <= 40 entries on average and the slot-window format does not
-                                apply (bosons);
+                                <= 40 entries on average, n >= 65536 and the slot-window format
+                                does not apply (bosons);
                                 7 warp-specialised ring: one producer warp bulk-copies (TMA
                                 engine) rowptr/col/val of nnz-balanced tiles into a 3-4 stage
                                 shared-memory ring, 15 consumer warps (TPR lanes per row, 8-16

@@ -58,6 +58,7 @@ struct KDev {
   const void* sw_dict;       // [sw_ndict <= 255] off-diagonal values (VT)
   int64_t sw_nslice;
   int sw_ndict;
+  int sw_bits;               // 16: code << 8 | offset, groups of 4 slots; 8: code << 5 | offset, groups of 8
   int accw;             // SpMV writes W += s_j (H V_j) instead of W = (column-blocked passes > 0)
   const double2* halo;  // received halo entries (distributed, NCCL exchange); nullptr otherwise
   // distributed handles: the entries of local rows whose columns live on other ranks, kept apart
@@ -145,7 +146,7 @@ void configure_xs_kernels(void (*set_attr)(const void*, size_t, void*), void* ct
 void launch_spmv_xs(const KDev& d, bool cplx, int j, const Launch& L);
 // slot-window SELL-32 SpMV (spmv_sw.cu): build (count / fill passes) and launch
 constexpr int kSwGroup = 4;      // slots per 8-byte entry load of a lane
-void launch_sw_build(bool fill, bool cplx, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
+void launch_sw_build(bool fill, bool cplx, bool b8, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
                      const double2* dict_keys, int nd, const int64_t* sptr, int32_t* nslot, int32_t* base,
                      uint16_t* ent, void* diag, int* err, cudaStream_t st);
 void launch_spmv_sw(const KDev& d, bool cplx, int j, const Launch& L);

@@ -26,7 +26,6 @@
 namespace te {
 
 namespace {
-constexpr int kSwPad = 0xFF00;  // code 255: padding slot entry
 
 template <bool CPLX>
 __device__ __forceinline__ int dict_code(const double2* __restrict__ dk, int nd, double re, double im) {
@@ -108,11 +107,20 @@ size_t dict_slot_bytes() { return sizeof(DictSlot); }
 // Build, one warp per slice.  FILL = false: slot count of each slice (rounded up to kSwGroup);
 // FILL = true: window bases, 16-bit entries and the diagonal.  dk: the nd dictionary values sorted
 // by (re bits, im bits).  err bit 1: an off-diagonal value missing from the dictionary.
-template <bool CPLX, bool FILL>
+// B8: 8-bit entries (3-bit code | 5-bit offset; dictionaries of <= 7 values, code 7 = padding) in
+// groups of 8 slots per lane; else 16-bit entries (8-bit code | 8-bit offset) in groups of 4.
+template <bool CPLX, bool FILL, bool B8>
 __global__ void __launch_bounds__(256) k_sw_build(int64_t n, const int64_t* __restrict__ rowptr,
                                                   const int32_t* __restrict__ col, const void* __restrict__ val,
                                                   const double2* __restrict__ dk, int nd, const int64_t* __restrict__ sptr,
                                                   int32_t* nslot, int32_t* base, uint16_t* ent, void* diag, int* err) {
+  constexpr int GRP = B8 ? 8 : kSwGroup;
+  uint8_t* ent8 = reinterpret_cast<uint8_t*>(ent);
+  auto put = [&](int64_t K, int lane_, unsigned code, unsigned off) {
+    if (B8) ent8[((K >> 3) * 32 + lane_) * 8 + (K & 7)] = (uint8_t)(code << 5 | off);
+    else ent[((K >> 2) * 32 + lane_) * 4 + (K & 3)] = (uint16_t)(code << 8 | off);
+  };
+  const unsigned pad_code = B8 ? 7u : 255u;
   using VT = typename ValT<CPLX>::T;
   const VT* v = static_cast<const VT*>(val);
   const int lane = threadIdx.x & 31;
@@ -153,15 +161,11 @@ __global__ void __launch_bounds__(256) k_sw_build(int64_t n, const int64_t* __re
           double re, im = 0.0;
           if constexpr (CPLX) { re = v[p].x; im = v[p].y; } else { re = v[p]; }
           const int code = dict_code<CPLX>(dk, nd, re, im);
-          if (code < 0 || code > 254) atomicOr(err, 1);
-          const int64_t K = slot + k;
-          ent[((K >> 2) * 32 + lane) * 4 + (K & 3)] = (uint16_t)((code & 0xFF) << 8 | (c & 31));
+          if (code < 0 || code >= (int)pad_code) atomicOr(err, 1);
+          put(slot + k, lane, (unsigned)code & (B8 ? 7u : 255u), (unsigned)(c & 31));
           ++k;
         }
-        for (; k < w; ++k) {
-          const int64_t K = slot + k;
-          ent[((K >> 2) * 32 + lane) * 4 + (K & 3)] = (uint16_t)kSwPad;
-        }
+        for (; k < w; ++k) put(slot + k, lane, pad_code, 0u);
         if (lane == 0)
           for (int i = 0; i < w; ++i) base[slot + i] = (int32_t)(kmin << 5);
       }
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(256) k_sw_build(int64_t n, const int64_t* __re
     }
     if (FILL) {
       for (int64_t K = slot; K < slot_end; ++K) {  // round-up padding of the last group
-        ent[((K >> 2) * 32 + lane) * 4 + (K & 3)] = (uint16_t)kSwPad;
+        put(K, lane, pad_code, 0u);
         if (lane == 0) base[K] = (int32_t)(s * 32);
       }
       if (r < n) {
@@ -178,21 +182,23 @@ __global__ void __launch_bounds__(256) k_sw_build(int64_t n, const int64_t* __re
         else static_cast<double*>(diag)[r] = dsum.x;
       }
     } else if (lane == 0) {
-      nslot[s] = (int32_t)((slot + kSwGroup - 1) / kSwGroup * kSwGroup);
+      nslot[s] = (int32_t)((slot + GRP - 1) / GRP * GRP);
     }
   }
 }
 
-void launch_sw_build(bool fill, bool cplx, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
+void launch_sw_build(bool fill, bool cplx, bool b8, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
                      const double2* dk, int nd, const int64_t* sptr, int32_t* nslot, int32_t* base, uint16_t* ent,
                      void* diag, int* err, cudaStream_t st) {
   const int64_t nsl = (n + 31) / 32;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (nsl + 7) / 8));
-#define TE_SWB(C, F) k_sw_build<C, F><<<grid, 256, 0, st>>>(n, rowptr, col, val, dk, nd, sptr, nslot, base, ent, diag, err)
-  if (cplx) {
-    if (fill) TE_SWB(true, true); else TE_SWB(true, false);
+#define TE_SWB(C, F, B) k_sw_build<C, F, B><<<grid, 256, 0, st>>>(n, rowptr, col, val, dk, nd, sptr, nslot, base, ent, diag, err)
+  if (b8) {
+    if (cplx) { if (fill) TE_SWB(true, true, true); else TE_SWB(true, false, true); }
+    else { if (fill) TE_SWB(false, true, true); else TE_SWB(false, false, true); }
   } else {
-    if (fill) TE_SWB(false, true); else TE_SWB(false, false);
+    if (cplx) { if (fill) TE_SWB(true, true, false); else TE_SWB(true, false, false); }
+    else { if (fill) TE_SWB(false, true, false); else TE_SWB(false, false, false); }
   }
 #undef TE_SWB
 }
@@ -282,6 +288,76 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmv_sw(KDev d, int j) {
   }
 }
 
+// 8-bit entries: one 8-byte load per lane covers a group of 8 slots; two 16-byte base loads per
+// warp; 8 x-window loads per iteration.  Same product order as the 16-bit kernel.
+template <bool CPLX>
+__global__ void __launch_bounds__(kThreads, 3) k_spmv_sw8(KDev d, int j) {
+  using VT = typename ValT<CPLX>::T;
+  __shared__ __align__(16) VT dict_s[8];
+  __shared__ double sj_s;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 8) {
+    VT z;
+    if constexpr (CPLX) z = make_double2(0.0, 0.0); else z = 0.0;
+    dict_s[tid] = tid < d.sw_ndict ? static_cast<const VT*>(d.sw_dict)[tid] : z;  // code 7 (padding): 0
+  }
+  if (tid == 0) sj_s = spmv_gate(d, j, blockIdx.x == 0);
+  __syncthreads();
+  const double sj = sj_s;
+  if (sj == 0.0) return;
+  const double2* __restrict__ x = d.V + (int64_t)j * d.ldv;
+  asm volatile("" : "+l"(x));
+  uint32_t dict_base = smem_u32(dict_s);
+  asm volatile("" : "+r"(dict_base));
+  constexpr uint32_t kVB = (uint32_t)sizeof(VT);
+  const VT* __restrict__ diag = static_cast<const VT*>(d.sw_diag);
+  const uint2* __restrict__ ent = reinterpret_cast<const uint2*>(d.sw_ent);
+  const int4* __restrict__ base = reinterpret_cast<const int4*>(d.sw_base);
+  const int64_t n = d.n, nsl = d.sw_nslice;
+  const int64_t tw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5; s < nsl; s += tw) {
+    const int64_t r = s * 32 + lane;
+    const bool act = r < n;
+    const int64_t g0 = __ldg(d.sw_sptr + s) / 8, g1 = __ldg(d.sw_sptr + s + 1) / 8;
+    double2 acc = make_double2(0.0, 0.0);
+    if (act) acc = ValT<CPLX>::mul(ValT<CPLX>::ldcs(diag + r), __ldg(x + r));
+    uint2 e = g0 < g1 ? __ldcs(ent + g0 * 32 + lane) : make_uint2(0u, 0u);
+    int4 b0 = g0 < g1 ? __ldg(base + 2 * g0) : make_int4(0, 0, 0, 0);
+    int4 b1 = g0 < g1 ? __ldg(base + 2 * g0 + 1) : make_int4(0, 0, 0, 0);
+    for (int64_t g = g0; g < g1; ++g) {
+      double2 xv[8];
+      uint32_t cd[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t h = ((k < 4 ? e.x : e.y) >> (8 * (k & 3))) & 0xFFu;
+        const int4& bq = k < 4 ? b0 : b1;
+        const uint32_t bb = (uint32_t)((k & 3) == 0 ? bq.x : ((k & 3) == 1 ? bq.y : ((k & 3) == 2 ? bq.z : bq.w)));
+        cd[k] = h >> 5;
+        xv[k] = __ldg(x + (bb + (h & 31u)));
+      }
+      if (g + 1 < g1) {
+        e = __ldcs(ent + (g + 1) * 32 + lane);
+        b0 = __ldg(base + 2 * (g + 1));
+        b1 = __ldg(base + 2 * (g + 1) + 1);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc = cadd(acc, ValT<CPLX>::mul(ld_dict<CPLX>(dict_base + cd[k] * kVB), xv[k]));
+    }
+    if (act) __stcs(d.W + r, make_double2(acc.x * sj, acc.y * sj));
+  }
+}
+
+template <bool CPLX>
+static int sw8_grid(const Launch& L, int64_t nsl) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmv_sw8<CPLX>, kThreads, 0) != cudaSuccess || b < 1) b = 1;
+    per_sm = b;
+  }
+  return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)L.grid_spmv * per_sm, (nsl + kWarps - 1) / kWarps));
+}
+
 // persistent grid: exactly the co-resident blocks (a grid-stride loop with more blocks than fit
 // runs the surplus blocks' whole share after the first wave: a long tail)
 template <bool CPLX, int U, int XM = 0, int MINB = 1>
@@ -301,6 +377,11 @@ static int sw_grid(const Launch& L, int64_t nsl) {
 // allocation, two-deep x pipelining and L2 prefetch of the next slice's codes all within +-0.3 %:
 // the time does not depend on the SM side
 void launch_spmv_sw(const KDev& d, bool cplx, int j, const Launch& L) {
+  if (d.sw_bits == 8) {
+    if (cplx) k_spmv_sw8<true><<<sw8_grid<true>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
+    else k_spmv_sw8<false><<<sw8_grid<false>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
+    return;
+  }
   if (cplx) k_spmv_sw<true, 2, 0, 3><<<sw_grid<true, 2, 0, 3>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
   else k_spmv_sw<false, 2, 0, 3><<<sw_grid<false, 2, 0, 3>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
 }

@@ -150,6 +150,7 @@ struct te_handle {
   void* d_sw_dict = nullptr;
   int64_t sw_nslice = 0, sw_slots = 0;
   int sw_ndict = 0;
+  int sw_bits = 16;
   double sw_fill = 0.0;  // slot entries (32 per slot) / off-diagonal entries
   // column-blocked copy of H for the ring (variant 10): one CSR + ring tile table per cb_cols
   // columns of x, built at create for large x (single rank)
@@ -272,6 +273,7 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.sw_dict = h->d_sw_dict;
   d.sw_nslice = h->sw_nslice;
   d.sw_ndict = h->sw_ndict;
+  d.sw_bits = h->sw_bits;
   d.scol = h->d_scol;
   d.sval = h->d_sval;
   d.sptr = h->d_sptr;
@@ -706,7 +708,7 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
   // slot-window SELL-32: 2 bytes per slot entry (padding included), the slot bases, the slice
   // pointers and the dense diagonal
   if (h->spmv_tiled == 9 && h->sw_nslice > 0)
-    bh = (double)h->sw_slots * (64.0 + 4.0) + 8.0 * (double)(h->sw_nslice + 1) + n * vbytes +
+    bh = (double)h->sw_slots * ((h->sw_bits == 8 ? 32.0 : 64.0) + 4.0) + 8.0 * (double)(h->sw_nslice + 1) + n * vbytes +
          (double)h->nh_entries * (vbytes + 4.0);
   te::launch_restart_init(d, L); LCHECK("restart_init");
   ++h->launches;
@@ -1142,7 +1144,11 @@ void free_sw(te_handle* h) {
 // at most 255 distinct values and the slot entries (32 per slot, padding included) stay within
 // kSwMaxFill times the off-diagonal entry count.  Not applicable: TE_OK with sw_nslice = 0
 // (sw_fill reports the padding ratio when the dictionary exists).
-constexpr double kSwMaxFill = 1.6;
+constexpr double kSwMaxFill = 1.6;    // 16-bit entries
+// staged-x is the default only from this many rows on (config 1, n = 4096: ring 31.1K vs staged-x
+// 28.9K Krylov steps/s; the tiny x is L1/L2-resident either way and the staging is overhead)
+constexpr int64_t kXsMinRows = 65536;
+constexpr double kSwMaxFill8 = 2.0;   // 8-bit entries (half the bytes per slot entry)
 int plan_sw(te_handle* h) {
   free_sw(h);
   h->sw_fill = 0.0;
@@ -1167,9 +1173,12 @@ int plan_sw(te_handle* h) {
     cleanup();
     return TE_OK;
   }
+  // 8-bit entries when the dictionary has <= 7 values (spin chains), else 16-bit (TE_SPMV_SW_BITS)
+  bool b8 = nd <= 7;
+  if (const char* e = getenv("TE_SPMV_SW_BITS")) b8 = b8 && atoi(e) != 16;
   CK(cudaMemcpyAsync(dkeys, kd.data(), sizeof(double2) * kd.size(), cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(derr, 0, sizeof(int), s));
-  te::launch_sw_build(false, h->cplx, n, h->d_rowptr, h->d_col, h->d_val, dkeys, nd, nullptr, nslot, nullptr, nullptr,
+  te::launch_sw_build(false, h->cplx, b8, n, h->d_rowptr, h->d_col, h->d_val, dkeys, nd, nullptr, nslot, nullptr, nullptr,
                       nullptr, derr, s);
   CK(cudaGetLastError());
   std::vector<int32_t> cnt((size_t)nsl);
@@ -1181,14 +1190,14 @@ int plan_sw(te_handle* h) {
   // off-diagonal entries: nnz - n (every row of the model Hamiltonians stores its diagonal)
   const double offd = std::max<double>(1.0, (double)h->nnz - (double)n);
   h->sw_fill = (double)slots * 32.0 / offd;
-  if (h->sw_fill > kSwMaxFill && !getenv("TE_SPMV_SW_FORCE")) {
+  if (h->sw_fill > (b8 ? kSwMaxFill8 : kSwMaxFill) && !getenv("TE_SPMV_SW_FORCE")) {
     cleanup();
     return TE_OK;
   }
   const size_t vb = h->cplx ? 16 : 8;
   if (cudaMalloc(&h->d_sw_sptr, sizeof(int64_t) * (nsl + 1)) != cudaSuccess ||
-      cudaMalloc(&h->d_sw_base, sizeof(int32_t) * (slots + 4)) != cudaSuccess ||
-      cudaMalloc(&h->d_sw_ent, sizeof(uint16_t) * 32 * (slots + 4)) != cudaSuccess ||
+      cudaMalloc(&h->d_sw_base, sizeof(int32_t) * (slots + 8)) != cudaSuccess ||
+      cudaMalloc(&h->d_sw_ent, (b8 ? 1 : 2) * 32 * (size_t)(slots + 8)) != cudaSuccess ||
       cudaMalloc(&h->d_sw_diag, vb * (n + 2)) != cudaSuccess || cudaMalloc(&h->d_sw_dict, vb * 256) != cudaSuccess) {
     cudaGetLastError();
     cleanup();
@@ -1201,7 +1210,7 @@ int plan_sw(te_handle* h) {
   else CK(cudaMemcpyAsync(h->d_sw_dict, vr.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(h->d_sw_sptr, sptr.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(h->d_sw_diag, 0, vb * (n + 2), s));
-  te::launch_sw_build(true, h->cplx, n, h->d_rowptr, h->d_col, h->d_val, dkeys, nd, h->d_sw_sptr, nullptr, h->d_sw_base,
+  te::launch_sw_build(true, h->cplx, b8, n, h->d_rowptr, h->d_col, h->d_val, dkeys, nd, h->d_sw_sptr, nullptr, h->d_sw_base,
                       h->d_sw_ent, h->d_sw_diag, derr, s);
   CK(cudaGetLastError());
   int herr = 0;
@@ -1215,6 +1224,7 @@ int plan_sw(te_handle* h) {
   h->sw_nslice = nsl;
   h->sw_slots = slots;
   h->sw_ndict = nd;
+  h->sw_bits = b8 ? 8 : 16;
   return TE_OK;
 }
 
@@ -1417,17 +1427,17 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     int want = 0;
     if (const char* e = getenv("TE_SPMV_DEFAULT")) {
       const int v = atoi(e);
-      if (v == 6 || v == 7 || v == 8 || v == 9) want = v;
+      if (v == 6 || v == 7 || v == 8 || v == 9 || v == 10) want = v;
     }
     if (want == 0 || want == 9) {
       if (plan_sw(h) != TE_OK) return fail(TE_ERR_CUDA, "slot-window SELL build");
       if (h->sw_nslice > 0) def = 9;
     }
-    if (def != 9 && (want == 0 || want == 8) && avg <= 40.0) {
+    if (def != 9 && (want == 0 || want == 8) && avg <= 40.0 && (n >= kXsMinRows || want == 8)) {
       if (plan_xs(h, rowptr) != TE_OK) return fail(TE_ERR_OOM, "staged-x plan");
       if (h->ntiles_xs > 0 && (h->xs_global_frac <= 0.05 || want == 8)) def = 8;
     }
-    if (want == 6 || want == 7) def = want;
+    if (want == 6 || want == 7 || want == 10) def = want == 10 ? 7 : want;
     if (def != 8) free_xs(h);
     if (def != 9) free_sw(h);
     h->spmv_tiled = def == 6 ? 7 : def;
@@ -1435,7 +1445,7 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     // * the ring over column blocks (10) when x outgrows L2 (16 n > kColBlkMinX) on a single rank:
     //   each pass gathers from one L2-resident 2^22-column block of x instead of DRAM
     const char* cbe = getenv("TE_SPMV_COLBLK");
-    if (h->spmv_tiled == 7 && want == 0 && 16.0 * (double)n > kColBlkMinX && !(cbe && atoi(cbe) == 0)) {
+    if ((h->spmv_tiled == 7 && want == 0 && 16.0 * (double)n > kColBlkMinX && !(cbe && atoi(cbe) == 0)) || want == 10) {
       if (build_colblk(h, colblk_cols(n)) != TE_OK) return fail(TE_ERR_CUDA, "column-blocked copy");
       if (!h->cb.empty()) h->spmv_tiled = 10;
     }
@@ -1743,7 +1753,7 @@ int te_set_option(te_handle* h, int option, double value) {
         if (rc != TE_OK) return rc;
         if (h->sw_nslice == 0)
           return set_err(TE_ERR_ARG, "TE_OPT_SPMV 9: not applicable to this matrix (more than 255 distinct off-diagonal values, "
-                                     "halo columns, or slot padding %.2f > %.2f)", h->sw_fill, kSwMaxFill);
+                                     "halo columns, or slot padding %.2f above the limit 1.6 (16-bit) / 2.0 (8-bit))", h->sw_fill);
       }
       if (value == 8.0 && h->ntiles_xs == 0) {
         std::vector<int64_t> rp((size_t)h->n + 1);

@@ -102,13 +102,21 @@ def fake_nccl(tmp_path_factory):
     return lib
 
 
+FORMATS = {"auto": {}, "slotwindow": {"TE_SPMV_SW_FORCE": "1"},
+           "colblk": {"TE_SPMV_DEFAULT": "10", "TE_SPMV_COLBLK_MB": "0.002"}}
+
+
+@pytest.mark.parametrize("fmt", list(FORMATS))
 @pytest.mark.parametrize("halo", [0, 1], ids=["nccl_exchange", "peer_loads"])
 @pytest.mark.parametrize("ws", [2, 3])
 @pytest.mark.parametrize("case", ["xxz", "bh", "random", "blockdiag"])
-def test_multirank_device_path_on_one_gpu(gpu_lib, fake_nccl, ws, case, halo):
+def test_multirank_device_path_on_one_gpu(gpu_lib, fake_nccl, ws, case, halo, fmt):
     """halo 0: staged NCCL send/recv exchange before each SpMV; halo 1 (TE_OPT_HALO): the
-    SpMV reads halo columns directly from the owning rank's V column (same address space here)."""
-    env = dict(os.environ, TE_NCCL_LIB=fake_nccl)
+    SpMV reads halo columns directly from the owning rank's V column (same address space here).
+    fmt: each rank's local SpMV format as chosen at create ("auto"), the slot-window SELL-32 forced
+    on every rank whose local values fit the dictionary, or the column-blocked ring (128-column
+    blocks) — the halo entries are added by k_spmv_halo after the local format's passes."""
+    env = dict(os.environ, TE_NCCL_LIB=fake_nccl, **FORMATS[fmt])
     p = subprocess.run([sys.executable, "-c", SCRIPT, str(ws), case, ROOT, str(halo)], env=env, capture_output=True,
                        text=True, timeout=300)
     line = [l for l in p.stdout.splitlines() if l.startswith("RESULT ")]

@@ -183,14 +183,17 @@ SW_CASES = [("xxz_L12", configs.build(2, L=12)), ("xxznnn_L12", configs.build(5,
             ("xxz_L5", configs.build(2, L=5))]
 
 
+@pytest.mark.parametrize("bits", [8, 16])
 @pytest.mark.parametrize("name,c", SW_CASES, ids=[x[0] for x in SW_CASES])
-def test_spmv_sw_variants(gpu_lib, name, c, monkeypatch):
+def test_spmv_sw_variants(gpu_lib, name, c, bits, monkeypatch):
     """Slot-window SELL-32 SpMV (TE_OPT_SPMV = 9) vs the oracle's Arnoldi basis: spin chains (real
     and complex dictionary values), a ragged last slice, rows without a diagonal and empty rows, a
     single slice (n = 32), and a boson matrix whose windows align poorly (the padding check is
-    overridden for all of these small matrices)."""
+    overridden for all of these small matrices); 8-bit entries (3-bit code, dictionaries of <= 7
+    values: the spin chains) and 16-bit entries."""
     te = gpu_lib
     monkeypatch.setenv("TE_SPMV_SW_FORCE", "1")  # small chains: more slices straddle the window edges
+    monkeypatch.setenv("TE_SPMV_SW_BITS", str(bits))  # 8-bit entries apply to dictionaries of <= 7 values
     h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
     te.te_set_option(h, te.TE_OPT_SPMV, 9)
     assert te.te_get_option(h, te.TE_OPT_SPMV) == 9
@@ -253,20 +256,22 @@ def test_spmv_sw_not_applicable(gpu_lib):
 
 
 def test_spmv_default_choice(gpu_lib):
-    """At create: the slot-window SELL-32 for spin chains (dictionary + aligned windows), the
-    staged-x ring when its plan stages >= 95 % of the entries (bosons), the plain ring otherwise
-    (uniform random columns); TE_OPT_SPMV switches either way with the same result."""
+    """At create: the slot-window SELL-32 for spin chains (dictionary + aligned windows, padding
+    <= 2.0x with 8-bit entries), the staged-x ring when its plan stages >= 95 % of the entries
+    (bosons, n >= 65536), the plain ring otherwise (uniform random columns, small n); TE_OPT_SPMV
+    switches either way with the same result."""
     te = gpu_lib
     # (a random matrix must be large enough that a tile's uniform columns are isolated in x)
-    # spin chains: the slot-window SELL when its padding is <= 1.6x (L = 18: 1.2x; XXZ L = 12: 1.8x,
-    # more of the small chain's slices straddle window edges -> staged-x)
-    for c, want in ((configs.build(5, L=18), 9), (configs.build(2, L=12), 8), (configs.build(3, L=7, N=7), 8),
-                    (configs.build(1, n=1 << 18), 7)):
+    for c, want in ((configs.build(5, L=18), 9), (configs.build(2, L=12), None), (configs.build(3, L=10, N=10), 8),
+                    (configs.build(3, L=7, N=7), 7), (configs.build(1, n=1 << 18), 7)):
         h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
         fill = te.te_get_option(h, te.TE_INFO_SW_FILL)
+        if want is None:  # small chain: the slot-window format iff its padding is within the limit
+            assert fill > 0
+            want = 9 if fill <= 2.0 else (8 if c["n"] >= 65536 else 7)
         assert te.te_get_option(h, te.TE_OPT_SPMV) == want, fill
         if c["cfg"] in (2, 5):
-            assert (want == 9) == (0 < fill <= 1.6)
+            assert (want == 9) == (0 < fill <= 2.0)
         other = 7 if want in (8, 9) else 8
         v1, _ = te.te_evolve(h, c["v0"], 0.5, 1e-9, 16)
         te.te_set_option(h, te.TE_OPT_SPMV, other)
