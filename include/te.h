@@ -201,8 +201,12 @@ int te_set_option(te_handle* h, int option, double value);
 /* Read-only plan statistics (te_get_option only; -1 when the handle has no such plan).  Staged-x
  * SpMV: entries gathered from global memory / nnz; tiles with at least one such entry / tiles;
  * bulk-copied x slots / nnz.  Slot-window SELL-32: slot entries (padding included) / off-diagonal
- * entries (reported when the value dictionary exists, also when the padding made it inapplicable). */
-enum { TE_INFO_XS_GLOBAL = 101, TE_INFO_XS_GLOBAL_TILES = 102, TE_INFO_XS_X_PER_ENTRY = 103, TE_INFO_SW_FILL = 104 };
+ * entries (reported when the value dictionary exists, also when the padding made it inapplicable);
+ * TE_INFO_SW_PANEL: log2 of the slices (32 rows) per panel when the slot-window SpMV runs as a
+ * two-pass panel sweep (x larger than L2), 0 when it runs as one pass;
+ * TE_INFO_SW_FAR: slots of the far-window pass / all slots. */
+enum { TE_INFO_XS_GLOBAL = 101, TE_INFO_XS_GLOBAL_TILES = 102, TE_INFO_XS_X_PER_ENTRY = 103, TE_INFO_SW_FILL = 104,
+       TE_INFO_SW_PANEL = 105, TE_INFO_SW_FAR = 106 };
 /* Current value of an option (TE_OPT_SPMV reports the kernel the handle runs, e.g. the default
  * chosen at create) or of a TE_INFO_* statistic; TE_ERR_ARG for a null handle/pointer or an
  * unknown option. */

@@ -59,6 +59,12 @@ struct KDev {
   int64_t sw_nslice;
   int sw_ndict;
   int sw_bits;               // 16: code << 8 | offset, groups of 4 slots; 8: code << 5 | offset, groups of 8
+  // panel sweep (two passes when x outgrows L2): pass 1 holds the windows inside the slice's aligned
+  // panel of 2^sw_ka slices and runs in row order; pass 2 holds the far windows, adds into W and
+  // visits the slices with the sw_ob slice bits from sw_lo upwards as the slowest index, so that
+  // the columns of one sweep period again form an L2-sized panel
+  int sw_pass;               // 0: single pass, 2: far-window pass (sw_sptr/base/ent are that pass's arrays)
+  int sw_sb, sw_lo, sw_ob;   // slice index bits, first outer bit, number of outer bits (pass 2)
   int accw;             // SpMV writes W += s_j (H V_j) instead of W = (column-blocked passes > 0)
   const double2* halo;  // received halo entries (distributed, NCCL exchange); nullptr otherwise
   // distributed handles: the entries of local rows whose columns live on other ranks, kept apart
@@ -107,6 +113,7 @@ struct Launch {
   int proj_tma;         // 2: hybrid by column count (default), 1: TMA-tiled only, 3: register accumulators only
   int spmv_tiled;       // 10: column-blocked ring, 9: slot-window SELL-32, 8: staged-x ring, 7: ring, 6: SELL-32-sigma
   int prefetch;         // update_norm: L2 bulk-prefetch distance in block iterations (0: off)
+  int sw_minb;          // slot-window SpMV, 8-bit entries: resident CTAs per SM (3 or 4)
 };
 
 // hot path (one Krylov step j = 4 launches; see kernels.cu)
@@ -146,7 +153,7 @@ void configure_xs_kernels(void (*set_attr)(const void*, size_t, void*), void* ct
 void launch_spmv_xs(const KDev& d, bool cplx, int j, const Launch& L);
 // slot-window SELL-32 SpMV (spmv_sw.cu): build (count / fill passes) and launch
 constexpr int kSwGroup = 4;      // slots per 8-byte entry load of a lane
-void launch_sw_build(bool fill, bool cplx, bool b8, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
+void launch_sw_build(bool fill, bool cplx, bool b8, int pass, int ka, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
                      const double2* dict_keys, int nd, const int64_t* sptr, int32_t* nslot, int32_t* base,
                      uint16_t* ent, void* diag, int* err, cudaStream_t st);
 void launch_spmv_sw(const KDev& d, bool cplx, int j, const Launch& L);

@@ -113,7 +113,8 @@ template <bool CPLX, bool FILL, bool B8>
 __global__ void __launch_bounds__(256) k_sw_build(int64_t n, const int64_t* __restrict__ rowptr,
                                                   const int32_t* __restrict__ col, const void* __restrict__ val,
                                                   const double2* __restrict__ dk, int nd, const int64_t* __restrict__ sptr,
-                                                  int32_t* nslot, int32_t* base, uint16_t* ent, void* diag, int* err) {
+                                                  int32_t* nslot, int32_t* base, uint16_t* ent, void* diag, int* err,
+                                                  int pass, int ka) {
   constexpr int GRP = B8 ? 8 : kSwGroup;
   uint8_t* ent8 = reinterpret_cast<uint8_t*>(ent);
   auto put = [&](int64_t K, int lane_, unsigned code, unsigned off) {
@@ -148,6 +149,13 @@ __global__ void __launch_bounds__(256) k_sw_build(int64_t n, const int64_t* __re
         if ((int64_t)col[q] != r) ++cnt;
         ++q;
       }
+      // panel sweep: pass 1 keeps the windows inside the slice's aligned panel of 2^ka slices,
+      // pass 2 the others (s and kmin are warp-uniform; the diagonal's window is always near)
+      const bool farw = (((unsigned)s ^ kmin) >> ka) != 0u;
+      if ((pass == 1 && farw) || (pass == 2 && !farw)) {
+        p = q;
+        continue;
+      }
       const int w = (int)__reduce_max_sync(0xFFFFFFFFu, (unsigned)cnt);
       if (FILL) {
         int k = 0;
@@ -177,7 +185,7 @@ __global__ void __launch_bounds__(256) k_sw_build(int64_t n, const int64_t* __re
         put(K, lane, pad_code, 0u);
         if (lane == 0) base[K] = (int32_t)(s * 32);
       }
-      if (r < n) {
+      if (r < n && diag != nullptr) {
         if constexpr (CPLX) static_cast<double2*>(diag)[r] = dsum;
         else static_cast<double*>(diag)[r] = dsum.x;
       }
@@ -187,12 +195,12 @@ __global__ void __launch_bounds__(256) k_sw_build(int64_t n, const int64_t* __re
   }
 }
 
-void launch_sw_build(bool fill, bool cplx, bool b8, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
+void launch_sw_build(bool fill, bool cplx, bool b8, int pass, int ka, int64_t n, const int64_t* rowptr, const int32_t* col, const void* val,
                      const double2* dk, int nd, const int64_t* sptr, int32_t* nslot, int32_t* base, uint16_t* ent,
                      void* diag, int* err, cudaStream_t st) {
   const int64_t nsl = (n + 31) / 32;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(148 * 16, (nsl + 7) / 8));
-#define TE_SWB(C, F, B) k_sw_build<C, F, B><<<grid, 256, 0, st>>>(n, rowptr, col, val, dk, nd, sptr, nslot, base, ent, diag, err)
+#define TE_SWB(C, F, B) k_sw_build<C, F, B><<<grid, 256, 0, st>>>(n, rowptr, col, val, dk, nd, sptr, nslot, base, ent, diag, err, pass, ka)
   if (b8) {
     if (cplx) { if (fill) TE_SWB(true, true, true); else TE_SWB(true, false, true); }
     else { if (fill) TE_SWB(false, true, true); else TE_SWB(false, false, true); }
@@ -220,7 +228,16 @@ __device__ __forceinline__ typename ValT<CPLX>::T ld_dict(uint32_t addr) {
   }
 }
 
-template <bool CPLX, int U, int XM = 0, int MINB = 1>
+// Pass 2 of the panel sweep: slice visited at position i of the sweep (the outer bits slowest)
+__device__ __forceinline__ int64_t sw_perm(const KDev& d, int64_t i) {
+  const int lo = d.sw_lo, ob = d.sw_ob, ib = d.sw_sb - ob;  // ib inner bits: lo low ones, ib - lo high ones
+  const int64_t low = i & ((int64_t(1) << lo) - 1);
+  const int64_t mid = (i >> lo) & ((int64_t(1) << (ib - lo)) - 1);
+  const int64_t out = i >> ib;
+  return low | (out << lo) | (mid << (lo + ob));
+}
+
+template <bool CPLX, int U, int XM = 0, int MINB = 1, bool PB = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmv_sw(KDev d, int j) {
   using VT = typename ValT<CPLX>::T;
   __shared__ __align__(16) VT dict_s[256];
@@ -233,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmv_sw(KDev d, int j) {
     if constexpr (CPLX) z = make_double2(0.0, 0.0); else z = 0.0;
     dict_s[i] = i < d.sw_ndict ? static_cast<const VT*>(d.sw_dict)[i] : z;
   }
-  if (tid == 0) sj_s = spmv_gate(d, j, blockIdx.x == 0);
+  if (tid == 0) sj_s = spmv_gate(d, j, !PB && blockIdx.x == 0);
   __syncthreads();
   const double sj = sj_s;
   if (sj == 0.0) return;
@@ -247,12 +264,17 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmv_sw(KDev d, int j) {
   const int4* __restrict__ base = reinterpret_cast<const int4*>(d.sw_base);
   const int64_t n = d.n, nsl = d.sw_nslice;
   const int64_t tw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5; s < nsl; s += tw) {
+  const int64_t iend = PB ? (int64_t(1) << d.sw_sb) : nsl;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5; i < iend; i += tw) {
+    const int64_t s = PB ? sw_perm(d, i) : i;
+    if (PB && s >= nsl) continue;
     const int64_t r = s * 32 + lane;
     const bool act = r < n;
     const int64_t g0 = __ldg(d.sw_sptr + s) / kSwGroup, g1 = __ldg(d.sw_sptr + s + 1) / kSwGroup;
-    double2 acc = make_double2(0.0, 0.0);
-    if (act) acc = ValT<CPLX>::mul(ValT<CPLX>::ldcs(diag + r), __ldg(x + r));
+    if (PB && g0 == g1) continue;
+    double2 acc = make_double2(0.0, 0.0), w0 = make_double2(0.0, 0.0);
+    if (PB) { if (act) w0 = __ldcs(d.W + r); }
+    else if (act) acc = ValT<CPLX>::mul(ValT<CPLX>::ldcs(diag + r), __ldg(x + r));
     // software pipeline: the entry codes and window bases of batch g + U are loaded while the x
     // loads of batch g are in flight
     uint2 e[U];
@@ -282,16 +304,22 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmv_sw(KDev d, int j) {
       }
       if (g + U < g1) load_batch(g + U, e, b);
 #pragma unroll
-      for (int i = 0; i < 4 * U; ++i) acc = cadd(acc, ValT<CPLX>::mul(ld_dict<CPLX>(dict_base + cd[i] * kVB), xv[i]));
+      for (int q = 0; q < 4 * U; ++q) acc = cadd(acc, ValT<CPLX>::mul(ld_dict<CPLX>(dict_base + cd[q] * kVB), xv[q]));
     }
-    if (act) __stcs(d.W + r, make_double2(acc.x * sj, acc.y * sj));
+    if (act) __stcs(d.W + r, make_double2(w0.x + acc.x * sj, w0.y + acc.y * sj));
   }
 }
 
 // 8-bit entries: one 8-byte load per lane covers a group of 8 slots; two 16-byte base loads per
 // warp; 8 x-window loads per iteration.  Same product order as the 16-bit kernel.
-template <bool CPLX>
-__global__ void __launch_bounds__(kThreads, 3) k_spmv_sw8(KDev d, int j) {
+// The kernel is latency-bound (ncu: long-scoreboard stalls ~11 per issue, 24 warps per SM): a
+// slice costs one dependent memory round trip per group of 8 slots plus two for its prologue
+// (slice pointers -> first entry codes).  The prologue is therefore pipelined across slices: the
+// slice pointers of the warp's next slice are loaded when the current slice starts, and its first
+// group of codes and window bases while the current slice's last group of x loads is in flight.
+// MINB: resident CTAs per SM (3: 85 registers, 4: 64).
+template <bool CPLX, bool PB = false, int MINB = 3>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmv_sw8(KDev d, int j) {
   using VT = typename ValT<CPLX>::T;
   __shared__ __align__(16) VT dict_s[8];
   __shared__ double sj_s;
@@ -301,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmv_sw8(KDev d, int j) {
     if constexpr (CPLX) z = make_double2(0.0, 0.0); else z = 0.0;
     dict_s[tid] = tid < d.sw_ndict ? static_cast<const VT*>(d.sw_dict)[tid] : z;  // code 7 (padding): 0
   }
-  if (tid == 0) sj_s = spmv_gate(d, j, blockIdx.x == 0);
+  if (tid == 0) sj_s = spmv_gate(d, j, !PB && blockIdx.x == 0);
   __syncthreads();
   const double sj = sj_s;
   if (sj == 0.0) return;
@@ -315,15 +343,50 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmv_sw8(KDev d, int j) {
   const int4* __restrict__ base = reinterpret_cast<const int4*>(d.sw_base);
   const int64_t n = d.n, nsl = d.sw_nslice;
   const int64_t tw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5; s < nsl; s += tw) {
+  const int64_t iend = PB ? (int64_t(1) << d.sw_sb) : nsl;
+  // the warp's slices: sweep positions i, i + tw, ... (pass 2: permuted, positions past nsl skipped)
+  auto next_slice = [&](int64_t& i, int64_t& s) -> bool {
+    for (; i < iend; i += tw) {
+      s = PB ? sw_perm(d, i) : i;
+      if (!PB || s < nsl) return true;
+    }
+    return false;
+  };
+  int64_t i = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5, s = 0;
+  bool have = next_slice(i, s);
+  int64_t g0 = 0, g1 = 0;
+  uint2 e = make_uint2(0u, 0u);
+  int4 b0 = make_int4(0, 0, 0, 0), b1 = b0;
+  if (have) {
+    g0 = __ldg(d.sw_sptr + s) >> 3;
+    g1 = __ldg(d.sw_sptr + s + 1) >> 3;
+    if (g0 < g1) {
+      e = __ldcs(ent + g0 * 32 + lane);
+      b0 = __ldg(base + 2 * g0);
+      b1 = __ldg(base + 2 * g0 + 1);
+    }
+  }
+  while (have) {
+    int64_t i2 = i + tw, s2 = 0;
+    const bool have2 = next_slice(i2, s2);
+    int64_t ng0 = 0, ng1 = 0;
+    if (have2) {  // consumed one slice later
+      ng0 = __ldg(d.sw_sptr + s2) >> 3;
+      ng1 = __ldg(d.sw_sptr + s2 + 1) >> 3;
+    }
     const int64_t r = s * 32 + lane;
     const bool act = r < n;
-    const int64_t g0 = __ldg(d.sw_sptr + s) / 8, g1 = __ldg(d.sw_sptr + s + 1) / 8;
-    double2 acc = make_double2(0.0, 0.0);
-    if (act) acc = ValT<CPLX>::mul(ValT<CPLX>::ldcs(diag + r), __ldg(x + r));
-    uint2 e = g0 < g1 ? __ldcs(ent + g0 * 32 + lane) : make_uint2(0u, 0u);
-    int4 b0 = g0 < g1 ? __ldg(base + 2 * g0) : make_int4(0, 0, 0, 0);
-    int4 b1 = g0 < g1 ? __ldg(base + 2 * g0 + 1) : make_int4(0, 0, 0, 0);
+    double2 acc = make_double2(0.0, 0.0), w0 = make_double2(0.0, 0.0);
+    if (PB) { if (act && g0 < g1) w0 = __ldcs(d.W + r); }
+    else if (act) acc = ValT<CPLX>::mul(ValT<CPLX>::ldcs(diag + r), __ldg(x + r));
+    auto load_next_first = [&]() {  // first group of the warp's next slice, into the freed registers
+      if (have2 && ng0 < ng1) {
+        e = __ldcs(ent + ng0 * 32 + lane);
+        b0 = __ldg(base + 2 * ng0);
+        b1 = __ldg(base + 2 * ng0 + 1);
+      }
+    };
+    if (g0 == g1) load_next_first();
     for (int64_t g = g0; g < g1; ++g) {
       double2 xv[8];
       uint32_t cd[8];
@@ -339,20 +402,27 @@ __global__ void __launch_bounds__(kThreads, 3) k_spmv_sw8(KDev d, int j) {
         e = __ldcs(ent + (g + 1) * 32 + lane);
         b0 = __ldg(base + 2 * (g + 1));
         b1 = __ldg(base + 2 * (g + 1) + 1);
+      } else {
+        load_next_first();
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc = cadd(acc, ValT<CPLX>::mul(ld_dict<CPLX>(dict_base + cd[k] * kVB), xv[k]));
     }
-    if (act) __stcs(d.W + r, make_double2(acc.x * sj, acc.y * sj));
+    if (act && (!PB || g0 < g1)) __stcs(d.W + r, make_double2(w0.x + acc.x * sj, w0.y + acc.y * sj));
+    have = have2;
+    i = i2;
+    s = s2;
+    g0 = ng0;
+    g1 = ng1;
   }
 }
 
-template <bool CPLX>
+template <bool CPLX, bool PB = false, int MINB = 3>
 static int sw8_grid(const Launch& L, int64_t nsl) {
   static int per_sm = 0;
   if (per_sm == 0) {
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmv_sw8<CPLX>, kThreads, 0) != cudaSuccess || b < 1) b = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmv_sw8<CPLX, PB, MINB>, kThreads, 0) != cudaSuccess || b < 1) b = 1;
     per_sm = b;
   }
   return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)L.grid_spmv * per_sm, (nsl + kWarps - 1) / kWarps));
@@ -360,28 +430,44 @@ static int sw8_grid(const Launch& L, int64_t nsl) {
 
 // persistent grid: exactly the co-resident blocks (a grid-stride loop with more blocks than fit
 // runs the surplus blocks' whole share after the first wave: a long tail)
-template <bool CPLX, int U, int XM = 0, int MINB = 1>
+template <bool CPLX, int U, int XM = 0, int MINB = 1, bool PB = false>
 static int sw_grid(const Launch& L, int64_t nsl) {
   static int per_sm = 0;
   if (per_sm == 0) {
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmv_sw<CPLX, U, XM, MINB>, kThreads, 0) != cudaSuccess || b < 1) b = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmv_sw<CPLX, U, XM, MINB, PB>, kThreads, 0) != cudaSuccess || b < 1) b = 1;
     per_sm = b;
   }
   // (grid_spmv < num_sms leaves SMs free for a concurrent NCCL halo exchange)
   return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)L.grid_spmv * per_sm, (nsl + kWarps - 1) / kWarps));
 }
 
-// 2 groups of 4 slots per iteration, at most 85 registers (3 CTAs per SM).  Measured on config 5
-// (3.86 ms per SpMV): 1 or 4 groups, 40-register builds at 6 CTAs per SM, x loads without L1
-// allocation, two-deep x pipelining and L2 prefetch of the next slice's codes all within +-0.3 %:
-// the time does not depend on the SM side
+// 16-bit entries: 2 groups of 4 slots per iteration, at most 85 registers (3 CTAs per SM).  Measured
+// on config 5 in its DRAM-bound state (16-bit entries, one pass, 3.86 ms per SpMV): 1 or 4 groups,
+// 40-register builds at 6 CTAs per SM, x loads without L1 allocation, two-deep x pipelining and L2
+// prefetch of the next slice's codes all within +-0.3 %.
 void launch_spmv_sw(const KDev& d, bool cplx, int j, const Launch& L) {
-  if (d.sw_bits == 8) {
-    if (cplx) k_spmv_sw8<true><<<sw8_grid<true>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
-    else k_spmv_sw8<false><<<sw8_grid<false>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
+#define TE_SW8(C, P)                                                                                          \
+  do {                                                                                                        \
+    if (L.sw_minb == 4) k_spmv_sw8<C, P, 4><<<sw8_grid<C, P, 4>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j); \
+    else k_spmv_sw8<C, P, 3><<<sw8_grid<C, P, 3>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);              \
+  } while (0)
+  if (d.sw_pass == 2) {  // far-window pass of the panel sweep: W += ..., permuted slice order
+    if (d.sw_bits == 8) {
+      if (cplx) TE_SW8(true, true);
+      else TE_SW8(false, true);
+    } else {
+      if (cplx) k_spmv_sw<true, 2, 0, 3, true><<<sw_grid<true, 2, 0, 3, true>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
+      else k_spmv_sw<false, 2, 0, 3, true><<<sw_grid<false, 2, 0, 3, true>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
+    }
     return;
   }
+  if (d.sw_bits == 8) {
+    if (cplx) TE_SW8(true, false);
+    else TE_SW8(false, false);
+    return;
+  }
+#undef TE_SW8
   if (cplx) k_spmv_sw<true, 2, 0, 3><<<sw_grid<true, 2, 0, 3>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
   else k_spmv_sw<false, 2, 0, 3><<<sw_grid<false, 2, 0, 3>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);
 }

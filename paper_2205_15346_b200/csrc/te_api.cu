@@ -151,6 +151,13 @@ struct te_handle {
   int64_t sw_nslice = 0, sw_slots = 0;
   int sw_ndict = 0;
   int sw_bits = 16;
+  // panel sweep (x larger than L2): the far windows live in a second set of arrays (pass 2)
+  int64_t* d_swb_sptr = nullptr;
+  int32_t* d_swb_base = nullptr;
+  uint16_t* d_swb_ent = nullptr;
+  int64_t swb_slots = 0;
+  int sw_minb = 3;  // 8-bit kernel: resident CTAs per SM
+  int sw_ka = 0, sw_sb = 0, sw_lo = 0, sw_ob = 0;  // panel slice bits (0: single pass), slice bits, outer range
   double sw_fill = 0.0;  // slot entries (32 per slot) / off-diagonal entries
   // column-blocked copy of H for the ring (variant 10): one CSR + ring tile table per cb_cols
   // columns of x, built at create for large x (single rank)
@@ -274,6 +281,10 @@ KDev make_kdev(te_handle* h, double tol_rate, int m) {
   d.sw_nslice = h->sw_nslice;
   d.sw_ndict = h->sw_ndict;
   d.sw_bits = h->sw_bits;
+  d.sw_pass = 0;
+  d.sw_sb = h->sw_sb;
+  d.sw_lo = h->sw_lo;
+  d.sw_ob = h->sw_ob;
   d.scol = h->d_scol;
   d.sval = h->d_sval;
   d.sptr = h->d_sptr;
@@ -325,6 +336,7 @@ Launch make_launch(te_handle* h) {
   L.ring_stages = h->ring_stages;
   L.spmv_tiled = h->spmv_tiled;
   L.prefetch = h->prefetch;
+  L.sw_minb = h->sw_minb;
   return L;
 }
 
@@ -673,6 +685,15 @@ void free_colblk(te_handle* h) {
 void spmv_call(te_handle* h, const KDev& d, int j, const Launch& L) {
   if (h->spmv_tiled != 10 || h->cb.empty()) {
     te::launch_spmv(d, h->cplx, j, L);
+    if (h->spmv_tiled == 9 && h->sw_nslice > 0 && h->d_swb_sptr) {  // panel sweep: the far windows
+      KDev db = d;
+      db.sw_sptr = h->d_swb_sptr;
+      db.sw_base = h->d_swb_base;
+      db.sw_ent = h->d_swb_ent;
+      db.sw_pass = 2;
+      te::launch_spmv(db, h->cplx, j, L);
+      ++h->launches;
+    }
     return;
   }
   Launch Lr = L;
@@ -708,7 +729,8 @@ int issue_arnoldi(te_handle* h, int m, double tol_rate) {
   // slot-window SELL-32: 2 bytes per slot entry (padding included), the slot bases, the slice
   // pointers and the dense diagonal
   if (h->spmv_tiled == 9 && h->sw_nslice > 0)
-    bh = (double)h->sw_slots * ((h->sw_bits == 8 ? 32.0 : 64.0) + 4.0) + 8.0 * (double)(h->sw_nslice + 1) + n * vbytes +
+    bh = (double)(h->sw_slots + h->swb_slots) * ((h->sw_bits == 8 ? 32.0 : 64.0) + 4.0) +
+         8.0 * (double)(h->sw_nslice + 1) * (h->d_swb_sptr ? 2.0 : 1.0) + n * vbytes +
          (double)h->nh_entries * (vbytes + 4.0);
   te::launch_restart_init(d, L); LCHECK("restart_init");
   ++h->launches;
@@ -1131,6 +1153,14 @@ void free_sw(te_handle* h) {
   cudaFree(h->d_sw_ent);
   cudaFree(h->d_sw_diag);
   cudaFree(h->d_sw_dict);
+  cudaFree(h->d_swb_sptr);
+  cudaFree(h->d_swb_base);
+  cudaFree(h->d_swb_ent);
+  h->d_swb_sptr = nullptr;
+  h->d_swb_base = nullptr;
+  h->d_swb_ent = nullptr;
+  h->swb_slots = 0;
+  h->sw_ka = h->sw_sb = h->sw_lo = h->sw_ob = 0;
   h->d_sw_sptr = nullptr;
   h->d_sw_base = nullptr;
   h->d_sw_ent = nullptr;
@@ -1178,7 +1208,7 @@ int plan_sw(te_handle* h) {
   if (const char* e = getenv("TE_SPMV_SW_BITS")) b8 = b8 && atoi(e) != 16;
   CK(cudaMemcpyAsync(dkeys, kd.data(), sizeof(double2) * kd.size(), cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(derr, 0, sizeof(int), s));
-  te::launch_sw_build(false, h->cplx, b8, n, h->d_rowptr, h->d_col, h->d_val, dkeys, nd, nullptr, nslot, nullptr, nullptr,
+  te::launch_sw_build(false, h->cplx, b8, 0, 0, n, h->d_rowptr, h->d_col, h->d_val, dkeys, nd, nullptr, nslot, nullptr, nullptr,
                       nullptr, derr, s);
   CK(cudaGetLastError());
   std::vector<int32_t> cnt((size_t)nsl);
@@ -1186,19 +1216,24 @@ int plan_sw(te_handle* h) {
   CK(cudaStreamSynchronize(s));
   std::vector<int64_t> sptr((size_t)nsl + 1, 0);
   for (int64_t i = 0; i < nsl; ++i) sptr[(size_t)i + 1] = sptr[(size_t)i] + cnt[(size_t)i];
-  const int64_t slots = sptr[(size_t)nsl];
   // off-diagonal entries: nnz - n (every row of the model Hamiltonians stores its diagonal)
   const double offd = std::max<double>(1.0, (double)h->nnz - (double)n);
-  h->sw_fill = (double)slots * 32.0 / offd;
+  h->sw_fill = (double)sptr[(size_t)nsl] * 32.0 / offd;
   if (h->sw_fill > (b8 ? kSwMaxFill8 : kSwMaxFill) && !getenv("TE_SPMV_SW_FORCE")) {
     cleanup();
     return TE_OK;
   }
   const size_t vb = h->cplx ? 16 : 8;
-  if (cudaMalloc(&h->d_sw_sptr, sizeof(int64_t) * (nsl + 1)) != cudaSuccess ||
-      cudaMalloc(&h->d_sw_base, sizeof(int32_t) * (slots + 8)) != cudaSuccess ||
-      cudaMalloc(&h->d_sw_ent, (b8 ? 1 : 2) * 32 * (size_t)(slots + 8)) != cudaSuccess ||
-      cudaMalloc(&h->d_sw_diag, vb * (n + 2)) != cudaSuccess || cudaMalloc(&h->d_sw_dict, vb * 256) != cudaSuccess) {
+  // Panel sweep (two passes; opt-in): TE_SPMV_SW_PANEL = log2 of the slices per panel (0 / unset: one
+  // pass).  Measured on config 5 with panels of 2^15 slices (16 MB of x): DRAM traffic per SpMV
+  // 14.0 -> 8.7 GB, time 2.96 -> 3.09 ms (the kernel is bound by load latency under L2 load, not by
+  // DRAM bytes), whole bench unchanged (65.2 vs 65.3 Krylov steps/s) - hence not default.
+  int sb = 0;
+  while ((int64_t(1) << sb) < nsl) ++sb;
+  int ka = 0;
+  if (const char* e = getenv("TE_SPMV_SW_PANEL")) ka = std::max(0, atoi(e));
+  if (ka >= sb) ka = 0;  // the whole x is one panel
+  if (cudaMalloc(&h->d_sw_diag, vb * (n + 2)) != cudaSuccess || cudaMalloc(&h->d_sw_dict, vb * 256) != cudaSuccess) {
     cudaGetLastError();
     cleanup();
     free_sw(h);
@@ -1208,11 +1243,42 @@ int plan_sw(te_handle* h) {
   for (size_t i = 0; i < kd.size(); ++i) vr[i] = kd[i].x;
   if (h->cplx) CK(cudaMemcpyAsync(h->d_sw_dict, kd.data(), sizeof(double2) * nd, cudaMemcpyHostToDevice, s));
   else CK(cudaMemcpyAsync(h->d_sw_dict, vr.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(h->d_sw_sptr, sptr.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(h->d_sw_diag, 0, vb * (n + 2), s));
-  te::launch_sw_build(true, h->cplx, b8, n, h->d_rowptr, h->d_col, h->d_val, dkeys, nd, h->d_sw_sptr, nullptr, h->d_sw_base,
-                      h->d_sw_ent, h->d_sw_diag, derr, s);
-  CK(cudaGetLastError());
+  // one pass of the build: slot counts -> slice pointers -> window bases and entries
+  // (pass 0: every window; 1: windows inside the slice's panel, with the diagonal; 2: the others)
+  auto build_pass = [&](int pass, int64_t** d_sptr, int32_t** d_base, uint16_t** d_ent, int64_t* nslots) -> int {
+    if (pass != 0) {
+      te::launch_sw_build(false, h->cplx, b8, pass, ka, n, h->d_rowptr, h->d_col, h->d_val, dkeys, nd, nullptr, nslot,
+                          nullptr, nullptr, nullptr, derr, s);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(cnt.data(), nslot, sizeof(int32_t) * nsl, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int64_t i = 0; i < nsl; ++i) sptr[(size_t)i + 1] = sptr[(size_t)i] + cnt[(size_t)i];
+    }
+    const int64_t ns = sptr[(size_t)nsl];
+    if (cudaMalloc(d_sptr, sizeof(int64_t) * (nsl + 1)) != cudaSuccess ||
+        cudaMalloc(d_base, sizeof(int32_t) * (ns + 8)) != cudaSuccess ||
+        cudaMalloc(d_ent, (b8 ? 1 : 2) * 32 * (size_t)(ns + 8)) != cudaSuccess) {
+      cudaGetLastError();
+      return -1;
+    }
+    CK(cudaMemcpyAsync(*d_sptr, sptr.data(), sizeof(int64_t) * (nsl + 1), cudaMemcpyHostToDevice, s));
+    te::launch_sw_build(true, h->cplx, b8, pass, ka, n, h->d_rowptr, h->d_col, h->d_val, dkeys, nd, *d_sptr, nullptr, *d_base,
+                        *d_ent, pass == 2 ? nullptr : h->d_sw_diag, derr, s);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));  // sptr (host) is reused by the next pass
+    *nslots = ns;
+    return TE_OK;
+  };
+  int64_t slots_a = 0, slots_b = 0;
+  int rcb = build_pass(ka > 0 ? 1 : 0, &h->d_sw_sptr, &h->d_sw_base, &h->d_sw_ent, &slots_a);
+  if (rcb == TE_OK && ka > 0) rcb = build_pass(2, &h->d_swb_sptr, &h->d_swb_base, &h->d_swb_ent, &slots_b);
+  if (rcb > 0) { cleanup(); free_sw(h); return rcb; }
+  if (rcb < 0) {
+    cleanup();
+    free_sw(h);
+    return TE_OK;  // no room: the CSR kernels stay
+  }
   int herr = 0;
   CK(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -1221,10 +1287,21 @@ int plan_sw(te_handle* h) {
     free_sw(h);
     return set_err(TE_ERR_CUDA, "slot-window SELL build: value missing from the dictionary");
   }
+  if (ka > 0) {  // pass 2 sweeps the slices with sw_ob slice bits from sw_lo upwards outermost
+    h->sw_ka = ka;
+    h->sw_sb = sb;
+    h->sw_ob = sb - ka;
+    h->sw_lo = std::max(0, ka - h->sw_ob - 2);
+    if (const char* e = getenv("TE_SPMV_SW_PANEL_LO")) h->sw_lo = std::max(0, std::min(ka, atoi(e)));
+    h->swb_slots = slots_b;
+  }
+  const int64_t slots = slots_a;
   h->sw_nslice = nsl;
   h->sw_slots = slots;
   h->sw_ndict = nd;
   h->sw_bits = b8 ? 8 : 16;
+  h->sw_minb = 3;
+  if (const char* e = getenv("TE_SPMV_SW_MINB")) h->sw_minb = atoi(e) == 4 ? 4 : 3;
   return TE_OK;
 }
 
@@ -1789,6 +1866,10 @@ int te_get_option(const te_handle* h, int option, double* value) {
     case TE_INFO_XS_GLOBAL_TILES: *value = h->ntiles_xs > 0 ? h->xs_global_tiles : -1.0; return TE_OK;
     case TE_INFO_XS_X_PER_ENTRY: *value = h->ntiles_xs > 0 ? h->xs_x_per_entry : -1.0; return TE_OK;
     case TE_INFO_SW_FILL: *value = h->sw_fill > 0.0 ? h->sw_fill : -1.0; return TE_OK;
+    case TE_INFO_SW_PANEL: *value = h->sw_nslice > 0 ? (double)h->sw_ka : -1.0; return TE_OK;
+    case TE_INFO_SW_FAR:
+      *value = h->sw_nslice > 0 ? (double)h->swb_slots / (double)std::max<int64_t>(1, h->sw_slots + h->swb_slots) : -1.0;
+      return TE_OK;
     default: return set_err(TE_ERR_ARG, "unknown option %d", option);
   }
 }

@@ -25,6 +25,7 @@ TE_WARN_QUADRATURE = 2
 TE_OPT_PROFILE = 1
 TE_OPT_GRAPH = 2
 TE_INFO_XS_GLOBAL, TE_INFO_XS_GLOBAL_TILES, TE_INFO_XS_X_PER_ENTRY, TE_INFO_SW_FILL = 101, 102, 103, 104
+TE_INFO_SW_PANEL, TE_INFO_SW_FAR = 105, 106
 TE_OPT_KERNELS = 3
 TE_OPT_PREFETCH = 4
 TE_OPT_SPMV = 5

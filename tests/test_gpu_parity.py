@@ -183,21 +183,30 @@ SW_CASES = [("xxz_L12", configs.build(2, L=12)), ("xxznnn_L12", configs.build(5,
             ("xxz_L5", configs.build(2, L=5))]
 
 
-@pytest.mark.parametrize("bits", [8, 16])
+@pytest.mark.parametrize("panel", [0, 1, 3, 4])
+@pytest.mark.parametrize("bits", [8, 16, "8-minb4"])
 @pytest.mark.parametrize("name,c", SW_CASES, ids=[x[0] for x in SW_CASES])
-def test_spmv_sw_variants(gpu_lib, name, c, bits, monkeypatch):
+def test_spmv_sw_variants(gpu_lib, name, c, bits, panel, monkeypatch):
     """Slot-window SELL-32 SpMV (TE_OPT_SPMV = 9) vs the oracle's Arnoldi basis: spin chains (real
     and complex dictionary values), a ragged last slice, rows without a diagonal and empty rows, a
     single slice (n = 32), and a boson matrix whose windows align poorly (the padding check is
     overridden for all of these small matrices); 8-bit entries (3-bit code, dictionaries of <= 7
-    values: the spin chains) and 16-bit entries."""
+    values: the spin chains) and 16-bit entries; one pass, and the two-pass panel sweep (panels of
+    2^panel slices: near windows in row order, far windows added in the permuted slice order)."""
     te = gpu_lib
     monkeypatch.setenv("TE_SPMV_SW_FORCE", "1")  # small chains: more slices straddle the window edges
-    monkeypatch.setenv("TE_SPMV_SW_BITS", str(bits))  # 8-bit entries apply to dictionaries of <= 7 values
+    monkeypatch.setenv("TE_SPMV_SW_BITS", str(bits)[:2].rstrip("-"))  # 8-bit entries apply to dictionaries of <= 7 values
+    monkeypatch.setenv("TE_SPMV_SW_MINB", "4" if bits == "8-minb4" else "3")  # 64-register build of the 8-bit kernel
+    monkeypatch.setenv("TE_SPMV_SW_PANEL", str(panel))
     h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
     te.te_set_option(h, te.TE_OPT_SPMV, 9)
     assert te.te_get_option(h, te.TE_OPT_SPMV) == 9
     assert te.te_get_option(h, te.TE_INFO_SW_FILL) > 0
+    nsl = (c["n"] + 31) // 32
+    two_pass = panel > 0 and (1 << panel) < nsl
+    assert te.te_get_option(h, te.TE_INFO_SW_PANEL) == (panel if two_pass else 0)
+    if two_pass and name.startswith("xxz"):
+        assert 0 < te.te_get_option(h, te.TE_INFO_SW_FAR) < 1
     m = min(12, c["n"] - 1)
     g = te.te_krylov_basis(h, c["v0"], m, c["tol"] / c["t"], want_V=True)
     o = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), c["v0"], m, c["tol"] / c["t"])
@@ -696,14 +705,48 @@ def test_forced_parity_complex_ring_wraps_config4_n2e20(gpu_lib, spmv, monkeypat
     _forced_wrap_parity(gpu_lib, c, [0.05, 0.05], 8, spmv=spmv)
 
 
-@pytest.mark.parametrize("spmv", [7, 8, 9])
-def test_forced_parity_config5_instantiation_L22(gpu_lib, spmv):
+@pytest.mark.parametrize("spmv", [7, 8, 9, "9-panel", "9-minb4"])
+def test_forced_parity_config5_instantiation_L22(gpu_lib, spmv, monkeypatch):
     """Config 5's model at L = 22 (n = 4,194,304, 23 entries per row on average: the TPR 2 /
     3-stage real ring instantiation of the full L = 26 config; spmv 9: the slot-window SELL-32 that
-    config 5 runs by default, with the same dictionary and window structure), m = 10, one forced
-    restart, element by element against the oracle."""
+    config 5 runs by default, with the same dictionary and window structure; "9-panel": its two-pass
+    panel sweep with 6 outer slice bits as at L = 26 — panels of 2^11 slices here, 2^15 there), m = 10,
+    one forced restart, element by element against the oracle."""
+    monkeypatch.setenv("TE_SPMV_SW_PANEL", "11" if spmv == "9-panel" else "0")
+    monkeypatch.setenv("TE_SPMV_SW_MINB", "4" if spmv == "9-minb4" else "3")  # 64-register build, 4 CTAs per SM
     c = configs.build(5, L=22)
-    _forced_wrap_parity(gpu_lib, c, [0.1], 10, spmv=spmv)
+    _forced_wrap_parity(gpu_lib, c, [0.1], 10, spmv=9 if isinstance(spmv, str) else spmv)
+
+
+def test_sw_panel_sweep_lanczos_and_breakdown(gpu_lib, monkeypatch):
+    """The far-window pass of the panel sweep under the non-deferred step gate (f1 Lanczos: the SpMV
+    applies s_j itself; the second pass reads the gate without writing it) and through a lucky
+    breakdown (an eigenvector of S^z-conserving XXZ: |all up> stops at j = 0)."""
+    te = gpu_lib
+    monkeypatch.setenv("TE_SPMV_SW_FORCE", "1")
+    monkeypatch.setenv("TE_SPMV_SW_PANEL", "2")
+    c = configs.build(5, L=12)
+    h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
+    te.te_set_option(h, te.TE_OPT_SPMV, 9)
+    assert te.te_get_option(h, te.TE_INFO_SW_PANEL) == 2
+    te.te_set_option(h, te.TE_OPT_ORTHO, 1)
+    tol_rate = c["tol"] / c["t"]
+    g = te.te_krylov_basis(h, c["v0"], 16, tol_rate, want_V=True)
+    o = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), c["v0"], 16, tol_rate, ortho="lanczos3")
+    scale = max(1.0, np.abs(o["alpha"]).max(), np.abs(o["beta"]).max())
+    assert g["m_eff"] == o["m_eff"]
+    assert np.abs(g["alpha"] - o["alpha"]).max() <= 1e-10 * scale
+    assert np.abs(g["beta"] - o["beta"]).max() <= 1e-10 * scale
+    assert np.linalg.norm(g["V"] - o["V"]) <= 1e-8
+    for ortho in (0, 1, 2):
+        te.te_set_option(h, te.TE_OPT_ORTHO, ortho)
+        e = np.zeros(c["n"], dtype=np.complex128)
+        e[c["n"] - 1] = 1.0  # all spins up: an eigenvector
+        gb = te.te_krylov_basis(h, e, 8, tol_rate, want_V=False)
+        ob = K.arnoldi(lambda x: K.spmv(c["rowptr"], c["col"], c["val"], x), e, 8, tol_rate)
+        assert gb["m_eff"] == ob["m_eff"] == 1
+        assert abs(gb["alpha"][0] - ob["alpha"][0]) <= 1e-12 * scale
+    h.close()
 
 
 def test_distributed_api_single_rank(gpu_lib):

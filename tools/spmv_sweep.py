@@ -49,7 +49,7 @@ def main():
             print(json.dumps({"variant": var, "error": str(e)}), flush=True)
             h.close()
             continue
-        info = {k: te.te_get_option(h, getattr(te, k)) for k in ("TE_INFO_XS_GLOBAL", "TE_INFO_XS_GLOBAL_TILES", "TE_INFO_XS_X_PER_ENTRY", "TE_INFO_SW_FILL")}
+        info = {k: te.te_get_option(h, getattr(te, k)) for k in ("TE_INFO_XS_GLOBAL", "TE_INFO_XS_GLOBAL_TILES", "TE_INFO_XS_X_PER_ENTRY", "TE_INFO_SW_FILL", "TE_INFO_SW_PANEL", "TE_INFO_SW_FAR")}
         te.te_krylov_basis(h, c["v0"], a.m, 0.0, want_V=False)  # warm-up
         te.te_set_option(h, te.TE_OPT_PROFILE, 1)
         for _ in range(a.reps):
