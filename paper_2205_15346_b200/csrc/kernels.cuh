@@ -113,7 +113,6 @@ struct Launch {
   int proj_tma;         // 2: hybrid by column count (default), 1: TMA-tiled only, 3: register accumulators only
   int spmv_tiled;       // 10: column-blocked ring, 9: slot-window SELL-32, 8: staged-x ring, 7: ring, 6: SELL-32-sigma
   int prefetch;         // update_norm: L2 bulk-prefetch distance in block iterations (0: off)
-  int sw_minb;          // slot-window SpMV, 8-bit entries: resident CTAs per SM (3 or 4)
 };
 
 // hot path (one Krylov step j = 4 launches; see kernels.cu)

@@ -317,9 +317,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmv_sw(KDev d, int j) {
 // (slice pointers -> first entry codes).  The prologue is therefore pipelined across slices: the
 // slice pointers of the warp's next slice are loaded when the current slice starts, and its first
 // group of codes and window bases while the current slice's last group of x loads is in flight.
-// MINB: resident CTAs per SM (3: 85 registers, 4: 64).
-template <bool CPLX, bool PB = false, int MINB = 3>
-__global__ void __launch_bounds__(kThreads, MINB) k_spmv_sw8(KDev d, int j) {
+// 3 CTAs per SM (79 registers); a 64-register build at 4 CTAs per SM spills and measured 3.6 ms.
+template <bool CPLX, bool PB = false>
+__global__ void __launch_bounds__(kThreads, 3) k_spmv_sw8(KDev d, int j) {
   using VT = typename ValT<CPLX>::T;
   __shared__ __align__(16) VT dict_s[8];
   __shared__ double sj_s;
@@ -417,12 +417,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmv_sw8(KDev d, int j) {
   }
 }
 
-template <bool CPLX, bool PB = false, int MINB = 3>
+template <bool CPLX, bool PB = false>
 static int sw8_grid(const Launch& L, int64_t nsl) {
   static int per_sm = 0;
   if (per_sm == 0) {
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmv_sw8<CPLX, PB, MINB>, kThreads, 0) != cudaSuccess || b < 1) b = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_spmv_sw8<CPLX, PB>, kThreads, 0) != cudaSuccess || b < 1) b = 1;
     per_sm = b;
   }
   return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)L.grid_spmv * per_sm, (nsl + kWarps - 1) / kWarps));
@@ -447,11 +447,7 @@ static int sw_grid(const Launch& L, int64_t nsl) {
 // 40-register builds at 6 CTAs per SM, x loads without L1 allocation, two-deep x pipelining and L2
 // prefetch of the next slice's codes all within +-0.3 %.
 void launch_spmv_sw(const KDev& d, bool cplx, int j, const Launch& L) {
-#define TE_SW8(C, P)                                                                                          \
-  do {                                                                                                        \
-    if (L.sw_minb == 4) k_spmv_sw8<C, P, 4><<<sw8_grid<C, P, 4>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j); \
-    else k_spmv_sw8<C, P, 3><<<sw8_grid<C, P, 3>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j);              \
-  } while (0)
+#define TE_SW8(C, P) k_spmv_sw8<C, P><<<sw8_grid<C, P>(L, d.sw_nslice), kThreads, 0, L.stream>>>(d, j)
   if (d.sw_pass == 2) {  // far-window pass of the panel sweep: W += ..., permuted slice order
     if (d.sw_bits == 8) {
       if (cplx) TE_SW8(true, true);

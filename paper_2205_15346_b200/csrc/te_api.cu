@@ -156,7 +156,6 @@ struct te_handle {
   int32_t* d_swb_base = nullptr;
   uint16_t* d_swb_ent = nullptr;
   int64_t swb_slots = 0;
-  int sw_minb = 3;  // 8-bit kernel: resident CTAs per SM
   int sw_ka = 0, sw_sb = 0, sw_lo = 0, sw_ob = 0;  // panel slice bits (0: single pass), slice bits, outer range
   double sw_fill = 0.0;  // slot entries (32 per slot) / off-diagonal entries
   // column-blocked copy of H for the ring (variant 10): one CSR + ring tile table per cb_cols
@@ -336,7 +335,6 @@ Launch make_launch(te_handle* h) {
   L.ring_stages = h->ring_stages;
   L.spmv_tiled = h->spmv_tiled;
   L.prefetch = h->prefetch;
-  L.sw_minb = h->sw_minb;
   return L;
 }
 
@@ -1300,8 +1298,6 @@ int plan_sw(te_handle* h) {
   h->sw_slots = slots;
   h->sw_ndict = nd;
   h->sw_bits = b8 ? 8 : 16;
-  h->sw_minb = 3;
-  if (const char* e = getenv("TE_SPMV_SW_MINB")) h->sw_minb = atoi(e) == 4 ? 4 : 3;
   return TE_OK;
 }
 

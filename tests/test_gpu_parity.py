@@ -184,7 +184,7 @@ SW_CASES = [("xxz_L12", configs.build(2, L=12)), ("xxznnn_L12", configs.build(5,
 
 
 @pytest.mark.parametrize("panel", [0, 1, 3, 4])
-@pytest.mark.parametrize("bits", [8, 16, "8-minb4"])
+@pytest.mark.parametrize("bits", [8, 16])
 @pytest.mark.parametrize("name,c", SW_CASES, ids=[x[0] for x in SW_CASES])
 def test_spmv_sw_variants(gpu_lib, name, c, bits, panel, monkeypatch):
     """Slot-window SELL-32 SpMV (TE_OPT_SPMV = 9) vs the oracle's Arnoldi basis: spin chains (real
@@ -195,8 +195,7 @@ def test_spmv_sw_variants(gpu_lib, name, c, bits, panel, monkeypatch):
     2^panel slices: near windows in row order, far windows added in the permuted slice order)."""
     te = gpu_lib
     monkeypatch.setenv("TE_SPMV_SW_FORCE", "1")  # small chains: more slices straddle the window edges
-    monkeypatch.setenv("TE_SPMV_SW_BITS", str(bits)[:2].rstrip("-"))  # 8-bit entries apply to dictionaries of <= 7 values
-    monkeypatch.setenv("TE_SPMV_SW_MINB", "4" if bits == "8-minb4" else "3")  # 64-register build of the 8-bit kernel
+    monkeypatch.setenv("TE_SPMV_SW_BITS", str(bits))  # 8-bit entries apply to dictionaries of <= 7 values
     monkeypatch.setenv("TE_SPMV_SW_PANEL", str(panel))
     h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
     te.te_set_option(h, te.TE_OPT_SPMV, 9)
@@ -705,7 +704,7 @@ def test_forced_parity_complex_ring_wraps_config4_n2e20(gpu_lib, spmv, monkeypat
     _forced_wrap_parity(gpu_lib, c, [0.05, 0.05], 8, spmv=spmv)
 
 
-@pytest.mark.parametrize("spmv", [7, 8, 9, "9-panel", "9-minb4"])
+@pytest.mark.parametrize("spmv", [7, 8, 9, "9-panel"])
 def test_forced_parity_config5_instantiation_L22(gpu_lib, spmv, monkeypatch):
     """Config 5's model at L = 22 (n = 4,194,304, 23 entries per row on average: the TPR 2 /
     3-stage real ring instantiation of the full L = 26 config; spmv 9: the slot-window SELL-32 that
@@ -713,7 +712,6 @@ def test_forced_parity_config5_instantiation_L22(gpu_lib, spmv, monkeypatch):
     panel sweep with 6 outer slice bits as at L = 26 — panels of 2^11 slices here, 2^15 there), m = 10,
     one forced restart, element by element against the oracle."""
     monkeypatch.setenv("TE_SPMV_SW_PANEL", "11" if spmv == "9-panel" else "0")
-    monkeypatch.setenv("TE_SPMV_SW_MINB", "4" if spmv == "9-minb4" else "3")  # 64-register build, 4 CTAs per SM
     c = configs.build(5, L=22)
     _forced_wrap_parity(gpu_lib, c, [0.1], 10, spmv=9 if isinstance(spmv, str) else spmv)
 
