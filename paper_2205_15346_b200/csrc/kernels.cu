@@ -13,6 +13,7 @@
 
 #include <cuda.h>
 #include <cstdio>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -35,6 +36,8 @@ namespace te {
 // sub-tiles per TMA tile: at least kProjMinTile bytes per tile (fewer, larger TMA operations;
 // a 128-row box is the largest single load).  Measured: tools/micro/mb_proj.cu.
 size_t g_proj_min_tile = 16384;
+int g_proj_grp = 0;      // experiment: column groups behind uniform branches in the dots loop (TE_PROJ_GRP = 4 / 8)
+int g_proj_const_r = 1;  // compile-time sub-tile count for the default tilings (TE_PROJ_CONST_R=0: runtime R)
 int proj_rsub(int ncols) {
   int r = 1;
   while (r < 4 && (size_t)(ncols + 1) * kTileR * 16 * r < g_proj_min_tile) r <<= 1;
@@ -159,9 +162,14 @@ __device__ __forceinline__ double2 colsum_reg(double (&re)[NREG], double (&im)[N
 // NREG: columns whose per-lane partial sums persist in registers across tiles (32 or 16; the
 // rest go through 16-wide butterflies per sub-tile).  MINB: resident CTAs per SM (the slot ring
 // shares the shared-memory budget between them).
-template <int MODE, int NREG = 32, int MINB = 1>
+// RT: the sub-tile count R as a compile-time constant (0: the runtime argument).  With a constant
+// tile stride the column loads of a lane become one base register plus immediate offsets; the
+// runtime-R build spends 3 of its ~9 instructions per column on address arithmetic (SASS: LDC R,
+// IMAD, IMAD.WIDE per LD.E.128), and the consumers are issue/latency-bound (8 warps per SM).
+template <int MODE, int NREG = 32, int MINB = 1, int RT = 0, int GRP = 0>
 __global__ void __launch_bounds__(kProjThreads, MINB)
-    k_proj_tma(const __grid_constant__ CUtensorMap tmV, KDev d, int j, int S, int R, int C, int write) {
+    k_proj_tma(const __grid_constant__ CUtensorMap tmV, KDev d, int j, int S, int R_arg, int C, int write) {
+  const int R = RT > 0 ? RT : R_arg;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kMaxSlots], empty[kMaxSlots];
   __shared__ double2 coef[kMaxCols];
@@ -278,6 +286,7 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
         const double2* Ws = reinterpret_cast<const double2*>(smem + (size_t)s * slot_bytes + vbytes);
         const int64_t r0 = tile * TR;
         const int rows = (int)min((int64_t)TR, n - r0);
+#pragma unroll 1
         for (int sub = 0; sub < R && MODE != 2; ++sub) {  // MODE 2: streaming only (microbenchmark)
           const int row = sub * kTileR + lane;
           if (sub * kTileR >= rows) break;  // warp-uniform
@@ -317,12 +326,30 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
               nrm = fma(p.x, p.x, fma(p.y, p.y, nrm));
             }
           }
+          // GRP > 0: columns in groups of GRP behind a warp-uniform branch: the groups at and above
+          // ncols are skipped instead of issued predicated-off (22 columns with NREG = 32: 8 of 32)
+          if constexpr (GRP > 0) {
 #pragma unroll
-          for (int c = 0; c < NREG; ++c) {
-            if (c < ncols) {
-              const double2 v = Vs[c * TR + row];
-              aR[c] = fma(v.x, p.x, fma(v.y, p.y, aR[c]));   // conj(v) * p
-              aI[c] = fma(v.x, p.y, fma(-v.y, p.x, aI[c]));
+            for (int c4 = 0; c4 < NREG; c4 += GRP) {
+              if (c4 < ncols) {
+#pragma unroll
+                for (int c = c4; c < c4 + GRP; ++c) {
+                  if (c < ncols) {
+                    const double2 v = Vs[c * TR + row];
+                    aR[c] = fma(v.x, p.x, fma(v.y, p.y, aR[c]));   // conj(v) * p
+                    aI[c] = fma(v.x, p.y, fma(-v.y, p.x, aI[c]));
+                  }
+                }
+              }
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < NREG; ++c) {
+              if (c < ncols) {
+                const double2 v = Vs[c * TR + row];
+                aR[c] = fma(v.x, p.x, fma(v.y, p.y, aR[c]));   // conj(v) * p
+                aI[c] = fma(v.x, p.y, fma(-v.y, p.x, aI[c]));
+              }
             }
           }
 #pragma unroll 1
@@ -873,6 +900,20 @@ cudaError_t configure_kernels() {
   set((const void*)k_proj_tma<1, 16>, kProjSmemBudget + 1024);
   configure_spmv_kernels(set_attr, &st);
   set((const void*)k_proj_tma<1>, kProjSmemBudget + 1024);
+#define TE_SET_RT(NREG, RT)                                                    \
+  set((const void*)k_proj_tma<0, NREG, 1, RT>, kProjSmemBudget + 1024);        \
+  set((const void*)k_proj_tma<1, NREG, 1, RT>, kProjSmemBudget + 1024);        \
+  set((const void*)k_proj_tma<3, NREG, 1, RT>, kProjSmemBudget + 1024);        \
+  set((const void*)k_proj_tma<0, NREG, 1, RT, 4>, kProjSmemBudget + 1024);     \
+  set((const void*)k_proj_tma<1, NREG, 1, RT, 4>, kProjSmemBudget + 1024);     \
+  set((const void*)k_proj_tma<3, NREG, 1, RT, 4>, kProjSmemBudget + 1024);     \
+  set((const void*)k_proj_tma<0, NREG, 1, RT, 8>, kProjSmemBudget + 1024);     \
+  set((const void*)k_proj_tma<1, NREG, 1, RT, 8>, kProjSmemBudget + 1024);     \
+  set((const void*)k_proj_tma<3, NREG, 1, RT, 8>, kProjSmemBudget + 1024);
+  TE_SET_RT(16, 4) TE_SET_RT(16, 2) TE_SET_RT(32, 2) TE_SET_RT(32, 1)
+#undef TE_SET_RT
+  if (const char* e = getenv("TE_PROJ_CONST_R")) g_proj_const_r = atoi(e) != 0;
+  if (const char* e = getenv("TE_PROJ_GRP")) g_proj_grp = atoi(e);
   status = st.err;
   return status;
 }
@@ -884,11 +925,30 @@ cudaError_t configure_kernels() {
 // covers ncols (fewer live registers at small ncols: 8 columns, update 3.7 -> 4.7 TB/s)
 constexpr int kRegMaxCols = 8;
 
-#define TE_PROJ_TMA(MODE, ncols, ...)                                                                   \
-  do {                                                                                                  \
-    if ((ncols) <= 8) k_proj_tma<MODE, 8><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__);      \
-    else if ((ncols) <= 16) k_proj_tma<MODE, 16><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__); \
-    else k_proj_tma<MODE, 32><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__);                   \
+// (NREG, R) pairs of the default tiling get compile-time R: 9-14 columns (16, 4), 15-16 (16, 2),
+// 17-30 (32, 2), 31-64 (32, 1); anything else (forced TMA below 9 columns, other g_proj_min_tile)
+// runs the runtime-R build
+#define TE_PROJ_TMA_L(MODE, NREG, RT, ncols, ...)                                                                       \
+  do {                                                                                                                  \
+    if (RT > 0 && g_proj_grp == 4)                                                                                      \
+      k_proj_tma<MODE, NREG, 1, RT, (RT > 0 ? 4 : 0)><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__); \
+    else if (RT > 0 && g_proj_grp == 8)                                                                                 \
+      k_proj_tma<MODE, NREG, 1, RT, (RT > 0 ? 8 : 0)><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__); \
+    else k_proj_tma<MODE, NREG, 1, RT><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__);     \
+  } while (0)
+#define TE_PROJ_TMA(MODE, ncols, ...)                                                       \
+  do {                                                                                      \
+    const int rsub_ = g_proj_const_r ? proj_rsub(ncols) : 0;                                \
+    if ((ncols) <= 8) TE_PROJ_TMA_L(MODE, 8, 0, ncols, __VA_ARGS__);                        \
+    else if ((ncols) <= 16) {                                                               \
+      if (rsub_ == 4) TE_PROJ_TMA_L(MODE, 16, 4, ncols, __VA_ARGS__);                       \
+      else if (rsub_ == 2) TE_PROJ_TMA_L(MODE, 16, 2, ncols, __VA_ARGS__);                  \
+      else TE_PROJ_TMA_L(MODE, 16, 0, ncols, __VA_ARGS__);                                  \
+    } else {                                                                                \
+      if (rsub_ == 2) TE_PROJ_TMA_L(MODE, 32, 2, ncols, __VA_ARGS__);                       \
+      else if (rsub_ == 1) TE_PROJ_TMA_L(MODE, 32, 1, ncols, __VA_ARGS__);                  \
+      else TE_PROJ_TMA_L(MODE, 32, 0, ncols, __VA_ARGS__);                                  \
+    }                                                                                       \
   } while (0)
 
 // register-accumulator kernel: CPL = 4 columns per lane, TPR = the smallest power of two with

@@ -3,7 +3,8 @@ staged-x, ring, SELL-sigma), projection kernel set and
 orthogonalisation mode, for compute-sanitizer (memcheck / racecheck / synccheck;
 tools/sanitize.sh).  Sizes span several tiles per CTA: the staged-x SpMV runs with small tiles
 (TE_SPMV_XS_ECAP=256) so its mbarrier ring wraps; the column-blocked ring with 1 KB column blocks;
-the slot-window format with the padding check overridden (small chains)."""
+the slot-window format with the padding check overridden (small chains), as one pass and as the
+two-pass panel sweep (panels of 4 slices)."""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -15,9 +16,12 @@ from workloads import configs  # noqa: E402
 
 cases = [configs.build(2, L=12), configs.build(3, L=6, N=6), configs.build(1, n=1000), configs.build(5, L=11)]
 # (kernel set, SpMV, ortho)
-runs = [(2, 9, 0), (2, 10, 0), (2, 8, 0), (2, 7, 0), (2, 6, 0), (3, 7, 0), (5, 7, 0), (2, 8, 2), (2, 8, 1)]
+runs = [(2, 9, 0), (2, "9-panel", 0), (2, "9-panel", 1), (2, 10, 0), (2, 8, 0), (2, 7, 0), (2, 6, 0), (3, 7, 0), (5, 7, 0),
+        (2, 8, 2), (2, 8, 1)]
 for c in cases:
     for kset, spmv, ortho in runs:
+        os.environ["TE_SPMV_SW_PANEL"] = "2" if spmv == "9-panel" else "0"
+        spmv = 9 if spmv == "9-panel" else spmv
         h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
         te.te_set_option(h, te.TE_OPT_KERNELS, kset)
         try:
