@@ -178,7 +178,12 @@ enum {
                                 the off-diagonal values take <= 255 distinct values and the slot
                                 entries are <= 2.0x (8-bit) / 1.6x (16-bit) the off-diagonal
                                 entries (spin chains); then
-                                the default.  TE_ERR_ARG when selected and not applicable;
+                                the default.  TE_ERR_ARG when selected and not applicable.
+                                env TE_SPMV_SW_PANEL=k (read when the format is built): two
+                                launches per SpMV - windows inside the slice's aligned panel of
+                                2^k slices in row order, then the far windows added into W in
+                                a permuted slice order (halves the DRAM traffic when x exceeds
+                                L2; same time on one B200, so not the default);
                                 8 staged-x ring: the ring below, and each tile's x windows (column
                                 ranges planned on the device at create: >= 2 distinct columns at
                                 >= 1/4 density) bulk-copied into shared memory too; entries are

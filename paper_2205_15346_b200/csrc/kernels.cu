@@ -36,8 +36,6 @@ namespace te {
 // sub-tiles per TMA tile: at least kProjMinTile bytes per tile (fewer, larger TMA operations;
 // a 128-row box is the largest single load).  Measured: tools/micro/mb_proj.cu.
 size_t g_proj_min_tile = 16384;
-int g_proj_grp = 0;      // experiment: column groups behind uniform branches in the dots loop (TE_PROJ_GRP = 4 / 8)
-int g_proj_const_r = 1;  // compile-time sub-tile count for the default tilings (TE_PROJ_CONST_R=0: runtime R)
 int proj_rsub(int ncols) {
   int r = 1;
   while (r < 4 && (size_t)(ncols + 1) * kTileR * 16 * r < g_proj_min_tile) r <<= 1;
@@ -166,7 +164,7 @@ __device__ __forceinline__ double2 colsum_reg(double (&re)[NREG], double (&im)[N
 // tile stride the column loads of a lane become one base register plus immediate offsets; the
 // runtime-R build spends 3 of its ~9 instructions per column on address arithmetic (SASS: LDC R,
 // IMAD, IMAD.WIDE per LD.E.128), and the consumers are issue/latency-bound (8 warps per SM).
-template <int MODE, int NREG = 32, int MINB = 1, int RT = 0, int GRP = 0>
+template <int MODE, int NREG = 32, int MINB = 1, int RT = 0>
 __global__ void __launch_bounds__(kProjThreads, MINB)
     k_proj_tma(const __grid_constant__ CUtensorMap tmV, KDev d, int j, int S, int R_arg, int C, int write) {
   const int R = RT > 0 ? RT : R_arg;
@@ -326,30 +324,12 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
               nrm = fma(p.x, p.x, fma(p.y, p.y, nrm));
             }
           }
-          // GRP > 0: columns in groups of GRP behind a warp-uniform branch: the groups at and above
-          // ncols are skipped instead of issued predicated-off (22 columns with NREG = 32: 8 of 32)
-          if constexpr (GRP > 0) {
 #pragma unroll
-            for (int c4 = 0; c4 < NREG; c4 += GRP) {
-              if (c4 < ncols) {
-#pragma unroll
-                for (int c = c4; c < c4 + GRP; ++c) {
-                  if (c < ncols) {
-                    const double2 v = Vs[c * TR + row];
-                    aR[c] = fma(v.x, p.x, fma(v.y, p.y, aR[c]));   // conj(v) * p
-                    aI[c] = fma(v.x, p.y, fma(-v.y, p.x, aI[c]));
-                  }
-                }
-              }
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < NREG; ++c) {
-              if (c < ncols) {
-                const double2 v = Vs[c * TR + row];
-                aR[c] = fma(v.x, p.x, fma(v.y, p.y, aR[c]));   // conj(v) * p
-                aI[c] = fma(v.x, p.y, fma(-v.y, p.x, aI[c]));
-              }
+          for (int c = 0; c < NREG; ++c) {
+            if (c < ncols) {
+              const double2 v = Vs[c * TR + row];
+              aR[c] = fma(v.x, p.x, fma(v.y, p.y, aR[c]));   // conj(v) * p
+              aI[c] = fma(v.x, p.y, fma(-v.y, p.x, aI[c]));
             }
           }
 #pragma unroll 1
@@ -903,17 +883,9 @@ cudaError_t configure_kernels() {
 #define TE_SET_RT(NREG, RT)                                                    \
   set((const void*)k_proj_tma<0, NREG, 1, RT>, kProjSmemBudget + 1024);        \
   set((const void*)k_proj_tma<1, NREG, 1, RT>, kProjSmemBudget + 1024);        \
-  set((const void*)k_proj_tma<3, NREG, 1, RT>, kProjSmemBudget + 1024);        \
-  set((const void*)k_proj_tma<0, NREG, 1, RT, 4>, kProjSmemBudget + 1024);     \
-  set((const void*)k_proj_tma<1, NREG, 1, RT, 4>, kProjSmemBudget + 1024);     \
-  set((const void*)k_proj_tma<3, NREG, 1, RT, 4>, kProjSmemBudget + 1024);     \
-  set((const void*)k_proj_tma<0, NREG, 1, RT, 8>, kProjSmemBudget + 1024);     \
-  set((const void*)k_proj_tma<1, NREG, 1, RT, 8>, kProjSmemBudget + 1024);     \
-  set((const void*)k_proj_tma<3, NREG, 1, RT, 8>, kProjSmemBudget + 1024);
+  set((const void*)k_proj_tma<3, NREG, 1, RT>, kProjSmemBudget + 1024);
   TE_SET_RT(16, 4) TE_SET_RT(16, 2) TE_SET_RT(32, 2) TE_SET_RT(32, 1)
 #undef TE_SET_RT
-  if (const char* e = getenv("TE_PROJ_CONST_R")) g_proj_const_r = atoi(e) != 0;
-  if (const char* e = getenv("TE_PROJ_GRP")) g_proj_grp = atoi(e);
   status = st.err;
   return status;
 }
@@ -928,17 +900,11 @@ constexpr int kRegMaxCols = 8;
 // (NREG, R) pairs of the default tiling get compile-time R: 9-14 columns (16, 4), 15-16 (16, 2),
 // 17-30 (32, 2), 31-64 (32, 1); anything else (forced TMA below 9 columns, other g_proj_min_tile)
 // runs the runtime-R build
-#define TE_PROJ_TMA_L(MODE, NREG, RT, ncols, ...)                                                                       \
-  do {                                                                                                                  \
-    if (RT > 0 && g_proj_grp == 4)                                                                                      \
-      k_proj_tma<MODE, NREG, 1, RT, (RT > 0 ? 4 : 0)><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__); \
-    else if (RT > 0 && g_proj_grp == 8)                                                                                 \
-      k_proj_tma<MODE, NREG, 1, RT, (RT > 0 ? 8 : 0)><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__); \
-    else k_proj_tma<MODE, NREG, 1, RT><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__);     \
-  } while (0)
+#define TE_PROJ_TMA_L(MODE, NREG, RT, ncols, ...) \
+  k_proj_tma<MODE, NREG, 1, RT><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(__VA_ARGS__)
 #define TE_PROJ_TMA(MODE, ncols, ...)                                                       \
   do {                                                                                      \
-    const int rsub_ = g_proj_const_r ? proj_rsub(ncols) : 0;                                \
+    const int rsub_ = L.proj_const_r ? proj_rsub(ncols) : 0;                                \
     if ((ncols) <= 8) TE_PROJ_TMA_L(MODE, 8, 0, ncols, __VA_ARGS__);                        \
     else if ((ncols) <= 16) {                                                               \
       if (rsub_ == 4) TE_PROJ_TMA_L(MODE, 16, 4, ncols, __VA_ARGS__);                       \

@@ -180,6 +180,7 @@ struct te_handle {
   int64_t nslices = 0;
   std::vector<CUtensorMap> tmaps;
   int prefetch = 0;
+  int proj_const_r = 1;  // TE_PROJ_CONST_R=0 (read at create): the runtime-R build of the TMA projection kernels
   cudaEvent_t ev0[kEvPool], ev1[kEvPool];
   int ev_cls[kEvPool];
   double ev_bytes[kEvPool];
@@ -335,6 +336,7 @@ Launch make_launch(te_handle* h) {
   L.ring_stages = h->ring_stages;
   L.spmv_tiled = h->spmv_tiled;
   L.prefetch = h->prefetch;
+  L.proj_const_r = h->proj_const_r;
   return L;
 }
 
@@ -1438,6 +1440,7 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     h->spmv_ring_tpr = t;
     h->spmv_nf_wide = !cplx && avg <= 16.0 * t;
     if (const char* e = getenv("TE_SPMV_NF_WIDE")) h->spmv_nf_wide = atoi(e) != 0;
+    if (const char* e = getenv("TE_PROJ_CONST_R")) h->proj_const_r = atoi(e) != 0;
     if (const char* e = getenv("TE_SPMV_FORCE_HALO")) h->spmv_force_halo = atoi(e) != 0;
   }
   {  // warp-specialised ring SpMV (variant 7, default) tiles: <= kSpmvTileNnz(C) entries and
