@@ -192,6 +192,17 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
     const double2 g = d.g1[tid];
     coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);   // e1'_k = s_k^2 g1_k
   }
+  if (MODE == 4) {  // K3 on the TMA ring: p'' = p' - V e2' (e2'_k = s_k^2 g2_k) -> column j + 1, ||p''||^2
+    if (tid < ncols) {
+      const double sk = d.s[tid];
+      const double2 g = d.g2[tid];
+      coef[tid] = make_double2(sk * sk * g.x, sk * sk * g.y);
+    }
+    if (tid == 0 && blockIdx.x == 0 && sj != 0.0) {  // alpha_j = Re(c1_j + c2_j) (reading C2)
+      const double s_j = d.s[j];
+      d.alpha[j] = s_j * (s_j * d.g1[j].x + d.g2[j].x);
+    }
+  }
   if (MODE == 3) {  // f2: c1' = s g1, c2' = c1' - G c1', coefficient on raw V_k: s_k (c1'_k + c2'_k)
     if (tid < ncols) {
       const double sk = tid == j ? sj : d.s[tid];
@@ -272,7 +283,7 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
     // 16-wide butterfly groups above NREG (<= 4): lane l & 15 owns column NREG + 16 g + (l & 15)
     double2 accb0 = make_double2(0.0, 0.0), accb1 = accb0, accb2 = accb0, accb3 = accb0;
     double nrm = 0.0;
-    double2* outV = (MODE == 3 && write) ? d.V + (int64_t)(j + 1) * d.ldv : nullptr;
+    double2* outV = ((MODE == 3 || MODE == 4) && write) ? d.V + (int64_t)(j + 1) * d.ldv : nullptr;
     bool more = true;
     for (int64_t base = 0; more; base += S) {
       for (int s = warp; s < S; s += C) {
@@ -289,7 +300,7 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
           const int row = sub * kTileR + lane;
           if (sub * kTileR >= rows) break;  // warp-uniform
           double2 p = row < rows ? Ws[row] : make_double2(0.0, 0.0);
-          if (MODE == 1 || MODE == 3) {
+          if (MODE == 1 || MODE == 3 || MODE == 4) {
             // eight independent FMA chains over the columns, 8 tile loads in flight
             double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0, a4 = a0, a5 = a0, a6 = a0, a7 = a0;
             int k = 0;
@@ -324,6 +335,7 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
               nrm = fma(p.x, p.x, fma(p.y, p.y, nrm));
             }
           }
+          if constexpr (MODE == 4) continue;  // no dots in the update + norm pass
 #pragma unroll
           for (int c = 0; c < NREG; ++c) {
             if (c < ncols) {
@@ -354,15 +366,17 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
         if (lane == 0) mbar_arrive(&empty[s]);
       }
     }
-    const double2 acc0 = colsum_reg<NREG>(aR, aI);
-    if (lane < NREG) red[warp][lane] = acc0;
-    if (lane < 16) {
-      const double2 ab[4] = {accb0, accb1, accb2, accb3};
+    if constexpr (MODE != 4) {
+      const double2 acc0 = colsum_reg<NREG>(aR, aI);
+      if (lane < NREG) red[warp][lane] = acc0;
+      if (lane < 16) {
+        const double2 ab[4] = {accb0, accb1, accb2, accb3};
 #pragma unroll
-      for (int g = 0; g < 4; ++g)
-        if (NREG + 16 * g + lane < kMaxCols) red[warp][NREG + 16 * g + lane] = ab[g];
+        for (int g = 0; g < 4; ++g)
+          if (NREG + 16 * g + lane < kMaxCols) red[warp][NREG + 16 * g + lane] = ab[g];
+      }
     }
-    if (MODE == 3) {
+    if (MODE == 3 || MODE == 4) {
       nrm = warp_sum(nrm);
       if (lane == 0) nrm_s[warp] = nrm;
     }
@@ -370,13 +384,13 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
   __syncthreads();
   // block partial in fixed warp order, then the last-CTA reduction
   double2* out = MODE == 0 ? d.g1 : d.g2;
-  const int ctr = MODE == 0 ? 0 : 1;
-  if (tid < ncols) {
+  const int ctr = MODE == 0 ? 0 : (MODE == 4 ? 2 : 1);
+  if (MODE != 4 && tid < ncols) {
     double2 t = red[0][tid];
     for (int w = 1; w < C; ++w) t = cadd(t, red[w][tid]);
     d.part[(size_t)blockIdx.x * kMaxCols + tid] = t;
   }
-  if (MODE == 3 && tid == 0) {
+  if ((MODE == 3 || MODE == 4) && tid == 0) {
     double t = 0.0;
     for (int w = 0; w < C; ++w) t += nrm_s[w];
     d.partn[blockIdx.x] = t;
@@ -391,7 +405,7 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
   __shared__ double2 seg[4][kMaxCols];
   const int G = gridDim.x;
   const int per = (G + 3) / 4;
-  {
+  if (MODE != 4) {
     const int c = tid & (kMaxCols - 1), sgi = tid >> 6;
     double2 sm = make_double2(0.0, 0.0);
     if (c < ncols) {
@@ -401,14 +415,14 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
     seg[sgi][c] = sm;
   }
   __syncthreads();
-  if (tid < ncols) {
+  if (MODE != 4 && tid < ncols) {
     double2 t = seg[0][tid];
     t = cadd(t, seg[1][tid]);
     t = cadd(t, seg[2][tid]);
     t = cadd(t, seg[3][tid]);
     out[tid] = t;
   }
-  if (MODE == 3 && tid == 0) {  // ||p''||^2 in fixed block order
+  if ((MODE == 3 || MODE == 4) && tid == 0) {  // ||p''||^2 in fixed block order
     double t = 0.0;
     for (int b = 0; b < G; ++b) t += __ldcg(d.partn + b);
     d.nrm2[j] = t;
@@ -886,6 +900,10 @@ cudaError_t configure_kernels() {
   set((const void*)k_proj_tma<3, NREG, 1, RT>, kProjSmemBudget + 1024);
   TE_SET_RT(16, 4) TE_SET_RT(16, 2) TE_SET_RT(32, 2) TE_SET_RT(32, 1)
 #undef TE_SET_RT
+  set((const void*)k_proj_tma<4, 8, 1, 0>, kProjSmemBudget + 1024);
+  set((const void*)k_proj_tma<4, 8, 1, 1>, kProjSmemBudget + 1024);
+  set((const void*)k_proj_tma<4, 8, 1, 2>, kProjSmemBudget + 1024);
+  set((const void*)k_proj_tma<4, 8, 1, 4>, kProjSmemBudget + 1024);
   status = st.err;
   return status;
 }
@@ -972,7 +990,23 @@ void launch_update_proj(const KDev& d, int j, const Launch& L) {
   TE_PROJ_TMA(1, j + 1, L.tmaps[j], d, j, S, R, C, 0);
 }
 
+// K3: above 8 columns the update + norm pass runs on the TMA ring too (k_proj_tma<4>: the ring reads
+// V at 7.1 TB/s where plain register streaming reaches 6.5; tools/micro/mb_proj.cu), else the
+// register-streaming kernel
 void launch_update_norm(const KDev& d, int j, bool write, const Launch& L) {
+  const int ncols = j + 1;
+  if (L.norm_tma && !use_reg(L, ncols)) {
+    const int S = proj_slots(ncols), R = proj_rsub(ncols), C = proj_consumers(ncols);
+    const int rt = L.proj_const_r ? R : 0;
+#define TE_NORM_TMA(RT) \
+  k_proj_tma<4, 8, 1, RT><<<L.num_sms, kProjThreads, proj_smem_bytes(ncols), L.stream>>>(L.tmaps[j], d, j, S, R, C, write ? 1 : 0)
+    if (rt == 1) TE_NORM_TMA(1);
+    else if (rt == 2) TE_NORM_TMA(2);
+    else if (rt == 4) TE_NORM_TMA(4);
+    else TE_NORM_TMA(0);
+#undef TE_NORM_TMA
+    return;
+  }
   k_update_norm<<<L.grid_k3, kThreads, 0, L.stream>>>(d, j, write ? 1 : 0, L.prefetch);
 }
 

@@ -113,6 +113,7 @@ struct Launch {
   int proj_tma;         // 2: hybrid by column count (default), 1: TMA-tiled only, 3: register accumulators only
   int spmv_tiled;       // 10: column-blocked ring, 9: slot-window SELL-32, 8: staged-x ring, 7: ring, 6: SELL-32-sigma
   int prefetch;         // update_norm: L2 bulk-prefetch distance in block iterations (0: off)
+  int norm_tma;         // K3 (update + norm) above 8 columns: 1 on the TMA ring (k_proj_tma<4>), 0 k_update_norm
   int proj_const_r;     // TMA projection kernels: 1 (default) the builds with a compile-time sub-tile count, 0 the runtime-R build
 };
 

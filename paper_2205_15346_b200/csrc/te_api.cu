@@ -180,6 +180,7 @@ struct te_handle {
   int64_t nslices = 0;
   std::vector<CUtensorMap> tmaps;
   int prefetch = 0;
+  int norm_tma = 0;      // K3 above 8 columns on the TMA ring (default from 2^22 rows; TE_NORM_TMA read at create)
   int proj_const_r = 1;  // TE_PROJ_CONST_R=0 (read at create): the runtime-R build of the TMA projection kernels
   cudaEvent_t ev0[kEvPool], ev1[kEvPool];
   int ev_cls[kEvPool];
@@ -337,6 +338,7 @@ Launch make_launch(te_handle* h) {
   L.spmv_tiled = h->spmv_tiled;
   L.prefetch = h->prefetch;
   L.proj_const_r = h->proj_const_r;
+  L.norm_tma = h->norm_tma;
   return L;
 }
 
@@ -1441,6 +1443,10 @@ te_handle* create_common(int64_t n, const int64_t* rowptr, const int32_t* col, c
     h->spmv_nf_wide = !cplx && avg <= 16.0 * t;
     if (const char* e = getenv("TE_SPMV_NF_WIDE")) h->spmv_nf_wide = atoi(e) != 0;
     if (const char* e = getenv("TE_PROJ_CONST_R")) h->proj_const_r = atoi(e) != 0;
+    // K3 on the TMA ring from 2^22 rows: config 5 (2^26) 6.10 -> 6.79 TB/s, config 4 (2^24) 6.19 -> 6.69;
+    // below, the ring's fill and drain cost more than it gains (config 2, 2^20 rows: 6.16 -> 5.50)
+    h->norm_tma = n >= (int64_t(1) << 22);
+    if (const char* e = getenv("TE_NORM_TMA")) h->norm_tma = atoi(e) != 0;
     if (const char* e = getenv("TE_SPMV_FORCE_HALO")) h->spmv_force_halo = atoi(e) != 0;
   }
   {  // warp-specialised ring SpMV (variant 7, default) tiles: <= kSpmvTileNnz(C) entries and

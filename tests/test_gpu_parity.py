@@ -366,16 +366,19 @@ def test_dense_exponential_and_bound(gpu_lib):
 
 
 @pytest.mark.parametrize("kset,ortho", [((2, 7), 0), ((3, 7), 0), ((5, 7), 0), ((2, 6), 0), ((2, 7), 2), ((2, 7), 1),
-                                        ((3, 7, "runtime-R"), 0), ((3, 7, "runtime-R"), 2)],
+                                        ((3, 7, "runtime-R"), 0), ((3, 7, "runtime-R"), 2), ((2, 7, "norm-tma"), 0),
+                                        ((3, 7, "norm-tma-runtime-R"), 0)],
                          ids=["hybrid-ring", "tma", "regacc", "hybrid-sell", "cgs2gram", "lanczos3", "tma-runtimeR",
-                              "cgs2gram-runtimeR"])
+                              "cgs2gram-runtimeR", "norm-tma", "norm-tma-runtimeR"])
 def test_maximum_krylov_dimension(gpu_lib, kset, ortho, monkeypatch):
     """m = TE_M_MAX = 64: every column group of the projection kernels (register partials and the
     16-wide butterflies up to column 63, the 64 x 64 Gram matrix of f2; the TMA kernels' builds with
     a compile-time sub-tile count for 9-14 / 15-16 / 17-30 / 31-64 columns, and their runtime-R
     fallback) against the oracle; one adaptive evolution at m = 64; m = 65 is rejected."""
     te = gpu_lib
-    monkeypatch.setenv("TE_PROJ_CONST_R", "0" if len(kset) > 2 else "1")
+    monkeypatch.setenv("TE_PROJ_CONST_R", "0" if len(kset) > 2 and "runtime-R" in kset[2] else "1")
+    # K3 (update + norm) on the TMA ring (k_proj_tma<4>; the default from 2^22 rows) at every column count
+    monkeypatch.setenv("TE_NORM_TMA", "1" if len(kset) > 2 and "norm-tma" in kset[2] else "0")
     c = configs.build(1)
     h = te.te_create_csr(c["n"], c["rowptr"], c["col"], c["val"])
     te.te_set_option(h, te.TE_OPT_KERNELS, kset[0])

@@ -59,7 +59,7 @@ int main(int argc, char** argv) {
   const int list[] = {2, 4, 6, 8, 12, 16, 20, 24, 28, 32, 40, 48, 64};
   const int NL = sizeof(list) / sizeof(list[0]);
   printf("n = %lld; GB/s (algorithmic bytes: dots 16n(ncols+1), update 16n(ncols+2))\n", (long long)n);
-  printf("ncols | tma dots upd | norm | r: TPR CPL dots upd (best) ...\n");
+  printf("ncols | tma dots upd | norm (no write, write) | r: TPR CPL dots upd (best) ...\n");
   for (int li = 0; li < NL; ++li) {
     const int nc = list[li], j = nc - 1;
     CUtensorMap tm;
@@ -104,7 +104,9 @@ int main(int argc, char** argv) {
       ttu = timeit([&] { k_proj_tma<1, 32><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
     }
     const double tn = timeit([&] { k_update_norm<<<8 * sms, kThreads>>>(d, j, 0, 0); }, 5);
-    printf("%5d | %5.0f %5.0f | %5.0f |", nc, gbs(ttd, bd), gbs(ttu, bu), gbs(tn, bd));
+    // the same pass writing column j + 1 (as in the restart loop): 16n more bytes
+    const double tnw = nc < mcap ? timeit([&] { k_update_norm<<<8 * sms, kThreads>>>(d, j, 1, 0); }, 5) : tn;
+    printf("%5d | %5.0f %5.0f | %5.0f %5.0f |", nc, gbs(ttd, bd), gbs(ttu, bu), gbs(tn, bd), nc < mcap ? gbs(tnw, bu) : 0.0);
     auto variant = [&](auto tpr_c, auto cpl_c, auto u_c, auto minb_c) {
       constexpr int TPR = decltype(tpr_c)::value, CPL = decltype(cpl_c)::value, U = decltype(u_c)::value, MINB = decltype(minb_c)::value;
       if (nc > TPR * CPL || (TPR > 1 && nc <= TPR * CPL / 2)) return;

@@ -9,7 +9,7 @@ import re
 import sys
 
 CLASS = [(r"k_spmv", "spmv"), (r"k_proj_tma<0[,>]|k_proj_r<0", "proj_dots"), (r"k_proj_tma<[13][,>]|k_proj_r<1", "update_proj"),
-         (r"k_update_norm", "update_norm"), (r"k_combine", "combine")]
+         (r"k_update_norm|k_proj_tma<4[,>]", "update_norm"), (r"k_combine", "combine")]
 
 
 def cls(name):
