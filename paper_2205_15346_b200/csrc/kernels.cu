@@ -17,6 +17,10 @@
 #include <utility>
 #include <vector>
 
+#ifndef TE_PROJ_LDS
+#define TE_PROJ_LDS 0
+#endif
+
 namespace te {
 
 // --------------------------------------------------------------------------------------
@@ -241,7 +245,11 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
   // 1024-B alignment through an integer cast: the consumers then read the tiles with generic
   // LD.E.128 instead of LDS.128 — measured faster here (tools/micro/mb_proj.cu: dots at 23
   // columns 6.0 vs 4.2 TB/s with the LDS build, which also spills), so kept deliberately
+#if TE_PROJ_LDS  // experiment: keep the shared address space (LDS.128 tile reads)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+#else
   unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+#endif
   const int TR = kTileR * R;
   const size_t vbytes = (size_t)ncols * TR * 16;
   const size_t slot_bytes = vbytes + (size_t)TR * 16;
