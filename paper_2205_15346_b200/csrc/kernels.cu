@@ -17,10 +17,6 @@
 #include <utility>
 #include <vector>
 
-#ifndef TE_PROJ_LDS
-#define TE_PROJ_LDS 0
-#endif
-
 namespace te {
 
 // --------------------------------------------------------------------------------------
@@ -242,14 +238,16 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
       if (tid == j && blockIdx.x == 0) d.alpha[j] = sj * c.x;  // Re(c1_j + c2_j) = s_j Re(c1'_j + c2'_j)
     }
   }
-  // 1024-B alignment through an integer cast: the consumers then read the tiles with generic
-  // LD.E.128 instead of LDS.128 — measured faster here (tools/micro/mb_proj.cu: dots at 23
-  // columns 6.0 vs 4.2 TB/s with the LDS build, which also spills), so kept deliberately
-#if TE_PROJ_LDS  // experiment: keep the shared address space (LDS.128 tile reads)
-  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-#else
-  unsigned char* smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-#endif
+  // 1024-B alignment of the slot ring.  Dots and update + norm passes (MODE 0, 4): through an integer
+  // cast, so that the consumers read the tiles with generic LD.E.128 — measured faster there than
+  // LDS.128 (round 1: dots at 23 columns 6.0 vs 4.2 TB/s; this round with the compile-time tile
+  // stride: equal within 1 %).  Update + dots passes (MODE 1, 3): LDS.128 — with the compile-time
+  // stride the LDS build no longer spills and wins (config 5: 6.10 -> 6.39 TB/s, config 2: 5.40 -> 5.49)
+  unsigned char* smem;
+  if constexpr (MODE == 1 || MODE == 3)  // shared address space kept: LDS.128 tile reads (see above)
+    smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  else
+    smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int TR = kTileR * R;
   const size_t vbytes = (size_t)ncols * TR * 16;
   const size_t slot_bytes = vbytes + (size_t)TR * 16;
