@@ -13,6 +13,17 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
 
+def pytest_sessionstart(session):
+    """Build libtimeevolver.so in-tree when it is missing or older than its sources (nvcc cross-compiles
+    without a GPU).  Test infrastructure only: the product path never builds or falls back by itself, and
+    the tests that need the library fail loudly if this build does not succeed."""
+    try:
+        from paper_2205_15346_b200 import build as b
+        b.build()
+    except Exception as e:  # noqa: BLE001
+        sys.stderr.write(f"[conftest] library build failed: {e}\n")
+
+
 @pytest.fixture(scope="session")
 def gpu_lib():
     """The CUDA library through its C ABI; fails loudly when absent."""
