@@ -59,7 +59,7 @@ int main(int argc, char** argv) {
   const int list[] = {2, 4, 6, 8, 12, 16, 20, 24, 28, 32, 40, 48, 64};
   const int NL = sizeof(list) / sizeof(list[0]);
   printf("n = %lld; GB/s (algorithmic bytes: dots 16n(ncols+1), update 16n(ncols+2))\n", (long long)n);
-  printf("ncols | tma dots upd | norm (no write, write) | r: TPR CPL dots upd (best) ...\n");
+  printf("ncols | tma ring dots upd | same, runtime R | update_norm: k_update_norm no write, write, tma ring write | k_proj_r: TPR/CPL/U/MINB dots upd ...\n");
   for (int li = 0; li < NL; ++li) {
     const int nc = list[li], j = nc - 1;
     CUtensorMap tm;
@@ -85,28 +85,31 @@ int main(int argc, char** argv) {
     };
     const double tcopy = timeit([&] {}, 5);
     auto gbs = [&](double ms, double b) { return b / ((ms - tcopy) * 1e6); };
+    // the library's own dispatch (launch_proj_dots / launch_update_proj / launch_update_norm) with the
+    // TMA ring forced at every column count: compile-time-R builds (default) and the runtime-R fallback
+    static CUtensorMap tms[kMaxCols];
+    tms[j] = tm;
+    Launch L{};
+    L.stream = 0; L.num_sms = sms; L.grid_k3 = 8 * sms; L.tmaps = tms; L.proj_tma = 1; L.prefetch = 0;
+    L.proj_const_r = 1; L.norm_tma = 0;
+    (void)S; (void)R; (void)C; (void)sm;
     // reference dots (TMA) for the check
     std::vector<double2> gref(nc), gr(nc);
     cudaMemcpy(W, W0, 16 * n, cudaMemcpyDeviceToDevice);
-    if (nc <= 8) k_proj_tma<0, 8><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
-    else if (nc <= 16) k_proj_tma<0, 16><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
-    else k_proj_tma<0, 32><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0);
+    launch_proj_dots(d, j, L);
     cudaMemcpy(gref.data(), d.g1, 16 * nc, cudaMemcpyDeviceToHost);
-    double ttd, ttu;
-    if (nc <= 8) {
-      ttd = timeit([&] { k_proj_tma<0, 8><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
-      ttu = timeit([&] { k_proj_tma<1, 8><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
-    } else if (nc <= 16) {
-      ttd = timeit([&] { k_proj_tma<0, 16><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
-      ttu = timeit([&] { k_proj_tma<1, 16><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
-    } else {
-      ttd = timeit([&] { k_proj_tma<0, 32><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
-      ttu = timeit([&] { k_proj_tma<1, 32><<<sms, kProjThreads, sm>>>(tm, d, j, S, R, C, 0); }, 5);
-    }
-    const double tn = timeit([&] { k_update_norm<<<8 * sms, kThreads>>>(d, j, 0, 0); }, 5);
+    const double ttd = timeit([&] { launch_proj_dots(d, j, L); }, 5);
+    const double ttu = timeit([&] { launch_update_proj(d, j, L); }, 5);
+    const double tn = timeit([&] { launch_update_norm(d, j, false, L); }, 5);
     // the same pass writing column j + 1 (as in the restart loop): 16n more bytes
-    const double tnw = nc < mcap ? timeit([&] { k_update_norm<<<8 * sms, kThreads>>>(d, j, 1, 0); }, 5) : tn;
-    printf("%5d | %5.0f %5.0f | %5.0f %5.0f |", nc, gbs(ttd, bd), gbs(ttu, bu), gbs(tn, bd), nc < mcap ? gbs(tnw, bu) : 0.0);
+    const double tnw = nc < mcap ? timeit([&] { launch_update_norm(d, j, true, L); }, 5) : tn;
+    L.norm_tma = 1;
+    const double tnt = nc < mcap ? timeit([&] { launch_update_norm(d, j, true, L); }, 5) : tn;
+    L.proj_const_r = 0;
+    const double ttd0 = timeit([&] { launch_proj_dots(d, j, L); }, 5);
+    const double ttu0 = timeit([&] { launch_update_proj(d, j, L); }, 5);
+    printf("%5d | %5.0f %5.0f | %5.0f %5.0f | %5.0f %5.0f %5.0f |", nc, gbs(ttd, bd), gbs(ttu, bu), gbs(ttd0, bd), gbs(ttu0, bu),
+           gbs(tn, bd), nc < mcap ? gbs(tnw, bu) : 0.0, nc < mcap ? gbs(tnt, bu) : 0.0);
     auto variant = [&](auto tpr_c, auto cpl_c, auto u_c, auto minb_c) {
       constexpr int TPR = decltype(tpr_c)::value, CPL = decltype(cpl_c)::value, U = decltype(u_c)::value, MINB = decltype(minb_c)::value;
       if (nc > TPR * CPL || (TPR > 1 && nc <= TPR * CPL / 2)) return;
