@@ -242,9 +242,10 @@ __global__ void __launch_bounds__(kProjThreads, MINB)
   // cast, so that the consumers read the tiles with generic LD.E.128 — measured faster there than
   // LDS.128 (round 1: dots at 23 columns 6.0 vs 4.2 TB/s; this round with the compile-time tile
   // stride: equal within 1 %).  Update + dots passes (MODE 1, 3): LDS.128 — with the compile-time
-  // stride the LDS build no longer spills and wins (config 5: 6.10 -> 6.39 TB/s, config 2: 5.40 -> 5.49)
+  // stride the LDS build no longer spills and wins (config 5: 6.10 -> 6.39 TB/s, config 2: 5.40 -> 5.49);
+  // the runtime-R fallback keeps the generic loads (its LDS build spills: 4.3-5.2 TB/s)
   unsigned char* smem;
-  if constexpr (MODE == 1 || MODE == 3)  // shared address space kept: LDS.128 tile reads (see above)
+  if constexpr ((MODE == 1 || MODE == 3) && RT > 0)  // shared address space kept: LDS.128 tile reads (see above)
     smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   else
     smem = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
